@@ -1,0 +1,132 @@
+// butterfly.h -- hybrid butterfly on the device (level-major padded layout)
+// and its host (reference-layout) twin.
+//
+// Reference container: HybridButterfly (butterfly.hpp:20-66): per level 2^L
+// blocks, flat index tau*2^(L-l)+nu; u_leaf, r_blocks[l-lm], b_blocks,
+// w_blocks[l-1], v_leaf.  On the device every level is ONE buffer of 2^L
+// equally-strided blocks (ld x cap, column major, zero padded):
+//   * leaves: ld = max leaf size, rows beyond the leaf are zero;
+//   * R/W transfer blocks are stored "padded-stacked": the first child's rows
+//     at [0, r1), the second child's at [gap, gap + r2) with gap = P(child
+//     level), so a stacked pair of child coefficient vectors is simply two
+//     adjacent P-row slots of a level-major coefficient buffer;
+//   * columns beyond the block's rank are zero; P = max rank of the level.
+// Zero padding contributes exact zeros to every product, so all blocks of a
+// level run as one uniform batched GEMM.
+#pragma once
+
+#include <complex>
+#include <memory>
+#include <vector>
+
+#include "context.h"
+#include "kernels.cuh"
+#include "tree.h"
+
+namespace bfly {
+
+inline int64_t bidx(int L, int l, int64_t tau, int64_t nu) { return tau * (int64_t(1) << (L - l)) + nu; }
+
+// --------------------------------------------------------- host layout
+struct HostBlock {
+  int64_t rows = 0, cols = 0;
+  std::vector<std::complex<double>> a;  // column major
+};
+
+struct HostButterfly {
+  int L = 0, lm = 0;
+  bool is_real = false;
+  Tree rt, ct;
+  std::vector<HostBlock> u, v, b;
+  std::vector<std::vector<HostBlock>> r, w;  // r[l-lm], w[l-1]
+
+  int64_t u_rank(int l, int64_t tau, int64_t nu) const {
+    return l == L ? u[tau].cols : r[l - lm][bidx(L, l, tau, nu)].cols;
+  }
+  int64_t v_rank(int l, int64_t tau, int64_t nu) const {
+    return l == 0 ? v[nu].cols : w[l - 1][bidx(L, l, tau, nu)].cols;
+  }
+  void validate() const;  // butterfly.hpp:290-326
+  int64_t nnz() const;
+  int64_t max_rank() const;
+  std::vector<uint8_t> serialize(int scalar_tag) const;  // serialize.hpp:103-127
+  static HostButterfly deserialize(const uint8_t* buf, int64_t n);
+};
+
+// -------------------------------------------------------- device layout
+template <typename R>
+struct Level {
+  DBuf<cx<R>> data;
+  int64_t ld = 0, cap = 0;  // padded rows / column capacity per block
+  int P = 0;                // max rank of the level (columns used by products)
+  int gap = 0;              // second-child row offset (transfer blocks)
+  std::vector<int32_t> ranks, rows;  // per block (host)
+  DBuf<int32_t> dranks;
+
+  int64_t stride() const { return ld * cap; }
+  cx<R>* block(int64_t i) const { return data.p + i * stride(); }
+  void alloc(Ctx* c, int64_t nb, int64_t ld_, int64_t cap_) {
+    ld = std::max<int64_t>(ld_, 1);
+    cap = std::max<int64_t>(cap_, 1);
+    data.reset(c, (size_t)(nb * ld * cap));
+    ranks.assign(nb, 0);
+    rows.assign(nb, 0);
+    dranks.reset(c, nb);
+  }
+  void finish_ranks(Ctx* c);  // download ranks, set P
+};
+
+template <typename R>
+struct DevButterfly {
+  Ctx* ctx = nullptr;
+  int L = 0, lm = 0;
+  bool is_real = false;
+  Tree rt, ct;
+  Level<R> uleaf, vleaf, b;
+  std::vector<Level<R>> r, w;  // r[l-lm] (l in [lm, L-1]), w[l-1] (l in [1, lm])
+  DBuf<int64_t> rperm, cperm;  // device permutations (non-identity trees)
+  bool leaves_uniform_r = true, leaves_uniform_c = true;
+
+  int64_t m() const { return rt.n; }
+  int64_t n() const { return ct.n; }
+  int64_t nb() const { return int64_t(1) << L; }
+  int PU(int l) const { return l == L ? uleaf.P : r[l - lm].P; }
+  int PV(int l) const { return l == 0 ? vleaf.P : w[l - 1].P; }
+  int u_rank(int l, int64_t tau, int64_t nu) const {
+    return l == L ? uleaf.ranks[tau] : r[l - lm].ranks[bidx(L, l, tau, nu)];
+  }
+  int v_rank(int l, int64_t tau, int64_t nu) const {
+    return l == 0 ? vleaf.ranks[nu] : w[l - 1].ranks[bidx(L, l, tau, nu)];
+  }
+  const Level<R>& ulevel(int l) const { return l == L ? uleaf : r[l - lm]; }
+  const Level<R>& vlevel(int l) const { return l == 0 ? vleaf : w[l - 1]; }
+
+  void setup_trees(Ctx* c, const Tree& row, const Tree& col, int levels, int center);
+  // K x / K^T y / K^H y ; device buffers, original ordering
+  void apply(int trans, const cx<R>* x, int64_t ldx, cx<R>* y, int64_t ldy, int64_t k);
+  int64_t nnz() const;
+  int64_t max_rank() const;
+  double apply_flops(int64_t k) const;   // 8 * nnz * k (complex)
+  double apply_bytes(int64_t k) const;   // nnz*s + (m+n)*k*s
+
+  HostButterfly to_host() const;
+  static std::unique_ptr<DevButterfly> from_host(Ctx* c, const HostButterfly& h);
+
+ private:
+  struct Plan {
+    std::vector<DBuf<GemmEnt>> stages;
+    std::vector<int> nent;
+  };
+  Plan plan_n_, plan_h_;
+  bool have_n_ = false, have_h_ = false;
+  void apply_n(const cx<R>* xt, int64_t ldx, cx<R>* yt, int64_t ldy, int64_t k);
+  void apply_h(const cx<R>* yt, int64_t ldy, cx<R>* xt, int64_t ldx, int64_t k);
+};
+
+// Builds a HostButterfly from a seeded generator (synth_butterfly,
+// operators.hpp:131-178, generalised to leaf b / rank r) + perturbation.
+HostButterfly synth_host(int levels, int64_t leaf, int64_t rank, uint64_t seed, bool is_real, double perturb);
+// host Gaussian block (same stream as the device K1 kernel)
+void host_gaussian(int64_t rows, int64_t cols, uint64_t seed, bool is_real, std::complex<double>* out);
+
+}  // namespace bfly

@@ -1,0 +1,46 @@
+// context.cu -- per-GPU context implementation.
+#include "context.h"
+
+namespace bfly {
+
+static thread_local Ctx* g_current = nullptr;
+Ctx* current_ctx() { return g_current; }
+void set_current_ctx(Ctx* c) { g_current = c; }
+
+void note_launch(const char*) {
+  if (g_current) ++g_current->launches;
+}
+
+Ctx::Ctx(int dev) : device(dev) {
+  BFLY_CUDA(cudaSetDevice(dev));
+  BFLY_CUDA(cudaStreamCreateWithFlags(&stream, cudaStreamNonBlocking));
+  BFLY_CUDA(cudaDeviceGetDefaultMemPool(&pool, dev));
+  // keep freed blocks cached in the pool: level buffers are re-allocated
+  // every phase and must not go back to the driver each time.
+  uint64_t threshold = UINT64_MAX;
+  BFLY_CUDA(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &threshold));
+  cudaDeviceProp p;
+  BFLY_CUDA(cudaGetDeviceProperties(&p, dev));
+  sm_count = p.multiProcessorCount;
+}
+
+Ctx::~Ctx() {
+  if (stream) {
+    cudaStreamSynchronize(stream);
+    cudaStreamDestroy(stream);
+  }
+}
+
+void* Ctx::alloc(size_t bytes) {
+  void* p = nullptr;
+  cudaError_t e = cudaMallocFromPoolAsync(&p, bytes, pool, stream);
+  if (e != cudaSuccess)
+    fail(CUDA_ERR, "device allocation of " + std::to_string(bytes) + " bytes failed: " + cudaGetErrorString(e));
+  return p;
+}
+
+void Ctx::release(void* p) { cudaFreeAsync(p, stream); }
+
+void Ctx::sync() { BFLY_CUDA(cudaStreamSynchronize(stream)); }
+
+}  // namespace bfly

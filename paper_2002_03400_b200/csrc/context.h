@@ -1,0 +1,105 @@
+// context.h -- per-GPU context: stream, stream-ordered memory pool, launch
+// accounting, optional NCCL communicator.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <cstring>
+#include <utility>
+#include <vector>
+
+#include "common.cuh"
+
+struct ncclComm;
+
+namespace bfly {
+
+struct Ctx {
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  cudaMemPool_t pool = nullptr;
+  int64_t launches = 0;
+  int sm_count = 148;
+  // multi-GPU (rank-sharded probes + NCCL all-gather of each level)
+  int rank = 0, world = 1;
+  ncclComm* comm = nullptr;
+
+  explicit Ctx(int dev);
+  ~Ctx();
+  void* alloc(size_t bytes);
+  void release(void* p);
+  void sync();
+};
+
+// The context kernels are currently being launched for (set by the C ABI
+// entry points; the library is used from one host thread per context).
+Ctx* current_ctx();
+void set_current_ctx(Ctx* c);
+
+struct CtxScope {
+  Ctx* prev;
+  explicit CtxScope(Ctx* c) : prev(current_ctx()) {
+    set_current_ctx(c);
+    if (c) BFLY_CUDA(cudaSetDevice(c->device));
+  }
+  ~CtxScope() { set_current_ctx(prev); }
+};
+
+// RAII device buffer on the context's stream-ordered pool.
+template <typename T>
+struct DBuf {
+  T* p = nullptr;
+  size_t n = 0;
+  Ctx* ctx = nullptr;
+
+  DBuf() = default;
+  DBuf(Ctx* c, size_t count) { reset(c, count); }
+  DBuf(const DBuf&) = delete;
+  DBuf& operator=(const DBuf&) = delete;
+  DBuf(DBuf&& o) noexcept : p(o.p), n(o.n), ctx(o.ctx) { o.p = nullptr; o.n = 0; }
+  DBuf& operator=(DBuf&& o) noexcept {
+    if (this != &o) {
+      free();
+      p = o.p; n = o.n; ctx = o.ctx;
+      o.p = nullptr; o.n = 0;
+    }
+    return *this;
+  }
+  ~DBuf() { free(); }
+
+  void reset(Ctx* c, size_t count) {
+    free();
+    ctx = c;
+    n = count;
+    p = count ? static_cast<T*>(c->alloc(count * sizeof(T))) : nullptr;
+  }
+  void zero() {
+    if (n) BFLY_CUDA(cudaMemsetAsync(p, 0, n * sizeof(T), ctx->stream));
+  }
+  void free() {
+    if (p && ctx) ctx->release(p);
+    p = nullptr;
+    n = 0;
+  }
+  void upload(const T* host, size_t count) {
+    if (count) BFLY_CUDA(cudaMemcpyAsync(p, host, count * sizeof(T), cudaMemcpyHostToDevice, ctx->stream));
+  }
+  void upload(const std::vector<T>& v) {
+    if (v.size() > n) reset(ctx, v.size());
+    upload(v.data(), v.size());
+  }
+  void download(T* host, size_t count) const {
+    if (count) BFLY_CUDA(cudaMemcpyAsync(host, p, count * sizeof(T), cudaMemcpyDeviceToHost, ctx->stream));
+  }
+  size_t bytes() const { return n * sizeof(T); }
+};
+
+template <typename T>
+DBuf<T> to_device(Ctx* c, const std::vector<T>& v) {
+  DBuf<T> d(c, v.size());
+  d.upload(v.data(), v.size());
+  return d;
+}
+
+}  // namespace bfly

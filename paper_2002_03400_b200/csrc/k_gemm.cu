@@ -1,0 +1,128 @@
+// k_gemm.cu -- batched small complex GEMM (butterfly apply levels, partial
+// chain projections; butterfly.hpp:71-193, 330-382).
+//
+// Every output block is C_e = sum_{s<S} op(A_s) B_s with uniform padded
+// shapes per launch (zero padding contributes exact zeros).  One CTA computes
+// a 32 x 32 tile of one block; A and B tiles are staged through shared memory.
+#include "kernels.cuh"
+
+namespace bfly {
+
+namespace {
+
+constexpr int TM = 32, TN = 32, TK = 16;
+
+template <typename R, int OP, int S>
+__global__ void __launch_bounds__(256) bgemm_kernel(const cx<R>* __restrict__ A, int64_t lda,
+                                                    const cx<R>* __restrict__ B, int64_t ldb, cx<R>* __restrict__ C,
+                                                    int64_t ldc, int M, int K, const GemmEnt* __restrict__ ents,
+                                                    int accumulate, int ncols_all) {
+  using V = cx<R>;
+  __shared__ V As[TK][TM + 1];
+  __shared__ V Bs[TK][TN + 1];
+  const GemmEnt e = ents[blockIdx.x];
+  const int ncols = ncols_all > 0 ? ncols_all : e.ncols;
+  const int Me = min(M, e.mrows), Ke = min(K, e.krows);
+  const int n0 = blockIdx.y * TN;
+  const int m0 = blockIdx.z * TM;
+  if (n0 >= ncols || m0 >= Me) return;
+  const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
+  V acc[2][2];
+#pragma unroll
+  for (int i = 0; i < 2; ++i)
+#pragma unroll
+    for (int j = 0; j < 2; ++j) acc[i][j] = mkc<R>(0, 0);
+
+#pragma unroll
+  for (int s = 0; s < S; ++s) {
+    const V* Ab = A + (s == 0 ? e.a0 : e.a1);
+    const V* Bb = B + (s == 0 ? e.b0 : e.b1);
+    for (int k0 = 0; k0 < K; k0 += TK) {
+      // A tile: element (m, k) of op(A), m in [m0, m0+32), k in [k0, k0+16)
+#pragma unroll
+      for (int q = 0; q < 2; ++q) {
+        int idx = threadIdx.x + q * 256;
+        int mm, kk;
+        if (OP == OP_N) {
+          mm = idx & 31;
+          kk = idx >> 5;
+        } else {
+          kk = idx & 15;
+          mm = idx >> 4;
+        }
+        int gm = m0 + mm, gk = k0 + kk;
+        V v = mkc<R>(0, 0);
+        if (gm < Me && gk < K) {
+          if (OP == OP_N) v = Ab[gm + (int64_t)gk * lda];
+          else {
+            v = Ab[gk + (int64_t)gm * lda];
+            if (OP == OP_H) v = cconj(v);
+          }
+        }
+        As[kk][mm] = v;
+      }
+#pragma unroll
+      for (int q = 0; q < 2; ++q) {
+        int idx = threadIdx.x + q * 256;
+        int kk = idx & 15, nn = idx >> 4;
+        int gk = k0 + kk, gn = n0 + nn;
+        V v = mkc<R>(0, 0);
+        if (gk < Ke && gn < ncols) v = Bb[gk + (int64_t)gn * ldb];
+        Bs[kk][nn] = v;
+      }
+      __syncthreads();
+#pragma unroll
+      for (int kk = 0; kk < TK; ++kk) {
+        V a0 = As[kk][ty], a1 = As[kk][ty + 16];
+        V b0 = Bs[kk][tx], b1 = Bs[kk][tx + 16];
+        cfma(acc[0][0], a0, b0);
+        cfma(acc[0][1], a0, b1);
+        cfma(acc[1][0], a1, b0);
+        cfma(acc[1][1], a1, b1);
+      }
+      __syncthreads();
+    }
+  }
+  V* Cb = C + e.c;
+#pragma unroll
+  for (int i = 0; i < 2; ++i)
+#pragma unroll
+    for (int j = 0; j < 2; ++j) {
+      int gm = m0 + ty + 16 * i, gn = n0 + tx + 16 * j;
+      if (gm < Me && gn < ncols) {
+        V* p = Cb + gm + (int64_t)gn * ldc;
+        *p = accumulate ? cadd(*p, acc[i][j]) : acc[i][j];
+      }
+    }
+}
+
+}  // namespace
+
+template <typename R>
+void launch_bgemm(Ctx* c, int op, int M, int K, int S, const cx<R>* A, int64_t lda, const cx<R>* B, int64_t ldb,
+                  cx<R>* C, int64_t ldc, const GemmEnt* ents, int nent, int max_ncols, bool accumulate,
+                  int ncols_all) {
+  if (nent <= 0 || M <= 0 || max_ncols <= 0) return;
+  // K == 0: the product is an exact zero block
+  dim3 grid(nent, (unsigned)ceil_div(max_ncols, TN), (unsigned)ceil_div(M, TM));
+  if (grid.y > 65535 || grid.z > 65535) fail(PRECONDITION, "bgemm: grid too large");
+#define BG(OPV, SV) bgemm_kernel<R, OPV, SV><<<grid, 256, 0, c->stream>>>(A, lda, B, ldb, C, ldc, M, K, ents, accumulate, ncols_all)
+  if (S == 1) {
+    if (op == OP_N) BG(OP_N, 1);
+    else if (op == OP_T) BG(OP_T, 1);
+    else BG(OP_H, 1);
+  } else {
+    if (op == OP_N) BG(OP_N, 2);
+    else if (op == OP_T) BG(OP_T, 2);
+    else BG(OP_H, 2);
+  }
+#undef BG
+  BFLY_LAUNCH_CHECK("bgemm");
+}
+
+template void launch_bgemm<double>(Ctx*, int, int, int, int, const double2*, int64_t, const double2*, int64_t, double2*,
+                                   int64_t, const GemmEnt*, int, int, bool, int);
+template void launch_bgemm<float>(Ctx*, int, int, int, int, const float2*, int64_t, const float2*, int64_t, float2*,
+                                  int64_t, const GemmEnt*, int, int, bool, int);
+
+}  // namespace bfly

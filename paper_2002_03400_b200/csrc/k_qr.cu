@@ -1,0 +1,427 @@
+// k_qr.cu -- K5 batched truncated column-pivoted QR and K6 batched core fit.
+//
+// K5 reproduces pivoted_qr_truncate (reference linalg.hpp:62-80) as computed
+// by Eigen::ColPivHouseholderQR + householderQ(): max-updated-norm pivoting
+// (first index on ties), Householder beta = -sign(Re c0)||x||,
+// tau = conj((beta-c0)/beta), LAWN-176 norm downdating with direct
+// recomputation at sqrt(eps), truncation |R_kk| > eps_t |R_00|.  The
+// factorization stops at the first rejected pivot (later steps cannot change
+// the kept columns), and Q(:,0:k) is formed in place (LAPACK ung2r order).
+// One CTA (8 warps) per block; the block lives in shared memory.
+//
+// K6 is core_block + pinv_solve (reconstruct.hpp:125-138, linalg.hpp:128-139):
+// B = (Q^H z) pinv(coeff), pinv through a one-sided Jacobi SVD of coeff^H
+// (parallel round-robin pair ordering), singular values <= 1e-12 smax dropped.
+#include <cfloat>
+
+#include "kernels.cuh"
+
+namespace bfly {
+
+namespace {
+
+constexpr int QR_THREADS = 256;
+constexpr int QR_WARPS = QR_THREADS / 32;
+
+template <typename T> __device__ __forceinline__ T warp_sum(T v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+template <typename R> struct QrTraits;
+template <> struct QrTraits<double> {
+  static constexpr double tiny = DBL_MIN;
+  static constexpr double sqrt_eps = 1.4901161193847656e-08;  // sqrt(DBL_EPSILON)
+  static constexpr double jacobi_tol = 1e-15;
+};
+template <> struct QrTraits<float> {
+  static constexpr float tiny = FLT_MIN;
+  static constexpr float sqrt_eps = 3.4526698e-04f;  // sqrt(FLT_EPSILON)
+  static constexpr float jacobi_tol = 1e-7f;
+};
+
+template <typename R>
+__global__ void __launch_bounds__(QR_THREADS) cpqr_kernel(const cx<R>* __restrict__ src, int64_t ld_src,
+                                                          cx<R>* __restrict__ dst, int64_t ld_dst, int cap,
+                                                          const QrEnt* __restrict__ ents, int32_t* ranks, double eps_t,
+                                                          int zld) {
+  using V = cx<R>;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  const QrEnt e = ents[blockIdx.x];
+  const int r = e.r1 + e.r2, w = e.cols;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  V* Z = reinterpret_cast<V*>(smem_raw);  // zld x w
+  R* nu = reinterpret_cast<R*>(Z + (size_t)zld * w);
+  R* nd = nu + w;
+  V* tau = reinterpret_cast<V*>(nd + w);
+  __shared__ int s_big;
+  __shared__ int s_k;
+  __shared__ R s_total;
+
+  V* out = dst + e.dst;
+  if (r == 0 || w == 0) {
+    for (int64_t i = threadIdx.x; i < ld_dst * cap; i += QR_THREADS) out[i] = mkc<R>(0, 0);
+    if (threadIdx.x == 0) ranks[e.rank_slot] = 0;
+    return;
+  }
+  // load the compact block
+  for (int idx = threadIdx.x; idx < r * w; idx += QR_THREADS) {
+    int i = idx % r, c = idx / r;
+    const V* s = src + e.src + (int64_t)c * ld_src;
+    Z[i + c * zld] = i < e.r1 ? s[i] : s[e.src_gap + (i - e.r1)];
+  }
+  __syncthreads();
+  for (int c = warp; c < w; c += QR_WARPS) {
+    R s = 0;
+    for (int i = lane; i < r; i += 32) s += cabs2(Z[i + c * zld]);
+    s = warp_sum(s);
+    if (lane == 0) nu[c] = nd[c] = sqrt(s);
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    R t = 0;
+    for (int c = 0; c < w; ++c) t += nu[c] * nu[c];
+    s_total = t;
+  }
+  __syncthreads();
+  if (s_total == R(0)) {  // all-zero input: rank 0 (linalg.hpp:67-71)
+    for (int64_t i = threadIdx.x; i < ld_dst * cap; i += QR_THREADS) out[i] = mkc<R>(0, 0);
+    if (threadIdx.x == 0) ranks[e.rank_slot] = 0;
+    return;
+  }
+  const int kmax = min(r, w);
+  R head = 0;
+  int k = kmax;
+  for (int j = 0; j < kmax; ++j) {
+    // ---- pivot: first column with the largest updated norm
+    if (warp == 0) {
+      R best = -1;
+      int bi = w;
+      for (int c = j + lane; c < w; c += 32)
+        if (nu[c] > best) { best = nu[c]; bi = c; }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        R ob = __shfl_xor_sync(0xffffffffu, best, o);
+        int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+        if (ob > best || (ob == best && oi < bi)) { best = ob; bi = oi; }
+      }
+      if (lane == 0) s_big = bi;
+    }
+    __syncthreads();
+    const int big = s_big;
+    if (big != j) {
+      for (int i = threadIdx.x; i < r; i += QR_THREADS) {
+        V t = Z[i + j * zld];
+        Z[i + j * zld] = Z[i + big * zld];
+        Z[i + big * zld] = t;
+      }
+      if (threadIdx.x == 0) {
+        R t = nu[j]; nu[j] = nu[big]; nu[big] = t;
+        t = nd[j]; nd[j] = nd[big]; nd[big] = t;
+      }
+    }
+    __syncthreads();
+    // ---- Householder reflector of column j (makeHouseholderInPlace)
+    if (warp == 0) {
+      R tail = 0;
+      for (int i = j + 1 + lane; i < r; i += 32) tail += cabs2(Z[i + j * zld]);
+      tail = warp_sum(tail);
+      V c0 = Z[j + j * zld];
+      V t;
+      R beta;
+      bool trivial = tail <= QrTraits<R>::tiny && c0.y * c0.y <= QrTraits<R>::tiny;
+      if (trivial) {
+        t = mkc<R>(0, 0);
+        beta = c0.x;
+        for (int i = j + 1 + lane; i < r; i += 32) Z[i + j * zld] = mkc<R>(0, 0);
+      } else {
+        beta = sqrt(cabs2(c0) + tail);
+        if (c0.x >= R(0)) beta = -beta;
+        V d = mkc<R>(c0.x - beta, c0.y);
+        // 1/d
+        R dn = cabs2(d);
+        V inv = mkc<R>(d.x / dn, -d.y / dn);
+        for (int i = j + 1 + lane; i < r; i += 32) Z[i + j * zld] = cmul(Z[i + j * zld], inv);
+        // tau = conj((beta - c0) / beta)
+        t = mkc<R>((beta - c0.x) / beta, c0.y / beta);
+      }
+      if (lane == 0) {
+        Z[j + j * zld] = mkc<R>(beta, 0);
+        tau[j] = t;
+      }
+    }
+    __syncthreads();
+    const R absb = fabs(Z[j + j * zld].x);
+    if (j == 0) head = absb;
+    if (!(absb > R(eps_t) * head)) {
+      k = j;
+      break;
+    }
+    // ---- apply H_j = I - tau v v^H to the trailing columns; downdate norms
+    const V tj = tau[j];
+    for (int c = j + 1 + warp; c < w; c += QR_WARPS) {
+      V dot = mkc<R>(0, 0);
+      for (int i = j + 1 + lane; i < r; i += 32) cfma_conj(dot, Z[i + j * zld], Z[i + c * zld]);
+      dot.x = warp_sum(dot.x);
+      dot.y = warp_sum(dot.y);
+      dot = cadd(dot, Z[j + c * zld]);
+      V tt = cmul(tj, dot);
+      for (int i = j + 1 + lane; i < r; i += 32) {
+        V z = Z[i + c * zld];
+        V v = Z[i + j * zld];
+        Z[i + c * zld] = csub(z, cmul(v, tt));
+      }
+      V top = csub(Z[j + c * zld], tt);
+      __syncwarp();
+      if (lane == 0) Z[j + c * zld] = top;
+      // LAWN-176 downdate (uniform across the warp)
+      const R nuc = nu[c], ndc = nd[c];
+      __syncwarp();
+      if (nuc != R(0)) {
+        R temp = sqrt(cabs2(top)) / nuc;
+        temp = (R(1) + temp) * (R(1) - temp);
+        if (temp < R(0)) temp = 0;
+        R ratio = nuc / ndc;
+        R temp2 = temp * ratio * ratio;
+        if (temp2 <= QrTraits<R>::sqrt_eps) {
+          R s = 0;
+          for (int i = j + 1 + lane; i < r; i += 32) s += cabs2(Z[i + c * zld]);
+          s = warp_sum(s);
+          if (lane == 0) nu[c] = nd[c] = sqrt(s);
+        } else if (lane == 0) {
+          nu[c] = nuc * sqrt(temp);
+        }
+      }
+      __syncwarp();
+    }
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) s_k = k;
+  __syncthreads();
+  k = s_k;
+  // ---- form Q(:, 0:k) in place: Q = H_0 ... H_{k-1} [I_k; 0], H_i = I - conj(tau_i) v v^H
+  for (int i = k - 1; i >= 0; --i) {
+    const V tq = cconj(tau[i]);
+    for (int c = i + 1 + warp; c < k; c += QR_WARPS) {
+      V dot = Z[i + c * zld];  // v_i = 1
+      V part = mkc<R>(0, 0);
+      for (int q = i + 1 + lane; q < r; q += 32) cfma_conj(part, Z[q + i * zld], Z[q + c * zld]);
+      part.x = warp_sum(part.x);
+      part.y = warp_sum(part.y);
+      dot = cadd(dot, part);
+      V tt = cmul(tq, dot);
+      for (int q = i + 1 + lane; q < r; q += 32) Z[q + c * zld] = csub(Z[q + c * zld], cmul(Z[q + i * zld], tt));
+      __syncwarp();
+      if (lane == 0) Z[i + c * zld] = csub(Z[i + c * zld], tt);
+    }
+    __syncthreads();
+    for (int q = i + 1 + threadIdx.x; q < r; q += QR_THREADS) {
+      V v = Z[q + i * zld];
+      V nt = mkc<R>(-tq.x, -tq.y);
+      Z[q + i * zld] = cmul(nt, v);
+    }
+    if (threadIdx.x == 0) Z[i + i * zld] = mkc<R>(R(1) - tq.x, -tq.y);
+    for (int q = threadIdx.x; q < i; q += QR_THREADS) Z[q + i * zld] = mkc<R>(0, 0);
+    __syncthreads();
+  }
+  // ---- write the padded-stacked Q block
+  for (int64_t idx = threadIdx.x; idx < ld_dst * cap; idx += QR_THREADS) {
+    int d = (int)(idx % ld_dst), c = (int)(idx / ld_dst);
+    V v = mkc<R>(0, 0);
+    if (c < k) {
+      if (d < e.r1) v = Z[d + c * zld];
+      else if (d >= e.dst_gap && d < e.dst_gap + e.r2) v = Z[e.r1 + (d - e.dst_gap) + c * zld];
+    }
+    out[idx] = v;
+  }
+  if (threadIdx.x == 0) ranks[e.rank_slot] = k;
+}
+
+// --------------------------------------------------------------- core fit
+template <typename R>
+__global__ void __launch_bounds__(QR_THREADS) core_fit_kernel(const cx<R>* __restrict__ Q, int64_t ldq,
+                                                              const cx<R>* __restrict__ Zg, int64_t ldz,
+                                                              const cx<R>* __restrict__ Cf, int64_t ldc,
+                                                              cx<R>* __restrict__ B, int64_t ldb, int bcap,
+                                                              const CoreEnt* __restrict__ ents, cx<R>* scratch,
+                                                              int64_t scratch_stride, bool literal, int32_t* err_flag) {
+  using V = cx<R>;
+  const CoreEnt e = ents[blockIdx.x];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int ku = e.ku, kv = e.kv, w = e.w, r = e.r1 + e.r2;
+  V* out = B + e.b;
+  // zero the whole block first (padding stays zero)
+  for (int64_t i = threadIdx.x; i < ldb * bcap; i += QR_THREADS) out[i] = mkc<R>(0, 0);
+  if (w < kv) {
+    if (threadIdx.x == 0) atomicExch(err_flag, 1);
+    return;
+  }
+  if (ku == 0 || kv == 0) return;
+  V* proj = scratch + blockIdx.x * scratch_stride;  // ku x w
+  V* A = proj + (int64_t)ku * w;                    // w x kvp (coeff^H)
+  const int kvp = kv + (kv & 1);
+  V* Vm = A + (int64_t)w * kvp;                     // kvp x kvp
+  V* T = Vm + (int64_t)kvp * kvp;                   // ku x kvp
+  R* sv = reinterpret_cast<R*>(T + (int64_t)ku * kvp);
+  __syncthreads();
+  // proj = Q^H z
+  for (int idx = threadIdx.x; idx < ku * w; idx += QR_THREADS) {
+    int i = idx % ku, c = idx / ku;
+    V s = mkc<R>(0, 0);
+    const V* qc = Q + e.q + (int64_t)i * ldq;
+    const V* zc = Zg + e.z + (int64_t)c * ldz;
+    for (int q = 0; q < e.r1; ++q) cfma_conj(s, qc[q], zc[q]);
+    for (int q = 0; q < e.r2; ++q) cfma_conj(s, qc[e.q_gap + q], zc[e.z_gap + q]);
+    proj[idx] = s;
+  }
+  __syncthreads();
+  if (literal) {
+    for (int idx = threadIdx.x; idx < ku * kv; idx += QR_THREADS) {
+      int i = idx % ku, j = idx / ku;
+      V s = mkc<R>(0, 0);
+      for (int c = 0; c < w; ++c) cfma(s, proj[i + c * ku], Cf[e.coeff + j + (int64_t)c * ldc]);
+      out[i + (int64_t)j * ldb] = s;
+    }
+    return;
+  }
+  // A = coeff^H (w x kv), padded with a zero column to even count; V = I
+  for (int idx = threadIdx.x; idx < w * kvp; idx += QR_THREADS) {
+    int i = idx % w, j = idx / w;
+    A[idx] = j < kv ? cconj(Cf[e.coeff + j + (int64_t)i * ldc]) : mkc<R>(0, 0);
+  }
+  for (int idx = threadIdx.x; idx < kvp * kvp; idx += QR_THREADS)
+    Vm[idx] = (idx % kvp == idx / kvp) ? mkc<R>(1, 0) : mkc<R>(0, 0);
+  __shared__ int s_rot;
+  __syncthreads();
+  const int npair = kvp / 2;
+  for (int sweep = 0; sweep < 60; ++sweep) {
+    if (threadIdx.x == 0) s_rot = 0;
+    __syncthreads();
+    for (int round = 0; round < kvp - 1; ++round) {
+      for (int pi = warp; pi < npair; pi += QR_WARPS) {
+        // round-robin tournament: position 0 fixed, others rotate
+        int a = (pi == 0) ? 0 : 1 + (pi - 1 + round) % (kvp - 1);
+        int b = 1 + (kvp - 2 - pi + round) % (kvp - 1);
+        int p = min(a, b), q = max(a, b);
+        V* ap = A + (int64_t)p * w;
+        V* aq = A + (int64_t)q * w;
+        R alpha = 0, beta = 0;
+        V g = mkc<R>(0, 0);
+        for (int i = lane; i < w; i += 32) {
+          alpha += cabs2(ap[i]);
+          beta += cabs2(aq[i]);
+          cfma_conj(g, ap[i], aq[i]);
+        }
+        alpha = warp_sum(alpha);
+        beta = warp_sum(beta);
+        g.x = warp_sum(g.x);
+        g.y = warp_sum(g.y);
+        R gm = sqrt(cabs2(g));
+        if (gm == R(0) || gm <= QrTraits<R>::jacobi_tol * sqrt(alpha * beta)) continue;
+        if (lane == 0) s_rot = 1;
+        V ph = mkc<R>(g.x / gm, -g.y / gm);  // conj(e^{i phi})
+        R zeta = (beta - alpha) / (R(2) * gm);
+        R t = (zeta >= R(0) ? R(1) : R(-1)) / (fabs(zeta) + sqrt(R(1) + zeta * zeta));
+        R cs = R(1) / sqrt(R(1) + t * t);
+        R sn = cs * t;
+        for (int i = lane; i < w; i += 32) {
+          V x = ap[i], y = cmul(aq[i], ph);
+          ap[i] = mkc<R>(cs * x.x - sn * y.x, cs * x.y - sn * y.y);
+          aq[i] = mkc<R>(sn * x.x + cs * y.x, sn * x.y + cs * y.y);
+        }
+        V* vp = Vm + (int64_t)p * kvp;
+        V* vq = Vm + (int64_t)q * kvp;
+        for (int i = lane; i < kvp; i += 32) {
+          V x = vp[i], y = cmul(vq[i], ph);
+          vp[i] = mkc<R>(cs * x.x - sn * y.x, cs * x.y - sn * y.y);
+          vq[i] = mkc<R>(sn * x.x + cs * y.x, sn * x.y + cs * y.y);
+        }
+      }
+      __syncthreads();
+    }
+    if (!s_rot) break;
+    __syncthreads();
+  }
+  // singular values and cutoff
+  for (int j = warp; j < kvp; j += QR_WARPS) {
+    R s = 0;
+    for (int i = lane; i < w; i += 32) s += cabs2(A[i + (int64_t)j * w]);
+    s = warp_sum(s);
+    if (lane == 0) sv[j] = sqrt(s);
+  }
+  __syncthreads();
+  __shared__ R s_max;
+  if (threadIdx.x == 0) {
+    R m = 0;
+    for (int j = 0; j < kvp; ++j) m = fmax(m, sv[j]);
+    s_max = m;
+  }
+  __syncthreads();
+  const R cutoff = R(1e-12) * s_max;
+  // A columns <- A_j / s_j^2 (U_j / s_j) or 0
+  for (int idx = threadIdx.x; idx < w * kvp; idx += QR_THREADS) {
+    int j = idx / w;
+    R s = sv[j];
+    R f = (s > cutoff && s > R(0)) ? R(1) / (s * s) : R(0);
+    A[idx] = mkc<R>(A[idx].x * f, A[idx].y * f);
+  }
+  __syncthreads();
+  // T = proj * A  (ku x kvp)
+  for (int idx = threadIdx.x; idx < ku * kvp; idx += QR_THREADS) {
+    int i = idx % ku, j = idx / ku;
+    V s = mkc<R>(0, 0);
+    for (int c = 0; c < w; ++c) cfma(s, proj[i + c * ku], A[c + (int64_t)j * w]);
+    T[idx] = s;
+  }
+  __syncthreads();
+  // B = T * V^H  (ku x kv)
+  for (int idx = threadIdx.x; idx < ku * kv; idx += QR_THREADS) {
+    int i = idx % ku, j = idx / ku;
+    V s = mkc<R>(0, 0);
+    for (int q = 0; q < kvp; ++q) cfma_conj(s, Vm[j + (int64_t)q * kvp], T[i + (int64_t)q * ku]);
+    // note: cfma_conj(s, a, b) = s + conj(a) b ; we need T(i,q) * conj(V(j,q))
+    out[i + (int64_t)j * ldb] = s;
+  }
+}
+
+}  // namespace
+
+template <typename R>
+void launch_cpqr(Ctx* c, const cx<R>* src, int64_t ld_src, cx<R>* dst, int64_t ld_dst, int cap, const QrEnt* ents,
+                 int nent, int max_rows, int max_cols, int32_t* ranks, double eps) {
+  if (nent <= 0) return;
+  int zld = max_rows > 0 ? max_rows : 1;
+  size_t smem = sizeof(cx<R>) * (size_t)zld * max_cols + 2 * sizeof(R) * max_cols + sizeof(cx<R>) * max_cols + 64;
+  if (smem > 227 * 1024)
+    fail(PRECONDITION, "cpqr: block " + std::to_string(max_rows) + "x" + std::to_string(max_cols) +
+                           " exceeds shared memory (ranks above the supported maximum)");
+  auto kern = cpqr_kernel<R>;
+  BFLY_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  kern<<<nent, QR_THREADS, smem, c->stream>>>(src, ld_src, dst, ld_dst, cap, ents, ranks, eps, zld);
+  BFLY_LAUNCH_CHECK("cpqr");
+}
+
+template <typename R>
+void launch_core_fit(Ctx* c, const cx<R>* Q, int64_t ldq, const cx<R>* Z, int64_t ldz, const cx<R>* Cf, int64_t ldc,
+                     cx<R>* B, int64_t ldb, int bcap, const CoreEnt* ents, int nent, int max_ku, int max_kv,
+                     int max_w, bool literal, int32_t* err_flag) {
+  if (nent <= 0) return;
+  int kvp = max_kv + 1;
+  int64_t stride = (int64_t)max_ku * max_w + (int64_t)max_w * kvp + (int64_t)kvp * kvp + (int64_t)max_ku * kvp + kvp + 8;
+  DBuf<cx<R>> scratch(c, (size_t)stride * nent);
+  core_fit_kernel<R><<<nent, QR_THREADS, 0, c->stream>>>(Q, ldq, Z, ldz, Cf, ldc, B, ldb, bcap, ents, scratch.p, stride,
+                                                          literal, err_flag);
+  BFLY_LAUNCH_CHECK("core_fit");
+}
+
+template void launch_cpqr<double>(Ctx*, const double2*, int64_t, double2*, int64_t, int, const QrEnt*, int, int, int,
+                                  int32_t*, double);
+template void launch_cpqr<float>(Ctx*, const float2*, int64_t, float2*, int64_t, int, const QrEnt*, int, int, int,
+                                 int32_t*, double);
+template void launch_core_fit<double>(Ctx*, const double2*, int64_t, const double2*, int64_t, const double2*, int64_t,
+                                      double2*, int64_t, int, const CoreEnt*, int, int, int, int, bool, int32_t*);
+template void launch_core_fit<float>(Ctx*, const float2*, int64_t, const float2*, int64_t, const float2*, int64_t,
+                                     float2*, int64_t, int, const CoreEnt*, int, int, int, int, bool, int32_t*);
+
+}  // namespace bfly

@@ -1,0 +1,226 @@
+// operators.cu -- device black boxes: kernel-evaluated (NUFFT, plates,
+// circle), dense, composition, butterfly and user callback.
+#include <algorithm>
+
+#include "operators.h"
+
+namespace bfly {
+
+template <typename R>
+DBuf<cx<R>> DevOp<R>::pad_probes(int mode, const cx<R>* X, const std::vector<MatvecSeg>& segs, int64_t& wtot) {
+  wtot = 0;
+  for (const auto& s : segs) wtot = std::max<int64_t>(wtot, s.col0 + s.ncols);
+  const int64_t nin = in_dim(mode);
+  DBuf<cx<R>> p(ctx, (size_t)(nin * std::max<int64_t>(wtot, 1)));
+  p.zero();
+  for (const auto& s : segs)
+    if (s.rows > 0 && s.ncols > 0)
+      launch_copy2d<R>(ctx, p.p + s.row0 + s.col0 * nin, nin, X + s.x_off, s.ldx, s.rows, s.ncols);
+  return p;
+}
+
+namespace {
+
+// ------------------------------------------------ kernel-evaluated ops
+template <typename R>
+struct KernelOp : DevOp<R> {
+  DBuf<double> tx, ty, tz, sx, sy, sz;
+  double kappa = 0;
+  void do_apply(int mode, const cx<R>* X, const std::vector<MatvecSeg>& segs, cx<R>* Y, int64_t ldy) override {
+    Points tp{tx.p, ty.p, tz.p}, sp{sx.p, sy.p, sz.p};
+    Points outp = mode == OP_N ? tp : sp, inp = mode == OP_N ? sp : tp;
+    int64_t mout = this->out_dim(mode);
+    for (const auto& s : segs) {
+      this->evals += (double)mout * (double)s.rows;
+      this->flops += 8.0 * (double)mout * (double)s.rows * (double)s.ncols;
+    }
+    launch_kernel_matvec<R>(this->ctx, this->kind, mode, outp, inp, kappa, mout, X, Y, ldy, segs.data(),
+                            (int)segs.size());
+  }
+};
+
+// ---------------------------------------------------------- dense op
+template <typename R>
+struct DenseOp : DevOp<R> {
+  DBuf<cx<R>> a;  // m x n column major
+  void do_apply(int mode, const cx<R>* X, const std::vector<MatvecSeg>& segs, cx<R>* Y, int64_t ldy) override {
+    Ctx* c = this->ctx;
+    const int64_t m = this->m;
+    for (const auto& s : segs) {
+      int64_t mout = this->out_dim(mode);
+      if (s.ncols <= 0) continue;
+      if (s.rows <= 0) {
+        BFLY_CUDA(cudaMemset2DAsync(Y + s.col0 * ldy, ldy * sizeof(cx<R>), 0, mout * sizeof(cx<R>), s.ncols, c->stream));
+        continue;
+      }
+      GemmEnt e{};
+      e.a0 = mode == OP_N ? s.row0 * m : s.row0;
+      e.b0 = 0;
+      e.c = 0;
+      e.ncols = s.ncols;
+      e.mrows = 1 << 30;
+      e.krows = 1 << 30;
+      DBuf<GemmEnt> de = to_device(c, std::vector<GemmEnt>{e});
+      launch_bgemm<R>(c, mode, (int)mout, (int)s.rows, 1, a.p, m, X + s.x_off, s.ldx, Y + s.col0 * ldy, ldy, de.p, 1,
+                      s.ncols, false);
+      this->flops += 8.0 * (double)mout * (double)s.rows * (double)s.ncols;
+    }
+  }
+};
+
+// ---------------------------------------------------- composition op
+template <typename R>
+struct ComposeOp : DevOp<R> {
+  std::unique_ptr<DevOp<R>> f1, f2;  // A = f2 * f1
+  void do_apply(int mode, const cx<R>* X, const std::vector<MatvecSeg>& segs, cx<R>* Y, int64_t ldy) override {
+    DevOp<R>* first = mode == OP_N ? f1.get() : f2.get();
+    DevOp<R>* second = mode == OP_N ? f2.get() : f1.get();
+    const int64_t mid = first->out_dim(mode);
+    int64_t wtot = 0;
+    for (const auto& s : segs) wtot = std::max<int64_t>(wtot, s.col0 + s.ncols);
+    DBuf<cx<R>> t(this->ctx, (size_t)(mid * std::max<int64_t>(wtot, 1)));
+    double f0 = first->flops + second->flops, e0 = first->evals + second->evals;
+    first->apply_segs(mode, X, segs, t.p, mid);
+    std::vector<MatvecSeg> dense;
+    for (const auto& s : segs) dense.push_back(MatvecSeg{0, mid, s.col0 * mid, mid, s.col0, s.ncols, 0});
+    second->apply_segs(mode, t.p, dense, Y, ldy);
+    this->flops += first->flops + second->flops - f0;
+    this->evals += first->evals + second->evals - e0;
+  }
+};
+
+// ------------------------------------------------------ butterfly op
+template <typename R>
+struct ButterflyOp : DevOp<R> {
+  std::unique_ptr<DevButterfly<R>> bf;
+  void do_apply(int mode, const cx<R>* X, const std::vector<MatvecSeg>& segs, cx<R>* Y, int64_t ldy) override {
+    int64_t wtot = 0;
+    DBuf<cx<R>> xp = this->pad_probes(mode, X, segs, wtot);
+    if (wtot <= 0) return;
+    bf->apply(mode, xp.p, this->in_dim(mode), Y, ldy, wtot);
+    int64_t cols = 0;
+    for (const auto& s : segs) cols += s.ncols;
+    this->flops += bf->apply_flops(cols);
+  }
+};
+
+// ------------------------------------------------------- callback op
+template <typename R>
+struct CallbackOp : DevOp<R> {
+  bfly_apply_fn fn = nullptr;
+  void* user = nullptr;
+  void do_apply(int mode, const cx<R>* X, const std::vector<MatvecSeg>& segs, cx<R>* Y, int64_t ldy) override {
+    Ctx* c = this->ctx;
+    int64_t wtot = 0;
+    DBuf<cx<R>> xp = this->pad_probes(mode, X, segs, wtot);
+    if (wtot <= 0) return;
+    const int64_t nin = this->in_dim(mode), nout = this->out_dim(mode);
+    if (mode == OP_H) launch_conj<R>(c, xp.p, nin, wtot, nin);
+    int rc = fn(user, mode == OP_N ? 0 : 1, xp.p, nin, Y, ldy, wtot, (void*)c->stream);
+    if (rc != 0) fail(rc, "black-box callback failed with status " + std::to_string(rc));
+    if (mode == OP_H) launch_conj<R>(c, Y, nout, wtot, ldy);
+  }
+};
+
+std::vector<double> column(const double* p, int64_t n, int axis) {
+  std::vector<double> v(n);
+  for (int64_t i = 0; i < n; ++i) v[i] = p[i * 3 + axis];
+  return v;
+}
+
+}  // namespace
+
+template <typename R>
+std::unique_ptr<DevOp<R>> make_kernel_op(Ctx* c, int kind, int64_t m, int64_t n, const double* tgt, const double* src,
+                                         double kappa) {
+  if (kind != KK_NUFFT && kind != KK_PLATES && kind != KK_CIRCLE) fail(PRECONDITION, "unknown kernel operator kind");
+  if (m < 1 || n < 1) fail(PRECONDITION, "kernel operator: empty point set");
+  auto op = std::make_unique<KernelOp<R>>();
+  op->kind = kind;
+  op->m = m;
+  op->n = n;
+  op->ctx = c;
+  op->kappa = kappa;
+  op->tx = to_device(c, column(tgt, m, 0));
+  op->ty = to_device(c, column(tgt, m, 1));
+  op->tz = to_device(c, column(tgt, m, 2));
+  op->sx = to_device(c, column(src, n, 0));
+  op->sy = to_device(c, column(src, n, 1));
+  op->sz = to_device(c, column(src, n, 2));
+  c->sync();
+  return op;
+}
+
+template <typename R>
+std::unique_ptr<DevOp<R>> make_dense_op(Ctx* c, int64_t m, int64_t n, const std::vector<cx<R>>& a, bool is_real) {
+  auto op = std::make_unique<DenseOp<R>>();
+  op->kind = 0;
+  op->m = m;
+  op->n = n;
+  op->ctx = c;
+  op->is_real = is_real;
+  op->a = to_device(c, a);
+  c->sync();
+  return op;
+}
+
+template <typename R>
+std::unique_ptr<DevOp<R>> make_compose_op(Ctx* c, std::unique_ptr<DevOp<R>> f2, std::unique_ptr<DevOp<R>> f1) {
+  if (f2->n != f1->m) fail(DIMENSION, "composition: inner dimensions differ");
+  auto op = std::make_unique<ComposeOp<R>>();
+  op->kind = 4;
+  op->m = f2->m;
+  op->n = f1->n;
+  op->ctx = c;
+  op->is_real = f1->is_real && f2->is_real;
+  op->f1 = std::move(f1);
+  op->f2 = std::move(f2);
+  return op;
+}
+
+template <typename R>
+std::unique_ptr<DevOp<R>> make_butterfly_op(Ctx* c, std::unique_ptr<DevButterfly<R>> bf) {
+  auto op = std::make_unique<ButterflyOp<R>>();
+  op->kind = 5;
+  op->m = bf->m();
+  op->n = bf->n();
+  op->ctx = c;
+  op->is_real = bf->is_real;
+  op->bf = std::move(bf);
+  return op;
+}
+
+template <typename R>
+std::unique_ptr<DevOp<R>> make_callback_op(Ctx* c, int64_t m, int64_t n, bool is_real, bfly_apply_fn fn, void* user) {
+  if (!fn) fail(PRECONDITION, "callback operator: null function");
+  auto op = std::make_unique<CallbackOp<R>>();
+  op->kind = 6;
+  op->m = m;
+  op->n = n;
+  op->ctx = c;
+  op->is_real = is_real;
+  op->fn = fn;
+  op->user = user;
+  return op;
+}
+
+template <typename R>
+DevButterfly<R>* butterfly_of(DevOp<R>* op) {
+  auto* b = dynamic_cast<ButterflyOp<R>*>(op);
+  return b ? b->bf.get() : nullptr;
+}
+
+#define INST(R)                                                                                                  \
+  template struct DevOp<R>;                                                                                      \
+  template std::unique_ptr<DevOp<R>> make_kernel_op<R>(Ctx*, int, int64_t, int64_t, const double*, const double*, \
+                                                       double);                                                  \
+  template std::unique_ptr<DevOp<R>> make_dense_op<R>(Ctx*, int64_t, int64_t, const std::vector<cx<R>>&, bool);  \
+  template std::unique_ptr<DevOp<R>> make_compose_op<R>(Ctx*, std::unique_ptr<DevOp<R>>, std::unique_ptr<DevOp<R>>); \
+  template std::unique_ptr<DevOp<R>> make_butterfly_op<R>(Ctx*, std::unique_ptr<DevButterfly<R>>);                \
+  template std::unique_ptr<DevOp<R>> make_callback_op<R>(Ctx*, int64_t, int64_t, bool, bfly_apply_fn, void*);      \
+  template DevButterfly<R>* butterfly_of<R>(DevOp<R>*);
+INST(double)
+INST(float)
+#undef INST
+
+}  // namespace bfly

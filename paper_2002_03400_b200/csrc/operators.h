@@ -1,0 +1,73 @@
+// operators.h -- device black-box operators (BlackBoxOperator,
+// reference operators.hpp:17-66).
+//
+// The factorizer hands an operator a batch of structured probes: probe s has
+// nonzero input rows [row0, row0+rows) (operator index space) whose values
+// live at X + x_off (ld ldx), and owns output columns [col0, col0+ncols) of Y.
+// Built-in kinds exploit the zero rows (the reference pads and multiplies
+// the zeros, reconstruct.hpp:72-85); generic kinds see the padded probe.
+#pragma once
+
+#include <memory>
+#include <vector>
+
+#include "butterfly.h"
+#include "context.h"
+#include "kernels.cuh"
+
+extern "C" {
+typedef int (*bfly_apply_fn)(void* user, int trans, const void* x_dev, int64_t ldx, void* y_dev, int64_t ldy, int64_t k,
+                             void* stream);
+}
+
+namespace bfly {
+
+template <typename R>
+struct DevOp {
+  int kind = 0;
+  int64_t m = 0, n = 0;
+  bool is_real = false;
+  Ctx* ctx = nullptr;
+  int64_t fwd = 0, tr = 0;  // column counters (operators.hpp:41-47)
+  double flops = 0, evals = 0;  // algorithmic work of every product so far
+
+  virtual ~DevOp() = default;
+  int64_t in_dim(int mode) const { return mode == OP_N ? n : m; }
+  int64_t out_dim(int mode) const { return mode == OP_N ? m : n; }
+
+  // Y(:, seg cols) = op(A) X_seg for every segment; mode N, T or H (the
+  // adjoint, derived exactly as apply_adjoint in the reference).
+  void apply_segs(int mode, const cx<R>* X, const std::vector<MatvecSeg>& segs, cx<R>* Y, int64_t ldy) {
+    int64_t cols = 0;
+    for (const auto& s : segs) cols += s.ncols;
+    if (mode == OP_N) fwd += cols;
+    else tr += cols;
+    do_apply(mode, X, segs, Y, ldy);
+  }
+  void apply_dense(int mode, const cx<R>* X, int64_t ldx, cx<R>* Y, int64_t ldy, int64_t k) {
+    MatvecSeg s{0, in_dim(mode), 0, ldx, 0, (int32_t)k, 0};
+    apply_segs(mode, X, {s}, Y, ldy);
+  }
+
+ protected:
+  virtual void do_apply(int mode, const cx<R>* X, const std::vector<MatvecSeg>& segs, cx<R>* Y, int64_t ldy) = 0;
+  // materialise the padded probes (zeros outside the segment rows) as one
+  // in_dim x Wtot buffer whose columns line up with Y's
+  DBuf<cx<R>> pad_probes(int mode, const cx<R>* X, const std::vector<MatvecSeg>& segs, int64_t& wtot);
+};
+
+template <typename R>
+std::unique_ptr<DevOp<R>> make_kernel_op(Ctx* c, int kind, int64_t m, int64_t n, const double* tgt, const double* src,
+                                         double kappa);
+template <typename R>
+std::unique_ptr<DevOp<R>> make_dense_op(Ctx* c, int64_t m, int64_t n, const std::vector<cx<R>>& a, bool is_real);
+template <typename R>
+std::unique_ptr<DevOp<R>> make_compose_op(Ctx* c, std::unique_ptr<DevOp<R>> f2, std::unique_ptr<DevOp<R>> f1);
+template <typename R>
+std::unique_ptr<DevOp<R>> make_butterfly_op(Ctx* c, std::unique_ptr<DevButterfly<R>> bf);
+template <typename R>
+std::unique_ptr<DevOp<R>> make_callback_op(Ctx* c, int64_t m, int64_t n, bool is_real, bfly_apply_fn fn, void* user);
+template <typename R>
+DevButterfly<R>* butterfly_of(DevOp<R>* op);
+
+}  // namespace bfly

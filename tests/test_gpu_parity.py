@@ -1,0 +1,264 @@
+"""GPU parity: the sm_100a construction path against the CPU oracle.
+
+Bar (BASELINE north_star): identical per-level rank profiles, identical
+phase bookkeeping (columns, rounds, widths), and butterfly-apply outputs on
+seeded probes within 1e-10 relative (complex128).  Cases follow the
+reference's own tests (tests/test_reconstruct.cpp) plus every BASELINE
+config at sizes the oracle finishes in seconds.
+"""
+import numpy as np
+import pytest
+
+import oracle as O
+from helpers import oracle_config, rel_err
+
+pytestmark = pytest.mark.gpu
+
+APPLY_TOL = 1e-10
+
+
+@pytest.fixture(scope="module")
+def B():
+    import paper_2002_03400_b200 as B
+
+    return B
+
+
+def _compare(bf_gpu, log_gpu, bf_or, log_or, n_rows, n_cols, seed=5, real=False, tol=APPLY_TOL):
+    # rank profiles: every block of every level
+    np.testing.assert_array_equal(bf_gpu.rank_profile(), bf_or.rank_profile())
+    # phase bookkeeping (reconstruct.hpp:87-120)
+    names = [p.name for p in log_gpu.phases]
+    assert names == [p["name"] for p in log_or["phases"]]
+    for pg, po in zip(log_gpu.phases, log_or["phases"]):
+        assert pg.forward_columns == po["forward_columns"], pg.name
+        assert pg.transpose_columns == po["transpose_columns"], pg.name
+        assert pg.rounds == po["rounds"], pg.name
+        assert pg.probe_width == po["probe_width"], pg.name
+    assert log_gpu.rank_capped == log_or["rank_capped"]
+    # apply outputs on seeded probes
+    x = O.gaussian_matrix(n_cols, 16, O.seed_mix(seed, 5), real=real)
+    y = O.gaussian_matrix(n_rows, 16, O.seed_mix(seed, 6), real=real)
+    e_n = rel_err(bf_gpu.apply(x), bf_or.apply(x))
+    e_h = rel_err(bf_gpu.apply_adjoint(y), bf_or.apply_adjoint(y))
+    e_t = rel_err(bf_gpu.apply_transpose(y), bf_or.apply_transpose(y))
+    assert e_n <= tol and e_h <= tol and e_t <= tol, (e_n, e_h, e_t)
+    return e_n, e_h
+
+
+def _run_config(B, cfg_id, n, oracle_threads):
+    op_o, rt_o, ct_o, cfg = oracle_config(cfg_id, n)
+    bf_o, log_o = O.factorize(op_o, rt_o, ct_o, dict(cfg, threads=oracle_threads))
+    w = B.configs.build(cfg_id, n)
+    assert np.array_equal(w.row_tree.perm, rt_o.perm) and np.array_equal(w.col_tree.flat_ranges, ct_o.range_flat)
+    bf_g, log_g = B.factorize(w.op, w.row_tree, w.col_tree, w.recon)
+    errs = _compare(bf_g, log_g, bf_o, log_o, w.op.rows, w.op.cols)
+    # sampled error of the GPU factorization through the GPU black box
+    e_gpu = B.estimate_error(w.op, bf_g, 16, 3)
+    e_or = O.estimate_error(op_o, bf_o, 16, 3)
+    assert abs(e_gpu - e_or) <= 1e-3 * e_or + 1e-12
+    return errs, e_gpu
+
+
+def test_black_box_products_match_oracle(B, oracle_threads):
+    """K2: every kernel operator, N / T / H, dense and structured probes."""
+    for cfg_id, n in ((0, 1024), (1, 1024), (2, 1024), (3, 512)):
+        op_o, rt, ct, _ = oracle_config(cfg_id, n)
+        w = B.configs.build(cfg_id, n)
+        x = O.gaussian_matrix(n, 7, 11)
+        for name, fo, fg in (("N", op_o.apply, w.op.apply), ("T", op_o.apply_transpose, w.op.apply_transpose),
+                             ("H", op_o.apply_adjoint, w.op.apply_adjoint)):
+            e = rel_err(fg(x), fo(x))
+            assert e < 1e-12, (cfg_id, name, e)
+        # structured probe: only one node's rows nonzero
+        xs = np.zeros_like(x)
+        b, e_ = rt.node_range(2, 1)
+        xs[b:e_] = x[b:e_]
+        assert rel_err(w.op.apply_adjoint(xs), op_o.apply_adjoint(xs)) < 1e-12
+
+
+def test_gaussian_stream_matches_oracle(B):
+    for seed in (0, 1, 123456789):
+        for rows, cols in ((1, 1), (7, 3), (1000, 5)):
+            g = B.gaussian_matrix(rows, cols, seed)
+            o = O.gaussian_matrix(rows, cols, seed)
+            assert np.max(np.abs(g - o)) <= 4e-15 * max(1.0, np.max(np.abs(o)))
+            gr = B.gaussian_matrix(rows, cols, seed, scalar=B.REAL64)
+            orr = O.gaussian_matrix(rows, cols, seed, real=True)
+            assert np.max(np.abs(gr - orr)) <= 4e-15 * max(1.0, np.max(np.abs(orr)))
+
+
+def test_cpqr_matches_oracle(B):
+    rng = np.random.default_rng(0)
+    for rows, cols, rank in ((32, 18, 18), (64, 66, 20), (104, 106, 50), (30, 10, 3), (8, 20, 8)):
+        a = rng.standard_normal((rows, rank)) + 1j * rng.standard_normal((rows, rank))
+        b = rng.standard_normal((rank, cols)) + 1j * rng.standard_normal((rank, cols))
+        s = np.logspace(0, -12, rank)
+        z = (a * s) @ b
+        qo, ko, _, _ = O.pivoted_qr_truncate(z, 0.25e-6)
+        qg = B.pivoted_qr_truncate(z, 0.25e-6)
+        assert qg.shape[1] == ko
+        # same span, same phase convention (Eigen's beta = -sign(Re c0)||x||)
+        assert rel_err(qg, qo) < 1e-9
+    z0 = np.zeros((5, 3), complex)
+    assert B.pivoted_qr_truncate(z0, 1e-8).shape[1] == 0
+
+
+def test_pinv_matches_oracle(B):
+    rng = np.random.default_rng(1)
+    for rows, cols in ((4, 6), (15, 32), (32, 66), (6, 4), (5, 3)):
+        m = rng.standard_normal((rows, cols)) + 1j * rng.standard_normal((rows, cols))
+        assert rel_err(B.pinv_solve(m), O.pinv_solve(m)) < 1e-12
+    d = np.zeros((2, 2), complex)
+    d[0, 0] = 2.0
+    p = B.pinv_solve(d)
+    assert abs(p[0, 0] - 0.5) < 1e-14 and abs(p[1, 1]) < 1e-14
+
+
+@pytest.mark.parametrize("real,levels,rank,seed", [(True, 5, 8, 7), (False, 4, 4, 21), (False, 6, 2, 3)])
+def test_synthetic_exact_recovery(B, real, levels, rank, seed):
+    """test_reconstruct.cpp:109-157 on the GPU, checked against the oracle."""
+    scalar = B.REAL64 if real else B.COMPLEX128
+    bf_in_g = B.synth_butterfly(levels, rank, seed, scalar=scalar)
+    bf_in_o = O.synth_butterfly(levels, rank, seed, real=real)
+    n = (1 << levels) * 8
+    op_g = B.ButterflyOperator(bf_in_g)
+    op_o = O.butterfly_operator(bf_in_o)
+    rt_g = B.PartitionTree.build(np.arange(n, dtype=float), levels)
+    rt_o = O.PartitionTree.build(np.arange(n, dtype=float), levels)
+    cfg = dict(levels=levels, tolerance=1e-10, rank_guess=4, oversampling=2, seed=seed + 1000)
+    bf_g, log_g = B.factorize(op_g, rt_g, rt_g, B.ReconstructionConfig(**cfg))
+    bf_o, log_o = O.factorize(op_o, rt_o, rt_o, cfg)
+    _compare(bf_g, log_g, bf_o, log_o, n, n, real=real)
+    assert B.estimate_error(op_g, bf_g, 16, 1) <= 1e-10
+    assert (bf_g.rank_profile() == rank).all()
+    if rank == 8:
+        assert log_g.phase("leaf_v").rounds == 2
+        assert log_g.phase("leaf_v").transpose_columns == (4 + 2) + (8 + 2) + (16 + 2)
+    assert log_g.forward_columns() + log_g.transpose_columns() == op_g.total_columns()
+
+
+@pytest.mark.parametrize("cfg_id,n", [(0, 4096), (1, 1024), (2, 4096), (3, 1024), (4, 4096)])
+def test_config_parity(B, oracle_threads, cfg_id, n):
+    """Every BASELINE config (config 0 at its full size) against the oracle."""
+    (e_n, e_h), e = _run_config(B, cfg_id, n, oracle_threads)
+    print(f"config {cfg_id} n={n}: apply rel diff {e_n:.2e} / adjoint {e_h:.2e}; sampled error {e:.2e}")
+
+
+def test_zero_operator(B):
+    """test_reconstruct.cpp:159-169."""
+    op = B.DenseOperator(np.zeros((64, 64)))
+    t = B.PartitionTree.build(np.arange(64, dtype=float), 3)
+    bf, log = B.factorize(op, t, t, B.ReconstructionConfig(levels=3, tolerance=1e-8))
+    assert bf.max_rank() == 0
+    assert log.phase("leaf_v").rounds == 0
+    with pytest.raises(B.ConditioningError):
+        B.estimate_error(op, bf)
+
+
+def test_phase_sequencing(B):
+    """test_reconstruct.cpp:171-196."""
+    bf = B.synth_butterfly(4, 2, 3, scalar=B.REAL64)
+    op = B.ButterflyOperator(bf)
+    t = B.PartitionTree.build(np.arange(128, dtype=float), 4)
+    cfg = B.ReconstructionConfig(levels=4, tolerance=1e-10, seed=1003)
+    f = B.Factorizer(op, t, t, cfg)
+    with pytest.raises(B.SequencingError):
+        f.transfer_level_w(1)
+    f.leaf_row_bases()
+    with pytest.raises(B.SequencingError):
+        f.leaf_row_bases()
+    f.leaf_col_bases()
+    with pytest.raises(B.SequencingError):
+        f.transfer_level_r(3)
+    with pytest.raises(B.SequencingError):
+        f.transfer_level_w(2)
+    f.transfer_level_w(1)
+    f.transfer_level_w(2)
+    with pytest.raises(B.SequencingError):
+        f.transfer_level_r(2)
+    f.transfer_level_r(3)
+    f.transfer_level_r(2)
+    assert f.complete()
+    bf2, _ = f.take()
+    assert B.estimate_error(op, bf2, 16, 1) < 1e-10
+
+
+def test_determinism_and_container_roundtrip(B):
+    """test_reconstruct.cpp:198-209: byte-identical containers across runs."""
+    bf = B.synth_butterfly(4, 4, 11, scalar=B.REAL64)
+    op = B.ButterflyOperator(bf)
+    t = B.PartitionTree.build(np.arange(128, dtype=float), 4)
+    cfg = B.ReconstructionConfig(levels=4, tolerance=1e-10, seed=1011)
+    a, _ = B.factorize(op, t, t, cfg)
+    b, _ = B.factorize(op, t, t, cfg)
+    assert a.serialize() == b.serialize()
+    # container parses in the oracle (the reference format) and round-trips
+    o = O.HybridButterfly.deserialize(a.serialize())
+    assert o.serialize() == a.serialize()
+    c = B.HybridButterfly.deserialize(a.serialize(), scalar=B.REAL64)
+    assert c.serialize() == a.serialize()
+
+
+def test_literal_transpose_core_is_worse(B):
+    """test_reconstruct.cpp:211-221."""
+    bf = B.synth_butterfly(4, 4, 31, scalar=B.REAL64)
+    op = B.ButterflyOperator(bf)
+    t = B.PartitionTree.build(np.arange(128, dtype=float), 4)
+    good, _ = B.factorize(op, t, t, B.ReconstructionConfig(levels=4, tolerance=1e-10, seed=1031))
+    lit, _ = B.factorize(op, t, t, B.ReconstructionConfig(levels=4, tolerance=1e-10, seed=1031,
+                                                          literal_transpose_core=True))
+    e_good, e_lit = B.estimate_error(op, good, 16, 5), B.estimate_error(op, lit, 16, 5)
+    assert e_good <= 1e-10 and e_lit > e_good
+
+
+def test_batched_probes_match_unbatched(B):
+    """Probe batching is a scheduling knob: results are bit-identical."""
+    w = B.configs.build(2, 2048)
+    a, la = B.factorize(w.op, w.row_tree, w.col_tree, w.recon)
+    import dataclasses
+
+    rc = dataclasses.replace(w.recon, max_batch_probes=3)
+    b, lb = B.factorize(w.op, w.row_tree, w.col_tree, rc)
+    np.testing.assert_array_equal(a.rank_profile(), b.rank_profile())
+    x = O.gaussian_matrix(2048, 4, 9)
+    assert rel_err(a.apply(x), b.apply(x)) < 1e-13
+    assert lb.peak_concurrent_probes <= 3 < la.peak_concurrent_probes
+
+
+def test_dense_callback_operator(B):
+    """User black box through the C-ABI callback (stream-ordered)."""
+    import torch
+
+    rng = np.random.default_rng(3)
+    n = 256
+    a = rng.standard_normal((n, n)) + 1j * rng.standard_normal((n, n))
+    at = torch.tensor(a, dtype=torch.complex128, device="cuda")
+
+    def fn(trans, x, ldx, y, ldy, k, stream):
+        return _torch_apply(at, trans, x, ldx, y, ldy, k, stream)
+
+    op = B.CallbackOperator(n, n, fn)
+    x = O.gaussian_matrix(n, 3, 4)
+    assert rel_err(op.apply(x), a @ x) < 1e-13
+    assert rel_err(op.apply_transpose(x), a.T @ x) < 1e-13
+    assert rel_err(op.apply_adjoint(x), a.conj().T @ x) < 1e-13
+
+
+def _torch_apply(at, trans, x, ldx, y, ldy, k, stream):
+    import torch
+
+    n = at.shape[0]
+
+    class _CAI:
+        def __init__(self, ptr, shape, strides):
+            self.__cuda_array_interface__ = {"data": (ptr, False), "shape": shape, "typestr": "<c16",
+                                             "strides": strides, "version": 3}
+
+    # stream-ordered: run on the library's stream
+    with torch.cuda.stream(torch.cuda.ExternalStream(stream)):
+        X = torch.as_tensor(_CAI(x, (n, k), (16, 16 * ldx)), device="cuda")
+        Y = torch.as_tensor(_CAI(y, (n, k), (16, 16 * ldy)), device="cuda")
+        A = at if trans == 0 else at.t()
+        Y.copy_(A @ X)
+    return 0
