@@ -195,6 +195,10 @@ void bo_factorizer_free(bo_factorizer* f);
 
 int bo_factorize(const bo_op* op, const bo_tree* rt, const bo_tree* ct, const bo_cfg* cfg,
                  bo_bf** bf_out, bo_log* log);
+int bo_core_block(int64_t zr, int64_t w, const bo_cplx* z, int64_t ur, int64_t uc, const bo_cplx* u, int64_t cr,
+                  int64_t cc, const bo_cplx* coeff, int literal, bo_cplx* out);
+int bo_probe_with(const bo_op* op, const bo_tree* t, int level, int64_t node, const bo_cplx* core, int64_t core_rows,
+                  int64_t width, int forward, bo_cplx* out);
 int bo_estimate_error(const bo_op* op, const bo_bf* bf, int64_t k, uint64_t seed, double* err);
 
 #ifdef __cplusplus

@@ -313,6 +313,34 @@ static int core_block(const bo_mat* z, const bo_mat* u, const bo_mat* coeff, int
   return BO_OK;
 }
 
+/* exported for tests: core_block on plain arrays; out is (u_cols x coeff_rows) */
+int bo_core_block(int64_t zr, int64_t w, const bo_cplx* z, int64_t ur, int64_t uc, const bo_cplx* u, int64_t cr,
+                  int64_t cc, const bo_cplx* coeff, int literal, bo_cplx* out) {
+  bo_mat Z = {zr, w, (bo_cplx*)z}, U = {ur, uc, (bo_cplx*)u}, Cf = {cr, cc, (bo_cplx*)coeff}, B;
+  int e = core_block(&Z, &U, &Cf, literal, &B);
+  if (e != BO_OK) return e;
+  if (B.rows * B.cols > 0) memcpy(out, B.a, sizeof(bo_cplx) * (size_t)(B.rows * B.cols));
+  bo_mat_free(&B);
+  return BO_OK;
+}
+
+/* exported for tests: probe_with (reconstruct.hpp:72-85) */
+int bo_probe_with(const bo_op* op, const bo_tree* t, int level, int64_t node, const bo_cplx* core, int64_t core_rows,
+                  int64_t width, int forward, bo_cplx* out) {
+  if (core_rows != bo_node_e(t, level, node) - bo_node_b(t, level, node))
+    return bo_fail(BO_DIMENSION, "probe_with: core height does not match the owner node");
+  if (t->n != (forward ? bo_op_cols(op) : bo_op_rows(op)))
+    return bo_fail(BO_DIMENSION, "probe_with: tree size does not match the operator");
+  bo_factorizer tmp;
+  memset(&tmp, 0, sizeof tmp);
+  tmp.op = op;
+  bo_cplx* y = probe_with(&tmp, t, level, node, core, width, forward);
+  int64_t rows = forward ? bo_op_rows(op) : bo_op_cols(op);
+  memcpy(out, y, sizeof(bo_cplx) * (size_t)(rows * width));
+  free(y);
+  return BO_OK;
+}
+
 /* transfer_level_r (reconstruct.hpp:245-305) */
 int bo_factorizer_transfer_r(bo_factorizer* f, int l) {
   bo_bf* bf = f->bf;

@@ -87,6 +87,8 @@ def lib():
             "bo_factorizer_take": (p, [p, p]),
             "bo_factorizer_free": (None, [p]),
             "bo_estimate_error": (i32, [p, p, i64, u64, p]),
+            "bo_core_block": (i32, [i64, i64, p, i64, i64, p, i64, i64, p, i32, p]),
+            "bo_probe_with": (i32, [p, p, i32, i64, p, i64, i64, i32, p]),
         }
         for name, (res, args) in sig.items():
             fn = getattr(L, name)
@@ -448,3 +450,21 @@ def estimate_error(op: Operator, bf: HybridButterfly, k=16, seed=0):
     e = C.c_double(0)
     _check(lib().bo_estimate_error(op.h, bf.h, k, C.c_uint64(seed), C.byref(e)))
     return e.value
+
+
+def core_block(k_omega, u, v_coeff, literal=False):
+    """core_block (reconstruct.hpp:125-138)."""
+    z, u, cf = _cmat(k_omega), _cmat(u), _cmat(v_coeff)
+    out = np.zeros((u.shape[1], cf.shape[0]), np.complex128, order="F") if u.shape[1] * cf.shape[0] else np.zeros(1, np.complex128)
+    _check(lib().bo_core_block(z.shape[0], z.shape[1], _ptr(z), u.shape[0], u.shape[1], _ptr(u), cf.shape[0],
+                               cf.shape[1], _ptr(cf), int(literal), _ptr(out)))
+    return out.reshape(u.shape[1], cf.shape[0], order="F")
+
+
+def probe_with(op: Operator, tree: PartitionTree, level, node, core, forward=True):
+    """probe_with (reconstruct.hpp:72-85)."""
+    c = _cmat(core)
+    rows = op.rows if forward else op.cols
+    out = np.zeros((rows, c.shape[1]), np.complex128, order="F")
+    _check(lib().bo_probe_with(op.h, tree.h, level, node, _ptr(c), c.shape[0], c.shape[1], int(forward), _ptr(out)))
+    return out

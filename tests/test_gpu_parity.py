@@ -129,13 +129,13 @@ def test_synthetic_exact_recovery(B, real, levels, rank, seed):
     cfg = dict(levels=levels, tolerance=1e-10, rank_guess=4, oversampling=2, seed=seed + 1000)
     bf_g, log_g = B.factorize(op_g, rt_g, rt_g, B.ReconstructionConfig(**cfg))
     bf_o, log_o = O.factorize(op_o, rt_o, rt_o, cfg)
+    assert log_g.forward_columns() + log_g.transpose_columns() == op_g.total_columns()
     _compare(bf_g, log_g, bf_o, log_o, n, n, real=real)
     assert B.estimate_error(op_g, bf_g, 16, 1) <= 1e-10
     assert (bf_g.rank_profile() == rank).all()
     if rank == 8:
         assert log_g.phase("leaf_v").rounds == 2
         assert log_g.phase("leaf_v").transpose_columns == (4 + 2) + (8 + 2) + (16 + 2)
-    assert log_g.forward_columns() + log_g.transpose_columns() == op_g.total_columns()
 
 
 @pytest.mark.parametrize("cfg_id,n", [(0, 4096), (1, 1024), (2, 4096), (3, 1024), (4, 4096)])
