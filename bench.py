@@ -1,0 +1,307 @@
+#!/usr/bin/env python
+"""Benchmark: adaptive butterfly construction on BASELINE config 2.
+
+Workload (BASELINE.json metric "butterfly construction sec & GFLOP/s at
+n=65536 complex128; apply GB/s"): the weak-admissibility 2D Helmholtz
+operator exp(ikr)/r between two half circles, n = 65536 points each,
+complex128, tol 1e-6, leaf 32 (L = 11), r0 = 4, evaluated on the fly.
+A step = one full factorize() (both adaptive leaf phases, 5 W levels,
+6 R levels + core fit).  GFLOP/s = algorithmic flops (DESIGN.md 8d:
+black-box contraction + chain projections + QR + core fit; kernel-entry
+evaluations are not counted as flops) / construction time.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl reference]
+
+N > 1 runs under torchrun: one process per GPU, each rank factorizes its own
+replica (weak scaling; the probe-sharded single construction is a library
+feature exercised by tests/test_multirank.py).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "butterfly construction GFLOP/s at n=65536 complex128 (config 2)"
+FP64_PEAK_TFLOPS = 36.99  # measured DMMA m8n8k4 f64 on this pool (profiles/r01_fp64_peaks.txt)
+CFG_ID = 2
+
+
+def _env_rank():
+    return int(os.environ.get("RANK", 0)), int(os.environ.get("WORLD_SIZE", 1)), int(os.environ.get("LOCAL_RANK", 0))
+
+
+# ------------------------------------------------------------ CPU baseline
+def cpu_sample(n=65536, probes=8, width=32, threads=None):
+    """Bounded sample of the same workload on the CPU oracle: the adjoint
+    black-box products of `probes` level-5 row probes (|T_tau| = n/32 rows,
+    `width` columns) over all n output points -- the operation that carries
+    >90% of the construction's flops -- through the oracle's operator."""
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    import numpy as np
+
+    import oracle as O
+
+    sys.path.insert(0, os.path.join(ROOT, "tests"))
+    from helpers import oracle_config
+
+    threads = threads or os.cpu_count() or 1
+    O.set_threads(threads)
+    op, rt, ct, cfg = oracle_config(CFG_ID, n)
+    level = 5
+    t0 = time.perf_counter()
+    flops = 0.0
+    for tau in range(probes):
+        b, e = rt.node_range(level, tau)
+        core = O.gaussian_matrix(e - b, width, O.seed_mix(0, 3, level, tau))
+        O.probe_with(op, rt, level, tau, core, forward=False)
+        flops += 8.0 * n * (e - b) * width
+    dt = time.perf_counter() - t0
+    return flops / dt / 1e9, dt, threads, (
+        f"adjoint black-box products of {probes} W-level-{level} row probes of config 2 "
+        f"(n={n}, {n // 32} rows x {width} cols each) through the oracle operator, {threads} threads")
+
+
+def run_reference(args):
+    rank, world, _ = _env_rank()
+    if rank != 0:
+        return 0
+    vals = []
+    for i in range(args.warmup + args.steps):
+        v, dt, threads, sample = cpu_sample(probes=args.ref_probes)
+        if i >= args.warmup:
+            vals.append((v, dt))
+    value = statistics.median(v for v, _ in vals)
+    ms = statistics.mean(dt for _, dt in vals) * 1e3
+    line = {
+        "impl": "reference", "metric": METRIC, "value": round(value, 3), "unit": "GFLOP/s", "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms, 3), "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "complex128", "data": "synthetic",
+        "config": {"workload": "config2_helmholtz_circle_n65536", "n": 65536, "sample": sample},
+        "cpu_baseline": {"value": round(value, 3), "unit": "GFLOP/s", "cores": threads, "kind": "port",
+                         "sample": sample},
+        "e2e": {"value": round(value, 3), "unit": "GFLOP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# -------------------------------------------------------------- clocks
+class ClockSampler:
+    def __init__(self, index):
+        self.f = tempfile.NamedTemporaryFile("w+", suffix=".csv", delete=False)
+        q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+             "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+        try:
+            self.p = subprocess.Popen(["nvidia-smi", f"--id={index}", f"--query-gpu={q}", "--format=csv,noheader,nounits",
+                                       "-lms", "200"], stdout=self.f, stderr=subprocess.DEVNULL)
+        except Exception:
+            self.p = None
+
+    def stop(self):
+        if self.p is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.p.terminate()
+        self.p.wait()
+        self.f.flush()
+        self.f.seek(0)
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in self.f.read().splitlines():
+            parts = [x.strip() for x in line.split(",")]
+            if len(parts) < 9:
+                continue
+            try:
+                sm.append(float(parts[1]))
+                mx = float(parts[2])
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[5:9]):
+                if v.lower() == "active":
+                    reasons.add(nm)
+        os.unlink(self.f.name)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+# ------------------------------------------------------------------ ours
+def run_ours(args):
+    import numpy as np
+    import torch
+
+    import paper_2002_03400_b200 as B
+
+    rank, world, local = _env_rank()
+    torch.cuda.set_device(local)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+
+    def barrier():
+        if dist is not None:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    ctx = B.Context(local)
+    stream = torch.cuda.ExternalStream(ctx.stream)
+    w = B.configs.build(CFG_ID, args.n or None, ctx=ctx)
+    op, rt, ct, rc = w.op, w.row_tree, w.col_tree, w.recon
+    flush = torch.empty(64 * 1024 * 1024, dtype=torch.float32, device="cuda")  # 256 MB > L2
+
+    def l2_flush():
+        flush.zero_()
+        torch.cuda.synchronize()
+
+    for _ in range(args.warmup):
+        bf, log = B.factorize(op, rt, ct, rc)
+    # ----------------------------------------------------------- timed
+    barrier()
+    clocks = ClockSampler(local)
+    ctx.profile(-1)
+    ctx.profile(1)
+    launches0 = ctx.launches
+    total_ms, flops, logs = 0.0, 0.0, []
+    for _ in range(args.steps):
+        l2_flush()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        bf, log = B.factorize(op, rt, ct, rc)
+        e1.record(stream)
+        e1.synchronize()
+        total_ms += e0.elapsed_time(e1)
+        flops += log.flops
+        logs.append(log)
+    launches = ctx.launches - launches0
+    kernels = ctx.profile_report()
+    ctx.profile(0)
+    barrier()
+    clk = clocks.stop()
+    t = torch.tensor([total_ms], dtype=torch.float64, device="cuda")
+    fl = torch.tensor([flops], dtype=torch.float64, device="cuda")
+    if dist is not None:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        dist.all_reduce(fl, op=dist.ReduceOp.SUM)
+    max_ms = t.item()
+    value = fl.item() / (max_ms / 1e3) / 1e9
+    ms_per_step = max_ms / args.steps
+
+    # ----------------------------------------------- apply bandwidth (device)
+    apply = {}
+    for k in (1, 16):
+        x = torch.randn((k, op.cols), dtype=torch.complex128, device="cuda").t()
+        y = torch.empty((k, op.rows), dtype=torch.complex128, device="cuda").t()
+        for _ in range(3):
+            B.api.check(B.api.lib().bfly_apply(bf.h, 0, B.api.C.c_void_p(x.data_ptr()), op.cols,
+                                               B.api.C.c_void_p(y.data_ptr()), op.rows, k, 1))
+        ts = []
+        for _ in range(10):
+            l2_flush()
+            a0, a1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a0.record(stream)
+            B.api.check(B.api.lib().bfly_apply(bf.h, 0, B.api.C.c_void_p(x.data_ptr()), op.cols,
+                                               B.api.C.c_void_p(y.data_ptr()), op.rows, k, 1))
+            a1.record(stream)
+            a1.synchronize()
+            ts.append(a0.elapsed_time(a1))
+        ms = statistics.median(ts)
+        nbytes = 16.0 * (bf.nnz() + (op.rows + op.cols) * k)
+        apply[f"k{k}"] = {"ms": round(ms, 4), "GB/s": round(nbytes / (ms / 1e3) / 1e9, 1),
+                          "frac_of_hbm": round(nbytes / (ms / 1e3) / 1e9 / 6554.9, 3)}
+
+    # --------------------------------------------------- e2e (host buffers)
+    import ctypes as C
+
+    pts_t = torch.from_numpy(np.ascontiguousarray(op.targets)).pin_memory()
+    pts_s = torch.from_numpy(np.ascontiguousarray(op.sources)).pin_memory()
+    kappa = op.wavenumber
+    e2e_steps = max(1, min(args.steps, 3))
+    h2d = (pts_t.numel() + pts_s.numel()) * 8
+    d2h = 0
+    barrier()
+    te0 = time.perf_counter()
+    for _ in range(e2e_steps):
+        h = C.c_void_p()
+        B.api.check(B.api.lib().bfly_op_kernel(ctx.h, B.api.OP_CIRCLE, op.rows, op.cols,
+                                               C.c_void_p(pts_t.data_ptr()), C.c_void_p(pts_s.data_ptr()), kappa,
+                                               B.api.COMPLEX128, C.byref(h)))
+        op_e = B.api.BlackBoxOperator(h, ctx, B.api.COMPLEX128)
+        bf_e, log_e = B.factorize(op_e, rt, ct, rc)
+        blob = bf_e.serialize()  # every factor block back on the host
+        d2h = len(blob)
+    barrier()
+    te = (time.perf_counter() - te0) / e2e_steps
+    e2e_val = logs[0].flops / te / 1e9
+
+    # ------------------------------------------------------------ roofline
+    mv = kernels.get("kernel_matvec", {"launches": 1, "ms": 1, "flops": 0, "bytes": 0})
+    achieved = mv["flops"] / (mv["ms"] / 1e3) / 1e12 if mv["ms"] > 0 else 0.0
+    roofline = {
+        "bound": "tensor", "kernel": "kernel_matvec (K2, FP64 complex contraction + on-the-fly kernel evaluation)",
+        "achieved": round(achieved, 3), "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s",
+        "frac": round(achieved / FP64_PEAK_TFLOPS, 4), "traffic": None,
+        "peak_source": "measured FP64 DMMA peak (tools/microbench/fp64_peaks.cu, profiles/r01_fp64_peaks.txt); "
+                       "MEASURED_PEAKS.json has no FP64 entry",
+        "flops_per_launch": mv["flops"] / max(1, mv["launches"]), "avg_launch_ms": mv["ms"] / max(1, mv["launches"]),
+        "share_of_step": round(mv["ms"] / total_ms, 4) if total_ms else None,
+    }
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": round(value, 3), "unit": "GFLOP/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": round(ms_per_step, 3), "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "complex128", "data": "synthetic",
+            "config": {"workload": "config2_helmholtz_circle_n65536", "n": w.n, "levels": rc.levels, "leaf": 32,
+                       "tol": rc.tolerance, "r0": rc.rank_guess, "oversampling": rc.oversampling,
+                       "parallelism": f"replicas{world}" if world > 1 else "single",
+                       "l2": "flushed before every step (256 MB write); probe products 0.1-1 GB > L2"},
+            "construct_seconds": round(ms_per_step / 1e3, 4),
+            "flops_per_step": logs[0].flops, "kernel_evals_per_step": logs[0].kernel_evals,
+            "max_rank": bf.max_rank(), "nnz": bf.nnz(),
+            "roofline": roofline,
+            "apply": apply,
+            "kernels": {k: {"launches": v["launches"], "ms_per_step": round(v["ms"] / args.steps, 3)}
+                        for k, v in kernels.items()},
+            "e2e": {"value": round(e2e_val, 3), "unit": "GFLOP/s", "h2d_bytes_per_step": int(h2d),
+                    "d2h_bytes_per_step": int(d2h), "seconds_per_step": round(te, 4)},
+            "gpu_launches": int(launches),
+            "clocks": clk,
+        }
+        if world == 1 and not args.no_cpu:
+            v, dt, threads, sample = cpu_sample(probes=args.ref_probes)
+            line["cpu_baseline"] = {"value": round(v, 3), "unit": "GFLOP/s", "cores": threads, "kind": "port",
+                                    "sample": sample, "seconds": round(dt, 2)}
+        print(json.dumps(line), flush=True)
+    if dist is not None:
+        dist.barrier()
+        dist.destroy_process_group()
+    return 0
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--n", type=int, default=0, help="override n (testing only)")
+    ap.add_argument("--ref-probes", type=int, default=8)
+    ap.add_argument("--no-cpu", action="store_true")
+    args = ap.parse_args()
+    if args.impl == "reference":
+        return run_reference(args)
+    return run_ours(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

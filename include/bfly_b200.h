@@ -60,6 +60,11 @@ int64_t bfly_ctx_launches(const bfly_ctx* ctx);
 int bfly_ctx_synchronize(bfly_ctx* ctx);
 /* raw stream handle (cudaStream_t) the library launches on */
 void* bfly_ctx_stream(bfly_ctx* ctx);
+/* per-kernel device timing with CUDA events on the library stream:
+ * enable = 1 on, 0 off, -1 off and clear.  The report is a JSON object
+ * {kernel: {launches, ms, flops, bytes}}; returns the length needed. */
+int bfly_ctx_profile(bfly_ctx* ctx, int enable);
+int64_t bfly_ctx_profile_report(bfly_ctx* ctx, char* buf, int64_t len);
 /* Multi-GPU: join an NCCL communicator (ncclUniqueId bytes from rank 0).
  * Probes and butterfly blocks are sharded across ranks; each level's new
  * blocks are all-gathered. */

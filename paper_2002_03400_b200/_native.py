@@ -92,6 +92,8 @@ def lib():
         "bfly_ctx_launches": (i64, [p]),
         "bfly_ctx_synchronize": (i32, [p]),
         "bfly_ctx_stream": (p, [p]),
+        "bfly_ctx_profile": (i32, [p, i32]),
+        "bfly_ctx_profile_report": (i64, [p, C.c_char_p, i64]),
         "bfly_comm_unique_id": (i32, [p]),
         "bfly_ctx_set_comm": (i32, [p, i32, i32, p]),
         "bfly_tree_build": (i32, [i32, i64, p, i32, pp]),

@@ -58,6 +58,18 @@ class Context:
     def synchronize(self):
         check(lib().bfly_ctx_synchronize(self.h))
 
+    def profile(self, enable: int = 1):
+        """Per-kernel CUDA-event timing on the library stream (1 on, 0 off, -1 off+clear)."""
+        check(lib().bfly_ctx_profile(self.h, enable))
+
+    def profile_report(self) -> dict:
+        import json
+
+        n = lib().bfly_ctx_profile_report(self.h, None, 0)
+        buf = C.create_string_buffer(int(n))
+        lib().bfly_ctx_profile_report(self.h, buf, n)
+        return json.loads(buf.value.decode())
+
     def set_comm(self, rank: int, world: int, unique_id: bytes):
         buf = (C.c_uint8 * 128).from_buffer_copy(unique_id.ljust(128, b"\0")[:128])
         check(lib().bfly_ctx_set_comm(self.h, rank, world, buf))

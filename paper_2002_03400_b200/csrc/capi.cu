@@ -239,6 +239,39 @@ int bfly_ctx_synchronize(bfly_ctx* ctx) {
 }
 void* bfly_ctx_stream(bfly_ctx* ctx) { return ctx ? (void*)ctx->c->stream : nullptr; }
 
+int bfly_ctx_profile(bfly_ctx* ctx, int enable) {
+  return guard(C_(ctx), [&] {
+    Ctx* c = C_(ctx);
+    c->resolve_records();
+    if (enable < 0) c->stats.clear();
+    c->profiling = enable > 0;
+  });
+}
+
+int64_t bfly_ctx_profile_report(bfly_ctx* ctx, char* buf, int64_t len) {
+  std::string js = "{";
+  int rc = guard(C_(ctx), [&] {
+    Ctx* c = C_(ctx);
+    c->resolve_records();
+    bool first = true;
+    for (auto& kv : c->stats) {
+      char tmp[256];
+      std::snprintf(tmp, sizeof tmp, "%s\"%s\": {\"launches\": %lld, \"ms\": %.6f, \"flops\": %.6e, \"bytes\": %.6e}",
+                    first ? "" : ", ", kv.first.c_str(), (long long)kv.second.launches, kv.second.ms, kv.second.flops,
+                    kv.second.bytes);
+      js += tmp;
+      first = false;
+    }
+  });
+  js += "}";
+  if (rc != BFLY_OK) return -1;
+  if (buf && len > 0) {
+    std::strncpy(buf, js.c_str(), (size_t)len - 1);
+    buf[len - 1] = 0;
+  }
+  return (int64_t)js.size() + 1;
+}
+
 int bfly_comm_unique_id(uint8_t* id_out) {
   return guard(nullptr, [&] { comm_unique_id(id_out); });
 }

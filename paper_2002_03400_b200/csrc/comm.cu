@@ -1,5 +1,10 @@
 // comm.cu -- NCCL communicator management and the few collectives the
 // sharded construction needs.
+//
+// libnccl is bound lazily with dlopen on first use, so the library never
+// forces a particular libnccl.so.2 into a process: when PyTorch has already
+// loaded its bundled NCCL, dlopen returns that same object (same soname).
+#include <dlfcn.h>
 #include <nccl.h>
 
 #include <cstring>
@@ -8,15 +13,47 @@
 
 namespace bfly {
 
-#define BFLY_NCCL(call)                                                                                 \
-  do {                                                                                                  \
-    ncclResult_t r_ = (call);                                                                           \
-    if (r_ != ncclSuccess) fail(NCCL_ERR, std::string(#call) + ": " + ncclGetErrorString(r_));          \
-  } while (0)
+namespace {
+
+struct NcclApi {
+  ncclResult_t (*GetUniqueId)(ncclUniqueId*) = nullptr;
+  ncclResult_t (*CommInitRank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
+  ncclResult_t (*CommDestroy)(ncclComm_t) = nullptr;
+  ncclResult_t (*AllGather)(const void*, void*, size_t, ncclDataType_t, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*AllReduce)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t, cudaStream_t) = nullptr;
+  const char* (*GetErrorString)(ncclResult_t) = nullptr;
+};
+
+const NcclApi& nccl() {
+  static NcclApi api;
+  static bool loaded = false;
+  if (loaded) return api;
+  void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+  if (!h) fail(NCCL_ERR, std::string("cannot load libnccl.so.2: ") + dlerror());
+  auto sym = [&](const char* name) {
+    void* p = dlsym(h, name);
+    if (!p) fail(NCCL_ERR, std::string("libnccl.so.2 lacks ") + name);
+    return p;
+  };
+  api.GetUniqueId = reinterpret_cast<decltype(api.GetUniqueId)>(sym("ncclGetUniqueId"));
+  api.CommInitRank = reinterpret_cast<decltype(api.CommInitRank)>(sym("ncclCommInitRank"));
+  api.CommDestroy = reinterpret_cast<decltype(api.CommDestroy)>(sym("ncclCommDestroy"));
+  api.AllGather = reinterpret_cast<decltype(api.AllGather)>(sym("ncclAllGather"));
+  api.AllReduce = reinterpret_cast<decltype(api.AllReduce)>(sym("ncclAllReduce"));
+  api.GetErrorString = reinterpret_cast<decltype(api.GetErrorString)>(sym("ncclGetErrorString"));
+  loaded = true;
+  return api;
+}
+
+void nccl_check(ncclResult_t r, const char* what) {
+  if (r != ncclSuccess) fail(NCCL_ERR, std::string(what) + ": " + nccl().GetErrorString(r));
+}
+
+}  // namespace
 
 void comm_unique_id(uint8_t* id_out) {
   ncclUniqueId id;
-  BFLY_NCCL(ncclGetUniqueId(&id));
+  nccl_check(nccl().GetUniqueId(&id), "ncclGetUniqueId");
   std::memcpy(id_out, &id, sizeof id);
 }
 
@@ -29,13 +66,13 @@ void comm_init(Ctx* c, int rank, int world, const uint8_t* id_bytes) {
   ncclUniqueId id;
   std::memcpy(&id, id_bytes, sizeof id);
   ncclComm_t comm;
-  BFLY_NCCL(ncclCommInitRank(&comm, world, id, rank));
+  nccl_check(nccl().CommInitRank(&comm, world, id, rank), "ncclCommInitRank");
   c->comm = comm;
 }
 
 void comm_destroy(Ctx* c) {
   if (c && c->comm) {
-    ncclCommDestroy(c->comm);
+    nccl().CommDestroy(c->comm);
     c->comm = nullptr;
   }
   if (c) {
@@ -46,17 +83,17 @@ void comm_destroy(Ctx* c) {
 
 void comm_allgather_bytes(Ctx* c, const void* send, void* recv, size_t bytes) {
   if (c->world == 1 || !c->comm) return;
-  BFLY_NCCL(ncclAllGather(send, recv, bytes, ncclUint8, c->comm, c->stream));
+  nccl_check(nccl().AllGather(send, recv, bytes, ncclUint8, c->comm, c->stream), "ncclAllGather");
 }
 
 void comm_allreduce_max_i32(Ctx* c, int32_t* buf, size_t count) {
   if (c->world == 1 || !c->comm) return;
-  BFLY_NCCL(ncclAllReduce(buf, buf, count, ncclInt32, ncclMax, c->comm, c->stream));
+  nccl_check(nccl().AllReduce(buf, buf, count, ncclInt32, ncclMax, c->comm, c->stream), "ncclAllReduce");
 }
 
 void comm_allreduce_sum_f64(Ctx* c, double* buf, size_t count) {
   if (c->world == 1 || !c->comm) return;
-  BFLY_NCCL(ncclAllReduce(buf, buf, count, ncclFloat64, ncclSum, c->comm, c->stream));
+  nccl_check(nccl().AllReduce(buf, buf, count, ncclFloat64, ncclSum, c->comm, c->stream), "ncclAllReduce");
 }
 
 void comm_barrier(Ctx* c) {

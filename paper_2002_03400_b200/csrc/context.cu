@@ -43,4 +43,27 @@ void Ctx::release(void* p) { cudaFreeAsync(p, stream); }
 
 void Ctx::sync() { BFLY_CUDA(cudaStreamSynchronize(stream)); }
 
+void Ctx::resolve_records() {
+  if (records.empty()) return;
+  BFLY_CUDA(cudaStreamSynchronize(stream));
+  for (auto& r : records) {
+    float ms = 0;
+    cudaEventElapsedTime(&ms, r.start, r.stop);
+    cudaEventDestroy(r.start);
+    cudaEventDestroy(r.stop);
+    KStat* s = nullptr;
+    for (auto& kv : stats)
+      if (kv.first == r.name) s = &kv.second;
+    if (!s) {
+      stats.emplace_back(r.name, KStat{});
+      s = &stats.back().second;
+    }
+    s->launches += 1;
+    s->ms += ms;
+    s->flops += r.flops;
+    s->bytes += r.bytes;
+  }
+  records.clear();
+}
+
 }  // namespace bfly

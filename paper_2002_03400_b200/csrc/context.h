@@ -15,12 +15,28 @@ struct ncclComm;
 
 namespace bfly {
 
+// Per-kernel device timing (CUDA events on the library stream) for the
+// roofline numbers; off unless requested, resolved lazily.
+struct KRecord {
+  const char* name;
+  cudaEvent_t start, stop;
+  double flops, bytes;
+};
+struct KStat {
+  int64_t launches = 0;
+  double ms = 0, flops = 0, bytes = 0;
+};
+
 struct Ctx {
   int device = 0;
   cudaStream_t stream = nullptr;
   cudaMemPool_t pool = nullptr;
   int64_t launches = 0;
   int sm_count = 148;
+  bool profiling = false;
+  std::vector<KRecord> records;
+  std::vector<std::pair<std::string, KStat>> stats;
+  void resolve_records();  // fold finished records into stats
   // multi-GPU (rank-sharded probes + NCCL all-gather of each level)
   int rank = 0, world = 1;
   ncclComm* comm = nullptr;
@@ -36,6 +52,27 @@ struct Ctx {
 // entry points; the library is used from one host thread per context).
 Ctx* current_ctx();
 void set_current_ctx(Ctx* c);
+
+// RAII: brackets one kernel launch with events when profiling is on.
+struct KTimer {
+  Ctx* c;
+  KRecord rec{};
+  bool on;
+  KTimer(Ctx* ctx, const char* name, double flops, double bytes) : c(ctx), on(ctx && ctx->profiling) {
+    if (!on) return;
+    rec.name = name;
+    rec.flops = flops;
+    rec.bytes = bytes;
+    cudaEventCreate(&rec.start);
+    cudaEventCreate(&rec.stop);
+    cudaEventRecord(rec.start, c->stream);
+  }
+  ~KTimer() {
+    if (!on) return;
+    cudaEventRecord(rec.stop, c->stream);
+    c->records.push_back(rec);
+  }
+};
 
 struct CtxScope {
   Ctx* prev;

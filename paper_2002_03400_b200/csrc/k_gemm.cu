@@ -106,6 +106,9 @@ void launch_bgemm(Ctx* c, int op, int M, int K, int S, const cx<R>* A, int64_t l
   // K == 0: the product is an exact zero block
   dim3 grid(nent, (unsigned)ceil_div(max_ncols, TN), (unsigned)ceil_div(M, TM));
   if (grid.y > 65535 || grid.z > 65535) fail(PRECONDITION, "bgemm: grid too large");
+  const double nc = ncols_all > 0 ? ncols_all : max_ncols;
+  KTimer timer(c, "bgemm", 8.0 * M * K * S * (double)nent * nc,
+               sizeof(cx<R>) * ((double)nent * S * (M * (double)K + K * nc) + (double)nent * M * nc));
 #define BG(OPV, SV) bgemm_kernel<R, OPV, SV><<<grid, 256, 0, c->stream>>>(A, lda, B, ldb, C, ldc, M, K, ents, accumulate, ncols_all)
   if (S == 1) {
     if (op == OP_N) BG(OP_N, 1);

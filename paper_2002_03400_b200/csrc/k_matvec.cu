@@ -223,6 +223,12 @@ void run_cfg(Ctx* c, Points outp, Points inp, double kappa, int64_t m_out, const
 
   DBuf<MatvecItem> ditems(c, items.size());
   ditems.upload(items.data(), items.size());
+  double kflops = 0, kbytes = 0;
+  for (const auto& it : items) {
+    kflops += 8.0 * (double)m_out * (double)it.rows * (double)it.ncols;
+    kbytes += (double)sizeof(cx<R>) * ((double)it.rows + (double)m_out) * (double)it.ncols;
+  }
+  KTimer timer(c, "kernel_matvec", kflops, kbytes);
   size_t smem = sizeof(cx<R>) * (size_t)BK * (BM + BN);
   auto kern = matvec_kernel<R, KIND, MODE, BM, BN, TM, TN, BK>;
   BFLY_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));

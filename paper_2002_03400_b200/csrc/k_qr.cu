@@ -12,6 +12,7 @@
 // K6 is core_block + pinv_solve (reconstruct.hpp:125-138, linalg.hpp:128-139):
 // B = (Q^H z) pinv(coeff), pinv through a one-sided Jacobi SVD of coeff^H
 // (parallel round-robin pair ordering), singular values <= 1e-12 smax dropped.
+#include <algorithm>
 #include <cfloat>
 
 #include "kernels.cuh"
@@ -45,14 +46,16 @@ template <typename R>
 __global__ void __launch_bounds__(QR_THREADS) cpqr_kernel(const cx<R>* __restrict__ src, int64_t ld_src,
                                                           cx<R>* __restrict__ dst, int64_t ld_dst, int cap,
                                                           const QrEnt* __restrict__ ents, int32_t* ranks, double eps_t,
-                                                          int zld) {
+                                                          int zld, cx<R>* zglobal, int64_t zstride) {
   using V = cx<R>;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const QrEnt e = ents[blockIdx.x];
   const int r = e.r1 + e.r2, w = e.cols;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  V* Z = reinterpret_cast<V*>(smem_raw);  // zld x w
-  R* nu = reinterpret_cast<R*>(Z + (size_t)zld * w);
+  // the block lives in shared memory, or (oversized blocks) in a global
+  // scratch slice with the same code path
+  V* Z = zglobal ? zglobal + blockIdx.x * zstride : reinterpret_cast<V*>(smem_raw);  // zld x w
+  R* nu = zglobal ? reinterpret_cast<R*>(smem_raw) : reinterpret_cast<R*>(Z + (size_t)zld * w);
   R* nd = nu + w;
   V* tau = reinterpret_cast<V*>(nd + w);
   __shared__ int s_big;
@@ -392,14 +395,27 @@ void launch_cpqr(Ctx* c, const cx<R>* src, int64_t ld_src, cx<R>* dst, int64_t l
                  int nent, int max_rows, int max_cols, int32_t* ranks, double eps) {
   if (nent <= 0) return;
   int zld = max_rows > 0 ? max_rows : 1;
-  size_t smem = sizeof(cx<R>) * (size_t)zld * max_cols + 2 * sizeof(R) * max_cols + sizeof(cx<R>) * max_cols + 64;
-  if (smem > 227 * 1024)
-    fail(PRECONDITION, "cpqr: block " + std::to_string(max_rows) + "x" + std::to_string(max_cols) +
-                           " exceeds shared memory (ranks above the supported maximum)");
+  const size_t aux = 2 * sizeof(R) * max_cols + sizeof(cx<R>) * max_cols + 64;
+  size_t smem = sizeof(cx<R>) * (size_t)zld * max_cols + aux;
   auto kern = cpqr_kernel<R>;
-  BFLY_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-  kern<<<nent, QR_THREADS, smem, c->stream>>>(src, ld_src, dst, ld_dst, cap, ents, ranks, eps, zld);
-  BFLY_LAUNCH_CHECK("cpqr");
+  KTimer timer(c, "cpqr", 0.0, (double)sizeof(cx<R>) * nent * ((double)max_rows * max_cols + (double)ld_dst * cap));
+  if (smem <= 200 * 1024) {
+    BFLY_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    kern<<<nent, QR_THREADS, smem, c->stream>>>(src, ld_src, dst, ld_dst, cap, ents, ranks, eps, zld, nullptr, 0);
+    BFLY_LAUNCH_CHECK("cpqr");
+    return;
+  }
+  // oversized blocks (saturating ranks): blocks in global scratch, bounded chunks
+  if (aux > 200 * 1024) fail(PRECONDITION, "cpqr: probe width " + std::to_string(max_cols) + " too large");
+  BFLY_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)aux));
+  const int64_t zstride = (int64_t)zld * max_cols;
+  const int64_t chunk = std::max<int64_t>(1, std::min<int64_t>(nent, ((int64_t)1 << 31) / (zstride * sizeof(cx<R>))));
+  DBuf<cx<R>> zbuf(c, (size_t)(chunk * zstride));
+  for (int64_t e0 = 0; e0 < nent; e0 += chunk) {
+    int n = (int)std::min<int64_t>(chunk, nent - e0);
+    kern<<<n, QR_THREADS, aux, c->stream>>>(src, ld_src, dst, ld_dst, cap, ents + e0, ranks, eps, zld, zbuf.p, zstride);
+    BFLY_LAUNCH_CHECK("cpqr");
+  }
 }
 
 template <typename R>
@@ -410,6 +426,7 @@ void launch_core_fit(Ctx* c, const cx<R>* Q, int64_t ldq, const cx<R>* Z, int64_
   int kvp = max_kv + 1;
   int64_t stride = (int64_t)max_ku * max_w + (int64_t)max_w * kvp + (int64_t)kvp * kvp + (int64_t)max_ku * kvp + kvp + 8;
   DBuf<cx<R>> scratch(c, (size_t)stride * nent);
+  KTimer timer(c, "core_fit", 0.0, 0.0);
   core_fit_kernel<R><<<nent, QR_THREADS, 0, c->stream>>>(Q, ldq, Z, ldz, Cf, ldc, B, ldb, bcap, ents, scratch.p, stride,
                                                           literal, err_flag);
   BFLY_LAUNCH_CHECK("core_fit");

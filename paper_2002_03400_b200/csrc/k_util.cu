@@ -106,6 +106,7 @@ void launch_gauss(Ctx* c, cx<R>* base, const GaussEnt* ents, int nent, int64_t m
   int64_t gx = ceil_div(max_elems, 256);
   int64_t cap = std::max<int64_t>(1, (int64_t)c->sm_count * 16 / nent);
   if (gx > cap) gx = cap;
+  KTimer timer(c, "gauss", 0.0, (double)sizeof(cx<R>) * (double)max_elems * nent);
   for (int off = 0; off < nent; off += 65535) {
     int n = std::min(65535, nent - off);
     gauss_kernel<R><<<dim3((unsigned)gx, n), 256, 0, c->stream>>>(base, ents + off, is_real ? 1 : 0);
