@@ -13,6 +13,7 @@
 // Entry arithmetic is written so r, the phase and 1/r match the CPU oracle
 // bit-for-bit (explicit __dmul_rn/fma, no contraction); sin/cos differ by ulps.
 #include <algorithm>
+#include <type_traits>
 #include <vector>
 
 #include "kernels.cuh"
@@ -164,6 +165,263 @@ __global__ void __launch_bounds__(256) matvec_kernel(Points outp, Points inp, do
   }
 }
 
+// ----------------------------------------------------------------------------
+// complex128 path: contraction on the FP64 tensor path (mma.sync m8n8k4 f64).
+// DMMA and DFMA share the FP64 pipe on B200 (profiles/r01_matvec_ncu.txt), so
+// the win is issue slots: one DMMA does the work of 8 warp-wide DFMAs, which
+// leaves the issue bandwidth to the kernel-entry evaluation.
+// ----------------------------------------------------------------------------
+
+// sin/cos of an argument reduced by the 2-term FMA Cody-Waite step (|ph| up to
+// ~1e5 here) and evaluated with Taylor polynomials on [-pi/4, pi/4]
+// (truncation < 1e-19); ~20 FP64 ops instead of ~47 for libdevice sincos.
+__device__ __forceinline__ void sincos_red(double f, int q, double& s, double& c) {
+  const double x2 = f * f;
+  double ps = 2.8114572543455207632e-15;                 //  1/17!
+  ps = fma(ps, x2, -7.6471637318198164759e-13);          // -1/15!
+  ps = fma(ps, x2, 1.6059043836821614599e-10);           //  1/13!
+  ps = fma(ps, x2, -2.5052108385441718775e-08);          // -1/11!
+  ps = fma(ps, x2, 2.7557319223985890653e-06);           //  1/9!
+  ps = fma(ps, x2, -1.9841269841269841270e-04);          // -1/7!
+  ps = fma(ps, x2, 8.3333333333333333333e-03);           //  1/5!
+  ps = fma(ps, x2, -1.6666666666666666667e-01);          // -1/3!
+  const double sn = fma(f * x2, ps, f);
+  double pc = 4.7794773323873852974e-14;                 //  1/16!
+  pc = fma(pc, x2, -1.1470745597729724714e-11);          // -1/14!
+  pc = fma(pc, x2, 2.0876756987868098979e-09);           //  1/12!
+  pc = fma(pc, x2, -2.7557319223985890653e-07);          // -1/10!
+  pc = fma(pc, x2, 2.4801587301587301587e-05);           //  1/8!
+  pc = fma(pc, x2, -1.3888888888888888889e-03);          // -1/6!
+  pc = fma(pc, x2, 4.1666666666666666667e-02);           //  1/4!
+  pc = fma(pc, x2, -0.5);                                // -1/2!
+  const double cs = fma(x2, pc, 1.0);
+  // quadrant q mod 4: (s, c) <- (s, c), (c, -s), (-s, -c), (-c, s)
+  const bool swap = q & 1;
+  double rs = swap ? cs : sn, rc = swap ? sn : cs;
+  if ((q + 1) & 2) rc = -rc;
+  if (q & 2) rs = -rs;
+  s = rs;
+  c = rc;
+}
+
+__device__ __forceinline__ void fast_sincos(double ph, double& s, double& c) {
+  const double q = rint(ph * 0.63661977236758134308);    // 2/pi
+  double f = fma(-q, 1.5707963267948965580, ph);         // pi/2 high
+  f = fma(-q, 6.1232339957367658e-17, f);                // pi/2 low
+  sincos_red(f, (int)(long long)q, s, c);
+}
+
+// 1/r to ~1 ulp: MUFU.RCP64H seed + two Newton steps (amplitude only; the
+// phase uses the correctly rounded r).
+__device__ __forceinline__ double fast_rcp(double r) {
+  double y;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(r));
+  double e = fma(-r, y, 1.0);
+  y = fma(y, e, y);
+  e = fma(-r, y, 1.0);
+  return fma(y, e, y);
+}
+
+template <int KIND>
+__device__ __forceinline__ double2 kernel_entry_fast(double tx, double ty, double tz, double sx, double sy, double sz,
+                                                     double kappa) {
+  double sn, cs;
+  if (KIND == KK_NUFFT) {
+    // exp(2 pi i x xi): t = x xi, f = t - rint(t) in [-1/2, 1/2]; quarter turns exact
+    const double ph = __dmul_rn(tx, sx);
+    const double f = __dsub_rn(ph, rint(ph));
+    const double qq = rint(4.0 * f);
+    const double g = __dsub_rn(f, 0.25 * qq);
+    sincos_red(__dmul_rn(kTwoPi, g), (int)qq, sn, cs);
+    return make_double2(cs, sn);
+  } else if (KIND == KK_PLATES) {
+    const double dx = __dsub_rn(tx, sx), dy = __dsub_rn(ty, sy), dz = __dsub_rn(tz, sz);
+    const double r = __dsqrt_rn(fma(dz, dz, fma(dy, dy, __dmul_rn(dx, dx))));
+    fast_sincos(__dmul_rn(kappa, r), sn, cs);
+    const double sc = fast_rcp(__dmul_rn(kFourPi, r));
+    return make_double2(cs * sc, sn * sc);
+  } else {
+    const double dx = __dsub_rn(tx, sx), dy = __dsub_rn(ty, sy);
+    const double r = __dsqrt_rn(fma(dy, dy, __dmul_rn(dx, dx)));
+    fast_sincos(__dmul_rn(kappa, r), sn, cs);
+    const double sc = fast_rcp(r);
+    return make_double2(cs * sc, sn * sc);
+  }
+}
+
+__device__ __forceinline__ void dmma(double& d0, double& d1, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+               : "+d"(d0), "+d"(d1)
+               : "d"(a), "d"(b));
+}
+__device__ __forceinline__ double dneg(double a) {
+  return __longlong_as_double(__double_as_longlong(a) ^ (long long)0x8000000000000000ULL);
+}
+
+// 8 warps stacked along the output rows; warp w owns rows [w*8*MT, (w+1)*8*MT)
+// of the CTA tile and all 8*NT columns.  Shared memory (doubles):
+//   Kre, Kim [BK][BM+8]   kernel tile, k-major: A fragments conflict free
+//   Xre, Xim [BN][BK+4]   probe tile, column-major: B fragments conflict free
+//   P[3][BK]              input points of the tile
+template <int KIND, int MODE, int MT, int NT, int BK>
+__global__ void __launch_bounds__(256, 1) matvec_dmma_kernel(Points outp, Points inp, double kappa, int64_t m_out,
+                                                             const double2* __restrict__ X, double2* __restrict__ Y,
+                                                             int64_t ldy, const MatvecItem* __restrict__ items,
+                                                             int64_t rows_per_split, int64_t pstride) {
+  constexpr int BM = 64 * MT, BN = 8 * NT, SM = BM + 8, SX = BK + 4;
+  constexpr int XPT = (BK * BN + 255) / 256;  // probe-tile elements per thread
+  extern __shared__ __align__(16) double sm_d[];
+  double* Kre = sm_d;
+  double* Kim = Kre + BK * SM;
+  double* Xb = Kim + BK * SM;  // 2 buffers x [re|im] x BN x SX
+  double* Pb = Xb + 4 * BN * SX;  // 2 buffers x [3][BK]
+
+  const MatvecItem it = items[blockIdx.y];
+  const int64_t i0 = (int64_t)blockIdx.x * BM;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int g = lane >> 2, t = lane & 3;
+  const int64_t kb = (int64_t)blockIdx.z * rows_per_split;
+  const int64_t ke = min(it.rows, kb + rows_per_split);
+
+  // evaluation mapping: thread -> fixed output row(s), strided k
+  constexpr int EROWS = BM < 256 ? BM : 256;
+  constexpr int EKSTEP = 256 / EROWS;
+  constexpr int EREPS = BM / EROWS;
+  const int erow = tid % EROWS, ek0 = tid / EROWS;
+  double ox[EREPS], oy[EREPS], oz[EREPS];
+  bool ovalid[EREPS];
+#pragma unroll
+  for (int q = 0; q < EREPS; ++q) {
+    const int64_t gi = i0 + erow + q * EROWS;
+    ovalid[q] = gi < m_out;
+    const int64_t gs = ovalid[q] ? gi : 0;
+    ox[q] = outp.x[gs];
+    oy[q] = KIND == KK_NUFFT ? 0.0 : outp.y[gs];
+    oz[q] = KIND == KK_PLATES ? outp.z[gs] : 0.0;
+  }
+
+  // register staging of the next probe tile / input points
+  double2 xr[XPT];
+  double pr[3];
+  auto fetch = [&](int64_t k0) {
+#pragma unroll
+    for (int q = 0; q < XPT; ++q) {
+      const int idx = tid + 256 * q;
+      const int kk = idx % BK, cc = idx / BK;
+      const int64_t gj = k0 + kk;
+      xr[q] = (idx < BK * BN && gj < ke && cc < it.ncols) ? X[it.x_off + gj + (int64_t)cc * it.ldx]
+                                                          : make_double2(0.0, 0.0);
+    }
+    if (tid < BK) {
+      const int64_t gj = k0 + tid;
+      const int64_t pj = it.row0 + (gj < ke ? gj : kb);
+      pr[0] = inp.x[pj];
+      pr[1] = KIND == KK_NUFFT ? 0.0 : inp.y[pj];
+      pr[2] = KIND == KK_PLATES ? inp.z[pj] : 0.0;
+    }
+  };
+  auto commit = [&](int buf) {
+    double* xre = Xb + buf * 2 * BN * SX;
+    double* xim = xre + BN * SX;
+#pragma unroll
+    for (int q = 0; q < XPT; ++q) {
+      const int idx = tid + 256 * q;
+      if (idx < BK * BN) {
+        const int kk = idx % BK, cc = idx / BK;
+        xre[cc * SX + kk] = xr[q].x;
+        xim[cc * SX + kk] = xr[q].y;
+      }
+    }
+    if (tid < BK) {
+      double* p = Pb + buf * 3 * BK;
+      p[tid] = pr[0];
+      p[BK + tid] = pr[1];
+      p[2 * BK + tid] = pr[2];
+    }
+  };
+
+  double acc[MT][NT][2][2];  // [re|im][2 values]
+#pragma unroll
+  for (int a = 0; a < MT; ++a)
+#pragma unroll
+    for (int b = 0; b < NT; ++b) acc[a][b][0][0] = acc[a][b][0][1] = acc[a][b][1][0] = acc[a][b][1][1] = 0.0;
+
+  if (kb < ke) {
+    fetch(kb);
+    commit(0);
+  }
+  __syncthreads();
+  int buf = 0;
+  for (int64_t k0 = kb; k0 < ke; k0 += BK, buf ^= 1) {
+    const double* P = Pb + buf * 3 * BK;
+    // ---- evaluate the BM x BK kernel tile
+#pragma unroll
+    for (int q = 0; q < EREPS; ++q) {
+#pragma unroll 4
+      for (int kk = ek0; kk < BK; kk += EKSTEP) {
+        double2 v = make_double2(0.0, 0.0);
+        if (ovalid[q] && k0 + kk < ke) {
+          const double ix = P[kk], iy = P[BK + kk], iz = P[2 * BK + kk];
+          if (MODE == OP_N) v = kernel_entry_fast<KIND>(ox[q], oy[q], oz[q], ix, iy, iz, kappa);
+          else v = kernel_entry_fast<KIND>(ix, iy, iz, ox[q], oy[q], oz[q], kappa);
+          if (MODE == OP_H) v.y = -v.y;
+        }
+        Kre[kk * SM + erow + q * EROWS] = v.x;
+        Kim[kk * SM + erow + q * EROWS] = v.y;
+      }
+    }
+    __syncthreads();
+    const bool more = k0 + BK < ke;
+    if (more) fetch(k0 + BK);  // global loads in flight during the MMAs
+    // ---- complex contraction on DMMA: 4 real m8n8k4 per complex tile
+    const double* xre = Xb + buf * 2 * BN * SX;
+    const double* xim = xre + BN * SX;
+#pragma unroll
+    for (int ks = 0; ks < BK; ks += 4) {
+      double ar[MT], ai[MT], br[NT], bi[NT];
+#pragma unroll
+      for (int a = 0; a < MT; ++a) {
+        const int row = warp * 8 * MT + a * 8 + g;
+        ar[a] = Kre[(ks + t) * SM + row];
+        ai[a] = Kim[(ks + t) * SM + row];
+      }
+#pragma unroll
+      for (int b = 0; b < NT; ++b) {
+        const int col = b * 8 + g;
+        br[b] = xre[col * SX + ks + t];
+        bi[b] = xim[col * SX + ks + t];
+      }
+#pragma unroll
+      for (int a = 0; a < MT; ++a) {
+        const double nai = dneg(ai[a]);
+#pragma unroll
+        for (int b = 0; b < NT; ++b) {
+          dmma(acc[a][b][0][0], acc[a][b][0][1], ar[a], br[b]);
+          dmma(acc[a][b][0][0], acc[a][b][0][1], nai, bi[b]);
+          dmma(acc[a][b][1][0], acc[a][b][1][1], ar[a], bi[b]);
+          dmma(acc[a][b][1][0], acc[a][b][1][1], ai[a], br[b]);
+        }
+      }
+    }
+    if (more) commit(buf ^ 1);
+    __syncthreads();
+  }
+  // ---- store: lane (g, t) holds C[g][2t], C[g][2t+1] of every 8x8 tile
+  double2* Yb = Y + it.ybase + (int64_t)blockIdx.z * pstride;
+#pragma unroll
+  for (int a = 0; a < MT; ++a) {
+    const int64_t gi = i0 + warp * 8 * MT + a * 8 + g;
+    if (gi >= m_out) continue;
+#pragma unroll
+    for (int b = 0; b < NT; ++b)
+#pragma unroll
+      for (int v = 0; v < 2; ++v) {
+        const int cc = b * 8 + 2 * t + v;
+        if (cc < it.ncols) Yb[gi + (it.ycol + cc) * ldy] = make_double2(acc[a][b][0][v], acc[a][b][1][v]);
+      }
+  }
+}
+
 // Y(:, cols) = sum_z P_z(:, cols), fixed order
 template <typename R>
 __global__ void split_reduce_kernel(const cx<R>* __restrict__ P, int64_t pstride, int nsplit, cx<R>* Y, int64_t ldy,
@@ -178,7 +436,7 @@ __global__ void split_reduce_kernel(const cx<R>* __restrict__ P, int64_t pstride
   }
 }
 
-template <typename R, int KIND, int MODE, int BM, int BN, int TM, int TN>
+template <typename R, int KIND, int MODE, int BM, int BN, int TM, int TN, int DM = 0, int MT = 1, int NT = 1>
 void run_cfg(Ctx* c, Points outp, Points inp, double kappa, int64_t m_out, const cx<R>* X, cx<R>* Y, int64_t ldy,
              const MatvecSeg* segs, int nseg) {
   constexpr int BK = 16;
@@ -229,8 +487,18 @@ void run_cfg(Ctx* c, Points outp, Points inp, double kappa, int64_t m_out, const
     kbytes += (double)sizeof(cx<R>) * ((double)it.rows + (double)m_out) * (double)it.ncols;
   }
   KTimer timer(c, "kernel_matvec", kflops, kbytes);
-  size_t smem = sizeof(cx<R>) * (size_t)BK * (BM + BN);
-  auto kern = matvec_kernel<R, KIND, MODE, BM, BN, TM, TN, BK>;
+  using KernFn = void (*)(Points, Points, double, int64_t, const cx<R>*, cx<R>*, int64_t, const MatvecItem*, int64_t,
+                          int64_t);
+  size_t smem;
+  KernFn kern;
+  if constexpr (DM) {
+    static_assert(BM == 64 * MT && BN == 8 * NT, "dmma tile");
+    smem = sizeof(double) * (size_t)(2 * BK * (BM + 8) + 4 * BN * (BK + 4) + 6 * BK);
+    kern = matvec_dmma_kernel<KIND, MODE, MT, NT, BK>;
+  } else {
+    smem = sizeof(cx<R>) * (size_t)BK * (BM + BN);
+    kern = matvec_kernel<R, KIND, MODE, BM, BN, TM, TN, BK>;
+  }
   BFLY_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   if (items.size() > 65535) fail(PRECONDITION, "matvec: too many work items");
   dim3 grid((unsigned)gx, (unsigned)items.size(), (unsigned)nsplit);
@@ -263,6 +531,15 @@ void dispatch_width(Ctx* c, Points outp, Points inp, double kappa, int64_t m_out
                     int64_t ldy, const MatvecSeg* segs, int nseg) {
   int maxw = 0;
   for (int s = 0; s < nseg; ++s) maxw = std::max(maxw, segs[s].ncols);
+  if constexpr (std::is_same<R, double>::value) {
+    // complex128: DMMA tiles (BM = 64 MT rows, BN = 8 NT columns)
+    if (maxw <= 8) run_cfg<R, KIND, MODE, 256, 8, 1, 1, 1, 4, 1>(c, outp, inp, kappa, m_out, X, Y, ldy, segs, nseg);
+    else if (maxw <= 16) run_cfg<R, KIND, MODE, 256, 16, 1, 1, 1, 4, 2>(c, outp, inp, kappa, m_out, X, Y, ldy, segs, nseg);
+    else if (maxw <= 24) run_cfg<R, KIND, MODE, 256, 24, 1, 1, 1, 4, 3>(c, outp, inp, kappa, m_out, X, Y, ldy, segs, nseg);
+    else if (maxw <= 32) run_cfg<R, KIND, MODE, 256, 32, 1, 1, 1, 4, 4>(c, outp, inp, kappa, m_out, X, Y, ldy, segs, nseg);
+    else run_cfg<R, KIND, MODE, 128, 64, 1, 1, 1, 2, 8>(c, outp, inp, kappa, m_out, X, Y, ldy, segs, nseg);
+    return;
+  }
   if (maxw <= 8) run_cfg<R, KIND, MODE, 256, 8, 4, 2>(c, outp, inp, kappa, m_out, X, Y, ldy, segs, nseg);
   else if (maxw <= 16) run_cfg<R, KIND, MODE, 256, 16, 8, 2>(c, outp, inp, kappa, m_out, X, Y, ldy, segs, nseg);
   else if (maxw <= 32) run_cfg<R, KIND, MODE, 128, 32, 4, 4>(c, outp, inp, kappa, m_out, X, Y, ldy, segs, nseg);
