@@ -13,6 +13,8 @@
 // Entry arithmetic is written so r, the phase and 1/r match the CPU oracle
 // bit-for-bit (explicit __dmul_rn/fma, no contraction); sin/cos differ by ulps.
 #include <algorithm>
+#include <cstdlib>
+#include <string>
 #include <type_traits>
 #include <vector>
 
@@ -175,25 +177,26 @@ __global__ void __launch_bounds__(256) matvec_kernel(Points outp, Points inp, do
 // sin/cos of an argument reduced by the 2-term FMA Cody-Waite step (|ph| up to
 // ~1e5 here) and evaluated with Taylor polynomials on [-pi/4, pi/4]
 // (truncation < 1e-19); ~20 FP64 ops instead of ~47 for libdevice sincos.
+// Taylor coefficients in the constant bank: DFMA reads c[][] operands
+// directly (64-bit immediates would be re-materialised with UMOVs).
+__constant__ double kSinC[8] = {2.8114572543455207632e-15,  -7.6471637318198164759e-13,   // 1/17!, -1/15!
+                                1.6059043836821614599e-10,  -2.5052108385441718775e-08,   // 1/13!, -1/11!
+                                2.7557319223985890653e-06,  -1.9841269841269841270e-04,   // 1/9!,  -1/7!
+                                8.3333333333333333333e-03,  -1.6666666666666666667e-01};  // 1/5!,  -1/3!
+__constant__ double kCosC[8] = {4.7794773323873852974e-14,  -1.1470745597729724714e-11,   // 1/16!, -1/14!
+                                2.0876756987868098979e-09,  -2.7557319223985890653e-07,   // 1/12!, -1/10!
+                                2.4801587301587301587e-05,  -1.3888888888888888889e-03,   // 1/8!,  -1/6!
+                                4.1666666666666666667e-02,  -0.5};                        // 1/4!,  -1/2!
+
 __device__ __forceinline__ void sincos_red(double f, int q, double& s, double& c) {
   const double x2 = f * f;
-  double ps = 2.8114572543455207632e-15;                 //  1/17!
-  ps = fma(ps, x2, -7.6471637318198164759e-13);          // -1/15!
-  ps = fma(ps, x2, 1.6059043836821614599e-10);           //  1/13!
-  ps = fma(ps, x2, -2.5052108385441718775e-08);          // -1/11!
-  ps = fma(ps, x2, 2.7557319223985890653e-06);           //  1/9!
-  ps = fma(ps, x2, -1.9841269841269841270e-04);          // -1/7!
-  ps = fma(ps, x2, 8.3333333333333333333e-03);           //  1/5!
-  ps = fma(ps, x2, -1.6666666666666666667e-01);          // -1/3!
+  double ps = kSinC[0], pc = kCosC[0];
+#pragma unroll
+  for (int i = 1; i < 8; ++i) {
+    ps = fma(ps, x2, kSinC[i]);
+    pc = fma(pc, x2, kCosC[i]);
+  }
   const double sn = fma(f * x2, ps, f);
-  double pc = 4.7794773323873852974e-14;                 //  1/16!
-  pc = fma(pc, x2, -1.1470745597729724714e-11);          // -1/14!
-  pc = fma(pc, x2, 2.0876756987868098979e-09);           //  1/12!
-  pc = fma(pc, x2, -2.7557319223985890653e-07);          // -1/10!
-  pc = fma(pc, x2, 2.4801587301587301587e-05);           //  1/8!
-  pc = fma(pc, x2, -1.3888888888888888889e-03);          // -1/6!
-  pc = fma(pc, x2, 4.1666666666666666667e-02);           //  1/4!
-  pc = fma(pc, x2, -0.5);                                // -1/2!
   const double cs = fma(x2, pc, 1.0);
   // quadrant q mod 4: (s, c) <- (s, c), (c, -s), (-s, -c), (-c, s)
   const bool swap = q & 1;
@@ -263,8 +266,8 @@ __device__ __forceinline__ double dneg(double a) {
 //   Kre, Kim [BK][BM+8]   kernel tile, k-major: A fragments conflict free
 //   Xre, Xim [BN][BK+4]   probe tile, column-major: B fragments conflict free
 //   P[3][BK]              input points of the tile
-template <int KIND, int MODE, int MT, int NT, int BK>
-__global__ void __launch_bounds__(256, 1) matvec_dmma_kernel(Points outp, Points inp, double kappa, int64_t m_out,
+template <int KIND, int MODE, int MT, int NT, int BK, int MINB>
+__global__ void __launch_bounds__(256, MINB) matvec_dmma_kernel(Points outp, Points inp, double kappa, int64_t m_out,
                                                              const double2* __restrict__ X, double2* __restrict__ Y,
                                                              int64_t ldy, const MatvecItem* __restrict__ items,
                                                              int64_t rows_per_split, int64_t pstride) {
@@ -391,14 +394,21 @@ __global__ void __launch_bounds__(256, 1) matvec_dmma_kernel(Points outp, Points
         br[b] = xre[col * SX + ks + t];
         bi[b] = xim[col * SX + ks + t];
       }
+      // two passes over the MT x NT tiles: a dependent MMA pair is 2*MT*NT
+      // instructions apart (no fixed-latency waits between them)
+#pragma unroll
+      for (int a = 0; a < MT; ++a)
+#pragma unroll
+        for (int b = 0; b < NT; ++b) {
+          dmma(acc[a][b][0][0], acc[a][b][0][1], ar[a], br[b]);
+          dmma(acc[a][b][1][0], acc[a][b][1][1], ar[a], bi[b]);
+        }
 #pragma unroll
       for (int a = 0; a < MT; ++a) {
         const double nai = dneg(ai[a]);
 #pragma unroll
         for (int b = 0; b < NT; ++b) {
-          dmma(acc[a][b][0][0], acc[a][b][0][1], ar[a], br[b]);
           dmma(acc[a][b][0][0], acc[a][b][0][1], nai, bi[b]);
-          dmma(acc[a][b][1][0], acc[a][b][1][1], ar[a], bi[b]);
           dmma(acc[a][b][1][0], acc[a][b][1][1], ai[a], br[b]);
         }
       }
@@ -494,7 +504,7 @@ void run_cfg(Ctx* c, Points outp, Points inp, double kappa, int64_t m_out, const
   if constexpr (DM) {
     static_assert(BM == 64 * MT && BN == 8 * NT, "dmma tile");
     smem = sizeof(double) * (size_t)(2 * BK * (BM + 8) + 4 * BN * (BK + 4) + 6 * BK);
-    kern = matvec_dmma_kernel<KIND, MODE, MT, NT, BK>;
+    kern = matvec_dmma_kernel<KIND, MODE, MT, NT, BK, (MT * NT <= 8 ? 2 : 1)>;
   } else {
     smem = sizeof(cx<R>) * (size_t)BK * (BM + BN);
     kern = matvec_kernel<R, KIND, MODE, BM, BN, TM, TN, BK>;
@@ -536,7 +546,11 @@ void dispatch_width(Ctx* c, Points outp, Points inp, double kappa, int64_t m_out
     if (maxw <= 8) run_cfg<R, KIND, MODE, 256, 8, 1, 1, 1, 4, 1>(c, outp, inp, kappa, m_out, X, Y, ldy, segs, nseg);
     else if (maxw <= 16) run_cfg<R, KIND, MODE, 256, 16, 1, 1, 1, 4, 2>(c, outp, inp, kappa, m_out, X, Y, ldy, segs, nseg);
     else if (maxw <= 24) run_cfg<R, KIND, MODE, 256, 24, 1, 1, 1, 4, 3>(c, outp, inp, kappa, m_out, X, Y, ldy, segs, nseg);
-    else if (maxw <= 32) run_cfg<R, KIND, MODE, 256, 32, 1, 1, 1, 4, 4>(c, outp, inp, kappa, m_out, X, Y, ldy, segs, nseg);
+    else if (maxw <= 32) {
+      static const bool small = std::getenv("BFLY_MV_TILE") && std::string(std::getenv("BFLY_MV_TILE")) == "2x4";
+      if (small) run_cfg<R, KIND, MODE, 128, 32, 1, 1, 1, 2, 4>(c, outp, inp, kappa, m_out, X, Y, ldy, segs, nseg);
+      else run_cfg<R, KIND, MODE, 256, 32, 1, 1, 1, 4, 4>(c, outp, inp, kappa, m_out, X, Y, ldy, segs, nseg);
+    }
     else run_cfg<R, KIND, MODE, 128, 64, 1, 1, 1, 2, 8>(c, outp, inp, kappa, m_out, X, Y, ldy, segs, nseg);
     return;
   }
