@@ -144,6 +144,9 @@ typedef struct bfly_recon_cfg {
   int32_t threads;      /* accepted for API parity; the GPU path ignores it */
   int32_t literal_transpose_core;
   int64_t max_batch_probes; /* probes per black-box launch; <= 0: a whole level */
+  int32_t virtual_ranks;    /* >1: execute the rank-sharded schedule for this many ranks in one
+                               process (tests the multi-GPU exchange on one GPU); 0/1: off */
+  int32_t reserved_;
 } bfly_recon_cfg;
 
 void bfly_cfg_default(bfly_recon_cfg* cfg);

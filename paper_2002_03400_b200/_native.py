@@ -57,6 +57,7 @@ class Cfg(C.Structure):
         ("tolerance", C.c_double), ("oversampling", C.c_int64), ("rank_guess", C.c_int64),
         ("levels", C.c_int32), ("center", C.c_int32), ("seed", C.c_uint64), ("hard_cap", C.c_int64),
         ("threads", C.c_int32), ("literal_transpose_core", C.c_int32), ("max_batch_probes", C.c_int64),
+        ("virtual_ranks", C.c_int32), ("reserved_", C.c_int32),
     ]
 
 

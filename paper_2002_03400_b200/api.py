@@ -391,6 +391,7 @@ class ReconstructionConfig:
     threads: int = 1
     literal_transpose_core: bool = False
     max_batch_probes: int = 0
+    virtual_ranks: int = 0
 
     def center_level(self) -> int:
         return self.levels // 2 if self.center < 0 else self.center

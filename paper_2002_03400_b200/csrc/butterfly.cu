@@ -757,6 +757,107 @@ std::unique_ptr<DevButterfly<R>> DevButterfly<R>::from_host(Ctx* c, const HostBu
   return d;
 }
 
+namespace {
+struct ByteSink {
+  uint8_t* out;
+  int64_t pos = 0;
+  void put(const void* p, size_t n) {
+    if (out) std::memcpy(out + pos, p, n);
+    pos += (int64_t)n;
+  }
+  void u32(uint32_t v) { put(&v, 4); }
+  void u64(uint64_t v) { put(&v, 8); }
+};
+}  // namespace
+
+template <typename R>
+int64_t DevButterfly<R>::serialize(int tag, uint8_t* out) const {
+  ByteSink bs{out};
+  const bool real = tag == 0;
+  const int64_t NB = nb();
+  bs.u32(0x31484642u);
+  bs.u32(1);
+  uint8_t t8 = (uint8_t)tag;
+  bs.put(&t8, 1);
+  bs.u32((uint32_t)L);
+  bs.u32((uint32_t)lm);
+  bs.u64((uint64_t)rt.n);
+  bs.u64((uint64_t)ct.n);
+  bs.u64((uint64_t)nnz());
+  bs.u64((uint64_t)max_rank());
+  for (const Tree* t : {&rt, &ct}) {
+    bs.u64((uint64_t)t->n);
+    bs.u32((uint32_t)t->levels);
+    bs.put(t->perm.data(), sizeof(int64_t) * t->perm.size());
+    for (const auto& lv : t->ranges) bs.put(lv.data(), sizeof(int64_t) * lv.size());
+  }
+  std::vector<cx<R>> raw;
+  cx<R>* stage = nullptr;
+  size_t stage_n = 0;
+  // one level: rows/gap per block given by row_split(i) -> (r1, r2)
+  auto emit = [&](const Level<R>& lv, auto rows_of) {
+    if (out) {
+      size_t n = (size_t)(NB * lv.stride());
+      if (n > stage_n) {
+        if (stage) cudaFreeHost(stage);
+        BFLY_CUDA(cudaMallocHost(&stage, n * sizeof(cx<R>)));
+        stage_n = n;
+      }
+      lv.data.download(stage, n);
+      BFLY_CUDA(cudaStreamSynchronize(lv.data.ctx->stream));
+    }
+    for (int64_t i = 0; i < NB; ++i) {
+      int64_t r1, r2;
+      rows_of(i, r1, r2);
+      const int64_t cols = lv.ranks[i], rows = r1 + r2;
+      bs.u64((uint64_t)rows);
+      bs.u64((uint64_t)cols);
+      if (!out) {
+        bs.pos += rows * cols * (real ? 8 : 16);
+        continue;
+      }
+      const cx<R>* blk = stage + i * lv.stride();
+      for (int64_t c = 0; c < cols; ++c) {
+        const cx<R>* col = blk + c * lv.ld;
+        for (int part = 0; part < 2; ++part) {
+          const cx<R>* src = part == 0 ? col : col + lv.gap;
+          const int64_t cnt = part == 0 ? r1 : r2;
+          if (real) {
+            for (int64_t q = 0; q < cnt; ++q) {
+              double v = (double)src[q].x;
+              bs.put(&v, 8);
+            }
+          } else if (sizeof(R) == 8) {
+            bs.put(src, (size_t)cnt * 16);
+          } else {
+            for (int64_t q = 0; q < cnt; ++q) {
+              double v[2] = {(double)src[q].x, (double)src[q].y};
+              bs.put(v, 16);
+            }
+          }
+        }
+      }
+    }
+  };
+  emit(uleaf, [&](int64_t i, int64_t& r1, int64_t& r2) { r1 = rt.size(L, i); r2 = 0; });
+  for (int l = lm; l < L; ++l)
+    emit(r[l - lm], [&](int64_t i, int64_t& r1, int64_t& r2) {
+      int64_t tau = i >> (L - l), nu = i & ((int64_t(1) << (L - l)) - 1);
+      r1 = u_rank(l + 1, 2 * tau, nu / 2);
+      r2 = u_rank(l + 1, 2 * tau + 1, nu / 2);
+    });
+  emit(b, [&](int64_t i, int64_t& r1, int64_t& r2) { r1 = b.rows[i]; r2 = 0; });
+  for (int l = 1; l <= lm; ++l)
+    emit(w[l - 1], [&](int64_t i, int64_t& r1, int64_t& r2) {
+      int64_t tau = i >> (L - l), nu = i & ((int64_t(1) << (L - l)) - 1);
+      r1 = v_rank(l - 1, tau / 2, 2 * nu);
+      r2 = v_rank(l - 1, tau / 2, 2 * nu + 1);
+    });
+  emit(vleaf, [&](int64_t i, int64_t& r1, int64_t& r2) { r1 = ct.size(L, i); r2 = 0; });
+  if (stage) cudaFreeHost(stage);
+  return bs.pos;
+}
+
 template struct Level<double>;
 template struct Level<float>;
 template struct DevButterfly<double>;

@@ -65,13 +65,16 @@ struct Level {
 
   int64_t stride() const { return ld * cap; }
   cx<R>* block(int64_t i) const { return data.p + i * stride(); }
-  void alloc(Ctx* c, int64_t nb, int64_t ld_, int64_t cap_) {
+  // cap_blocks >= nb reserves room for an in-place all-gather whose per-rank
+  // chunks overhang the last block
+  void alloc(Ctx* c, int64_t nb, int64_t ld_, int64_t cap_, int64_t cap_blocks = 0) {
     ld = std::max<int64_t>(ld_, 1);
     cap = std::max<int64_t>(cap_, 1);
-    data.reset(c, (size_t)(nb * ld * cap));
+    const int64_t nblk = std::max(nb, cap_blocks);
+    data.reset(c, (size_t)(nblk * ld * cap));
     ranks.assign(nb, 0);
     rows.assign(nb, 0);
-    dranks.reset(c, nb);
+    dranks.reset(c, nblk);
   }
   void finish_ranks(Ctx* c);  // download ranks, set P
 };
@@ -110,6 +113,9 @@ struct DevButterfly {
   double apply_bytes(int64_t k) const;   // nnz*s + (m+n)*k*s
 
   HostButterfly to_host() const;
+  // .bfh bytes straight from the padded device levels (one pinned staging
+  // copy per level); returns the size, writes only when out != nullptr.
+  int64_t serialize(int scalar_tag, uint8_t* out) const;
   static std::unique_ptr<DevButterfly> from_host(Ctx* c, const HostButterfly& h);
 
  private:

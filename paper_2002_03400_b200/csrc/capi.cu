@@ -473,6 +473,8 @@ void bfly_cfg_default(bfly_recon_cfg* c) {
   c->threads = 1;
   c->literal_transpose_core = 0;
   c->max_batch_probes = 0;
+  c->virtual_ranks = 0;
+  c->reserved_ = 0;
 }
 
 int bfly_factorizer_create(bfly_ctx* ctx, bfly_op* op, const bfly_tree* rt, const bfly_tree* ct,
@@ -590,10 +592,8 @@ int64_t bfly_rank_profile(const bfly_bf* bf, int32_t* out) {
 int64_t bfly_serialize(const bfly_bf* bf, uint8_t* buf) {
   int64_t n = -1;
   int rc = guard(C_(bf->ctx), [&] {
-    HostButterfly h = bf->z ? bf->z->to_host() : bf->c->to_host();
-    std::vector<uint8_t> bytes = h.serialize(bf->scalar == BFLY_D ? 0 : 1);
-    n = (int64_t)bytes.size();
-    if (buf) std::memcpy(buf, bytes.data(), bytes.size());
+    const int tag = bf->scalar == BFLY_D ? 0 : 1;
+    n = bf->z ? bf->z->serialize(tag, buf) : bf->c->serialize(tag, buf);
   });
   return rc == BFLY_OK ? n : -1;
 }

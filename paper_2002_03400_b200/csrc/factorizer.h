@@ -1,6 +1,13 @@
 // factorizer.h -- Algorithm 2 driver on the GPU (reference Factorizer,
 // reconstruct.hpp:145-410): same phase order, seeds, probe widths,
 // truncation and stop rule; every level runs as a handful of batched launches.
+//
+// Multi-GPU: every level's units (leaves, W probes tau, R probes nu) are split
+// into contiguous per-rank chunks.  Leaf and W blocks of a chunk are
+// contiguous in the tau-major level layout and are all-gathered in place;
+// R/B blocks of a nu chunk are strided and go through pack -> all-gather ->
+// unpack.  With virtual_ranks > 1 one process executes every rank's chunk
+// through the same pack/unpack path (single-GPU test of the sharding).
 #pragma once
 
 #include <chrono>
@@ -38,16 +45,27 @@ class Factorizer {
   bool v_done_ = false, u_done_ = false, core_done_ = false;
   int next_w_ = 1, next_r_ = 0;
   double flops_ = 0;  // chain + QR + core-fit work (black box counted by the operator)
+  // sharding
+  int world_ = 1, rank_ = 0;
+  bool virtual_ = false;
 
+  std::vector<int> my_ranks() const;
+  static std::pair<int64_t, int64_t> chunk(int64_t n, int world, int r);
   bfly_phase& new_phase(const std::string& name);
   void end_phase(bfly_phase& st, clock::time_point t0, int64_t f0, int64_t tr0);
   void note_probe_bytes(double scalars, int64_t probes);
   void run_leaf_phase(const char* name, bool row_side);
-  // black-box product of a batch of structured probes (cores in G) into Y
-  // (out_dim x wtot, tree ordered on return)
   void probe_products(int mode, const Tree& probe_tree, int level, const std::vector<int64_t>& nodes,
                       const std::vector<int>& widths, const std::vector<int64_t>& col0, const std::vector<int64_t>& goff,
                       const V* G, int64_t wtot, DBuf<V>& Y);
+  // W level: probes tau in [t0, t1)
+  void w_probes(int l, const std::vector<int>& width, int64_t t0, int64_t t1, int maxw);
+  // R level: probes nu in [n0, n1)
+  void r_probes(int l, const std::vector<int>& width, int64_t n0, int64_t n1, int maxw, int32_t* err_flag);
+  // in-place all-gather of `per_rank` consecutive blocks per rank (+ ranks)
+  void gather_inplace(Level<R>& lv, int64_t per_rank);
+  // pack/all-gather/unpack of block index lists (one list per rank)
+  void gather_packed(std::vector<Level<R>*> lvs, const std::vector<std::vector<int64_t>>& owned);
   double qr_flops(double a, double w, double k) const;
 };
 

@@ -547,8 +547,9 @@ void dispatch_width(Ctx* c, Points outp, Points inp, double kappa, int64_t m_out
     else if (maxw <= 16) run_cfg<R, KIND, MODE, 256, 16, 1, 1, 1, 4, 2>(c, outp, inp, kappa, m_out, X, Y, ldy, segs, nseg);
     else if (maxw <= 24) run_cfg<R, KIND, MODE, 256, 24, 1, 1, 1, 4, 3>(c, outp, inp, kappa, m_out, X, Y, ldy, segs, nseg);
     else if (maxw <= 32) {
-      static const bool small = std::getenv("BFLY_MV_TILE") && std::string(std::getenv("BFLY_MV_TILE")) == "2x4";
-      if (small) run_cfg<R, KIND, MODE, 128, 32, 1, 1, 1, 2, 4>(c, outp, inp, kappa, m_out, X, Y, ldy, segs, nseg);
+      // 2x4 warp tiles (122 regs, 2 CTAs/SM) beat 4x4 (232 regs, 1 CTA/SM) by 12% on config 2
+      static const bool big = std::getenv("BFLY_MV_TILE") && std::string(std::getenv("BFLY_MV_TILE")) == "4x4";
+      if (!big) run_cfg<R, KIND, MODE, 128, 32, 1, 1, 1, 2, 4>(c, outp, inp, kappa, m_out, X, Y, ldy, segs, nseg);
       else run_cfg<R, KIND, MODE, 256, 32, 1, 1, 1, 4, 4>(c, outp, inp, kappa, m_out, X, Y, ldy, segs, nseg);
     }
     else run_cfg<R, KIND, MODE, 128, 64, 1, 1, 1, 2, 8>(c, outp, inp, kappa, m_out, X, Y, ldy, segs, nseg);

@@ -82,6 +82,17 @@ __global__ void diff_norms_kernel(const cx<R>* a, const cx<R>* b, int64_t n, dou
   }
 }
 
+template <typename R>
+__global__ void copy_blocks_kernel(cx<R>* dst, const int64_t* idx_dst, const cx<R>* src, const int64_t* idx_src,
+                                   int64_t nblocks, int64_t stride) {
+  const int64_t total = nblocks * stride;
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total; t += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t b = t / stride, e = t % stride;
+    const int64_t bd = idx_dst ? idx_dst[b] : b, bs = idx_src ? idx_src[b] : b;
+    dst[bd * stride + e] = src[bs * stride + e];
+  }
+}
+
 __global__ void d2f_kernel(const double2* s, float2* d, int64_t n) {
   for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < n; t += (int64_t)gridDim.x * blockDim.x)
     d[t] = make_float2((float)s[t].x, (float)s[t].y);
@@ -143,6 +154,15 @@ void launch_diff_norms(Ctx* c, const cx<R>* a, const cx<R>* b, int64_t n, double
   BFLY_LAUNCH_CHECK("diff_norms");
 }
 
+template <typename R>
+void launch_copy_blocks(Ctx* c, cx<R>* dst, const int64_t* idx_dst, const cx<R>* src, const int64_t* idx_src,
+                        int64_t nblocks, int64_t stride) {
+  if (nblocks * stride <= 0) return;
+  copy_blocks_kernel<R><<<grid_for(c, nblocks * stride), 256, 0, c->stream>>>(dst, idx_dst, src, idx_src, nblocks,
+                                                                               stride);
+  BFLY_LAUNCH_CHECK("copy_blocks");
+}
+
 void launch_d2f(Ctx* c, const double2* s, float2* d, int64_t n) {
   if (n <= 0) return;
   d2f_kernel<<<grid_for(c, n), 256, 0, c->stream>>>(s, d, n);
@@ -160,7 +180,8 @@ void launch_f2d(Ctx* c, const float2* s, double2* d, int64_t n) {
   template void launch_permute_rows<R>(Ctx*, cx<R>*, int64_t, const cx<R>*, int64_t, int64_t, int64_t,    \
                                        const int64_t*, bool);                                              \
   template void launch_copy2d<R>(Ctx*, cx<R>*, int64_t, const cx<R>*, int64_t, int64_t, int64_t);         \
-  template void launch_diff_norms<R>(Ctx*, const cx<R>*, const cx<R>*, int64_t, double*);
+  template void launch_diff_norms<R>(Ctx*, const cx<R>*, const cx<R>*, int64_t, double*);                 \
+  template void launch_copy_blocks<R>(Ctx*, cx<R>*, const int64_t*, const cx<R>*, const int64_t*, int64_t, int64_t);
 INST(double)
 INST(float)
 #undef INST

@@ -97,6 +97,11 @@ void launch_copy2d(Ctx* c, cx<R>* dst, int64_t ldd, const cx<R>* src, int64_t ld
 // out[0] += ||a - b||_F^2, out[1] += ||a||_F^2 (double accumulators)
 template <typename R>
 void launch_diff_norms(Ctx* c, const cx<R>* a, const cx<R>* b, int64_t n, double* out);
+// dst block idx_dst[i] <- src block idx_src[i] (blocks of `stride` elements);
+// null index arrays mean the identity
+template <typename R>
+void launch_copy_blocks(Ctx* c, cx<R>* dst, const int64_t* idx_dst, const cx<R>* src, const int64_t* idx_src,
+                        int64_t nblocks, int64_t stride);
 // real-valued copy-converters between precisions
 void launch_d2f(Ctx* c, const double2* src, float2* dst, int64_t n);
 void launch_f2d(Ctx* c, const float2* src, double2* dst, int64_t n);

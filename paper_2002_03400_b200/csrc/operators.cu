@@ -26,15 +26,19 @@ template <typename R>
 struct KernelOp : DevOp<R> {
   DBuf<double> tx, ty, tz, sx, sy, sz;
   double kappa = 0;
-  void do_apply(int mode, const cx<R>* X, const std::vector<MatvecSeg>& segs, cx<R>* Y, int64_t ldy) override {
+  void do_apply(int mode, const cx<R>* X, const std::vector<MatvecSeg>& segs, cx<R>* Y, int64_t ldy, int64_t o0,
+                int64_t o1) override {
     Points tp{tx.p, ty.p, tz.p}, sp{sx.p, sy.p, sz.p};
     Points outp = mode == OP_N ? tp : sp, inp = mode == OP_N ? sp : tp;
-    int64_t mout = this->out_dim(mode);
+    outp.x += o0;
+    outp.y += o0;
+    outp.z += o0;
+    const int64_t mout = o1 - o0;
     for (const auto& s : segs) {
       this->evals += (double)mout * (double)s.rows;
       this->flops += 8.0 * (double)mout * (double)s.rows * (double)s.ncols;
     }
-    launch_kernel_matvec<R>(this->ctx, this->kind, mode, outp, inp, kappa, mout, X, Y, ldy, segs.data(),
+    launch_kernel_matvec<R>(this->ctx, this->kind, mode, outp, inp, kappa, mout, X, Y + o0, ldy, segs.data(),
                             (int)segs.size());
   }
 };
@@ -43,25 +47,27 @@ struct KernelOp : DevOp<R> {
 template <typename R>
 struct DenseOp : DevOp<R> {
   DBuf<cx<R>> a;  // m x n column major
-  void do_apply(int mode, const cx<R>* X, const std::vector<MatvecSeg>& segs, cx<R>* Y, int64_t ldy) override {
+  void do_apply(int mode, const cx<R>* X, const std::vector<MatvecSeg>& segs, cx<R>* Y, int64_t ldy, int64_t o0,
+                int64_t o1) override {
     Ctx* c = this->ctx;
     const int64_t m = this->m;
     for (const auto& s : segs) {
-      int64_t mout = this->out_dim(mode);
+      const int64_t mout = o1 - o0;
       if (s.ncols <= 0) continue;
       if (s.rows <= 0) {
-        BFLY_CUDA(cudaMemset2DAsync(Y + s.col0 * ldy, ldy * sizeof(cx<R>), 0, mout * sizeof(cx<R>), s.ncols, c->stream));
+        BFLY_CUDA(cudaMemset2DAsync(Y + o0 + s.col0 * ldy, ldy * sizeof(cx<R>), 0, mout * sizeof(cx<R>), s.ncols,
+                                    c->stream));
         continue;
       }
       GemmEnt e{};
-      e.a0 = mode == OP_N ? s.row0 * m : s.row0;
+      e.a0 = mode == OP_N ? s.row0 * m + o0 : s.row0 + o0 * m;
       e.b0 = 0;
       e.c = 0;
       e.ncols = s.ncols;
       e.mrows = 1 << 30;
       e.krows = 1 << 30;
       DBuf<GemmEnt> de = to_device(c, std::vector<GemmEnt>{e});
-      launch_bgemm<R>(c, mode, (int)mout, (int)s.rows, 1, a.p, m, X + s.x_off, s.ldx, Y + s.col0 * ldy, ldy, de.p, 1,
+      launch_bgemm<R>(c, mode, (int)mout, (int)s.rows, 1, a.p, m, X + s.x_off, s.ldx, Y + o0 + s.col0 * ldy, ldy, de.p, 1,
                       s.ncols, false);
       this->flops += 8.0 * (double)mout * (double)s.rows * (double)s.ncols;
     }
@@ -72,7 +78,8 @@ struct DenseOp : DevOp<R> {
 template <typename R>
 struct ComposeOp : DevOp<R> {
   std::unique_ptr<DevOp<R>> f1, f2;  // A = f2 * f1
-  void do_apply(int mode, const cx<R>* X, const std::vector<MatvecSeg>& segs, cx<R>* Y, int64_t ldy) override {
+  void do_apply(int mode, const cx<R>* X, const std::vector<MatvecSeg>& segs, cx<R>* Y, int64_t ldy, int64_t o0,
+                int64_t o1) override {
     DevOp<R>* first = mode == OP_N ? f1.get() : f2.get();
     DevOp<R>* second = mode == OP_N ? f2.get() : f1.get();
     const int64_t mid = first->out_dim(mode);
@@ -83,7 +90,7 @@ struct ComposeOp : DevOp<R> {
     first->apply_segs(mode, X, segs, t.p, mid);
     std::vector<MatvecSeg> dense;
     for (const auto& s : segs) dense.push_back(MatvecSeg{0, mid, s.col0 * mid, mid, s.col0, s.ncols, 0});
-    second->apply_segs(mode, t.p, dense, Y, ldy);
+    second->apply_segs(mode, t.p, dense, Y, ldy, o0, o1);
     this->flops += first->flops + second->flops - f0;
     this->evals += first->evals + second->evals - e0;
   }
@@ -93,7 +100,8 @@ struct ComposeOp : DevOp<R> {
 template <typename R>
 struct ButterflyOp : DevOp<R> {
   std::unique_ptr<DevButterfly<R>> bf;
-  void do_apply(int mode, const cx<R>* X, const std::vector<MatvecSeg>& segs, cx<R>* Y, int64_t ldy) override {
+  void do_apply(int mode, const cx<R>* X, const std::vector<MatvecSeg>& segs, cx<R>* Y, int64_t ldy, int64_t o0,
+                int64_t o1) override {
     int64_t wtot = 0;
     DBuf<cx<R>> xp = this->pad_probes(mode, X, segs, wtot);
     if (wtot <= 0) return;
@@ -109,7 +117,8 @@ template <typename R>
 struct CallbackOp : DevOp<R> {
   bfly_apply_fn fn = nullptr;
   void* user = nullptr;
-  void do_apply(int mode, const cx<R>* X, const std::vector<MatvecSeg>& segs, cx<R>* Y, int64_t ldy) override {
+  void do_apply(int mode, const cx<R>* X, const std::vector<MatvecSeg>& segs, cx<R>* Y, int64_t ldy, int64_t o0,
+                int64_t o1) override {
     Ctx* c = this->ctx;
     int64_t wtot = 0;
     DBuf<cx<R>> xp = this->pad_probes(mode, X, segs, wtot);

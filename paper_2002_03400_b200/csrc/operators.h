@@ -37,12 +37,16 @@ struct DevOp {
 
   // Y(:, seg cols) = op(A) X_seg for every segment; mode N, T or H (the
   // adjoint, derived exactly as apply_adjoint in the reference).
-  void apply_segs(int mode, const cx<R>* X, const std::vector<MatvecSeg>& segs, cx<R>* Y, int64_t ldy) {
+  // [o0, o1) restricts the output rows that must be produced (the rank's
+  // leaves in a sharded leaf phase); kinds that cannot restrict compute all.
+  void apply_segs(int mode, const cx<R>* X, const std::vector<MatvecSeg>& segs, cx<R>* Y, int64_t ldy,
+                  int64_t o0 = 0, int64_t o1 = -1) {
     int64_t cols = 0;
     for (const auto& s : segs) cols += s.ncols;
     if (mode == OP_N) fwd += cols;
     else tr += cols;
-    do_apply(mode, X, segs, Y, ldy);
+    if (o1 < 0) o1 = out_dim(mode);
+    do_apply(mode, X, segs, Y, ldy, o0, o1);
   }
   void apply_dense(int mode, const cx<R>* X, int64_t ldx, cx<R>* Y, int64_t ldy, int64_t k) {
     MatvecSeg s{0, in_dim(mode), 0, ldx, 0, (int32_t)k, 0};
@@ -50,7 +54,8 @@ struct DevOp {
   }
 
  protected:
-  virtual void do_apply(int mode, const cx<R>* X, const std::vector<MatvecSeg>& segs, cx<R>* Y, int64_t ldy) = 0;
+  virtual void do_apply(int mode, const cx<R>* X, const std::vector<MatvecSeg>& segs, cx<R>* Y, int64_t ldy,
+                        int64_t o0, int64_t o1) = 0;
   // materialise the padded probes (zeros outside the segment rows) as one
   // in_dim x Wtot buffer whose columns line up with Y's
   DBuf<cx<R>> pad_probes(int mode, const cx<R>* X, const std::vector<MatvecSeg>& segs, int64_t& wtot);
