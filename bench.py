@@ -12,9 +12,10 @@ evaluations are not counted as flops) / construction time.
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--impl reference]
 
-N > 1 runs under torchrun: one process per GPU, each rank factorizes its own
-replica (weak scaling; the probe-sharded single construction is a library
-feature exercised by tests/test_multirank.py).
+N > 1 runs under torchrun: one process per GPU.  Default (--mode shard): ONE
+construction whose level probes are sharded across the ranks with an NCCL
+all-gather of every level's new blocks (strong scaling).  --mode replica: every
+rank factorizes its own copy (weak scaling).
 """
 from __future__ import annotations
 
@@ -154,6 +155,11 @@ def run_ours(args):
         torch.cuda.synchronize()
 
     ctx = B.Context(local)
+    sharded = world > 1 and args.mode == "shard"
+    if sharded:
+        uid = [B.Context.unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(uid, src=0)
+        ctx.set_comm(rank, world, uid[0])
     stream = torch.cuda.ExternalStream(ctx.stream)
     w = B.configs.build(CFG_ID, args.n or None, ctx=ctx)
     op, rt, ct, rc = w.op, w.row_tree, w.col_tree, w.recon
@@ -198,7 +204,7 @@ def run_ours(args):
 
     # ----------------------------------------------- apply bandwidth (device)
     apply = {}
-    for k in (1, 16):
+    for k in ((1, 16) if rank == 0 else ()):
         x = torch.randn((k, op.cols), dtype=torch.complex128, device="cuda").t()
         y = torch.empty((k, op.rows), dtype=torch.complex128, device="cuda").t()
         for _ in range(3):
@@ -237,11 +243,12 @@ def run_ours(args):
                                                B.api.COMPLEX128, C.byref(h)))
         op_e = B.api.BlackBoxOperator(h, ctx, B.api.COMPLEX128)
         bf_e, log_e = B.factorize(op_e, rt, ct, rc)
-        blob = bf_e.serialize()  # every factor block back on the host
-        d2h = len(blob)
+        if rank == 0 or not sharded:
+            blob = bf_e.serialize()  # every factor block back on the host
+            d2h = len(blob)
     barrier()
     te = (time.perf_counter() - te0) / e2e_steps
-    e2e_val = logs[0].flops / te / 1e9
+    e2e_val = (fl.item() / args.steps) / te / 1e9  # whole-job flops of one construction
 
     # ------------------------------------------------------------ roofline
     mv = kernels.get("kernel_matvec", {"launches": 1, "ms": 1, "flops": 0, "bytes": 0})
@@ -260,13 +267,15 @@ def run_ours(args):
         line = {
             "metric": METRIC, "value": round(value, 3), "unit": "GFLOP/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": round(ms_per_step, 3), "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "complex128", "data": "synthetic",
+            "scaling": "strong" if sharded else "weak", "vs_baseline": None, "dtype": "complex128",
+            "data": "synthetic",
             "config": {"workload": "config2_helmholtz_circle_n65536", "n": w.n, "levels": rc.levels, "leaf": 32,
                        "tol": rc.tolerance, "r0": rc.rank_guess, "oversampling": rc.oversampling,
-                       "parallelism": f"replicas{world}" if world > 1 else "single",
+                       "parallelism": (f"probe-sharded x{world} (NCCL all-gather per level)" if sharded
+                                       else f"replicas{world}" if world > 1 else "single"),
                        "l2": "flushed before every step (256 MB write); probe products 0.1-1 GB > L2"},
             "construct_seconds": round(ms_per_step / 1e3, 4),
-            "flops_per_step": logs[0].flops, "kernel_evals_per_step": logs[0].kernel_evals,
+            "flops_per_step": fl.item() / args.steps, "kernel_evals_per_step": logs[0].kernel_evals,
             "max_rank": bf.max_rank(), "nnz": bf.nnz(),
             "roofline": roofline,
             "apply": apply,
@@ -297,6 +306,7 @@ def main():
     ap.add_argument("--n", type=int, default=0, help="override n (testing only)")
     ap.add_argument("--ref-probes", type=int, default=8)
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--mode", default="shard", choices=["shard", "replica"], help="N > 1 schedule")
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference(args)

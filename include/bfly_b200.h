@@ -210,6 +210,13 @@ int bfly_synth_butterfly(bfly_ctx* ctx, int levels, int64_t leaf, int64_t rank, 
 int bfly_bf_convert(bfly_bf* bf, int scalar, bfly_bf** out);
 void bfly_bf_destroy(bfly_bf* bf);
 
+/* ---------------------------------------------------------------- shard plan */
+/* How the multi-GPU construction splits a level (host logic): contiguous chunk
+ * of n units for a rank, and the block indices a rank produces (side 0 leaves,
+ * 1 W level (row probes), 2 R level (column probes)); returns the count. */
+int bfly_shard_chunk(int64_t n, int world, int rank, int64_t* begin, int64_t* end);
+int64_t bfly_shard_blocks(int levels, int level, int side, int world, int rank, int64_t* out);
+
 /* ------------------------------------------------------------- dense helpers */
 /* gaussian_matrix (linalg.hpp:16-25) generated on the device, copied to host */
 int bfly_gaussian(bfly_ctx* ctx, int64_t rows, int64_t cols, uint64_t seed, int scalar, void* out_host);

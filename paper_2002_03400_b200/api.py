@@ -495,13 +495,15 @@ class HybridButterfly(_Applicable):
         lib().bfly_rank_profile(self.h, _vp(out))
         return out.reshape(self.levels + 2, 1 << self.levels)
 
-    def serialize(self) -> bytes:
+    def serialize(self) -> bytearray:
+        """.bfh container bytes (reference format, serialize.hpp:103-127)."""
         n = lib().bfly_serialize(self.h, None)
         if n < 0:
             check(6)
-        buf = np.zeros(n, np.uint8)
-        lib().bfly_serialize(self.h, _vp(buf))
-        return buf.tobytes()
+        buf = bytearray(n)
+        if lib().bfly_serialize(self.h, (C.c_uint8 * n).from_buffer(buf)) < 0:
+            check(6)
+        return buf
 
     @staticmethod
     def deserialize(data: bytes, scalar=COMPLEX128, ctx=None) -> "HybridButterfly":

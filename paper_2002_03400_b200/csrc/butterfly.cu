@@ -791,18 +791,12 @@ int64_t DevButterfly<R>::serialize(int tag, uint8_t* out) const {
     bs.put(t->perm.data(), sizeof(int64_t) * t->perm.size());
     for (const auto& lv : t->ranges) bs.put(lv.data(), sizeof(int64_t) * lv.size());
   }
-  std::vector<cx<R>> raw;
   cx<R>* stage = nullptr;
-  size_t stage_n = 0;
   // one level: rows/gap per block given by row_split(i) -> (r1, r2)
   auto emit = [&](const Level<R>& lv, auto rows_of) {
     if (out) {
       size_t n = (size_t)(NB * lv.stride());
-      if (n > stage_n) {
-        if (stage) cudaFreeHost(stage);
-        BFLY_CUDA(cudaMallocHost(&stage, n * sizeof(cx<R>)));
-        stage_n = n;
-      }
+      stage = static_cast<cx<R>*>(lv.data.ctx->pinned(n * sizeof(cx<R>)));
       lv.data.download(stage, n);
       BFLY_CUDA(cudaStreamSynchronize(lv.data.ctx->stream));
     }
@@ -854,7 +848,6 @@ int64_t DevButterfly<R>::serialize(int tag, uint8_t* out) const {
       r2 = v_rank(l - 1, tau / 2, 2 * nu + 1);
     });
   emit(vleaf, [&](int64_t i, int64_t& r1, int64_t& r2) { r1 = ct.size(L, i); r2 = 0; });
-  if (stage) cudaFreeHost(stage);
   return bs.pos;
 }
 

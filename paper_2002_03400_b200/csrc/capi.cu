@@ -739,3 +739,22 @@ int bfly_pinv(bfly_ctx* ctx, int64_t rows, int64_t cols, const double* m_host, d
 }
 
 }  // extern "C"
+
+// ------------------------------------------------------------- shard plan
+#include "shard.h"
+extern "C" {
+int bfly_shard_chunk(int64_t n, int world, int rank, int64_t* begin, int64_t* end) {
+  if (world < 1 || rank < 0 || rank >= world || n < 0) return BFLY_PRECONDITION;
+  auto be = shard_chunk(n, world, rank);
+  *begin = be.first;
+  *end = be.second;
+  return BFLY_OK;
+}
+int64_t bfly_shard_blocks(int levels, int level, int side, int world, int rank, int64_t* out) {
+  if (world < 1 || rank < 0 || rank >= world || levels < 0 || level < 0 || level > levels || side < 0 || side > 2)
+    return -1;
+  std::vector<int64_t> v = shard_blocks(levels, level, side, world, rank);
+  if (out) std::copy(v.begin(), v.end(), out);
+  return (int64_t)v.size();
+}
+}

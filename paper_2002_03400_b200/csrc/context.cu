@@ -29,6 +29,7 @@ Ctx::~Ctx() {
     cudaStreamSynchronize(stream);
     cudaStreamDestroy(stream);
   }
+  if (pinned_p) cudaFreeHost(pinned_p);
 }
 
 void* Ctx::alloc(size_t bytes) {
@@ -40,6 +41,17 @@ void* Ctx::alloc(size_t bytes) {
 }
 
 void Ctx::release(void* p) { cudaFreeAsync(p, stream); }
+
+void* Ctx::pinned(size_t bytes) {
+  if (bytes > pinned_n) {
+    if (pinned_p) cudaFreeHost(pinned_p);
+    pinned_p = nullptr;
+    pinned_n = 0;
+    BFLY_CUDA(cudaMallocHost(&pinned_p, bytes));
+    pinned_n = bytes;
+  }
+  return pinned_p;
+}
 
 void Ctx::sync() { BFLY_CUDA(cudaStreamSynchronize(stream)); }
 

@@ -44,6 +44,10 @@ struct Ctx {
   explicit Ctx(int dev);
   ~Ctx();
   void* alloc(size_t bytes);
+  // pinned host staging buffer (grown on demand, reused across calls)
+  void* pinned(size_t bytes);
+  void* pinned_p = nullptr;
+  size_t pinned_n = 0;
   void release(void* p);
   void sync();
 };

@@ -96,6 +96,65 @@ __global__ void __launch_bounds__(256) bgemm_kernel(const cx<R>* __restrict__ A,
     }
 }
 
+// Small-k path (butterfly apply with few columns: HBM/latency bound).  One
+// 128-thread CTA per output block: op(A_s) is staged in shared memory with
+// coalesced reads for both N (down the columns) and H (along the rows of the
+// stored block), the K x k input slice next to it; each thread then owns
+// (row, column) outputs.  Every factor element is read exactly once.
+template <typename R, int OP, int S>
+__global__ void __launch_bounds__(128) bgemm_small_kernel(const cx<R>* __restrict__ A, int64_t lda,
+                                                          const cx<R>* __restrict__ B, int64_t ldb,
+                                                          cx<R>* __restrict__ C, int64_t ldc, int M, int K,
+                                                          const GemmEnt* __restrict__ ents, int accumulate,
+                                                          int ncols_all) {
+  using V = cx<R>;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  V* As = reinterpret_cast<V*>(smem_raw);  // [S][K][M+1]: op(A)(m, kk) at m + kk*(M+1)
+  const GemmEnt e = ents[blockIdx.x];
+  const int ncols = ncols_all > 0 ? ncols_all : e.ncols;
+  const int Me = min(M, e.mrows), Ke = min(K, e.krows);
+  const int SMA = M + 1;
+  V* Bs = As + S * K * SMA;                // [S][ncols][K]
+#pragma unroll
+  for (int s = 0; s < S; ++s) {
+    const V* Ab = A + (s == 0 ? e.a0 : e.a1);
+    const V* Bb = B + (s == 0 ? e.b0 : e.b1);
+    V* as = As + s * K * SMA;
+    if (OP == OP_N) {
+      for (int idx = threadIdx.x; idx < M * K; idx += 128) {
+        const int m = idx % M, kk = idx / M;
+        as[m + kk * SMA] = Ab[m + (int64_t)kk * lda];
+      }
+    } else {
+      for (int idx = threadIdx.x; idx < M * K; idx += 128) {
+        const int kk = idx % K, m = idx / K;
+        V v = Ab[kk + (int64_t)m * lda];
+        if (OP == OP_H) v = cconj(v);
+        as[m + kk * SMA] = v;
+      }
+    }
+    V* bs = Bs + s * ncols * K;
+    for (int idx = threadIdx.x; idx < K * ncols; idx += 128) {
+      const int kk = idx % K, cc = idx / K;
+      bs[kk + cc * K] = kk < Ke ? Bb[kk + (int64_t)cc * ldb] : mkc<R>(0, 0);
+    }
+  }
+  __syncthreads();
+  V* Cb = C + e.c;
+  for (int idx = threadIdx.x; idx < Me * ncols; idx += 128) {
+    const int m = idx % Me, cc = idx / Me;
+    V acc = mkc<R>(0, 0);
+#pragma unroll
+    for (int s = 0; s < S; ++s) {
+      const V* as = As + s * K * SMA + m;
+      const V* bs = Bs + s * ncols * K + cc * K;
+      for (int kk = 0; kk < K; ++kk) cfma(acc, as[kk * SMA], bs[kk]);
+    }
+    V* p = Cb + m + (int64_t)cc * ldc;
+    *p = accumulate ? cadd(*p, acc) : acc;
+  }
+}
+
 }  // namespace
 
 template <typename R>
@@ -103,6 +162,31 @@ void launch_bgemm(Ctx* c, int op, int M, int K, int S, const cx<R>* A, int64_t l
                   cx<R>* C, int64_t ldc, const GemmEnt* ents, int nent, int max_ncols, bool accumulate,
                   int ncols_all) {
   if (nent <= 0 || M <= 0 || max_ncols <= 0) return;
+  const int kcols = ncols_all > 0 ? ncols_all : max_ncols;
+  const size_t small_smem = sizeof(cx<R>) * (size_t)S * ((size_t)K * (M + 1) + (size_t)K * kcols);
+  if (kcols <= 16 && K > 0 && small_smem <= 96 * 1024 && nent <= 0x7fffffff) {
+    KTimer timer(c, "bgemm_small", 8.0 * M * K * S * (double)nent * kcols,
+                 sizeof(cx<R>) * ((double)nent * S * (M * (double)K + K * kcols) + (double)nent * M * kcols));
+#define BGS(OPV, SV)                                                                                           \
+  do {                                                                                                         \
+    auto kern = bgemm_small_kernel<R, OPV, SV>;                                                                \
+    if (small_smem > 48 * 1024)                                                                                \
+      BFLY_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)small_smem));     \
+    kern<<<nent, 128, small_smem, c->stream>>>(A, lda, B, ldb, C, ldc, M, K, ents, accumulate, ncols_all);     \
+  } while (0)
+    if (S == 1) {
+      if (op == OP_N) BGS(OP_N, 1);
+      else if (op == OP_T) BGS(OP_T, 1);
+      else BGS(OP_H, 1);
+    } else {
+      if (op == OP_N) BGS(OP_N, 2);
+      else if (op == OP_T) BGS(OP_T, 2);
+      else BGS(OP_H, 2);
+    }
+#undef BGS
+    BFLY_LAUNCH_CHECK("bgemm_small");
+    return;
+  }
   // K == 0: the product is an exact zero block
   dim3 grid(nent, (unsigned)ceil_div(max_ncols, TN), (unsigned)ceil_div(M, TM));
   if (grid.y > 65535 || grid.z > 65535) fail(PRECONDITION, "bgemm: grid too large");
