@@ -8,6 +8,7 @@
 #include <atomic>
 #include <cfloat>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <thread>
 
@@ -424,9 +425,72 @@ double DevButterfly<R>::apply_bytes(int64_t k) const {
 }
 
 template <typename R>
+int DevButterfly<R>::max_p() const {
+  int maxP = 1;
+  for (int l = 0; l <= lm; ++l) maxP = std::max(maxP, PV(l));
+  for (int l = lm; l <= L; ++l) maxP = std::max(maxP, PU(l));
+  return maxP;
+}
+
+template <typename R>
+DevButterfly<R>::~DevButterfly() {
+  for (auto& g : graphs_)
+    if (g->exec) cudaGraphExecDestroy(g->exec);
+}
+
+template <typename R>
+bool DevButterfly<R>::apply_graph(int trans, const cx<R>* x, int64_t ldx, cx<R>* y, int64_t ldy, int64_t k) {
+  static const bool disabled = std::getenv("BFLY_NO_GRAPHS") != nullptr;
+  if (disabled || ctx->profiling || trans == OP_T || !rt.identity || !ct.identity) return false;
+  GraphEntry* g = nullptr;
+  for (auto& e : graphs_)
+    if (e->trans == trans && e->x == x && e->y == y && e->ldx == ldx && e->ldy == ldy && e->k == k) g = e.get();
+  if (!g) {
+    if (graphs_.size() >= 8) {
+      if (graphs_.front()->exec) cudaGraphExecDestroy(graphs_.front()->exec);
+      graphs_.erase(graphs_.begin());
+    }
+    graphs_.push_back(std::make_unique<GraphEntry>());
+    g = graphs_.back().get();
+    g->trans = trans;
+    g->x = x;
+    g->y = y;
+    g->ldx = ldx;
+    g->ldy = ldy;
+    g->k = k;
+  }
+  if (++g->uses < 2) return false;  // first call runs eagerly (builds the stage plan)
+  if (!g->exec) {
+    const size_t nbuf = (size_t)(nb() * max_p() * k);
+    g->b0.reset(ctx, nbuf);
+    g->b1.reset(ctx, nbuf);
+    ctx->sync();
+    const int64_t l0 = ctx->launches;
+    cudaGraph_t graph;
+    BFLY_CUDA(cudaStreamBeginCapture(ctx->stream, cudaStreamCaptureModeThreadLocal));
+    try {
+      if (trans == OP_N) apply_n(x, ldx, y, ldy, k, g->b0.p, g->b1.p);
+      else apply_h(x, ldx, y, ldy, k, g->b0.p, g->b1.p);
+    } catch (...) {
+      cudaStreamEndCapture(ctx->stream, &graph);
+      throw;
+    }
+    BFLY_CUDA(cudaStreamEndCapture(ctx->stream, &graph));
+    g->kernels = ctx->launches - l0;
+    ctx->launches = l0;
+    BFLY_CUDA(cudaGraphInstantiate(&g->exec, graph, 0));
+    cudaGraphDestroy(graph);
+  }
+  BFLY_CUDA(cudaGraphLaunch(g->exec, ctx->stream));
+  ctx->launches += g->kernels;
+  return true;
+}
+
+template <typename R>
 void DevButterfly<R>::apply(int trans, const cx<R>* x, int64_t ldx, cx<R>* y, int64_t ldy, int64_t k) {
   Ctx* c = ctx;
   if (k <= 0) return;
+  if (apply_graph(trans, x, ldx, y, ldy, k)) return;
   const bool fwd = trans == OP_N;
   const Tree& tin = fwd ? ct : rt;
   const Tree& tout = fwd ? rt : ct;
@@ -467,7 +531,8 @@ GemmEnt ent(int64_t a0, int64_t a1, int64_t b0, int64_t b1, int64_t c, int mrows
 }  // namespace
 
 template <typename R>
-void DevButterfly<R>::apply_n(const cx<R>* xt, int64_t ldx, cx<R>* yt, int64_t ldy, int64_t k) {
+void DevButterfly<R>::apply_n(const cx<R>* xt, int64_t ldx, cx<R>* yt, int64_t ldy, int64_t k, cx<R>* buf0,
+                               cx<R>* buf1) {
   Ctx* c = ctx;
   const int64_t NB = nb();
   const int BIG = 1 << 30;
@@ -508,12 +573,13 @@ void DevButterfly<R>::apply_n(const cx<R>* xt, int64_t ldx, cx<R>* yt, int64_t l
     plan_n_.stages.push_back(to_device(c, e));
     have_n_ = true;
   }
-  int maxP = 1;
-  for (int l = 0; l <= lm; ++l) maxP = std::max(maxP, PV(l));
-  for (int l = lm; l <= L; ++l) maxP = std::max(maxP, PU(l));
-  DBuf<cx<R>> b0(c, (size_t)(NB * maxP * k)), b1(c, (size_t)(NB * maxP * k));
-  cx<R>* cur = b0.p;
-  cx<R>* nxt = b1.p;
+  DBuf<cx<R>> b0, b1;
+  if (!buf0) {
+    b0.reset(c, (size_t)(NB * max_p() * k));
+    b1.reset(c, (size_t)(NB * max_p() * k));
+  }
+  cx<R>* cur = buf0 ? buf0 : b0.p;
+  cx<R>* nxt = buf1 ? buf1 : b1.p;
   int st = 0;
   const int kk = (int)k;
   launch_bgemm<R>(c, OP_H, PV(0), (int)vleaf.ld, 1, vleaf.data.p, vleaf.ld, xt, ldx, cur, NB * PV(0),
@@ -538,7 +604,8 @@ void DevButterfly<R>::apply_n(const cx<R>* xt, int64_t ldx, cx<R>* yt, int64_t l
 }
 
 template <typename R>
-void DevButterfly<R>::apply_h(const cx<R>* yt, int64_t ldy, cx<R>* xt, int64_t ldx, int64_t k) {
+void DevButterfly<R>::apply_h(const cx<R>* yt, int64_t ldy, cx<R>* xt, int64_t ldx, int64_t k, cx<R>* buf0,
+                               cx<R>* buf1) {
   Ctx* c = ctx;
   const int64_t NB = nb();
   const int BIG = 1 << 30;
@@ -580,12 +647,13 @@ void DevButterfly<R>::apply_h(const cx<R>* yt, int64_t ldy, cx<R>* xt, int64_t l
     plan_h_.stages.push_back(to_device(c, e));
     have_h_ = true;
   }
-  int maxP = 1;
-  for (int l = 0; l <= lm; ++l) maxP = std::max(maxP, PV(l));
-  for (int l = lm; l <= L; ++l) maxP = std::max(maxP, PU(l));
-  DBuf<cx<R>> b0(c, (size_t)(NB * maxP * k)), b1(c, (size_t)(NB * maxP * k));
-  cx<R>* cur = b0.p;
-  cx<R>* nxt = b1.p;
+  DBuf<cx<R>> b0, b1;
+  if (!buf0) {
+    b0.reset(c, (size_t)(NB * max_p() * k));
+    b1.reset(c, (size_t)(NB * max_p() * k));
+  }
+  cx<R>* cur = buf0 ? buf0 : b0.p;
+  cx<R>* nxt = buf1 ? buf1 : b1.p;
   int st = 0;
   const int kk = (int)k;
   launch_bgemm<R>(c, OP_H, PU(L), (int)uleaf.ld, 1, uleaf.data.p, uleaf.ld, yt, ldy, cur, NB * PU(L),

@@ -125,8 +125,29 @@ struct DevButterfly {
   };
   Plan plan_n_, plan_h_;
   bool have_n_ = false, have_h_ = false;
-  void apply_n(const cx<R>* xt, int64_t ldx, cx<R>* yt, int64_t ldy, int64_t k);
-  void apply_h(const cx<R>* yt, int64_t ldy, cx<R>* xt, int64_t ldx, int64_t k);
+  // buf0/buf1: level coefficient buffers (NB*maxP*k each); null -> allocate
+  void apply_n(const cx<R>* xt, int64_t ldx, cx<R>* yt, int64_t ldy, int64_t k, cx<R>* buf0 = nullptr,
+               cx<R>* buf1 = nullptr);
+  void apply_h(const cx<R>* yt, int64_t ldy, cx<R>* xt, int64_t ldx, int64_t k, cx<R>* buf0 = nullptr,
+               cx<R>* buf1 = nullptr);
+  int max_p() const;
+  // CUDA graphs of repeated device-resident applies (same buffers, same k):
+  // the ~2L+2 dependent stage launches replay as one graph launch.
+  struct GraphEntry {
+    int trans;
+    const void* x;
+    void* y;
+    int64_t ldx, ldy, k;
+    int uses = 0;
+    int64_t kernels = 0;
+    cudaGraphExec_t exec = nullptr;
+    DBuf<cx<R>> b0, b1;
+  };
+  std::vector<std::unique_ptr<GraphEntry>> graphs_;
+  bool apply_graph(int trans, const cx<R>* x, int64_t ldx, cx<R>* y, int64_t ldy, int64_t k);
+
+ public:
+  ~DevButterfly();
 };
 
 // Builds a HostButterfly from a seeded generator (synth_butterfly,

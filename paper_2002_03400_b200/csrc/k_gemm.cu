@@ -170,8 +170,11 @@ void launch_bgemm(Ctx* c, int op, int M, int K, int S, const cx<R>* A, int64_t l
 #define BGS(OPV, SV)                                                                                           \
   do {                                                                                                         \
     auto kern = bgemm_small_kernel<R, OPV, SV>;                                                                \
-    if (small_smem > 48 * 1024)                                                                                \
-      BFLY_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)small_smem));     \
+    static size_t attr_bytes = 48 * 1024; /* set once per kernel, never during graph capture */              \
+    if (small_smem > attr_bytes) {                                                                             \
+      BFLY_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024));           \
+      attr_bytes = 96 * 1024;                                                                                  \
+    }                                                                                                          \
     kern<<<nent, 128, small_smem, c->stream>>>(A, lda, B, ldb, C, ldc, M, K, ents, accumulate, ncols_all);     \
   } while (0)
     if (S == 1) {
