@@ -266,7 +266,7 @@ __device__ __forceinline__ double dneg(double a) {
 //   Kre, Kim [BK][BM+8]   kernel tile, k-major: A fragments conflict free
 //   Xre, Xim [BN][BK+4]   probe tile, column-major: B fragments conflict free
 //   P[3][BK]              input points of the tile
-template <int KIND, int MODE, int MT, int NT, int BK, int MINB>
+template <int KIND, int MODE, int MT, int NT, int BK, int MINB, bool G3>
 __global__ void __launch_bounds__(256, MINB) matvec_dmma_kernel(Points outp, Points inp, double kappa, int64_t m_out,
                                                              const double2* __restrict__ X, double2* __restrict__ Y,
                                                              int64_t ldy, const MatvecItem* __restrict__ items,
@@ -274,10 +274,14 @@ __global__ void __launch_bounds__(256, MINB) matvec_dmma_kernel(Points outp, Poi
   constexpr int BM = 64 * MT, BN = 8 * NT, SM = BM + 8, SX = BK + 4;
   constexpr int XPT = (BK * BN + 255) / 256;  // probe-tile elements per thread
   extern __shared__ __align__(16) double sm_d[];
+  // G3: Gauss's 3-multiplication complex product (P1 = a c, P2 = b d,
+  // P3 = (a+b)(c+d); re = P1 - P2, im = P3 - P1 - P2): a third "sum" plane
+  constexpr int NPL = G3 ? 3 : 2;
   double* Kre = sm_d;
   double* Kim = Kre + BK * SM;
-  double* Xb = Kim + BK * SM;  // 2 buffers x [re|im] x BN x SX
-  double* Pb = Xb + 4 * BN * SX;  // 2 buffers x [3][BK]
+  double* Ksu = Kim + BK * SM;  // G3 only
+  double* Xb = Kre + NPL * BK * SM;  // 2 buffers x NPL planes x BN x SX
+  double* Pb = Xb + 2 * NPL * BN * SX;  // 2 buffers x [3][BK]
 
   const MatvecItem it = items[blockIdx.y];
   const int64_t i0 = (int64_t)blockIdx.x * BM;
@@ -324,8 +328,9 @@ __global__ void __launch_bounds__(256, MINB) matvec_dmma_kernel(Points outp, Poi
     }
   };
   auto commit = [&](int buf) {
-    double* xre = Xb + buf * 2 * BN * SX;
+    double* xre = Xb + buf * NPL * BN * SX;
     double* xim = xre + BN * SX;
+    double* xsu = xim + BN * SX;
 #pragma unroll
     for (int q = 0; q < XPT; ++q) {
       const int idx = tid + 256 * q;
@@ -333,6 +338,7 @@ __global__ void __launch_bounds__(256, MINB) matvec_dmma_kernel(Points outp, Poi
         const int kk = idx % BK, cc = idx / BK;
         xre[cc * SX + kk] = xr[q].x;
         xim[cc * SX + kk] = xr[q].y;
+        if (G3) xsu[cc * SX + kk] = xr[q].x + xr[q].y;
       }
     }
     if (tid < BK) {
@@ -343,11 +349,13 @@ __global__ void __launch_bounds__(256, MINB) matvec_dmma_kernel(Points outp, Poi
     }
   };
 
-  double acc[MT][NT][2][2];  // [re|im][2 values]
+  double acc[MT][NT][NPL][2];  // [re|im] or [P1|P2|P3], 2 values
 #pragma unroll
   for (int a = 0; a < MT; ++a)
 #pragma unroll
-    for (int b = 0; b < NT; ++b) acc[a][b][0][0] = acc[a][b][0][1] = acc[a][b][1][0] = acc[a][b][1][1] = 0.0;
+    for (int b = 0; b < NT; ++b)
+#pragma unroll
+      for (int p = 0; p < NPL; ++p) acc[a][b][p][0] = acc[a][b][p][1] = 0.0;
 
   if (kb < ke) {
     fetch(kb);
@@ -371,45 +379,60 @@ __global__ void __launch_bounds__(256, MINB) matvec_dmma_kernel(Points outp, Poi
         }
         Kre[kk * SM + erow + q * EROWS] = v.x;
         Kim[kk * SM + erow + q * EROWS] = v.y;
+        if (G3) Ksu[kk * SM + erow + q * EROWS] = v.x + v.y;
       }
     }
     __syncthreads();
     const bool more = k0 + BK < ke;
     if (more) fetch(k0 + BK);  // global loads in flight during the MMAs
     // ---- complex contraction on DMMA: 4 real m8n8k4 per complex tile
-    const double* xre = Xb + buf * 2 * BN * SX;
+    const double* xre = Xb + buf * NPL * BN * SX;
     const double* xim = xre + BN * SX;
+    const double* xsu = xim + BN * SX;
 #pragma unroll
     for (int ks = 0; ks < BK; ks += 4) {
-      double ar[MT], ai[MT], br[NT], bi[NT];
+      double ar[MT], ai[MT], br[NT], bi[NT], as_[MT], bs_[NT];
 #pragma unroll
       for (int a = 0; a < MT; ++a) {
         const int row = warp * 8 * MT + a * 8 + g;
         ar[a] = Kre[(ks + t) * SM + row];
         ai[a] = Kim[(ks + t) * SM + row];
+        if (G3) as_[a] = Ksu[(ks + t) * SM + row];
       }
 #pragma unroll
       for (int b = 0; b < NT; ++b) {
         const int col = b * 8 + g;
         br[b] = xre[col * SX + ks + t];
         bi[b] = xim[col * SX + ks + t];
+        if (G3) bs_[b] = xsu[col * SX + ks + t];
       }
-      // two passes over the MT x NT tiles: a dependent MMA pair is 2*MT*NT
-      // instructions apart (no fixed-latency waits between them)
+      if constexpr (G3) {
 #pragma unroll
-      for (int a = 0; a < MT; ++a)
+        for (int a = 0; a < MT; ++a)
 #pragma unroll
-        for (int b = 0; b < NT; ++b) {
-          dmma(acc[a][b][0][0], acc[a][b][0][1], ar[a], br[b]);
-          dmma(acc[a][b][1][0], acc[a][b][1][1], ar[a], bi[b]);
-        }
+          for (int b = 0; b < NT; ++b) {
+            dmma(acc[a][b][0][0], acc[a][b][0][1], ar[a], br[b]);
+            dmma(acc[a][b][1][0], acc[a][b][1][1], ai[a], bi[b]);
+            dmma(acc[a][b][2][0], acc[a][b][2][1], as_[a], bs_[b]);
+          }
+      } else {
+        // two passes over the MT x NT tiles: a dependent MMA pair is 2*MT*NT
+        // instructions apart (no fixed-latency waits between them)
 #pragma unroll
-      for (int a = 0; a < MT; ++a) {
-        const double nai = dneg(ai[a]);
+        for (int a = 0; a < MT; ++a)
 #pragma unroll
-        for (int b = 0; b < NT; ++b) {
-          dmma(acc[a][b][0][0], acc[a][b][0][1], nai, bi[b]);
-          dmma(acc[a][b][1][0], acc[a][b][1][1], ai[a], br[b]);
+          for (int b = 0; b < NT; ++b) {
+            dmma(acc[a][b][0][0], acc[a][b][0][1], ar[a], br[b]);
+            dmma(acc[a][b][1][0], acc[a][b][1][1], ar[a], bi[b]);
+          }
+#pragma unroll
+        for (int a = 0; a < MT; ++a) {
+          const double nai = dneg(ai[a]);
+#pragma unroll
+          for (int b = 0; b < NT; ++b) {
+            dmma(acc[a][b][0][0], acc[a][b][0][1], nai, bi[b]);
+            dmma(acc[a][b][1][0], acc[a][b][1][1], ai[a], br[b]);
+          }
         }
       }
     }
@@ -427,7 +450,13 @@ __global__ void __launch_bounds__(256, MINB) matvec_dmma_kernel(Points outp, Poi
 #pragma unroll
       for (int v = 0; v < 2; ++v) {
         const int cc = b * 8 + 2 * t + v;
-        if (cc < it.ncols) Yb[gi + (it.ycol + cc) * ldy] = make_double2(acc[a][b][0][v], acc[a][b][1][v]);
+        if (cc >= it.ncols) continue;
+        if constexpr (G3) {
+          const double p1 = acc[a][b][0][v], p2 = acc[a][b][1][v], p3 = acc[a][b][NPL - 1][v];
+          Yb[gi + (it.ycol + cc) * ldy] = make_double2(p1 - p2, p3 - p1 - p2);
+        } else {
+          Yb[gi + (it.ycol + cc) * ldy] = make_double2(acc[a][b][0][v], acc[a][b][1][v]);
+        }
       }
   }
 }
@@ -503,8 +532,11 @@ void run_cfg(Ctx* c, Points outp, Points inp, double kappa, int64_t m_out, const
   KernFn kern;
   if constexpr (DM) {
     static_assert(BM == 64 * MT && BN == 8 * NT, "dmma tile");
-    smem = sizeof(double) * (size_t)(2 * BK * (BM + 8) + 4 * BN * (BK + 4) + 6 * BK);
-    kern = matvec_dmma_kernel<KIND, MODE, MT, NT, BK, (MT * NT <= 8 ? 2 : 1)>;
+    static const bool g3 = !std::getenv("BFLY_MV_4M");  // Gauss 3M unless disabled
+    const int npl = g3 ? 3 : 2;
+    smem = sizeof(double) * (size_t)(npl * BK * (BM + 8) + 2 * npl * BN * (BK + 4) + 6 * BK);
+    if (g3) kern = matvec_dmma_kernel<KIND, MODE, MT, NT, BK, (MT * NT <= 8 ? 2 : 1), true>;
+    else kern = matvec_dmma_kernel<KIND, MODE, MT, NT, BK, (MT * NT <= 8 ? 2 : 1), false>;
   } else {
     smem = sizeof(cx<R>) * (size_t)BK * (BM + BN);
     kern = matvec_kernel<R, KIND, MODE, BM, BN, TM, TN, BK>;
