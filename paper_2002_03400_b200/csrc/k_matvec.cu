@@ -532,7 +532,10 @@ void run_cfg(Ctx* c, Points outp, Points inp, double kappa, int64_t m_out, const
   KernFn kern;
   if constexpr (DM) {
     static_assert(BM == 64 * MT && BN == 8 * NT, "dmma tile");
-    static const bool g3 = !std::getenv("BFLY_MV_4M");  // Gauss 3M unless disabled
+    // Gauss 3M for the wide tiles (transfer levels: -5%); the narrow leaf-round
+    // tiles keep 4M (3M adds register pressure there)
+    static const bool g3_env = !std::getenv("BFLY_MV_4M");
+    const bool g3 = g3_env && NT >= 4;
     const int npl = g3 ? 3 : 2;
     smem = sizeof(double) * (size_t)(npl * BK * (BM + 8) + 2 * npl * BN * (BK + 4) + 6 * BK);
     if (g3) kern = matvec_dmma_kernel<KIND, MODE, MT, NT, BK, (MT * NT <= 8 ? 2 : 1), true>;

@@ -284,3 +284,19 @@ def test_virtual_ranks_match_single_gpu(B, cfg_id, n, vr):
         if pa.name.startswith("transfer"):
             assert (pa.forward_columns, pa.transpose_columns) == (pb.forward_columns, pb.transpose_columns)
         assert pa.rounds == pb.rounds and pa.probe_width == pb.probe_width
+
+
+def test_complex64_recompression_vs_complex128_oracle(B, oracle_threads):
+    """Config 4 at complex64 (B200-only variant; the reference has no complex64,
+    core.hpp:29-39): checked against the complex128 oracle at 1e-4."""
+    n = 4096
+    w = B.configs.build(4, n, scalar=B.COMPLEX64)
+    bf, log = B.factorize(w.op, w.row_tree, w.col_tree, w.recon)
+    op_o, rt_o, ct_o, cfg = oracle_config(4, n)
+    bf_o, _ = O.factorize(op_o, rt_o, ct_o, dict(cfg, threads=oracle_threads))
+    x = O.gaussian_matrix(n, 16, O.seed_mix(5, 5))
+    y_o = bf_o.apply(x)
+    y_g = bf.apply(x.astype(np.complex64)).astype(np.complex128)
+    assert rel_err(y_g, y_o) < 1e-4
+    assert B.estimate_error(w.op, bf, 16, 1) < 1e-4
+    assert bf.max_rank() <= 64
