@@ -42,33 +42,43 @@ def _env_rank():
 
 # ------------------------------------------------------------ CPU baseline
 def cpu_sample(n=65536, probes=8, width=32, threads=None):
-    """Bounded sample of the same workload on the CPU oracle: the adjoint
-    black-box products of `probes` level-5 row probes (|T_tau| = n/32 rows,
-    `width` columns) over all n output points -- the operation that carries
-    >90% of the construction's flops -- through the oracle's operator."""
+    """Bounded sample of the same workload on the CPU: the adjoint black-box
+    products of `probes` level-5 row probes (|T_tau| = n/32 rows, `width`
+    columns, all n output points) -- the operation that carries >90% of the
+    construction's flops.  Runs the REFERENCE code path (oracle/_ref:
+    reference headers compiled unmodified against the Eigen-API shim;
+    probe_with -> apply_adjoint -> conj(apply_transpose(conj))) when it was
+    built, else the C oracle port of the same path."""
     sys.path.insert(0, os.path.join(ROOT, "oracle"))
-    import numpy as np
-
-    import oracle as O
-
     sys.path.insert(0, os.path.join(ROOT, "tests"))
-    from helpers import oracle_config
+    import oracle as O
+    import refpy as RP
+    from helpers import _half_circle, _tree_order, oracle_config
 
     threads = threads or os.cpu_count() or 1
-    O.set_threads(threads)
-    op, rt, ct, cfg = oracle_config(CFG_ID, n)
     level = 5
-    t0 = time.perf_counter()
-    flops = 0.0
-    for tau in range(probes):
-        b, e = rt.node_range(level, tau)
-        core = O.gaussian_matrix(e - b, width, O.seed_mix(0, 3, level, tau))
-        O.probe_with(op, rt, level, tau, core, forward=False)
-        flops += 8.0 * n * (e - b) * width
-    dt = time.perf_counter() - t0
-    return flops / dt / 1e9, dt, threads, (
+    flops = 8.0 * n * (n >> level) * width * probes
+    if RP.available():
+        RP.lib().ref_set_threads(threads)
+        L = O.depth_for(n, 32)
+        t, _ = _tree_order(_half_circle(n, True), L, 2)
+        s, _ = _tree_order(_half_circle(n, False), L, 2)
+        op = RP.kernel_op(3, t, s, 2.0 * n / 10.0, 2, L)
+        dt = RP.lib().ref_probe_sample(op.h, level, probes, width, 0)
+        kind, what = "reference", "reference probe_with (oracle/_ref)"
+    else:
+        O.set_threads(threads)
+        op, rt, ct, cfg = oracle_config(CFG_ID, n)
+        t0 = time.perf_counter()
+        for tau in range(probes):
+            b, e = rt.node_range(level, tau)
+            core = O.gaussian_matrix(e - b, width, O.seed_mix(0, 3, level, tau))
+            O.probe_with(op, rt, level, tau, core, forward=False)
+        dt = time.perf_counter() - t0
+        kind, what = "port", "C oracle port"
+    return flops / dt / 1e9, dt, threads, kind, (
         f"adjoint black-box products of {probes} W-level-{level} row probes of config 2 "
-        f"(n={n}, {n // 32} rows x {width} cols each) through the oracle operator, {threads} threads")
+        f"(n={n}, {n >> level} rows x {width} cols each) via the {what}, {threads} threads")
 
 
 def run_reference(args):
@@ -77,7 +87,7 @@ def run_reference(args):
         return 0
     vals = []
     for i in range(args.warmup + args.steps):
-        v, dt, threads, sample = cpu_sample(probes=args.ref_probes)
+        v, dt, threads, kind, sample = cpu_sample(probes=args.ref_probes)
         if i >= args.warmup:
             vals.append((v, dt))
     value = statistics.median(v for v, _ in vals)
@@ -87,7 +97,7 @@ def run_reference(args):
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms, 3), "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "complex128", "data": "synthetic",
         "config": {"workload": "config2_helmholtz_circle_n65536", "n": 65536, "sample": sample},
-        "cpu_baseline": {"value": round(value, 3), "unit": "GFLOP/s", "cores": threads, "kind": "port",
+        "cpu_baseline": {"value": round(value, 3), "unit": "GFLOP/s", "cores": threads, "kind": kind,
                          "sample": sample},
         "e2e": {"value": round(value, 3), "unit": "GFLOP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
@@ -287,8 +297,8 @@ def run_ours(args):
             "clocks": clk,
         }
         if world == 1 and not args.no_cpu:
-            v, dt, threads, sample = cpu_sample(probes=args.ref_probes)
-            line["cpu_baseline"] = {"value": round(v, 3), "unit": "GFLOP/s", "cores": threads, "kind": "port",
+            v, dt, threads, kind, sample = cpu_sample(probes=args.ref_probes)
+            line["cpu_baseline"] = {"value": round(v, 3), "unit": "GFLOP/s", "cores": threads, "kind": kind,
                                     "sample": sample, "seconds": round(dt, 2)}
         print(json.dumps(line), flush=True)
     if dist is not None:

@@ -300,3 +300,27 @@ def test_complex64_recompression_vs_complex128_oracle(B, oracle_threads):
     assert rel_err(y_g, y_o) < 1e-4
     assert B.estimate_error(w.op, bf, 16, 1) < 1e-4
     assert bf.max_rank() <= 64
+
+
+@pytest.mark.parametrize("cfg_id,n", [(0, 4096), (2, 4096), (4, 4096)])
+def test_gpu_matches_reference_implementation(B, oracle_threads, cfg_id, n):
+    """Directly against the reference implementation (oracle/_ref: the
+    reference's own headers compiled against the Eigen-API shim)."""
+    import refpy as R
+
+    if not R.available():
+        pytest.skip("oracle/_ref not built")
+    from test_ref_pin import _ref_config
+
+    R.lib().ref_set_threads(oracle_threads)
+    op_r, L, tol, r0 = _ref_config(cfg_id, n)
+    bf_r = R.factorize(op_r, tol, r0, L, seed=0, threads=oracle_threads)
+    w = B.configs.build(cfg_id, n)
+    bf_g, log_g = B.factorize(w.op, w.row_tree, w.col_tree, w.recon)
+    np.testing.assert_array_equal(bf_g.rank_profile(), bf_r.rank_profile(L))
+    phases_r, _ = bf_r.log()
+    assert [(p.forward_columns, p.transpose_columns, p.rounds, p.probe_width) for p in log_g.phases] == phases_r
+    x = O.gaussian_matrix(n, 16, O.seed_mix(9, 5))
+    y = O.gaussian_matrix(n, 16, O.seed_mix(9, 6))
+    assert rel_err(bf_g.apply(x), bf_r.apply(x, 0)) < APPLY_TOL
+    assert rel_err(bf_g.apply_adjoint(y), bf_r.apply(y, 2)) < APPLY_TOL
