@@ -324,3 +324,20 @@ def test_gpu_matches_reference_implementation(B, oracle_threads, cfg_id, n):
     y = O.gaussian_matrix(n, 16, O.seed_mix(9, 6))
     assert rel_err(bf_g.apply(x), bf_r.apply(x, 0)) < APPLY_TOL
     assert rel_err(bf_g.apply_adjoint(y), bf_r.apply(y, 2)) < APPLY_TOL
+
+
+def test_cpp_adapter_drop_in():
+    """include/bfly_b200.hpp: the reference's own operators (synthetic real /
+    complex, Helmholtz3D hemispheres) factorized on the GPU through the C-ABI
+    callback from a C++ program built against the reference headers; ranks,
+    bookkeeping and apply outputs equal the reference's CPU factorize()."""
+    import os
+    import subprocess
+
+    exe = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "oracle", "_ref", "adapter_demo")
+    if not os.path.exists(exe):
+        pytest.skip("adapter demo not built (needs /root/reference at build time)")
+    r = subprocess.run([exe], capture_output=True, text=True, timeout=600)
+    print(r.stdout)
+    assert r.returncode == 0, r.stdout + r.stderr
+    assert "ADAPTER PARITY OK" in r.stdout
