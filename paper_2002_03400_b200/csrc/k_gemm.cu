@@ -4,6 +4,9 @@
 // Every output block is C_e = sum_{s<S} op(A_s) B_s with uniform padded
 // shapes per launch (zero padding contributes exact zeros).  One CTA computes
 // a 32 x 32 tile of one block; A and B tiles are staged through shared memory.
+#include <cstdlib>
+#include <type_traits>
+
 #include "kernels.cuh"
 
 namespace bfly {
@@ -155,6 +158,128 @@ __global__ void __launch_bounds__(128) bgemm_small_kernel(const cx<R>* __restric
   }
 }
 
+// Large-k complex128 path on DMMA (mma.sync m8n8k4 f64): one CTA = 8 warps
+// (4 along rows x 2 along columns) computes all M <= 64 rows of one output
+// block for a 64-column slab; op(A_s) and B_s chunks of 16 along K are staged
+// in shared memory (A k-major planes, stride 8*MT*4+8; B column-major planes,
+// stride 20 -> conflict-free fragments).  Complex MAC = 4 real DMMAs.
+__device__ __forceinline__ void dmma884(double& d0, double& d1, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+               : "+d"(d0), "+d"(d1)
+               : "d"(a), "d"(b));
+}
+
+template <int OP, int S, int MT>
+__global__ void __launch_bounds__(256) bgemm_dmma_kernel(const double2* __restrict__ A, int64_t lda,
+                                                         const double2* __restrict__ B, int64_t ldb,
+                                                         double2* __restrict__ C, int64_t ldc, int M, int K,
+                                                         const GemmEnt* __restrict__ ents, int accumulate,
+                                                         int ncols_all) {
+  constexpr int BM = 32 * MT, BN = 64, BK = 16, SA = BM + 8, SB = BK + 4, NT = 4;
+  __shared__ __align__(16) double Are[BK * SA], Aim[BK * SA], Bre[BN * SB], Bim[BN * SB];
+  const GemmEnt e = ents[blockIdx.x];
+  const int ncols = ncols_all > 0 ? ncols_all : e.ncols;
+  const int Me = min(M, e.mrows), Ke = min(K, e.krows);
+  const int n0 = blockIdx.y * BN;
+  if (n0 >= ncols) return;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int g = lane >> 2, t = lane & 3;
+  const int wm = warp & 3, wn = warp >> 2;  // 4 x 2 warps
+  double acc[MT][NT][2][2];
+#pragma unroll
+  for (int a = 0; a < MT; ++a)
+#pragma unroll
+    for (int b = 0; b < NT; ++b) acc[a][b][0][0] = acc[a][b][0][1] = acc[a][b][1][0] = acc[a][b][1][1] = 0.0;
+#pragma unroll
+  for (int s = 0; s < S; ++s) {
+    const double2* Ab = A + (s == 0 ? e.a0 : e.a1);
+    const double2* Bb = B + (s == 0 ? e.b0 : e.b1);
+    for (int k0 = 0; k0 < K; k0 += BK) {
+      // op(A) chunk: rows m < BM, k in [k0, k0+BK)
+      for (int idx = tid; idx < BM * BK; idx += 256) {
+        int m, kk;
+        if (OP == OP_N) {
+          m = idx % BM;
+          kk = idx / BM;
+        } else {
+          kk = idx % BK;
+          m = idx / BK;
+        }
+        double2 v = make_double2(0.0, 0.0);
+        const int gk = k0 + kk;
+        if (m < M && gk < K) {
+          if (OP == OP_N) v = Ab[m + (int64_t)gk * lda];
+          else {
+            v = Ab[gk + (int64_t)m * lda];
+            if (OP == OP_H) v.y = -v.y;
+          }
+        }
+        Are[kk * SA + m] = v.x;
+        Aim[kk * SA + m] = v.y;
+      }
+      for (int idx = tid; idx < BK * BN; idx += 256) {
+        const int kk = idx % BK, cc = idx / BK;
+        const int gk = k0 + kk, gc = n0 + cc;
+        double2 v = make_double2(0.0, 0.0);
+        if (gk < Ke && gc < ncols) v = Bb[gk + (int64_t)gc * ldb];
+        Bre[cc * SB + kk] = v.x;
+        Bim[cc * SB + kk] = v.y;
+      }
+      __syncthreads();
+#pragma unroll
+      for (int ks = 0; ks < BK; ks += 4) {
+        double ar[MT], ai[MT], br[NT], bi[NT];
+#pragma unroll
+        for (int a = 0; a < MT; ++a) {
+          const int row = wm * 8 * MT + a * 8 + g;
+          ar[a] = Are[(ks + t) * SA + row];
+          ai[a] = Aim[(ks + t) * SA + row];
+        }
+#pragma unroll
+        for (int b = 0; b < NT; ++b) {
+          const int col = wn * 32 + b * 8 + g;
+          br[b] = Bre[col * SB + ks + t];
+          bi[b] = Bim[col * SB + ks + t];
+        }
+#pragma unroll
+        for (int a = 0; a < MT; ++a)
+#pragma unroll
+          for (int b = 0; b < NT; ++b) {
+            dmma884(acc[a][b][0][0], acc[a][b][0][1], ar[a], br[b]);
+            dmma884(acc[a][b][1][0], acc[a][b][1][1], ar[a], bi[b]);
+          }
+#pragma unroll
+        for (int a = 0; a < MT; ++a) {
+          const double nai = -ai[a];
+#pragma unroll
+          for (int b = 0; b < NT; ++b) {
+            dmma884(acc[a][b][0][0], acc[a][b][0][1], nai, bi[b]);
+            dmma884(acc[a][b][1][0], acc[a][b][1][1], ai[a], br[b]);
+          }
+        }
+      }
+      __syncthreads();
+    }
+  }
+  double2* Cb = C + e.c;
+#pragma unroll
+  for (int a = 0; a < MT; ++a) {
+    const int m = wm * 8 * MT + a * 8 + g;
+    if (m >= Me) continue;
+#pragma unroll
+    for (int b = 0; b < NT; ++b)
+#pragma unroll
+      for (int v = 0; v < 2; ++v) {
+        const int gc = n0 + wn * 32 + b * 8 + 2 * t + v;
+        if (gc >= ncols) continue;
+        double2* p = Cb + m + (int64_t)gc * ldc;
+        double2 r = make_double2(acc[a][b][0][v], acc[a][b][1][v]);
+        if (accumulate) r = make_double2(p->x + r.x, p->y + r.y);
+        *p = r;
+      }
+  }
+}
+
 }  // namespace
 
 template <typename R>
@@ -189,6 +314,36 @@ void launch_bgemm(Ctx* c, int op, int M, int K, int S, const cx<R>* A, int64_t l
 #undef BGS
     BFLY_LAUNCH_CHECK("bgemm_small");
     return;
+  }
+  if constexpr (std::is_same<R, double>::value) {
+    static const bool no_dmma = std::getenv("BFLY_NO_DMMA_GEMM") != nullptr;
+    if (!no_dmma && kcols > 16 && M <= 64 && K > 0) {
+      const unsigned gy = (unsigned)ceil_div(max_ncols, 64);
+      if (gy > 65535) fail(PRECONDITION, "bgemm: grid too large");
+      dim3 grid(nent, gy);
+      KTimer timer(c, "bgemm_dmma", 8.0 * M * K * S * (double)nent * kcols,
+                   sizeof(cx<R>) * ((double)nent * S * (M * (double)K + K * kcols) + (double)nent * M * kcols));
+#define BD(OPV, SV, MTV)                                                                                  \
+  bgemm_dmma_kernel<OPV, SV, MTV><<<grid, 256, 0, c->stream>>>(A, lda, B, ldb, C, ldc, M, K, ents, accumulate, \
+                                                                 ncols_all)
+#define BD_OP(SV, MTV)                   \
+  do {                                   \
+    if (op == OP_N) BD(OP_N, SV, MTV);   \
+    else if (op == OP_T) BD(OP_T, SV, MTV); \
+    else BD(OP_H, SV, MTV);              \
+  } while (0)
+      if (M <= 32) {
+        if (S == 1) BD_OP(1, 1);
+        else BD_OP(2, 1);
+      } else {
+        if (S == 1) BD_OP(1, 2);
+        else BD_OP(2, 2);
+      }
+#undef BD_OP
+#undef BD
+      BFLY_LAUNCH_CHECK("bgemm_dmma");
+      return;
+    }
   }
   // K == 0: the product is an exact zero block
   dim3 grid(nent, (unsigned)ceil_div(max_ncols, TN), (unsigned)ceil_div(M, TM));
