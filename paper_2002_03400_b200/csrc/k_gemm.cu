@@ -321,7 +321,10 @@ void launch_bgemm(Ctx* c, int op, int M, int K, int S, const cx<R>* A, int64_t l
       const unsigned gy = (unsigned)ceil_div(max_ncols, 64);
       if (gy > 65535) fail(PRECONDITION, "bgemm: grid too large");
       dim3 grid(nent, gy);
-      KTimer timer(c, "bgemm_dmma", 8.0 * M * K * S * (double)nent * kcols,
+      static const char* names[3][2][2] = {{{"bgemm_dmma_N1_m32", "bgemm_dmma_N1_m64"}, {"bgemm_dmma_N2_m32", "bgemm_dmma_N2_m64"}},
+                                           {{"bgemm_dmma_T1_m32", "bgemm_dmma_T1_m64"}, {"bgemm_dmma_T2_m32", "bgemm_dmma_T2_m64"}},
+                                           {{"bgemm_dmma_H1_m32", "bgemm_dmma_H1_m64"}, {"bgemm_dmma_H2_m32", "bgemm_dmma_H2_m64"}}};
+      KTimer timer(c, names[op][S - 1][M > 32], 8.0 * M * K * S * (double)nent * kcols,
                    sizeof(cx<R>) * ((double)nent * S * (M * (double)K + K * kcols) + (double)nent * M * kcols));
 #define BD(OPV, SV, MTV)                                                                                  \
   bgemm_dmma_kernel<OPV, SV, MTV><<<grid, 256, 0, c->stream>>>(A, lda, B, ldb, C, ldc, M, K, ents, accumulate, \
