@@ -16,6 +16,12 @@
 
 #include <stdint.h>
 
+#if defined(__GNUC__)
+#define BFLY_API __attribute__((visibility("default")))
+#else
+#define BFLY_API
+#endif
+
 #ifdef __cplusplus
 extern "C" {
 #endif
@@ -47,47 +53,47 @@ typedef struct bfly_op bfly_op;
 typedef struct bfly_bf bfly_bf;
 typedef struct bfly_factorizer bfly_factorizer;
 
-const char* bfly_last_error(void);
-const char* bfly_version(void);
+BFLY_API const char* bfly_last_error(void);
+BFLY_API const char* bfly_version(void);
 
 /* ---------------------------------------------------------------- context */
 /* One context per GPU/process: streams, memory pool, counters.
  * (reference: none -- it is single-process CPU code) */
-int bfly_ctx_create(int device, bfly_ctx** out);
-int bfly_ctx_destroy(bfly_ctx* ctx);
+BFLY_API int bfly_ctx_create(int device, bfly_ctx** out);
+BFLY_API int bfly_ctx_destroy(bfly_ctx* ctx);
 /* kernels launched by the library on this context since creation */
-int64_t bfly_ctx_launches(const bfly_ctx* ctx);
-int bfly_ctx_synchronize(bfly_ctx* ctx);
+BFLY_API int64_t bfly_ctx_launches(const bfly_ctx* ctx);
+BFLY_API int bfly_ctx_synchronize(bfly_ctx* ctx);
 /* raw stream handle (cudaStream_t) the library launches on */
-void* bfly_ctx_stream(bfly_ctx* ctx);
+BFLY_API void* bfly_ctx_stream(bfly_ctx* ctx);
 /* per-kernel device timing with CUDA events on the library stream:
  * enable = 1 on, 0 off, -1 off and clear.  The report is a JSON object
  * {kernel: {launches, ms, flops, bytes}}; returns the length needed. */
-int bfly_ctx_profile(bfly_ctx* ctx, int enable);
-int64_t bfly_ctx_profile_report(bfly_ctx* ctx, char* buf, int64_t len);
+BFLY_API int bfly_ctx_profile(bfly_ctx* ctx, int enable);
+BFLY_API int64_t bfly_ctx_profile_report(bfly_ctx* ctx, char* buf, int64_t len);
 /* Multi-GPU: join an NCCL communicator (ncclUniqueId bytes from rank 0).
  * Probes and butterfly blocks are sharded across ranks; each level's new
  * blocks are all-gathered. */
-int bfly_comm_unique_id(uint8_t* id_out /* 128 bytes */);
-int bfly_ctx_set_comm(bfly_ctx* ctx, int rank, int world, const uint8_t* nccl_id);
+BFLY_API int bfly_comm_unique_id(uint8_t* id_out /* 128 bytes */);
+BFLY_API int bfly_ctx_set_comm(bfly_ctx* ctx, int rank, int world, const uint8_t* nccl_id);
 
 /* ------------------------------------------------------------------- trees */
 /* PartitionTree::build (tree.hpp:75-101); coords n x 3 row-major */
-int bfly_tree_build(int dim, int64_t n, const double* coords, int levels, bfly_tree** out);
+BFLY_API int bfly_tree_build(int dim, int64_t n, const double* coords, int levels, bfly_tree** out);
 /* PartitionTree::set_permutation (tree.hpp:153-159) with the serialized table
  * layout (serialize.hpp:64-71): perm[n], ranges = concat_l (2^l + 1 entries) */
-int bfly_tree_from_table(int64_t n, int levels, const int64_t* perm, const int64_t* ranges, bfly_tree** out);
-int bfly_tree_info(const bfly_tree* t, int64_t* n, int* levels);
-int bfly_tree_table(const bfly_tree* t, int64_t* perm, int64_t* ranges);
-void bfly_tree_destroy(bfly_tree* t);
+BFLY_API int bfly_tree_from_table(int64_t n, int levels, const int64_t* perm, const int64_t* ranges, bfly_tree** out);
+BFLY_API int bfly_tree_info(const bfly_tree* t, int64_t* n, int* levels);
+BFLY_API int bfly_tree_table(const bfly_tree* t, int64_t* perm, int64_t* ranges);
+BFLY_API void bfly_tree_destroy(bfly_tree* t);
 /* PartitionTree::depth_for (tree.hpp:163-168) */
-int bfly_depth_for(int64_t n, int64_t leaf_cap);
+BFLY_API int bfly_depth_for(int64_t n, int64_t leaf_cap);
 
 /* ------------------------------------------------------- point generators */
 /* Seeded point sets of the BASELINE configs (host). */
-void bfly_points_uniform(int64_t n, uint64_t seed, uint64_t tag, double lo, double hi, double* out);
-void bfly_points_plate(int64_t side, double z, double* out);
-void bfly_points_half_circle(int64_t n, int upper, double* out);
+BFLY_API void bfly_points_uniform(int64_t n, uint64_t seed, uint64_t tag, double lo, double hi, double* out);
+BFLY_API void bfly_points_plate(int64_t side, double z, double* out);
+BFLY_API void bfly_points_half_circle(int64_t n, int upper, double* out);
 
 /* --------------------------------------------------------------- operators */
 /* BlackBoxOperator<Scalar> (operators.hpp:17-56).  Built-in kinds evaluate
@@ -111,25 +117,25 @@ typedef int (*bfly_apply_fn)(void* user, int trans, const void* x_dev, int64_t l
                              int64_t ldy, int64_t k, void* stream);
 
 /* tgt (m x 3) and src (n x 3) row-major host points, already in tree order */
-int bfly_op_kernel(bfly_ctx* ctx, int kind, int64_t m, int64_t n, const double* tgt, const double* src,
+BFLY_API int bfly_op_kernel(bfly_ctx* ctx, int kind, int64_t m, int64_t n, const double* tgt, const double* src,
                    double wavenumber, int scalar, bfly_op** out);
 /* A = f2 * f1; takes ownership of both factors */
-int bfly_op_compose(bfly_ctx* ctx, bfly_op* f2, bfly_op* f1, bfly_op** out);
+BFLY_API int bfly_op_compose(bfly_ctx* ctx, bfly_op* f2, bfly_op* f1, bfly_op** out);
 /* a: host m x n column-major interleaved complex (or real for BFLY_D) */
-int bfly_op_dense(bfly_ctx* ctx, int64_t m, int64_t n, const double* a, int scalar, bfly_op** out);
+BFLY_API int bfly_op_dense(bfly_ctx* ctx, int64_t m, int64_t n, const double* a, int scalar, bfly_op** out);
 /* wraps a butterfly as a black box; takes ownership */
-int bfly_op_butterfly(bfly_ctx* ctx, bfly_bf* bf, bfly_op** out);
-int bfly_op_callback(bfly_ctx* ctx, int64_t m, int64_t n, int scalar, bfly_apply_fn fn, void* user,
+BFLY_API int bfly_op_butterfly(bfly_ctx* ctx, bfly_bf* bf, bfly_op** out);
+BFLY_API int bfly_op_callback(bfly_ctx* ctx, int64_t m, int64_t n, int scalar, bfly_apply_fn fn, void* user,
                      bfly_op** out);
-int bfly_op_info(const bfly_op* op, int64_t* m, int64_t* n, int* scalar, int* kind);
+BFLY_API int bfly_op_info(const bfly_op* op, int64_t* m, int64_t* n, int* scalar, int* kind);
 /* apply / apply_transpose / apply_adjoint.  on_device = 0: host buffers (copied
  * in and out inside the call); 1: device pointers, stream-ordered. */
-int bfly_op_apply(bfly_op* op, int trans, const void* x, int64_t ldx, void* y, int64_t ldy, int64_t k,
+BFLY_API int bfly_op_apply(bfly_op* op, int trans, const void* x, int64_t ldx, void* y, int64_t ldy, int64_t k,
                   int on_device);
 /* forward_columns / transpose_columns (operators.hpp:41-47) */
-int bfly_op_counters(const bfly_op* op, int64_t* fwd, int64_t* tr);
-int bfly_op_reset_counters(bfly_op* op);
-void bfly_op_destroy(bfly_op* op);
+BFLY_API int bfly_op_counters(const bfly_op* op, int64_t* fwd, int64_t* tr);
+BFLY_API int bfly_op_reset_counters(bfly_op* op);
+BFLY_API void bfly_op_destroy(bfly_op* op);
 
 /* ---------------------------------------------------------- reconstruction */
 /* ReconstructionConfig (reconstruct.hpp:10-36) + batching knob */
@@ -149,7 +155,7 @@ typedef struct bfly_recon_cfg {
   int32_t reserved_;
 } bfly_recon_cfg;
 
-void bfly_cfg_default(bfly_recon_cfg* cfg);
+BFLY_API void bfly_cfg_default(bfly_recon_cfg* cfg);
 
 /* PhaseStat / FactorizationLog (reconstruct.hpp:87-120) */
 #define BFLY_MAX_PHASES 64
@@ -174,58 +180,58 @@ typedef struct bfly_log {
 } bfly_log;
 
 /* factorize() (reconstruct.hpp:412-419) */
-int bfly_factorize(bfly_ctx* ctx, bfly_op* op, const bfly_tree* row_tree, const bfly_tree* col_tree,
+BFLY_API int bfly_factorize(bfly_ctx* ctx, bfly_op* op, const bfly_tree* row_tree, const bfly_tree* col_tree,
                    const bfly_recon_cfg* cfg, bfly_bf** out, bfly_log* log);
 /* Factorizer phase-stepping API (reconstruct.hpp:145-321) */
-int bfly_factorizer_create(bfly_ctx* ctx, bfly_op* op, const bfly_tree* row_tree, const bfly_tree* col_tree,
+BFLY_API int bfly_factorizer_create(bfly_ctx* ctx, bfly_op* op, const bfly_tree* row_tree, const bfly_tree* col_tree,
                            const bfly_recon_cfg* cfg, bfly_factorizer** out);
-int bfly_factorizer_leaf_row_bases(bfly_factorizer* f);
-int bfly_factorizer_leaf_col_bases(bfly_factorizer* f);
-int bfly_factorizer_transfer_level_w(bfly_factorizer* f, int l);
-int bfly_factorizer_transfer_level_r(bfly_factorizer* f, int l);
-int bfly_factorizer_complete(const bfly_factorizer* f);
+BFLY_API int bfly_factorizer_leaf_row_bases(bfly_factorizer* f);
+BFLY_API int bfly_factorizer_leaf_col_bases(bfly_factorizer* f);
+BFLY_API int bfly_factorizer_transfer_level_w(bfly_factorizer* f, int l);
+BFLY_API int bfly_factorizer_transfer_level_r(bfly_factorizer* f, int l);
+BFLY_API int bfly_factorizer_complete(const bfly_factorizer* f);
 /* hands the finished butterfly to the caller (validates it first) */
-int bfly_factorizer_take(bfly_factorizer* f, bfly_bf** out, bfly_log* log);
-void bfly_factorizer_destroy(bfly_factorizer* f);
+BFLY_API int bfly_factorizer_take(bfly_factorizer* f, bfly_bf** out, bfly_log* log);
+BFLY_API void bfly_factorizer_destroy(bfly_factorizer* f);
 
 /* estimate_error (reconstruct.hpp:423-434) */
-int bfly_estimate_error(bfly_op* op, bfly_bf* bf, int64_t k, uint64_t seed, double* err);
+BFLY_API int bfly_estimate_error(bfly_op* op, bfly_bf* bf, int64_t k, uint64_t seed, double* err);
 
 /* ---------------------------------------------------------------- butterfly */
 /* HybridButterfly::apply / apply_transpose / apply_adjoint (butterfly.hpp:71-193) */
-int bfly_apply(bfly_bf* bf, int trans, const void* x, int64_t ldx, void* y, int64_t ldy, int64_t k,
+BFLY_API int bfly_apply(bfly_bf* bf, int trans, const void* x, int64_t ldx, void* y, int64_t ldy, int64_t k,
                int on_device);
-int bfly_bf_info(const bfly_bf* bf, int* levels, int* center, int64_t* m, int64_t* n, int64_t* nnz,
+BFLY_API int bfly_bf_info(const bfly_bf* bf, int* levels, int* center, int64_t* m, int64_t* n, int64_t* nnz,
                  int64_t* max_rank, int* scalar);
 /* u ranks for levels center..L, then v ranks for levels 0..center (2^L each,
  * index tau*2^(L-l)+nu, butterfly.hpp:38-66) */
-int64_t bfly_rank_profile(const bfly_bf* bf, int32_t* out);
+BFLY_API int64_t bfly_rank_profile(const bfly_bf* bf, int32_t* out);
 /* .bfh container (serialize.hpp:103-191; proj/docs/formats.md:3-54) */
-int64_t bfly_serialize(const bfly_bf* bf, uint8_t* buf);
-int bfly_deserialize(bfly_ctx* ctx, const uint8_t* buf, int64_t nbytes, int scalar, bfly_bf** out);
+BFLY_API int64_t bfly_serialize(const bfly_bf* bf, uint8_t* buf);
+BFLY_API int bfly_deserialize(bfly_ctx* ctx, const uint8_t* buf, int64_t nbytes, int scalar, bfly_bf** out);
 /* seeded synthetic butterfly (synth_butterfly, operators.hpp:131-178,
  * generalised to leaf size b and rank r; perturb = relative Gaussian noise) */
-int bfly_synth_butterfly(bfly_ctx* ctx, int levels, int64_t leaf, int64_t rank, uint64_t seed, int scalar,
+BFLY_API int bfly_synth_butterfly(bfly_ctx* ctx, int levels, int64_t leaf, int64_t rank, uint64_t seed, int scalar,
                          double perturb, bfly_bf** out);
-int bfly_bf_convert(bfly_bf* bf, int scalar, bfly_bf** out);
-void bfly_bf_destroy(bfly_bf* bf);
+BFLY_API int bfly_bf_convert(bfly_bf* bf, int scalar, bfly_bf** out);
+BFLY_API void bfly_bf_destroy(bfly_bf* bf);
 
 /* ---------------------------------------------------------------- shard plan */
 /* How the multi-GPU construction splits a level (host logic): contiguous chunk
  * of n units for a rank, and the block indices a rank produces (side 0 leaves,
  * 1 W level (row probes), 2 R level (column probes)); returns the count. */
-int bfly_shard_chunk(int64_t n, int world, int rank, int64_t* begin, int64_t* end);
-int64_t bfly_shard_blocks(int levels, int level, int side, int world, int rank, int64_t* out);
+BFLY_API int bfly_shard_chunk(int64_t n, int world, int rank, int64_t* begin, int64_t* end);
+BFLY_API int64_t bfly_shard_blocks(int levels, int level, int side, int world, int rank, int64_t* out);
 
 /* ------------------------------------------------------------- dense helpers */
 /* gaussian_matrix (linalg.hpp:16-25) generated on the device, copied to host */
-int bfly_gaussian(bfly_ctx* ctx, int64_t rows, int64_t cols, uint64_t seed, int scalar, void* out_host);
-uint64_t bfly_seed_mix(uint64_t seed, int nwords, const uint64_t* words);
+BFLY_API int bfly_gaussian(bfly_ctx* ctx, int64_t rows, int64_t cols, uint64_t seed, int scalar, void* out_host);
+BFLY_API uint64_t bfly_seed_mix(uint64_t seed, int nwords, const uint64_t* words);
 /* pivoted_qr_truncate (linalg.hpp:62-80) on the device, batch of one */
-int bfly_cpqr_truncate(bfly_ctx* ctx, int64_t rows, int64_t cols, const double* z_host, double eps,
+BFLY_API int bfly_cpqr_truncate(bfly_ctx* ctx, int64_t rows, int64_t cols, const double* z_host, double eps,
                        double* q_host, int64_t* k_out);
 /* pinv_solve (linalg.hpp:128-139) on the device, batch of one */
-int bfly_pinv(bfly_ctx* ctx, int64_t rows, int64_t cols, const double* m_host, double tol, double* out_host);
+BFLY_API int bfly_pinv(bfly_ctx* ctx, int64_t rows, int64_t cols, const double* m_host, double tol, double* out_host);
 
 #ifdef __cplusplus
 }

@@ -19,6 +19,8 @@
 #include <cuda_runtime.h>
 
 #include <complex>
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <sstream>
 #include <stdexcept>
@@ -68,6 +70,9 @@ struct Bridge {
   static int call(void* user, int trans, const void* x_dev, int64_t ldx, void* y_dev, int64_t ldy, int64_t k,
                   void* stream) {
     auto* self = static_cast<Bridge*>(user);
+    if (std::getenv("BFLY_ADAPTER_TRACE"))
+      std::fprintf(stderr, "[bridge] trans %d ldx %lld ldy %lld k %lld\n", trans, (long long)ldx, (long long)ldy,
+                   (long long)k);
     try {
       auto s = static_cast<cudaStream_t>(stream);
       const bfly::Index nin = trans ? self->op->rows() : self->op->cols();

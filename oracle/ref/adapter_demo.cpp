@@ -14,8 +14,11 @@ using cplx = std::complex<double>;
 template <class S>
 static int compare(const char* name, const BlackBoxOperator<S>& op, const PartitionTree& rt, const PartitionTree& ct,
                    const ReconstructionConfig& cfg, bfly_b200::Context& gpu) {
+  std::fprintf(stderr, "[demo] %s: cpu factorize\n", name);
   auto cpu = factorize<S>(op, rt, ct, cfg);
+  std::fprintf(stderr, "[demo] %s: gpu factorize\n", name);
   auto gpu_res = bfly_b200::factorize<S>(gpu, op, rt, ct, cfg);
+  std::fprintf(stderr, "[demo] %s: compare\n", name);
   const HybridButterfly<S>& a = cpu.first;
   const HybridButterfly<S>& b = gpu_res.first;
   bool ranks = true;
@@ -39,6 +42,7 @@ static int compare(const char* name, const BlackBoxOperator<S>& op, const Partit
 }
 
 int main() {
+  std::fprintf(stderr, "[demo] context\n");
   bfly_b200::Context gpu(0);
   int bad = 0;
   {

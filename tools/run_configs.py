@@ -15,13 +15,22 @@ def main():
     ap.add_argument("--cfg", type=int, nargs="+", default=[0, 1, 2])
     ap.add_argument("--n", type=int, default=0)
     ap.add_argument("--reps", type=int, default=2)
+    ap.add_argument("--profile", action="store_true")
     a = ap.parse_args()
     for c in a.cfg:
         t0 = time.time()
         w = B.configs.build(c, a.n or None)
         t1 = time.time()
         for r in range(a.reps):
+            if a.profile and r == a.reps - 1:
+                w.op.ctx.profile(-1)
+                w.op.ctx.profile(1)
             bf, log = B.factorize(w.op, w.row_tree, w.col_tree, w.recon)
+        if a.profile:
+            for k, v in sorted(w.op.ctx.profile_report().items(), key=lambda kv: -kv[1]["ms"]):
+                print(f"   kernel {k:22s} launches {v['launches']:5d} ms {v['ms']:9.2f} "
+                      f"TF/s {v['flops'] / max(v['ms'], 1e-9) / 1e9:7.2f} GB/s {v['bytes'] / max(v['ms'], 1e-9) / 1e6:8.1f}")
+            w.op.ctx.profile(0)
         prof = bf.rank_profile()
         err = B.estimate_error(w.op, bf, 16, 0)
         print(f"cfg {c} {w.name}: setup {t1-t0:.2f}s construct {log.total_seconds:.4f}s "
