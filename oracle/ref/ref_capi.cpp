@@ -292,6 +292,46 @@ int64_t ref_serialize(const ref_bf* b, uint8_t* buf) {
 
 void ref_bf_free(ref_bf* b) { delete b; }
 
+// ---- primitives for the golden vectors (tests/golden/make_golden.py)
+// seed_mix(seed, words...) core.hpp:78-88 (up to 4 words)
+uint64_t ref_seed_mix(uint64_t seed, int nw, const uint64_t* w) {
+  switch (nw) {
+    case 0: return seed_mix(seed);
+    case 1: return seed_mix(seed, w[0]);
+    case 2: return seed_mix(seed, w[0], w[1]);
+    case 3: return seed_mix(seed, w[0], w[1], w[2]);
+    default: return seed_mix(seed, w[0], w[1], w[2], w[3]);
+  }
+}
+
+// gaussian_matrix<Scalar>(rows, cols, seed) linalg.hpp:16-25; complex: interleaved
+int ref_gaussian(int is_complex, int64_t rows, int64_t cols, uint64_t seed, double* out) {
+  return guard([&] {
+    if (is_complex) {
+      Matrix<cplx> g = gaussian_matrix<cplx>(rows, cols, seed);
+      std::memcpy(out, g.data(), sizeof(cplx) * rows * cols);
+    } else {
+      Matrix<double> g = gaussian_matrix<double>(rows, cols, seed);
+      std::memcpy(out, g.data(), sizeof(double) * rows * cols);
+    }
+  });
+}
+
+// pivoted_qr_truncate(w, eps) linalg.hpp:63-80 on a complex column-major
+// matrix; q (rows x min(rows,cols)) receives the basis; returns the rank
+// (-1 on error, -2 for zero input)
+int64_t ref_cpqr(int64_t rows, int64_t cols, const double* w, double eps, double* q) {
+  int64_t rank = -1;
+  guard([&] {
+    Matrix<cplx> W(rows, cols);
+    std::memcpy(W.data(), w, sizeof(cplx) * rows * cols);
+    OrthonormalBasis<cplx> b = pivoted_qr_truncate<cplx>(W, eps);
+    rank = b.zero_input ? -2 : (int64_t)b.rank();
+    if (b.rank() > 0) std::memcpy(q, b.q.data(), sizeof(cplx) * rows * b.rank());
+  });
+  return rank;
+}
+
 // Bounded CPU-baseline sample through the reference's own probe path:
 // probe_with (padding + apply_adjoint = conj(apply_transpose(conj))) for
 // `probes` row probes of tree level `level`, width `width`.  Returns seconds.

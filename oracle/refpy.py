@@ -37,6 +37,9 @@ def lib():
             "ref_serialize": (i64, [p, p]),
             "ref_bf_free": (None, [p]),
             "ref_probe_sample": (dbl, [p, i32, i32, i64, u64]),
+            "ref_seed_mix": (u64, [u64, i32, p]),
+            "ref_gaussian": (i32, [i32, i64, i64, u64, p]),
+            "ref_cpqr": (i64, [i64, i64, p, dbl, p]),
         }
         for k, (r, a) in sig.items():
             f = getattr(L, k)
@@ -136,3 +139,27 @@ def factorize(op: RefOp, tol, r0, L, seed=0, p=2, threads=1):
     h = C.c_void_p()
     _check(lib().ref_factorize(op.h, tol, p, r0, L, seed, threads, C.byref(h)))
     return RefButterfly(h, op)
+
+
+def seed_mix(seed, *words):
+    w = np.array(words, dtype=np.uint64)
+    return int(lib().ref_seed_mix(seed, len(words), _vp(w) if len(words) else None))
+
+
+def gaussian_matrix(rows, cols, seed, complex_=True):
+    out = np.zeros((cols, rows), dtype=np.complex128 if complex_ else np.float64)
+    _check(lib().ref_gaussian(1 if complex_ else 0, rows, cols, seed, _vp(out)))
+    return out.T  # column-major storage -> (rows, cols) view
+
+
+def pivoted_qr_truncate(w, eps):
+    """returns (rank, Q); rank -2 marks the reference's zero_input case"""
+    w = np.asarray(w, dtype=np.complex128)
+    rows, cols = w.shape
+    buf = np.asfortranarray(w)
+    q = np.zeros((min(rows, cols), rows), dtype=np.complex128)
+    rank = lib().ref_cpqr(rows, cols, _vp(buf), eps, _vp(q))
+    if rank == -1:
+        raise RuntimeError(lib().ref_last_error().decode())
+    k = max(rank, 0)
+    return rank, q[:k].T.copy()
