@@ -18,14 +18,16 @@
 #include <type_traits>
 #include <vector>
 
+#include "k_eval.cuh"
 #include "kernels.cuh"
 
 namespace bfly {
 
 namespace {
 
-constexpr double kTwoPi = 6.283185307179586476925286766559;
-constexpr double kFourPi = 12.566370614359172953850573533118;
+using keval::kFourPi;
+using keval::kTwoPi;
+using keval::kernel_entry_fast;
 
 struct MatvecItem {
   int64_t row0, rows;  // input point range of this work item
@@ -173,84 +175,6 @@ __global__ void __launch_bounds__(256) matvec_kernel(Points outp, Points inp, do
 // the win is issue slots: one DMMA does the work of 8 warp-wide DFMAs, which
 // leaves the issue bandwidth to the kernel-entry evaluation.
 // ----------------------------------------------------------------------------
-
-// sin/cos of an argument reduced by the 2-term FMA Cody-Waite step (|ph| up to
-// ~1e5 here) and evaluated with Taylor polynomials on [-pi/4, pi/4]
-// (truncation < 1e-19); ~20 FP64 ops instead of ~47 for libdevice sincos.
-// Taylor coefficients in the constant bank: DFMA reads c[][] operands
-// directly (64-bit immediates would be re-materialised with UMOVs).
-__constant__ double kSinC[8] = {2.8114572543455207632e-15,  -7.6471637318198164759e-13,   // 1/17!, -1/15!
-                                1.6059043836821614599e-10,  -2.5052108385441718775e-08,   // 1/13!, -1/11!
-                                2.7557319223985890653e-06,  -1.9841269841269841270e-04,   // 1/9!,  -1/7!
-                                8.3333333333333333333e-03,  -1.6666666666666666667e-01};  // 1/5!,  -1/3!
-__constant__ double kCosC[8] = {4.7794773323873852974e-14,  -1.1470745597729724714e-11,   // 1/16!, -1/14!
-                                2.0876756987868098979e-09,  -2.7557319223985890653e-07,   // 1/12!, -1/10!
-                                2.4801587301587301587e-05,  -1.3888888888888888889e-03,   // 1/8!,  -1/6!
-                                4.1666666666666666667e-02,  -0.5};                        // 1/4!,  -1/2!
-
-__device__ __forceinline__ void sincos_red(double f, int q, double& s, double& c) {
-  const double x2 = f * f;
-  double ps = kSinC[0], pc = kCosC[0];
-#pragma unroll
-  for (int i = 1; i < 8; ++i) {
-    ps = fma(ps, x2, kSinC[i]);
-    pc = fma(pc, x2, kCosC[i]);
-  }
-  const double sn = fma(f * x2, ps, f);
-  const double cs = fma(x2, pc, 1.0);
-  // quadrant q mod 4: (s, c) <- (s, c), (c, -s), (-s, -c), (-c, s)
-  const bool swap = q & 1;
-  double rs = swap ? cs : sn, rc = swap ? sn : cs;
-  if ((q + 1) & 2) rc = -rc;
-  if (q & 2) rs = -rs;
-  s = rs;
-  c = rc;
-}
-
-__device__ __forceinline__ void fast_sincos(double ph, double& s, double& c) {
-  const double q = rint(ph * 0.63661977236758134308);    // 2/pi
-  double f = fma(-q, 1.5707963267948965580, ph);         // pi/2 high
-  f = fma(-q, 6.1232339957367658e-17, f);                // pi/2 low
-  sincos_red(f, (int)(long long)q, s, c);
-}
-
-// 1/r to ~1 ulp: MUFU.RCP64H seed + two Newton steps (amplitude only; the
-// phase uses the correctly rounded r).
-__device__ __forceinline__ double fast_rcp(double r) {
-  double y;
-  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(r));
-  double e = fma(-r, y, 1.0);
-  y = fma(y, e, y);
-  e = fma(-r, y, 1.0);
-  return fma(y, e, y);
-}
-
-template <int KIND>
-__device__ __forceinline__ double2 kernel_entry_fast(double tx, double ty, double tz, double sx, double sy, double sz,
-                                                     double kappa) {
-  double sn, cs;
-  if (KIND == KK_NUFFT) {
-    // exp(2 pi i x xi): t = x xi, f = t - rint(t) in [-1/2, 1/2]; quarter turns exact
-    const double ph = __dmul_rn(tx, sx);
-    const double f = __dsub_rn(ph, rint(ph));
-    const double qq = rint(4.0 * f);
-    const double g = __dsub_rn(f, 0.25 * qq);
-    sincos_red(__dmul_rn(kTwoPi, g), (int)qq, sn, cs);
-    return make_double2(cs, sn);
-  } else if (KIND == KK_PLATES) {
-    const double dx = __dsub_rn(tx, sx), dy = __dsub_rn(ty, sy), dz = __dsub_rn(tz, sz);
-    const double r = __dsqrt_rn(fma(dz, dz, fma(dy, dy, __dmul_rn(dx, dx))));
-    fast_sincos(__dmul_rn(kappa, r), sn, cs);
-    const double sc = fast_rcp(__dmul_rn(kFourPi, r));
-    return make_double2(cs * sc, sn * sc);
-  } else {
-    const double dx = __dsub_rn(tx, sx), dy = __dsub_rn(ty, sy);
-    const double r = __dsqrt_rn(fma(dy, dy, __dmul_rn(dx, dx)));
-    fast_sincos(__dmul_rn(kappa, r), sn, cs);
-    const double sc = fast_rcp(r);
-    return make_double2(cs * sc, sn * sc);
-  }
-}
 
 __device__ __forceinline__ void dmma(double& d0, double& d1, double a, double b) {
   asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
@@ -610,6 +534,10 @@ template <typename R>
 void launch_kernel_matvec(Ctx* c, int kind, int mode, Points outp, Points inp, double kappa, int64_t m_out,
                           const cx<R>* X, cx<R>* Y, int64_t ldy, const MatvecSeg* segs, int nseg) {
   if (m_out <= 0 || nseg <= 0) return;
+  if constexpr (std::is_same<R, double>::value) {
+    if (matvec_oz_enabled() && launch_kernel_matvec_oz(c, kind, mode, outp, inp, kappa, m_out, X, Y, ldy, segs, nseg))
+      return;
+  }
   if (kind == KK_NUFFT) dispatch_mode<R, KK_NUFFT>(c, mode, outp, inp, kappa, m_out, X, Y, ldy, segs, nseg);
   else if (kind == KK_PLATES) dispatch_mode<R, KK_PLATES>(c, mode, outp, inp, kappa, m_out, X, Y, ldy, segs, nseg);
   else if (kind == KK_CIRCLE) dispatch_mode<R, KK_CIRCLE>(c, mode, outp, inp, kappa, m_out, X, Y, ldy, segs, nseg);

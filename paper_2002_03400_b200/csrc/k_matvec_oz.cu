@@ -1,0 +1,693 @@
+// k_matvec_oz.cu -- K2 on the 5th-generation tensor cores: kernel-evaluated
+// black-box products (reference operators.hpp:430-439 pattern, probe_with
+// reconstruct.hpp:72-85) with the complex128 contraction done EXACTLY in
+// integer arithmetic on tcgen05 kind::i8 (an Ozaki-style slice scheme).
+//
+// Why: on B200 the FP64 DMMA and DFMA share one 37 TF/s pipe
+// (profiles/r01_fp64_peaks.txt), so in the FP64 path (k_matvec.cu) the
+// ~43-instruction kernel-entry evaluation competes with the contraction.
+// Here the FP64 pipe only evaluates entries; the contraction runs on the
+// int8 tensor cores (4.2 POPS measured, tools/microbench/tc_i8.cu).
+//
+// Arithmetic (per CTA: 128 output rows x 32 complex probe columns):
+//  * every kernel entry a (re and im separately) is scaled by 2^S_row and
+//    rounded to a signed integer |v| < 2^50; S_row is per output row and per
+//    1024-entry chunk of the input range, from a bound on |a| over the chunk
+//    (1 for NUFFT, 1/r_min or 1/(4 pi r_min) for the Helmholtz kernels);
+//  * v's two's-complement bytes ARE its base-256 digits: slices A_0..A_5
+//    unsigned, A_6 signed -- no decomposition work;
+//  * probe entries x are scaled per column by 2^T_c (|x| < 2^50) and split into
+//    balanced signed digits B_0..B_6 (prep kernel, once per launch);
+//  * sum_k v_ik w_kc = sum_{p,q} 2^{8(p+q)} A_p B_q^T; the products with
+//    p + q >= 5 (34 of 49 slice pairs) are accumulated exactly in int32 in
+//    TMEM, one 64-column block per diagonal e = p + q (8 blocks = 512 cols).
+//    The dropped terms are < 2^-50 relative to max|v| max|w| per entry;
+//  * every 1024-entry chunk the diagonals are drained into FP64 accumulators
+//    (Horner in 2^8, times 2^{40 - S_row - T_c}).
+// Complex: A_re slices multiply G1 = [B(Re x) | B(Im x)] and A_im slices
+// multiply G2 = [B(-Im x) | B(Re x)] into the same accumulator, so TMEM block
+// columns hold [Re y | Im y] directly.  For slice A_p the needed B_q
+// (q = e - p) form a contiguous window of the concatenated B slices, so one
+// MMA covers up to four diagonals.
+//
+// Pipeline (1 CTA / SM, TMEM fully allocated): 16 evaluation warps write A
+// stages (128 rows x 32 input entries, both planes) into a double-buffered
+// shared-memory ring and drain TMEM; one thread issues the B-stage bulk
+// copies; one thread of warp 16 issues the MMAs and commits them to mbarriers.
+//
+// Safety: if any scaled entry falls outside the representable range (a
+// coincident point, a bound that did not hold) the launch reports it and the
+// caller recomputes the product with the FP64 DMMA kernel.
+#include <algorithm>
+#include <cstdlib>
+#include <string>
+#include <vector>
+
+#include "k_eval.cuh"
+#include "kernels.cuh"
+
+namespace bfly {
+
+namespace {
+
+constexpr int OZ_NCB = 32;                        // complex probe columns per tile
+constexpr int OZ_BN2 = 2 * OZ_NCB;                // N-rows per B slice ([re | im])
+constexpr int OZ_NSL = 7;                         // slices per operand
+constexpr int OZ_NDIAG = 8;                       // kept diagonals e = 5..12
+constexpr int OZ_TMEM_COLS = OZ_NDIAG * OZ_BN2;   // 512
+constexpr int OZ_KS = 32;                         // input entries per stage (MMA K)
+constexpr int OZ_KD = 1024;                       // entries per drain / scale chunk
+constexpr int OZ_NST = 2;                         // ring depth
+constexpr int OZ_BM = 128;                        // output rows per CTA (= TMEM lanes)
+constexpr int OZ_EWARPS = 16;
+constexpr int OZ_ETHREADS = OZ_EWARPS * 32;
+constexpr int OZ_THREADS = OZ_ETHREADS + 32;      // + MMA warp
+constexpr int OZ_EPT = OZ_BM * OZ_KS / OZ_ETHREADS;  // 8 entries per thread per stage
+constexpr int OZ_ASLICE = OZ_BM * OZ_KS;           // 4096 B: one A slice (128 rows x 32 B)
+constexpr int OZ_APLANE = OZ_NSL * OZ_ASLICE;      // 28672 B
+constexpr int OZ_ASTAGE = 2 * OZ_APLANE;           // re + im planes
+constexpr int OZ_BROWS = OZ_NSL * OZ_BN2;          // 448 N-rows per B operand
+constexpr int OZ_BOPER = OZ_BROWS * OZ_KS;         // 14336 B (G1 or G2)
+constexpr int OZ_BSTAGE = 2 * OZ_BOPER;            // G1 + G2
+constexpr int OZ_MAXB = 256 / OZ_BN2;              // diagonal blocks per MMA (N <= 256)
+static_assert(OZ_EPT == 8, "thread mapping assumes 8 entries per thread");
+
+// shared memory map (bytes)
+constexpr int SM_A = 0;
+constexpr int SM_B = SM_A + OZ_NST * OZ_ASTAGE;
+constexpr int SM_PD = SM_B + OZ_NST * OZ_BSTAGE;   // double2 (x, y) [KD]
+constexpr int SM_PZ = SM_PD + OZ_KD * 16;          // double z [KD]
+constexpr int SM_PF = SM_PZ + OZ_KD * 8;           // float4 local (x, y, z, 0) [KD]
+constexpr int SM_S = SM_PF + OZ_KD * 16;           // int S_row [2][128]
+constexpr int SM_T = SM_S + 2 * OZ_BM * 4;         // int T [NCB]
+constexpr int SM_MIN = SM_T + OZ_NCB * 4;          // uint min d2 bits [128]
+constexpr int SM_TAB = SM_MIN + OZ_BM * 4;         // double2 sin/cos table [256]
+constexpr int SM_BAR = SM_TAB + 256 * 16;          // mbarriers
+constexpr int NBAR = 3 * OZ_NST + 2;
+constexpr int SM_TMEM = SM_BAR + NBAR * 8;
+constexpr int SM_TOTAL = SM_TMEM + 16;
+static_assert(SM_TOTAL <= 232448, "shared memory budget");
+
+struct OzItem {
+  int64_t row0, rows;   // input point range
+  int64_t x_off, ldx;   // probe block
+  int64_t ycol, ybase;  // output column, split-K slice base
+  int64_t bstage0;      // first B stage image of this item
+  int32_t ncols, pad_;
+};
+
+// ------------------------------------------------------------ PTX helpers
+__device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+
+__device__ __forceinline__ uint64_t smem_desc(uint32_t addr, uint32_t lbo, uint32_t sbo) {
+  // K-major, SWIZZLE_NONE canonical layout; version 1 (sm_100)
+  return (uint64_t)((addr >> 4) & 0x3FFF) | ((uint64_t)((lbo >> 4) & 0x3FFF) << 16) |
+         ((uint64_t)((sbo >> 4) & 0x3FFF) << 32) | ((uint64_t)1 << 46);
+}
+__host__ __device__ constexpr uint32_t idesc_i8(int M, int N, bool a_signed, bool b_signed) {
+  return (2u << 4) | ((a_signed ? 1u : 0u) << 7) | ((b_signed ? 1u : 0u) << 10) | ((uint32_t)(N >> 3) << 17) |
+         ((uint32_t)(M >> 4) << 24);
+}
+__device__ __forceinline__ void mma_i8(uint32_t d, uint64_t da, uint64_t db, uint32_t idesc, uint32_t acc) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n\t}\n" ::"r"(d),
+      "l"(da), "l"(db), "r"(idesc), "r"(acc));
+}
+__device__ __forceinline__ void mbar_init(uint32_t bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(bar), "r"(count));
+}
+__device__ __forceinline__ void mbar_arrive(uint32_t bar) {
+  asm volatile("mbarrier.arrive.release.cta.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint32_t bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.release.cta.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred done;\n\t"
+      "WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.acquire.cta.shared::cta.b64 done, [%0], %1;\n\t"
+      "@!done bra WAIT_%=;\n\t}\n" ::"r"(bar),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void mma_commit(uint32_t bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(bar) : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(uint32_t dst, const void* src, uint32_t bytes, uint32_t bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(dst),
+               "l"(src), "r"(bytes), "r"(bar)
+               : "memory");
+}
+__device__ __forceinline__ void eval_bar() { asm volatile("bar.sync 1, %0;" ::"n"(OZ_EWARPS * 32) : "memory"); }
+
+__device__ __forceinline__ void tmem_ld16(uint32_t addr, uint32_t (&v)[16]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+      : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]), "=r"(v[8]),
+        "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15])
+      : "r"(addr));
+}
+// wait with back-off: the MMA thread shares its scheduler with evaluation warps
+__device__ __forceinline__ void mbar_wait_sleep(uint32_t bar, uint32_t parity) {
+  uint32_t done = 0;
+  while (true) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "mbarrier.try_wait.parity.acquire.cta.shared::cta.b64 p, [%1], %2;\n\t"
+        "selp.u32 %0, 1, 0, p;\n\t}\n"
+        : "=r"(done)
+        : "r"(bar), "r"(parity)
+        : "memory");
+    if (done) return;
+    __nanosleep(100);
+  }
+}
+
+// exact int32 -> double (magic-number bias: one LOP + one DADD)
+__device__ __forceinline__ double i2d(uint32_t v) {
+  return __hiloint2double(0x43300000, (int)(v ^ 0x80000000u)) - 4503601774854144.0;  // 2^52 + 2^31
+}
+// x (|x| < 2^51) rounded to the nearest integer, as int64 (magic-number)
+__device__ __forceinline__ long long d2ll(double x) {
+  return __double_as_longlong(x + 6755399441055744.0) - 0x4338000000000000LL;  // 1.5 * 2^52
+}
+__device__ __forceinline__ double pow2(int e) { return __longlong_as_double((long long)(1023 + e) << 52); }
+
+// 4x4 byte transpose: o[b] = byte b of w0..w3 (in order)
+__device__ __forceinline__ void transpose4(uint32_t w0, uint32_t w1, uint32_t w2, uint32_t w3, uint32_t (&o)[4]) {
+  const uint32_t t0 = __byte_perm(w0, w1, 0x5140), t1 = __byte_perm(w2, w3, 0x5140);
+  const uint32_t t2 = __byte_perm(w0, w1, 0x7362), t3 = __byte_perm(w2, w3, 0x7362);
+  o[0] = __byte_perm(t0, t1, 0x5410);
+  o[1] = __byte_perm(t0, t1, 0x7632);
+  o[2] = __byte_perm(t2, t3, 0x5410);
+  o[3] = __byte_perm(t2, t3, 0x7632);
+}
+
+// kernel entry scaled by p2 = 2^S and rounded to an integer in one FMA each
+// (magic-number rounding: result = value + 1.5 * 2^52); amp = scaled |entry|
+// bound for the range check.  im is negated for the adjoint.
+template <int KIND, bool CONJ>
+__device__ __forceinline__ void entry_rounded(double tx, double ty, double tz, double sx, double sy, double sz,
+                                              double kappa, double p2, const double2* __restrict__ tab, double& re,
+                                              double& im, double& amp) {
+  double sn, cs, sc;
+  if (KIND == KK_NUFFT) {
+    const double ph = __dmul_rn(tx, sx);
+    keval::tab_sincos_turn(__dsub_rn(ph, rint(ph)), tab, sn, cs);
+    sc = p2;
+  } else if (KIND == KK_PLATES) {
+    const double dx = __dsub_rn(tx, sx), dy = __dsub_rn(ty, sy), dz = __dsub_rn(tz, sz);
+    const double r = __dsqrt_rn(fma(dz, dz, fma(dy, dy, __dmul_rn(dx, dx))));
+    keval::tab_sincos(__dmul_rn(kappa, r), tab, sn, cs);
+    sc = keval::fast_rcp(__dmul_rn(keval::kFourPi, r)) * p2;
+  } else {
+    const double dx = __dsub_rn(tx, sx), dy = __dsub_rn(ty, sy);
+    const double r = __dsqrt_rn(fma(dy, dy, __dmul_rn(dx, dx)));
+    keval::tab_sincos(__dmul_rn(kappa, r), tab, sn, cs);
+    sc = keval::fast_rcp(r) * p2;
+  }
+  amp = sc;
+  re = fma(cs, sc, keval::kMagic);
+  im = fma(sn, CONJ ? -sc : sc, keval::kMagic);
+}
+
+// ------------------------------------------------------- probe slicing
+// T_c = 49 - floor(log2 max_k |x_kc|_inf)  (scaled |x| < 2^50)
+__global__ void oz_colscale_kernel(const double2* __restrict__ X, const OzItem* __restrict__ items,
+                                   int32_t* __restrict__ T) {
+  const OzItem it = items[blockIdx.y];
+  const int c = blockIdx.x;
+  double m = 0.0;
+  if (c < it.ncols)
+    for (int64_t k = threadIdx.x; k < it.rows; k += blockDim.x) {
+      const double2 v = X[it.x_off + k + (int64_t)c * it.ldx];
+      m = fmax(m, fmax(fabs(v.x), fabs(v.y)));
+    }
+  __shared__ double red[256];
+  red[threadIdx.x] = m;
+  __syncthreads();
+  for (int s = 128; s > 0; s >>= 1) {
+    if (threadIdx.x < s) red[threadIdx.x] = fmax(red[threadIdx.x], red[threadIdx.x + s]);
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    const double mx = red[0];
+    // zero or non-finite columns: scale 0 (non-finite values trip the slice check)
+    T[blockIdx.y * OZ_NCB + c] = (mx > 0.0 && mx < 1e300) ? 49 - ilogb(mx) : 0;
+  }
+}
+
+// balanced base-256 digits of round(x), |x| < 2^50
+__device__ __forceinline__ void digits7(double x, int (&d)[OZ_NSL]) {
+  long long q = d2ll(x);
+#pragma unroll
+  for (int s = 0; s < OZ_NSL - 1; ++s) {
+    d[s] = (int)(signed char)(q & 0xFF);
+    q = (q - d[s]) >> 8;
+  }
+  d[OZ_NSL - 1] = (int)q;
+}
+
+// one thread per (item row k, column c): digits of round(x * 2^T_c) written
+// into the canonical K-major images of the item's stage k/32:
+//   G1 N-row q*64 + c:      Re x      G1 N-row q*64 + 32 + c:  Im x
+//   G2 N-row q*64 + c:     -Im x      G2 N-row q*64 + 32 + c:  Re x
+__global__ void oz_slice_kernel(const double2* __restrict__ X, const OzItem* __restrict__ items,
+                                const int32_t* __restrict__ T, uint8_t* __restrict__ img, int* __restrict__ flag) {
+  const OzItem it = items[blockIdx.y];
+  const int64_t kpad = ceil_div(it.rows, (int64_t)OZ_KS) * OZ_KS;
+  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= kpad * OZ_NCB) return;
+  const int c = (int)(t % OZ_NCB);
+  const int64_t k = t / OZ_NCB;
+  double2 v = make_double2(0.0, 0.0);
+  if (c < it.ncols && k < it.rows) v = X[it.x_off + k + (int64_t)c * it.ldx];
+  const double sc = pow2(T[blockIdx.y * OZ_NCB + c]);
+  const double xr = v.x * sc, xi = v.y * sc;
+  if (!(fabs(xr) < 1125899906842624.0 && fabs(xi) < 1125899906842624.0)) {  // 2^50; NaN fails too
+    atomicOr(flag, 1);
+    return;
+  }
+  uint8_t* g1 = img + (it.bstage0 + k / OZ_KS) * (int64_t)OZ_BSTAGE;
+  uint8_t* g2 = g1 + OZ_BOPER;
+  const int kk = (int)(k % OZ_KS);
+  int dr[OZ_NSL], di[OZ_NSL], dn[OZ_NSL];
+  digits7(xr, dr);
+  digits7(xi, di);
+  digits7(-xi, dn);
+  auto put = [&](uint8_t* base, int nrow, int d) {
+    base[((kk >> 4) * (OZ_BROWS / 8) + (nrow >> 3)) * 128 + (nrow & 7) * 16 + (kk & 15)] = (uint8_t)(d & 0xFF);
+  };
+#pragma unroll
+  for (int s = 0; s < OZ_NSL; ++s) {
+    put(g1, s * OZ_BN2 + c, dr[s]);
+    put(g1, s * OZ_BN2 + OZ_NCB + c, di[s]);
+    put(g2, s * OZ_BN2 + c, dn[s]);
+    put(g2, s * OZ_BN2 + OZ_NCB + c, dr[s]);
+  }
+}
+
+// ------------------------------------------------------------ main kernel
+template <int KIND, int MODE>
+__global__ void __launch_bounds__(OZ_THREADS, 1)
+    matvec_oz_kernel(Points outp, Points inp, double kappa, int64_t m_out, const uint8_t* __restrict__ bimg,
+                     const int32_t* __restrict__ Tg, double2* __restrict__ Y, int64_t ldy,
+                     const OzItem* __restrict__ items, int64_t rows_per_split, int64_t pstride, int* __restrict__ flag) {
+  extern __shared__ __align__(1024) uint8_t smem[];
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const OzItem it = items[blockIdx.y];
+  const int64_t i0 = (int64_t)blockIdx.x * OZ_BM;
+  const int64_t kb = (int64_t)blockIdx.z * rows_per_split;
+  const int64_t ke = min(it.rows, kb + rows_per_split);
+  const int64_t nk = ke > kb ? ke - kb : 0;
+  const int nchunks = (int)ceil_div(nk, (int64_t)OZ_KD);
+
+  double2* PD = reinterpret_cast<double2*>(smem + SM_PD);
+  double* PZ = reinterpret_cast<double*>(smem + SM_PZ);
+  float4* PF = reinterpret_cast<float4*>(smem + SM_PF);
+  int* Srow = reinterpret_cast<int*>(smem + SM_S);
+  int* Ts = reinterpret_cast<int*>(smem + SM_T);
+  unsigned* Smin = reinterpret_cast<unsigned*>(smem + SM_MIN);
+  const uint32_t bar0 = smem_u32(smem + SM_BAR);
+  auto fullA = [&](int s) { return bar0 + 8u * s; };
+  auto fullB = [&](int s) { return bar0 + 8u * (OZ_NST + s); };
+  auto empty = [&](int s) { return bar0 + 8u * (2 * OZ_NST + s); };
+  const uint32_t acc_full = bar0 + 8u * (3 * OZ_NST), acc_empty = acc_full + 8u;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + SM_TMEM);
+
+  if (warp == OZ_EWARPS) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                 "n"(OZ_TMEM_COLS));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  if (tid == 0) {
+    for (int s = 0; s < OZ_NST; ++s) {
+      mbar_init(fullA(s), OZ_EWARPS);
+      mbar_init(fullB(s), 1);
+      mbar_init(empty(s), 1);
+    }
+    mbar_init(acc_full, 1);
+    mbar_init(acc_empty, OZ_EWARPS);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (tid < OZ_NCB) Ts[tid] = Tg[blockIdx.y * OZ_NCB + tid];
+  double2* tab = reinterpret_cast<double2*>(smem + SM_TAB);
+  if (tid < 256) {
+    double s_, c_;
+    sincospi(tid / 128.0, &s_, &c_);
+    tab[tid] = make_double2(c_, s_);
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  const uint32_t tmem = *tmem_slot;
+  const uint32_t sA = smem_u32(smem + SM_A), sB = smem_u32(smem + SM_B);
+
+  if (warp == OZ_EWARPS) {
+    // ======================= MMA issuer (one thread) =======================
+    if (lane == 0) {
+      int g = 0;
+      for (int d = 0; d < nchunks; ++d) {
+        const int64_t c0 = kb + (int64_t)d * OZ_KD;
+        const int nst = (int)ceil_div(min((int64_t)OZ_KD, ke - c0), (int64_t)OZ_KS);
+        for (int s = 0; s < nst; ++s, ++g) {
+          const int slot = g % OZ_NST;
+          const uint32_t ph = (uint32_t)(g / OZ_NST) & 1u;
+          mbar_wait_sleep(fullA(slot), ph);
+          mbar_wait_sleep(fullB(slot), ph);
+          if (s == 0 && d > 0) mbar_wait_sleep(acc_empty, (uint32_t)(d - 1) & 1u);
+          asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+          const uint32_t a0 = sA + slot * OZ_ASTAGE, b0 = sB + slot * OZ_BSTAGE;
+          // plane h: A_re x G1, A_im x G2 into the same accumulator
+          auto issue = [&](int h, int p, int jlo, int nb, bool init) {
+            const uint64_t da = smem_desc(a0 + h * OZ_APLANE + p * OZ_ASLICE, (OZ_BM / 8) * 128, 128);
+            const int q0 = jlo + 5 - p;
+            const uint64_t db = smem_desc(b0 + h * OZ_BOPER + q0 * OZ_BN2 * 16, (OZ_BROWS / 8) * 128, 128);
+            mma_i8(tmem + jlo * OZ_BN2, da, db, idesc_i8(128, nb * OZ_BN2, p == OZ_NSL - 1, true),
+                   (init && s == 0) ? 0u : 1u);
+          };
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            const bool first = h == 0;
+            // initialising MMAs first (disjoint cover of the 8 diagonal blocks)
+            for (int j = 1; j <= 7; j += OZ_MAXB) issue(h, 6, j, min(OZ_MAXB, 8 - j), first);
+            issue(h, 5, 0, 1, first);
+            for (int j = 1; j <= 6; j += OZ_MAXB) issue(h, 5, j, min(OZ_MAXB, 7 - j), false);
+#pragma unroll
+            for (int p = 4; p >= 0; --p) {
+              const int jhi = p + 1;
+              for (int j = 0; j <= jhi; j += OZ_MAXB) issue(h, p, j, min(OZ_MAXB, jhi - j + 1), false);
+            }
+          }
+          mma_commit(empty(slot));
+          if (s == nst - 1) mma_commit(acc_full);
+        }
+      }
+    }
+  } else {
+    // ================== evaluation / drain warps ==================
+    // evaluation: row (warp & 7) * 16 + lane / 2, entries kofs .. kofs + 7 of each stage
+    const int erow = (warp & 7) * 16 + (lane >> 1);
+    const int kofs = (warp >> 3) * 16 + (lane & 1) * 8;
+    const int64_t gi = min(i0 + erow, m_out - 1);  // padded rows evaluate a valid row (never stored)
+    const double ox = outp.x[gi];
+    const double oy = KIND == KK_NUFFT ? 0.0 : outp.y[gi];
+    const double oz = KIND == KK_PLATES ? outp.z[gi] : 0.0;
+    // drain: TMEM lane quarter = warp & 3, column quarter = warp >> 2
+    // (0, 1: Re y columns 0-15 / 16-31; 2, 3: Im y columns 0-15 / 16-31)
+    const int drow = (warp & 3) * 32 + lane;
+    const int dq = warp >> 2;
+    double yacc[16];
+#pragma unroll
+    for (int c = 0; c < 16; ++c) yacc[c] = 0.0;
+    uint32_t amp_hi = 0;  // max high word of the scaled amplitudes
+
+    auto drain = [&](int d) {
+      mbar_wait(acc_full, (uint32_t)d & 1u);
+      asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+      double t[16];
+#pragma unroll
+      for (int j = OZ_NDIAG - 1; j >= 0; --j) {
+        uint32_t v[16];
+        tmem_ld16(tmem + ((uint32_t)((warp & 3) * 32) << 16) + j * OZ_BN2 + dq * 16, v);
+        asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+        for (int c = 0; c < 16; ++c) t[c] = (j == OZ_NDIAG - 1) ? i2d(v[c]) : fma(t[c], 256.0, i2d(v[c]));
+      }
+      asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+      __syncwarp();
+      if (lane == 0) mbar_arrive(acc_empty);
+      const int S = Srow[(d & 1) * OZ_BM + drow];
+      const int c0 = (dq & 1) * 16;
+#pragma unroll
+      for (int c = 0; c < 16; ++c) yacc[c] = fma(t[c], pow2(40 - S - Ts[c0 + c]), yacc[c]);
+    };
+
+    int g = 0;
+    for (int d = 0; d < nchunks; ++d) {
+      const int64_t c0 = kb + (int64_t)d * OZ_KD;
+      const int npts = (int)min((int64_t)OZ_KD, ke - c0);
+      const int nst = (int)ceil_div((int64_t)npts, (int64_t)OZ_KS);
+      // ---- chunk setup: input points, per-row scale S (bound on |a| over the chunk)
+      eval_bar();  // previous chunk's points no longer read
+      const int64_t p0 = it.row0 + c0;
+      const double bx = inp.x[p0];
+      const double by = KIND == KK_NUFFT ? 0.0 : inp.y[p0];
+      const double bz = KIND == KK_PLATES ? inp.z[p0] : 0.0;
+      for (int k = tid; k < nst * OZ_KS; k += OZ_ETHREADS) {
+        // entries past the chunk repeat its first point: finite values whose B rows are zero
+        const int64_t pk = p0 + (k < npts ? k : 0);
+        const double x = inp.x[pk];
+        const double y = KIND == KK_NUFFT ? 0.0 : inp.y[pk];
+        const double z = KIND == KK_PLATES ? inp.z[pk] : 0.0;
+        PD[k] = make_double2(x, y);
+        if (KIND == KK_PLATES) PZ[k] = z;
+        PF[k] = make_float4((float)(x - bx), (float)(y - by), (float)(z - bz), 0.f);
+      }
+      if (tid < OZ_BM) Smin[tid] = 0x7F7FFFFFu;  // FLT_MAX bits
+      eval_bar();
+      if (KIND != KK_NUFFT) {
+        const int r = tid & (OZ_BM - 1), part = tid >> 7;
+        const int64_t gr = min(i0 + r, m_out - 1);
+        const float lx = (float)(outp.x[gr] - bx), ly = (float)(outp.y[gr] - by);
+        const float lz = KIND == KK_PLATES ? (float)(outp.z[gr] - bz) : 0.f;
+        float mn = 3.0e38f;
+        for (int k = part; k < npts; k += OZ_ETHREADS / OZ_BM) {
+          const float4 p = PF[k];
+          const float dx = lx - p.x, dy = ly - p.y;
+          float d2 = fmaf(dx, dx, dy * dy);
+          if (KIND == KK_PLATES) {
+            const float dz = lz - p.z;
+            d2 = fmaf(dz, dz, d2);
+          }
+          mn = fminf(mn, d2);
+        }
+        atomicMin(&Smin[r], __float_as_uint(mn));
+      }
+      eval_bar();
+      if (tid < OZ_BM) {
+        int S = 49;  // NUFFT: |a| = 1
+        if (KIND != KK_NUFFT) {
+          const float mn = __uint_as_float(Smin[tid]);
+          // amplitude bound with a factor-2 margin for the float distance estimate
+          double amax = mn > 1e-36f ? 2.0 / sqrt((double)mn) : 1e300;
+          if (KIND == KK_PLATES) amax /= keval::kFourPi;
+          S = amax < 1e300 ? 49 - ilogb(amax) : 0;
+        }
+        Srow[(d & 1) * OZ_BM + tid] = S;
+      }
+      eval_bar();
+      const double p2 = pow2(Srow[(d & 1) * OZ_BM + erow]);
+      for (int s = 0; s < nst; ++s, ++g) {
+        const int slot = g % OZ_NST;
+        if (g >= OZ_NST) mbar_wait(empty(slot), (uint32_t)((g / OZ_NST) - 1) & 1u);
+        const int64_t k0 = c0 + (int64_t)s * OZ_KS;  // item-relative first entry of the stage
+        if (tid == 0) {
+          mbar_expect_tx(fullB(slot), OZ_BSTAGE);
+          bulk_g2s(sB + slot * OZ_BSTAGE, bimg + (it.bstage0 + k0 / OZ_KS) * (int64_t)OZ_BSTAGE, OZ_BSTAGE,
+                   fullB(slot));
+        }
+        // ---- evaluate 8 entries, scale, round (magic-number: low word = low
+        // 32 bits of the integer, high word - 0x43380000 = high 32 bits)
+        uint32_t lo_r[8], hi_r[8], lo_i[8], hi_i[8];
+        const int kl = s * OZ_KS + kofs;  // chunk-relative
+#pragma unroll
+        for (int e = 0; e < 8; ++e) {
+          const double2 sp = PD[kl + e];
+          const double sz = KIND == KK_PLATES ? PZ[kl + e] : 0.0;
+          double tr, ti, amp;
+          if (MODE == OP_N)
+            entry_rounded<KIND, false>(ox, oy, oz, sp.x, sp.y, sz, kappa, p2, tab, tr, ti, amp);
+          else
+            entry_rounded<KIND, MODE == OP_H>(sp.x, sp.y, sz, ox, oy, oz, kappa, p2, tab, tr, ti, amp);
+          amp_hi = max(amp_hi, (uint32_t)__double2hiint(amp));
+          lo_r[e] = (uint32_t)__double2loint(tr);
+          hi_r[e] = (uint32_t)__double2hiint(tr) - 0x43380000u;
+          lo_i[e] = (uint32_t)__double2loint(ti);
+          hi_i[e] = (uint32_t)__double2hiint(ti) - 0x43380000u;
+        }
+        // ---- byte slices -> canonical K-major A images (4x4 byte transposes)
+        uint8_t* a0 = smem + SM_A + slot * OZ_ASTAGE;
+        const int off = ((kofs >> 4) * (OZ_BM / 8) + (erow >> 3)) * 128 + (erow & 7) * 16 + (kofs & 15);
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const uint32_t* lo = h ? lo_i : lo_r;
+          const uint32_t* hi = h ? hi_i : hi_r;
+          uint32_t l0[4], l1[4], h0[4], h1[4];
+          transpose4(lo[0], lo[1], lo[2], lo[3], l0);
+          transpose4(lo[4], lo[5], lo[6], lo[7], l1);
+          transpose4(hi[0], hi[1], hi[2], hi[3], h0);
+          transpose4(hi[4], hi[5], hi[6], hi[7], h1);
+          uint8_t* pl = a0 + h * OZ_APLANE + off;
+#pragma unroll
+          for (int p = 0; p < 4; ++p) *reinterpret_cast<uint2*>(pl + p * OZ_ASLICE) = make_uint2(l0[p], l1[p]);
+#pragma unroll
+          for (int p = 0; p < 3; ++p) *reinterpret_cast<uint2*>(pl + (4 + p) * OZ_ASLICE) = make_uint2(h0[p], h1[p]);
+        }
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        __syncwarp();
+        if (lane == 0) mbar_arrive(fullA(slot));
+        if (s == 0 && d > 0) drain(d - 1);
+      }
+    }
+    if (nchunks > 0) drain(nchunks - 1);
+    // |v| < 2^50 <=> high word of the scaled amplitude < 0x43100000 (NaN / inf fail)
+    if (KIND != KK_NUFFT && amp_hi >= 0x43100000u) atomicOr(flag, 2);
+
+    // ---- store: thread owns row drow, columns (dq & 1) * 16 + c of Re (dq < 2) or Im y
+    const int64_t go = i0 + drow;
+    if (go < m_out) {
+      double* Yb = reinterpret_cast<double*>(Y + it.ybase + (int64_t)blockIdx.z * pstride);
+      const int cb = (dq & 1) * 16, comp = dq >> 1;
+#pragma unroll
+      for (int c = 0; c < 16; ++c)
+        if (cb + c < it.ncols) Yb[2 * (go + (it.ycol + cb + c) * ldy) + comp] = yacc[c];
+    }
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  if (warp == OZ_EWARPS) {
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(OZ_TMEM_COLS));
+  }
+}
+
+__global__ void oz_reduce_kernel(const double2* __restrict__ P, int64_t pstride, int nsplit, double2* Y, int64_t ldy,
+                                 int64_t m, int64_t col0, int64_t ncols) {
+  const int64_t total = m * ncols;
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total; t += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t i = t % m, c = t / m;
+    const int64_t off = i + (col0 + c) * ldy;
+    double2 s = P[off];
+    for (int z = 1; z < nsplit; ++z) {
+      const double2 v = P[z * pstride + off];
+      s.x += v.x;
+      s.y += v.y;
+    }
+    Y[off] = s;
+  }
+}
+
+template <int KIND, int MODE>
+bool run_oz(Ctx* c, Points outp, Points inp, double kappa, int64_t m_out, const double2* X, double2* Y, int64_t ldy,
+            const MatvecSeg* segs, int nseg) {
+  std::vector<OzItem> items;
+  std::vector<const MatvecSeg*> item_seg;
+  int64_t max_rows = 0, max_col = 0, nstages = 0;
+  for (int s = 0; s < nseg; ++s) {
+    const MatvecSeg& g = segs[s];
+    if (g.ncols <= 0) continue;
+    if (g.rows <= 0) {
+      BFLY_CUDA(cudaMemset2DAsync(Y + g.col0 * ldy, ldy * sizeof(double2), 0, m_out * sizeof(double2), g.ncols,
+                                  c->stream));
+      continue;
+    }
+    for (int tc = 0; tc < g.ncols; tc += OZ_NCB) {
+      OzItem it{};
+      it.row0 = g.row0;
+      it.rows = g.rows;
+      it.x_off = g.x_off + (int64_t)tc * g.ldx;
+      it.ldx = g.ldx;
+      it.ycol = g.col0 + tc;
+      it.ncols = std::min(OZ_NCB, g.ncols - tc);
+      it.bstage0 = nstages;
+      nstages += ceil_div(g.rows, (int64_t)OZ_KS);
+      items.push_back(it);
+    }
+    max_rows = std::max(max_rows, g.rows);
+    max_col = std::max(max_col, g.col0 + (int64_t)g.ncols);
+  }
+  if (items.empty()) return true;
+  if (items.size() > 65535) fail(PRECONDITION, "matvec: too many work items");
+  const int64_t gx = ceil_div(m_out, (int64_t)OZ_BM);
+  const int64_t base_ctas = gx * (int64_t)items.size();
+  // split long segments so the grid covers every SM a few times (1 CTA / SM)
+  const int64_t target = (int64_t)c->sm_count * 4;
+  int nsplit = 1;
+  if (base_ctas < target) nsplit = (int)std::min<int64_t>(ceil_div(target, base_ctas), ceil_div(max_rows, OZ_KD));
+  nsplit = std::max(1, std::min(nsplit, 64));
+  const int64_t rows_per_split = ceil_div(ceil_div(max_rows, (int64_t)nsplit), (int64_t)OZ_KD) * OZ_KD;
+  nsplit = (int)ceil_div(max_rows, rows_per_split);
+
+  DBuf<OzItem> ditems(c, items.size());
+  ditems.upload(items.data(), items.size());
+  DBuf<int32_t> T(c, items.size() * OZ_NCB);
+  DBuf<uint8_t> img(c, (size_t)(nstages * OZ_BSTAGE));
+  DBuf<int> flag(c, 1);
+  flag.zero();
+  double kflops = 0, kbytes = 0;
+  for (const auto& it : items) {
+    kflops += 8.0 * (double)m_out * (double)it.rows * (double)it.ncols;
+    kbytes += 16.0 * ((double)it.rows + (double)m_out) * (double)it.ncols;
+  }
+  {
+    KTimer timer(c, "oz_prep", 0.0, (double)nstages * OZ_BSTAGE);
+    oz_colscale_kernel<<<dim3(OZ_NCB, (unsigned)items.size()), 256, 0, c->stream>>>(X, ditems.p, T.p);
+    BFLY_LAUNCH_CHECK("oz_colscale");
+    const int64_t per_item = ceil_div(max_rows, (int64_t)OZ_KS) * OZ_KS * OZ_NCB;
+    oz_slice_kernel<<<dim3((unsigned)ceil_div(per_item, (int64_t)256), (unsigned)items.size()), 256, 0, c->stream>>>(
+        X, ditems.p, T.p, img.p, flag.p);
+    BFLY_LAUNCH_CHECK("oz_slice");
+  }
+  auto kern = matvec_oz_kernel<KIND, MODE>;
+  BFLY_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, SM_TOTAL));
+  dim3 grid((unsigned)gx, (unsigned)items.size(), (unsigned)nsplit);
+  DBuf<double2> part;
+  int64_t pstride = 0;
+  double2* Yt = Y;
+  if (nsplit > 1) {
+    pstride = ldy * max_col;
+    part.reset(c, (size_t)(pstride * nsplit));
+    Yt = part.p;
+  }
+  {
+    KTimer timer(c, "kernel_matvec", kflops, kbytes);
+    kern<<<grid, OZ_THREADS, SM_TOTAL, c->stream>>>(outp, inp, kappa, m_out, img.p, T.p, Yt, ldy, ditems.p,
+                                                    rows_per_split, pstride, flag.p);
+    BFLY_LAUNCH_CHECK("kernel_matvec_oz");
+  }
+  if (nsplit > 1) {
+    for (int s = 0; s < nseg; ++s) {
+      const MatvecSeg& g = segs[s];
+      if (g.ncols <= 0 || g.rows <= 0) continue;
+      const int64_t total = m_out * g.ncols;
+      const unsigned blocks = (unsigned)std::min<int64_t>(ceil_div(total, (int64_t)256), (int64_t)c->sm_count * 16);
+      oz_reduce_kernel<<<blocks, 256, 0, c->stream>>>(part.p, pstride, nsplit, Y, ldy, m_out, g.col0, g.ncols);
+      BFLY_LAUNCH_CHECK("oz_reduce");
+    }
+  }
+  int hflag = 0;
+  flag.download(&hflag, 1);
+  c->sync();
+  return hflag == 0;
+}
+
+template <int KIND>
+bool dispatch_oz_mode(Ctx* c, int mode, Points outp, Points inp, double kappa, int64_t m_out, const double2* X,
+                      double2* Y, int64_t ldy, const MatvecSeg* segs, int nseg) {
+  if (mode == OP_N) return run_oz<KIND, OP_N>(c, outp, inp, kappa, m_out, X, Y, ldy, segs, nseg);
+  if (mode == OP_T) return run_oz<KIND, OP_T>(c, outp, inp, kappa, m_out, X, Y, ldy, segs, nseg);
+  return run_oz<KIND, OP_H>(c, outp, inp, kappa, m_out, X, Y, ldy, segs, nseg);
+}
+
+}  // namespace
+
+bool matvec_oz_enabled() {
+  const char* e = std::getenv("BFLY_MATVEC");
+  return !(e && std::string(e) == "fp64");
+}
+
+bool launch_kernel_matvec_oz(Ctx* c, int kind, int mode, Points outp, Points inp, double kappa, int64_t m_out,
+                             const double2* X, double2* Y, int64_t ldy, const MatvecSeg* segs, int nseg) {
+  if (m_out <= 0 || nseg <= 0) return true;
+  if (kind == KK_NUFFT) return dispatch_oz_mode<KK_NUFFT>(c, mode, outp, inp, kappa, m_out, X, Y, ldy, segs, nseg);
+  if (kind == KK_PLATES) return dispatch_oz_mode<KK_PLATES>(c, mode, outp, inp, kappa, m_out, X, Y, ldy, segs, nseg);
+  if (kind == KK_CIRCLE) return dispatch_oz_mode<KK_CIRCLE>(c, mode, outp, inp, kappa, m_out, X, Y, ldy, segs, nseg);
+  fail(PRECONDITION, "kernel_matvec: unknown kernel kind");
+  return false;
+}
+
+}  // namespace bfly

@@ -41,6 +41,13 @@ struct Points {
 template <typename R>
 void launch_kernel_matvec(Ctx* c, int kind, int mode, Points out_pts, Points in_pts, double kappa, int64_t m_out,
                           const cx<R>* X, cx<R>* Y, int64_t ldy, const MatvecSeg* segs_host, int nseg);
+// complex128 contraction on tcgen05 int8 (exact integer-slice scheme,
+// k_matvec_oz.cu); returns false if an entry fell outside the representable
+// range (the caller then recomputes on the FP64 DMMA path).  BFLY_MATVEC=fp64
+// selects the FP64 path.
+bool matvec_oz_enabled();
+bool launch_kernel_matvec_oz(Ctx* c, int kind, int mode, Points out_pts, Points in_pts, double kappa, int64_t m_out,
+                             const double2* X, double2* Y, int64_t ldy, const MatvecSeg* segs_host, int nseg);
 
 // ------------------------------------------ K3/K4: batched block GEMM
 // C_e (M x ncols_e) (+)= sum_{s<S} op(A + a_s) (M x K) * (B + b_s) (K x ncols_e)
