@@ -39,6 +39,7 @@
 // coincident point, a bound that did not hold) the launch reports it and the
 // caller recomputes the product with the FP64 DMMA kernel.
 #include <algorithm>
+#include <cstdio>
 #include <cstdlib>
 #include <string>
 #include <vector>
@@ -61,7 +62,7 @@ constexpr int OZ_NST = 2;                         // ring depth
 constexpr int OZ_BM = 128;                        // output rows per CTA (= TMEM lanes)
 constexpr int OZ_EWARPS = 16;
 constexpr int OZ_ETHREADS = OZ_EWARPS * 32;
-constexpr int OZ_THREADS = OZ_ETHREADS + 32;      // + MMA warp
+constexpr int OZ_THREADS = OZ_ETHREADS;           // no dedicated MMA warp
 constexpr int OZ_EPT = OZ_BM * OZ_KS / OZ_ETHREADS;  // 8 entries per thread per stage
 constexpr int OZ_ASLICE = OZ_BM * OZ_KS;           // 4096 B: one A slice (128 rows x 32 B)
 constexpr int OZ_APLANE = OZ_NSL * OZ_ASLICE;      // 28672 B
@@ -82,8 +83,9 @@ constexpr int SM_S = SM_PF + OZ_KD * 16;           // int S_row [2][128]
 constexpr int SM_T = SM_S + 2 * OZ_BM * 4;         // int T [NCB]
 constexpr int SM_MIN = SM_T + OZ_NCB * 4;          // uint min d2 bits [128]
 constexpr int SM_TAB = SM_MIN + OZ_BM * 4;         // double2 sin/cos table [256]
-constexpr int SM_BAR = SM_TAB + 256 * 16;          // mbarriers
-constexpr int NBAR = 3 * OZ_NST + 2;
+constexpr int SM_CNT = SM_TAB + 256 * 16;          // uint stage arrival counters [NST]
+constexpr int SM_BAR = SM_CNT + 16;                // mbarriers
+constexpr int NBAR = 2 * OZ_NST + 1;
 constexpr int SM_TMEM = SM_BAR + NBAR * 8;
 constexpr int SM_TOTAL = SM_TMEM + 16;
 static_assert(SM_TOTAL <= 232448, "shared memory budget");
@@ -95,6 +97,21 @@ struct OzItem {
   int64_t bstage0;      // first B stage image of this item
   int32_t ncols, pad_;
 };
+
+// Per-stage MMA schedule.  Plane h (0: A_re x G1, 1: A_im x G2), slice p,
+// first diagonal block jlo, block count nb (N = 64 nb <= 256), init (first
+// K-step of a chunk writes instead of accumulating).  The initialising MMAs
+// (plane 0) come first and cover the 8 diagonal blocks disjointly.
+//   packed: h | p << 1 | jlo << 4 | nb << 7 | init << 10
+constexpr uint32_t mma_code(int h, int p, int jlo, int nb, int init) {
+  return (uint32_t)(h | (p << 1) | (jlo << 4) | (nb << 7) | (init << 10));
+}
+#define OZ_PLANE_LIST(h, I)                                                                                    \
+  mma_code(h, 6, 1, 4, I), mma_code(h, 6, 5, 3, I), mma_code(h, 5, 0, 1, I), mma_code(h, 5, 1, 4, 0),          \
+      mma_code(h, 5, 5, 2, 0), mma_code(h, 4, 0, 4, 0), mma_code(h, 4, 4, 2, 0), mma_code(h, 3, 0, 4, 0),      \
+      mma_code(h, 3, 4, 1, 0), mma_code(h, 2, 0, 4, 0), mma_code(h, 1, 0, 3, 0), mma_code(h, 0, 0, 2, 0)
+constexpr int OZ_NMMA = 24;
+static_assert(OZ_MAXB == 4, "schedule assumes 64-column diagonal blocks");
 
 // ------------------------------------------------------------ PTX helpers
 __device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
@@ -141,6 +158,14 @@ __device__ __forceinline__ void bulk_g2s(uint32_t dst, const void* src, uint32_t
                "l"(src), "r"(bytes), "r"(bar)
                : "memory");
 }
+#ifdef OZ_TRACE
+__device__ unsigned long long g_oz_trace[8];
+#define OZT_BEGIN(v) const long long v = clock64();
+#define OZT_END(v, slot) atomicAdd(&g_oz_trace[slot], (unsigned long long)(clock64() - v));
+#else
+#define OZT_BEGIN(v)
+#define OZT_END(v, slot)
+#endif
 __device__ __forceinline__ void eval_bar() { asm volatile("bar.sync 1, %0;" ::"n"(OZ_EWARPS * 32) : "memory"); }
 
 __device__ __forceinline__ void tmem_ld16(uint32_t addr, uint32_t (&v)[16]) {
@@ -291,6 +316,14 @@ __global__ void oz_slice_kernel(const double2* __restrict__ X, const OzItem* __r
 }
 
 // ------------------------------------------------------------ main kernel
+// Issue scheme: no dedicated MMA warp.  Each warp, after writing its part of
+// an A stage, bumps the stage's arrival counter; the LAST warp to arrive
+// issues the stage's MMAs (after the B bulk copy landed) and commits them to
+// the slot's `empty` barrier (and, on a chunk's last stage, to `acc_full`).
+// Chunk d-1 is drained by every warp BEFORE it arrives for stage 0 of chunk
+// d, so the issuer of that stage knows TMEM is free.  tcgen05 MMAs of a CTA
+// execute in issue order, so acc_full (committed by the last stage's
+// issuer) covers the whole chunk.
 template <int KIND, int MODE>
 __global__ void __launch_bounds__(OZ_THREADS, 1)
     matvec_oz_kernel(Points outp, Points inp, double kappa, int64_t m_out, const uint8_t* __restrict__ bimg,
@@ -298,6 +331,7 @@ __global__ void __launch_bounds__(OZ_THREADS, 1)
                      const OzItem* __restrict__ items, int64_t rows_per_split, int64_t pstride, int* __restrict__ flag) {
   extern __shared__ __align__(1024) uint8_t smem[];
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  OZT_BEGIN(t5)
   const OzItem it = items[blockIdx.y];
   const int64_t i0 = (int64_t)blockIdx.x * OZ_BM;
   const int64_t kb = (int64_t)blockIdx.z * rows_per_split;
@@ -311,26 +345,25 @@ __global__ void __launch_bounds__(OZ_THREADS, 1)
   int* Srow = reinterpret_cast<int*>(smem + SM_S);
   int* Ts = reinterpret_cast<int*>(smem + SM_T);
   unsigned* Smin = reinterpret_cast<unsigned*>(smem + SM_MIN);
+  unsigned* cnt = reinterpret_cast<unsigned*>(smem + SM_CNT);
   const uint32_t bar0 = smem_u32(smem + SM_BAR);
-  auto fullA = [&](int s) { return bar0 + 8u * s; };
-  auto fullB = [&](int s) { return bar0 + 8u * (OZ_NST + s); };
-  auto empty = [&](int s) { return bar0 + 8u * (2 * OZ_NST + s); };
-  const uint32_t acc_full = bar0 + 8u * (3 * OZ_NST), acc_empty = acc_full + 8u;
+  auto fullB = [&](int s) { return bar0 + 8u * s; };
+  auto empty = [&](int s) { return bar0 + 8u * (OZ_NST + s); };
+  const uint32_t acc_full = bar0 + 8u * (2 * OZ_NST);
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + SM_TMEM);
 
-  if (warp == OZ_EWARPS) {
+  if (warp == 0) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
                  "n"(OZ_TMEM_COLS));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
   }
-  if (tid == 0) {
+  if (tid == 32) {
     for (int s = 0; s < OZ_NST; ++s) {
-      mbar_init(fullA(s), OZ_EWARPS);
       mbar_init(fullB(s), 1);
       mbar_init(empty(s), 1);
+      cnt[s] = 0;
     }
     mbar_init(acc_full, 1);
-    mbar_init(acc_empty, OZ_EWARPS);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (tid < OZ_NCB) Ts[tid] = Tg[blockIdx.y * OZ_NCB + tid];
@@ -346,210 +379,203 @@ __global__ void __launch_bounds__(OZ_THREADS, 1)
   const uint32_t tmem = *tmem_slot;
   const uint32_t sA = smem_u32(smem + SM_A), sB = smem_u32(smem + SM_B);
 
-  if (warp == OZ_EWARPS) {
-    // ======================= MMA issuer (one thread) =======================
-    if (lane == 0) {
-      int g = 0;
-      for (int d = 0; d < nchunks; ++d) {
-        const int64_t c0 = kb + (int64_t)d * OZ_KD;
-        const int nst = (int)ceil_div(min((int64_t)OZ_KD, ke - c0), (int64_t)OZ_KS);
-        for (int s = 0; s < nst; ++s, ++g) {
-          const int slot = g % OZ_NST;
-          const uint32_t ph = (uint32_t)(g / OZ_NST) & 1u;
-          mbar_wait_sleep(fullA(slot), ph);
-          mbar_wait_sleep(fullB(slot), ph);
-          if (s == 0 && d > 0) mbar_wait_sleep(acc_empty, (uint32_t)(d - 1) & 1u);
-          asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-          const uint32_t a0 = sA + slot * OZ_ASTAGE, b0 = sB + slot * OZ_BSTAGE;
-          // plane h: A_re x G1, A_im x G2 into the same accumulator
-          auto issue = [&](int h, int p, int jlo, int nb, bool init) {
-            const uint64_t da = smem_desc(a0 + h * OZ_APLANE + p * OZ_ASLICE, (OZ_BM / 8) * 128, 128);
-            const int q0 = jlo + 5 - p;
-            const uint64_t db = smem_desc(b0 + h * OZ_BOPER + q0 * OZ_BN2 * 16, (OZ_BROWS / 8) * 128, 128);
-            mma_i8(tmem + jlo * OZ_BN2, da, db, idesc_i8(128, nb * OZ_BN2, p == OZ_NSL - 1, true),
-                   (init && s == 0) ? 0u : 1u);
-          };
+  // evaluation: row (warp & 7) * 16 + lane / 2, entries kofs .. kofs + 7 of each stage
+  const int erow = (warp & 7) * 16 + (lane >> 1);
+  const int kofs = (warp >> 3) * 16 + (lane & 1) * 8;
+  const int64_t gi = min(i0 + erow, m_out - 1);  // padded rows evaluate a valid row (never stored)
+  const double ox = outp.x[gi];
+  const double oy = KIND == KK_NUFFT ? 0.0 : outp.y[gi];
+  const double oz = KIND == KK_PLATES ? outp.z[gi] : 0.0;
+  // drain: TMEM lane quarter = warp & 3, column quarter = warp >> 2
+  // (0, 1: Re y columns 0-15 / 16-31; 2, 3: Im y columns 0-15 / 16-31)
+  const int drow = (warp & 3) * 32 + lane;
+  const int dq = warp >> 2;
+  double yacc[16];
 #pragma unroll
-          for (int h = 0; h < 2; ++h) {
-            const bool first = h == 0;
-            // initialising MMAs first (disjoint cover of the 8 diagonal blocks)
-            for (int j = 1; j <= 7; j += OZ_MAXB) issue(h, 6, j, min(OZ_MAXB, 8 - j), first);
-            issue(h, 5, 0, 1, first);
-            for (int j = 1; j <= 6; j += OZ_MAXB) issue(h, 5, j, min(OZ_MAXB, 7 - j), false);
-#pragma unroll
-            for (int p = 4; p >= 0; --p) {
-              const int jhi = p + 1;
-              for (int j = 0; j <= jhi; j += OZ_MAXB) issue(h, p, j, min(OZ_MAXB, jhi - j + 1), false);
-            }
-          }
-          mma_commit(empty(slot));
-          if (s == nst - 1) mma_commit(acc_full);
-        }
-      }
-    }
-  } else {
-    // ================== evaluation / drain warps ==================
-    // evaluation: row (warp & 7) * 16 + lane / 2, entries kofs .. kofs + 7 of each stage
-    const int erow = (warp & 7) * 16 + (lane >> 1);
-    const int kofs = (warp >> 3) * 16 + (lane & 1) * 8;
-    const int64_t gi = min(i0 + erow, m_out - 1);  // padded rows evaluate a valid row (never stored)
-    const double ox = outp.x[gi];
-    const double oy = KIND == KK_NUFFT ? 0.0 : outp.y[gi];
-    const double oz = KIND == KK_PLATES ? outp.z[gi] : 0.0;
-    // drain: TMEM lane quarter = warp & 3, column quarter = warp >> 2
-    // (0, 1: Re y columns 0-15 / 16-31; 2, 3: Im y columns 0-15 / 16-31)
-    const int drow = (warp & 3) * 32 + lane;
-    const int dq = warp >> 2;
-    double yacc[16];
-#pragma unroll
-    for (int c = 0; c < 16; ++c) yacc[c] = 0.0;
-    uint32_t amp_hi = 0;  // max high word of the scaled amplitudes
+  for (int c = 0; c < 16; ++c) yacc[c] = 0.0;
+  uint32_t amp_hi = 0;  // max high word of the scaled amplitudes
 
-    auto drain = [&](int d) {
-      mbar_wait(acc_full, (uint32_t)d & 1u);
-      asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-      double t[16];
+  auto drain = [&](int d) {
+    OZT_BEGIN(t4)
+    mbar_wait(acc_full, (uint32_t)d & 1u);
+    if (lane == 0) { OZT_END(t4, 4) }
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    double t[16];
 #pragma unroll
-      for (int j = OZ_NDIAG - 1; j >= 0; --j) {
-        uint32_t v[16];
-        tmem_ld16(tmem + ((uint32_t)((warp & 3) * 32) << 16) + j * OZ_BN2 + dq * 16, v);
-        asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+    for (int j = OZ_NDIAG - 1; j >= 0; --j) {
+      uint32_t v[16];
+      tmem_ld16(tmem + ((uint32_t)((warp & 3) * 32) << 16) + j * OZ_BN2 + dq * 16, v);
+      asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 #pragma unroll
-        for (int c = 0; c < 16; ++c) t[c] = (j == OZ_NDIAG - 1) ? i2d(v[c]) : fma(t[c], 256.0, i2d(v[c]));
+      for (int c = 0; c < 16; ++c) t[c] = (j == OZ_NDIAG - 1) ? i2d(v[c]) : fma(t[c], 256.0, i2d(v[c]));
+    }
+    const int S = Srow[(d & 1) * OZ_BM + drow];
+    const int c0 = (dq & 1) * 16;
+#pragma unroll
+    for (int c = 0; c < 16; ++c) yacc[c] = fma(t[c], pow2(40 - S - Ts[c0 + c]), yacc[c]);
+  };
+
+  // One MMA of a stage (index i < OZ_NMMA of the fixed schedule kMmaList)
+  auto issue_mma = [&](int i, uint32_t a0, uint32_t b0, int s) {
+    constexpr uint32_t kList[OZ_NMMA] = {OZ_PLANE_LIST(0, 1), OZ_PLANE_LIST(1, 0)};
+    const uint32_t e = kList[i];
+    const int h = e & 1, p = (e >> 1) & 7, jlo = (e >> 4) & 7, nb = (e >> 7) & 7;
+    const bool init = (e >> 10) & 1;
+    const uint64_t da = smem_desc(a0 + h * OZ_APLANE + p * OZ_ASLICE, (OZ_BM / 8) * 128, 128);
+    const int q0 = jlo + 5 - p;
+    const uint64_t db = smem_desc(b0 + h * OZ_BOPER + q0 * OZ_BN2 * 16, (OZ_BROWS / 8) * 128, 128);
+    mma_i8(tmem + jlo * OZ_BN2, da, db, idesc_i8(128, nb * OZ_BN2, p == OZ_NSL - 1, true),
+           (init && s == 0) ? 0u : 1u);
+  };
+  // all MMAs of a stage (called by the last-arriving warp's lane 0)
+  auto issue_stage = [&](int slot, uint32_t ph, int s, int nst) {
+    mbar_wait(fullB(slot), ph);
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    const uint32_t a0 = sA + slot * OZ_ASTAGE, b0 = sB + slot * OZ_BSTAGE;
+#pragma unroll
+    for (int i = 0; i < OZ_NMMA; ++i) issue_mma(i, a0, b0, s);
+    mma_commit(empty(slot));
+    if (s == nst - 1) mma_commit(acc_full);
+  };
+
+  int g = 0;
+  for (int d = 0; d < nchunks; ++d) {
+    const int64_t c0 = kb + (int64_t)d * OZ_KD;
+    const int npts = (int)min((int64_t)OZ_KD, ke - c0);
+    const int nst = (int)ceil_div((int64_t)npts, (int64_t)OZ_KS);
+    // ---- chunk setup: input points, per-row scale S (bound on |a| over the chunk)
+    OZT_BEGIN(t6)
+    __syncthreads();  // previous chunk's points no longer read
+    const int64_t p0 = it.row0 + c0;
+    const double bx = inp.x[p0];
+    const double by = KIND == KK_NUFFT ? 0.0 : inp.y[p0];
+    const double bz = KIND == KK_PLATES ? inp.z[p0] : 0.0;
+    for (int k = tid; k < nst * OZ_KS; k += OZ_THREADS) {
+      // entries past the chunk repeat its first point: finite values whose B rows are zero
+      const int64_t pk = p0 + (k < npts ? k : 0);
+      const double x = inp.x[pk];
+      const double y = KIND == KK_NUFFT ? 0.0 : inp.y[pk];
+      const double z = KIND == KK_PLATES ? inp.z[pk] : 0.0;
+      PD[k] = make_double2(x, y);
+      if (KIND == KK_PLATES) PZ[k] = z;
+      PF[k] = make_float4((float)(x - bx), (float)(y - by), (float)(z - bz), 0.f);
+    }
+    if (tid < OZ_BM) Smin[tid] = 0x7F7FFFFFu;  // FLT_MAX bits
+    __syncthreads();
+    if (KIND != KK_NUFFT) {
+      const int r = tid & (OZ_BM - 1), part = tid >> 7;
+      const int64_t gr = min(i0 + r, m_out - 1);
+      const float lx = (float)(outp.x[gr] - bx), ly = (float)(outp.y[gr] - by);
+      const float lz = KIND == KK_PLATES ? (float)(outp.z[gr] - bz) : 0.f;
+      float mn = 3.0e38f;
+      for (int k = part; k < npts; k += OZ_THREADS / OZ_BM) {
+        const float4 p = PF[k];
+        const float dx = lx - p.x, dy = ly - p.y;
+        float d2 = fmaf(dx, dx, dy * dy);
+        if (KIND == KK_PLATES) {
+          const float dz = lz - p.z;
+          d2 = fmaf(dz, dz, d2);
+        }
+        mn = fminf(mn, d2);
       }
+      atomicMin(&Smin[r], __float_as_uint(mn));
+    }
+    __syncthreads();
+    if (tid < OZ_BM) {
+      int S = 49;  // NUFFT: |a| = 1
+      if (KIND != KK_NUFFT) {
+        const float mn = __uint_as_float(Smin[tid]);
+        // amplitude bound with a factor-2 margin for the float distance estimate
+        double amax = mn > 1e-36f ? 2.0 / sqrt((double)mn) : 1e300;
+        if (KIND == KK_PLATES) amax /= keval::kFourPi;
+        S = amax < 1e300 ? 49 - ilogb(amax) : 0;
+      }
+      Srow[(d & 1) * OZ_BM + tid] = S;
+    }
+    __syncthreads();
+    if (lane == 0) { OZT_END(t6, 6) }
+    const double p2 = pow2(Srow[(d & 1) * OZ_BM + erow]);
+    for (int s = 0; s < nst; ++s, ++g) {
+      const int slot = g % OZ_NST;
+      const uint32_t ph = (uint32_t)(g / OZ_NST) & 1u;
+      OZT_BEGIN(t3)
+      if (g >= OZ_NST) mbar_wait(empty(slot), ph ^ 1u);
+      if (lane == 0) { OZT_END(t3, 3) }
+      const int64_t k0 = c0 + (int64_t)s * OZ_KS;  // item-relative first entry of the stage
+      if (tid == 0) {
+        mbar_expect_tx(fullB(slot), OZ_BSTAGE);
+        bulk_g2s(sB + slot * OZ_BSTAGE, bimg + (it.bstage0 + k0 / OZ_KS) * (int64_t)OZ_BSTAGE, OZ_BSTAGE,
+                 fullB(slot));
+      }
+      // ---- evaluate 8 entries, scale, round (magic-number: low word = low
+      // 32 bits of the integer, high word - 0x43380000 = high 32 bits)
+      uint32_t lo_r[8], hi_r[8], lo_i[8], hi_i[8];
+      const int kl = s * OZ_KS + kofs;  // chunk-relative
+#pragma unroll
+      for (int e = 0; e < 8; ++e) {
+        const double2 sp = PD[kl + e];
+        const double sz = KIND == KK_PLATES ? PZ[kl + e] : 0.0;
+        double tr, ti, amp;
+        if (MODE == OP_N)
+          entry_rounded<KIND, false>(ox, oy, oz, sp.x, sp.y, sz, kappa, p2, tab, tr, ti, amp);
+        else
+          entry_rounded<KIND, MODE == OP_H>(sp.x, sp.y, sz, ox, oy, oz, kappa, p2, tab, tr, ti, amp);
+        amp_hi = max(amp_hi, (uint32_t)__double2hiint(amp));
+        lo_r[e] = (uint32_t)__double2loint(tr);
+        hi_r[e] = (uint32_t)__double2hiint(tr) - 0x43380000u;
+        lo_i[e] = (uint32_t)__double2loint(ti);
+        hi_i[e] = (uint32_t)__double2hiint(ti) - 0x43380000u;
+      }
+      // ---- byte slices -> canonical K-major A images (4x4 byte transposes)
+      uint8_t* a0 = smem + SM_A + slot * OZ_ASTAGE;
+      const int off = ((kofs >> 4) * (OZ_BM / 8) + (erow >> 3)) * 128 + (erow & 7) * 16 + (kofs & 15);
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const uint32_t* lo = h ? lo_i : lo_r;
+        const uint32_t* hi = h ? hi_i : hi_r;
+        uint32_t l0[4], l1[4], h0[4], h1[4];
+        transpose4(lo[0], lo[1], lo[2], lo[3], l0);
+        transpose4(lo[4], lo[5], lo[6], lo[7], l1);
+        transpose4(hi[0], hi[1], hi[2], hi[3], h0);
+        transpose4(hi[4], hi[5], hi[6], hi[7], h1);
+        uint8_t* pl = a0 + h * OZ_APLANE + off;
+#pragma unroll
+        for (int p = 0; p < 4; ++p) *reinterpret_cast<uint2*>(pl + p * OZ_ASLICE) = make_uint2(l0[p], l1[p]);
+#pragma unroll
+        for (int p = 0; p < 3; ++p) *reinterpret_cast<uint2*>(pl + (4 + p) * OZ_ASLICE) = make_uint2(h0[p], h1[p]);
+      }
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      if (s == 0 && d > 0) drain(d - 1);  // TMEM must be free before this stage's MMAs
       asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
       __syncwarp();
-      if (lane == 0) mbar_arrive(acc_empty);
-      const int S = Srow[(d & 1) * OZ_BM + drow];
-      const int c0 = (dq & 1) * 16;
-#pragma unroll
-      for (int c = 0; c < 16; ++c) yacc[c] = fma(t[c], pow2(40 - S - Ts[c0 + c]), yacc[c]);
-    };
-
-    int g = 0;
-    for (int d = 0; d < nchunks; ++d) {
-      const int64_t c0 = kb + (int64_t)d * OZ_KD;
-      const int npts = (int)min((int64_t)OZ_KD, ke - c0);
-      const int nst = (int)ceil_div((int64_t)npts, (int64_t)OZ_KS);
-      // ---- chunk setup: input points, per-row scale S (bound on |a| over the chunk)
-      eval_bar();  // previous chunk's points no longer read
-      const int64_t p0 = it.row0 + c0;
-      const double bx = inp.x[p0];
-      const double by = KIND == KK_NUFFT ? 0.0 : inp.y[p0];
-      const double bz = KIND == KK_PLATES ? inp.z[p0] : 0.0;
-      for (int k = tid; k < nst * OZ_KS; k += OZ_ETHREADS) {
-        // entries past the chunk repeat its first point: finite values whose B rows are zero
-        const int64_t pk = p0 + (k < npts ? k : 0);
-        const double x = inp.x[pk];
-        const double y = KIND == KK_NUFFT ? 0.0 : inp.y[pk];
-        const double z = KIND == KK_PLATES ? inp.z[pk] : 0.0;
-        PD[k] = make_double2(x, y);
-        if (KIND == KK_PLATES) PZ[k] = z;
-        PF[k] = make_float4((float)(x - bx), (float)(y - by), (float)(z - bz), 0.f);
+      if (lane == 0) {
+        __threadfence_block();
+        if (atomicAdd(&cnt[slot], 1u) == OZ_EWARPS - 1) {  // last warp in: issue the stage
+          cnt[slot] = 0;
+          __threadfence_block();
+          issue_stage(slot, ph, s, nst);
+        }
       }
-      if (tid < OZ_BM) Smin[tid] = 0x7F7FFFFFu;  // FLT_MAX bits
-      eval_bar();
-      if (KIND != KK_NUFFT) {
-        const int r = tid & (OZ_BM - 1), part = tid >> 7;
-        const int64_t gr = min(i0 + r, m_out - 1);
-        const float lx = (float)(outp.x[gr] - bx), ly = (float)(outp.y[gr] - by);
-        const float lz = KIND == KK_PLATES ? (float)(outp.z[gr] - bz) : 0.f;
-        float mn = 3.0e38f;
-        for (int k = part; k < npts; k += OZ_ETHREADS / OZ_BM) {
-          const float4 p = PF[k];
-          const float dx = lx - p.x, dy = ly - p.y;
-          float d2 = fmaf(dx, dx, dy * dy);
-          if (KIND == KK_PLATES) {
-            const float dz = lz - p.z;
-            d2 = fmaf(dz, dz, d2);
-          }
-          mn = fminf(mn, d2);
-        }
-        atomicMin(&Smin[r], __float_as_uint(mn));
-      }
-      eval_bar();
-      if (tid < OZ_BM) {
-        int S = 49;  // NUFFT: |a| = 1
-        if (KIND != KK_NUFFT) {
-          const float mn = __uint_as_float(Smin[tid]);
-          // amplitude bound with a factor-2 margin for the float distance estimate
-          double amax = mn > 1e-36f ? 2.0 / sqrt((double)mn) : 1e300;
-          if (KIND == KK_PLATES) amax /= keval::kFourPi;
-          S = amax < 1e300 ? 49 - ilogb(amax) : 0;
-        }
-        Srow[(d & 1) * OZ_BM + tid] = S;
-      }
-      eval_bar();
-      const double p2 = pow2(Srow[(d & 1) * OZ_BM + erow]);
-      for (int s = 0; s < nst; ++s, ++g) {
-        const int slot = g % OZ_NST;
-        if (g >= OZ_NST) mbar_wait(empty(slot), (uint32_t)((g / OZ_NST) - 1) & 1u);
-        const int64_t k0 = c0 + (int64_t)s * OZ_KS;  // item-relative first entry of the stage
-        if (tid == 0) {
-          mbar_expect_tx(fullB(slot), OZ_BSTAGE);
-          bulk_g2s(sB + slot * OZ_BSTAGE, bimg + (it.bstage0 + k0 / OZ_KS) * (int64_t)OZ_BSTAGE, OZ_BSTAGE,
-                   fullB(slot));
-        }
-        // ---- evaluate 8 entries, scale, round (magic-number: low word = low
-        // 32 bits of the integer, high word - 0x43380000 = high 32 bits)
-        uint32_t lo_r[8], hi_r[8], lo_i[8], hi_i[8];
-        const int kl = s * OZ_KS + kofs;  // chunk-relative
-#pragma unroll
-        for (int e = 0; e < 8; ++e) {
-          const double2 sp = PD[kl + e];
-          const double sz = KIND == KK_PLATES ? PZ[kl + e] : 0.0;
-          double tr, ti, amp;
-          if (MODE == OP_N)
-            entry_rounded<KIND, false>(ox, oy, oz, sp.x, sp.y, sz, kappa, p2, tab, tr, ti, amp);
-          else
-            entry_rounded<KIND, MODE == OP_H>(sp.x, sp.y, sz, ox, oy, oz, kappa, p2, tab, tr, ti, amp);
-          amp_hi = max(amp_hi, (uint32_t)__double2hiint(amp));
-          lo_r[e] = (uint32_t)__double2loint(tr);
-          hi_r[e] = (uint32_t)__double2hiint(tr) - 0x43380000u;
-          lo_i[e] = (uint32_t)__double2loint(ti);
-          hi_i[e] = (uint32_t)__double2hiint(ti) - 0x43380000u;
-        }
-        // ---- byte slices -> canonical K-major A images (4x4 byte transposes)
-        uint8_t* a0 = smem + SM_A + slot * OZ_ASTAGE;
-        const int off = ((kofs >> 4) * (OZ_BM / 8) + (erow >> 3)) * 128 + (erow & 7) * 16 + (kofs & 15);
-#pragma unroll
-        for (int h = 0; h < 2; ++h) {
-          const uint32_t* lo = h ? lo_i : lo_r;
-          const uint32_t* hi = h ? hi_i : hi_r;
-          uint32_t l0[4], l1[4], h0[4], h1[4];
-          transpose4(lo[0], lo[1], lo[2], lo[3], l0);
-          transpose4(lo[4], lo[5], lo[6], lo[7], l1);
-          transpose4(hi[0], hi[1], hi[2], hi[3], h0);
-          transpose4(hi[4], hi[5], hi[6], hi[7], h1);
-          uint8_t* pl = a0 + h * OZ_APLANE + off;
-#pragma unroll
-          for (int p = 0; p < 4; ++p) *reinterpret_cast<uint2*>(pl + p * OZ_ASLICE) = make_uint2(l0[p], l1[p]);
-#pragma unroll
-          for (int p = 0; p < 3; ++p) *reinterpret_cast<uint2*>(pl + (4 + p) * OZ_ASLICE) = make_uint2(h0[p], h1[p]);
-        }
-        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-        __syncwarp();
-        if (lane == 0) mbar_arrive(fullA(slot));
-        if (s == 0 && d > 0) drain(d - 1);
-      }
+      __syncwarp();
     }
-    if (nchunks > 0) drain(nchunks - 1);
-    // |v| < 2^50 <=> high word of the scaled amplitude < 0x43100000 (NaN / inf fail)
-    if (KIND != KK_NUFFT && amp_hi >= 0x43100000u) atomicOr(flag, 2);
+  }
+  if (nchunks > 0) drain(nchunks - 1);
+  // |v| < 2^50 <=> high word of the scaled amplitude < 0x43100000 (NaN / inf fail)
+  if (KIND != KK_NUFFT && amp_hi >= 0x43100000u) atomicOr(flag, 2);
 
-    // ---- store: thread owns row drow, columns (dq & 1) * 16 + c of Re (dq < 2) or Im y
-    const int64_t go = i0 + drow;
-    if (go < m_out) {
-      double* Yb = reinterpret_cast<double*>(Y + it.ybase + (int64_t)blockIdx.z * pstride);
-      const int cb = (dq & 1) * 16, comp = dq >> 1;
+  // ---- store: thread owns row drow, columns (dq & 1) * 16 + c of Re (dq < 2) or Im y
+  const int64_t go = i0 + drow;
+  if (go < m_out) {
+    double* Yb = reinterpret_cast<double*>(Y + it.ybase + (int64_t)blockIdx.z * pstride);
+    const int cb = (dq & 1) * 16, comp = dq >> 1;
 #pragma unroll
-      for (int c = 0; c < 16; ++c)
-        if (cb + c < it.ncols) Yb[2 * (go + (it.ycol + cb + c) * ldy) + comp] = yacc[c];
-    }
+    for (int c = 0; c < 16; ++c)
+      if (cb + c < it.ncols) Yb[2 * (go + (it.ycol + cb + c) * ldy) + comp] = yacc[c];
   }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   __syncthreads();
-  if (warp == OZ_EWARPS) {
+  if (tid == 0) { OZT_END(t5, 5) }
+  if (warp == 0) {
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(OZ_TMEM_COLS));
   }
@@ -659,6 +685,18 @@ bool run_oz(Ctx* c, Points outp, Points inp, double kappa, int64_t m_out, const 
       BFLY_LAUNCH_CHECK("oz_reduce");
     }
   }
+#ifdef OZ_TRACE
+  {
+    unsigned long long tr[8];
+    c->sync();
+    BFLY_CUDA(cudaMemcpyFromSymbol(tr, g_oz_trace, sizeof(tr)));
+    const double ctas = (double)gx * items.size() * nsplit;
+    fprintf(stderr, "[oz] ctas %.0f per-CTA cycles: total %.0f | per warp: wait empty %.0f accF %.0f setup %.0f\n",
+            ctas, tr[5] / ctas, tr[3] / ctas / OZ_EWARPS, tr[4] / ctas / OZ_EWARPS, tr[6] / ctas / OZ_EWARPS);
+    unsigned long long z[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    BFLY_CUDA(cudaMemcpyToSymbol(g_oz_trace, z, sizeof(z)));
+  }
+#endif
   int hflag = 0;
   flag.download(&hflag, 1);
   c->sync();
