@@ -83,7 +83,8 @@ constexpr int SM_S = SM_PF + OZ_KD * 16;           // int S_row [2][128]
 constexpr int SM_T = SM_S + 2 * OZ_BM * 4;         // int T [NCB]
 constexpr int SM_MIN = SM_T + OZ_NCB * 4;          // uint min d2 bits [128]
 constexpr int SM_TAB = SM_MIN + OZ_BM * 4;         // double2 sin/cos table [256]
-constexpr int SM_CNT = SM_TAB + 256 * 16;          // uint stage arrival counters [NST]
+constexpr int SM_BOX = SM_TAB + 256 * 16;          // float4 sub-box bounds [32][2]
+constexpr int SM_CNT = SM_BOX + 64 * 16;           // uint stage arrival counters [NST]
 constexpr int SM_BAR = SM_CNT + 16;                // mbarriers
 constexpr int NBAR = 2 * OZ_NST + 1;
 constexpr int SM_TMEM = SM_BAR + NBAR * 8;
@@ -463,18 +464,55 @@ __global__ void __launch_bounds__(OZ_THREADS, 1)
     if (tid < OZ_BM) Smin[tid] = 0x7F7FFFFFu;  // FLT_MAX bits
     __syncthreads();
     if (KIND != KK_NUFFT) {
+      // bounding boxes of the 32 sub-boxes of 32 consecutive (tree-ordered) points
+      float4* BX = reinterpret_cast<float4*>(smem + SM_BOX);  // [32][lo, hi]
+#pragma unroll
+      for (int q = 0; q < 2; ++q) {
+        const int sb = warp * 2 + q;
+        const float4 pt = PF[min(sb * 32 + lane, OZ_KD - 1)];
+        float lx = pt.x, ly = pt.y, lz = pt.z, hx = pt.x, hy = pt.y, hz = pt.z;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+          lx = fminf(lx, __shfl_xor_sync(0xffffffffu, lx, o));
+          ly = fminf(ly, __shfl_xor_sync(0xffffffffu, ly, o));
+          lz = fminf(lz, __shfl_xor_sync(0xffffffffu, lz, o));
+          hx = fmaxf(hx, __shfl_xor_sync(0xffffffffu, hx, o));
+          hy = fmaxf(hy, __shfl_xor_sync(0xffffffffu, hy, o));
+          hz = fmaxf(hz, __shfl_xor_sync(0xffffffffu, hz, o));
+        }
+        if (lane == 0) {
+          BX[2 * sb] = make_float4(lx, ly, lz, 0.f);
+          BX[2 * sb + 1] = make_float4(hx, hy, hz, 0.f);
+        }
+      }
+      __syncthreads();
+      // per row: min squared distance to the boxes (a lower bound of the
+      // distance to every point); exact over a box's points only when the row
+      // point lies inside it
       const int r = tid & (OZ_BM - 1), part = tid >> 7;
       const int64_t gr = min(i0 + r, m_out - 1);
       const float lx = (float)(outp.x[gr] - bx), ly = (float)(outp.y[gr] - by);
       const float lz = KIND == KK_PLATES ? (float)(outp.z[gr] - bz) : 0.f;
+      const int nbox = (nst * OZ_KS) / 32;
       float mn = 3.0e38f;
-      for (int k = part; k < npts; k += OZ_THREADS / OZ_BM) {
-        const float4 p = PF[k];
-        const float dx = lx - p.x, dy = ly - p.y;
-        float d2 = fmaf(dx, dx, dy * dy);
-        if (KIND == KK_PLATES) {
-          const float dz = lz - p.z;
-          d2 = fmaf(dz, dz, d2);
+      for (int b = part; b < nbox; b += OZ_THREADS / OZ_BM) {
+        const float4 lo = BX[2 * b], hi = BX[2 * b + 1];
+        const float dx = fmaxf(fmaxf(lo.x - lx, lx - hi.x), 0.f);
+        const float dy = fmaxf(fmaxf(lo.y - ly, ly - hi.y), 0.f);
+        const float dz = KIND == KK_PLATES ? fmaxf(fmaxf(lo.z - lz, lz - hi.z), 0.f) : 0.f;
+        float d2 = fmaf(dz, dz, fmaf(dy, dy, dx * dx));
+        if (d2 == 0.f) {
+          d2 = 3.0e38f;
+          for (int k = b * 32; k < b * 32 + 32; ++k) {
+            const float4 p = PF[k];
+            const float ex = lx - p.x, ey = ly - p.y;
+            float e2 = fmaf(ex, ex, ey * ey);
+            if (KIND == KK_PLATES) {
+              const float ez = lz - p.z;
+              e2 = fmaf(ez, ez, e2);
+            }
+            d2 = fminf(d2, e2);
+          }
         }
         mn = fminf(mn, d2);
       }
