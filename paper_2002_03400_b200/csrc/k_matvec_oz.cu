@@ -51,45 +51,80 @@ namespace bfly {
 
 namespace {
 
-constexpr int OZ_NCB = 32;                        // complex probe columns per tile
-constexpr int OZ_BN2 = 2 * OZ_NCB;                // N-rows per B slice ([re | im])
 constexpr int OZ_NSL = 7;                         // slices per operand
 constexpr int OZ_NDIAG = 8;                       // kept diagonals e = 5..12
-constexpr int OZ_TMEM_COLS = OZ_NDIAG * OZ_BN2;   // 512
 constexpr int OZ_KS = 32;                         // input entries per stage (MMA K)
 constexpr int OZ_KD = 1024;                       // entries per drain / scale chunk
 constexpr int OZ_NST = 2;                         // ring depth
 constexpr int OZ_BM = 128;                        // output rows per CTA (= TMEM lanes)
 constexpr int OZ_EWARPS = 16;
-constexpr int OZ_ETHREADS = OZ_EWARPS * 32;
-constexpr int OZ_THREADS = OZ_ETHREADS;           // no dedicated MMA warp
-constexpr int OZ_EPT = OZ_BM * OZ_KS / OZ_ETHREADS;  // 8 entries per thread per stage
+constexpr int OZ_THREADS = OZ_EWARPS * 32;        // no dedicated MMA warp
+constexpr int OZ_EPT = OZ_BM * OZ_KS / OZ_THREADS;  // 8 entries per thread per stage
 constexpr int OZ_ASLICE = OZ_BM * OZ_KS;           // 4096 B: one A slice (128 rows x 32 B)
 constexpr int OZ_APLANE = OZ_NSL * OZ_ASLICE;      // 28672 B
 constexpr int OZ_ASTAGE = 2 * OZ_APLANE;           // re + im planes
-constexpr int OZ_BROWS = OZ_NSL * OZ_BN2;          // 448 N-rows per B operand
-constexpr int OZ_BOPER = OZ_BROWS * OZ_KS;         // 14336 B (G1 or G2)
-constexpr int OZ_BSTAGE = 2 * OZ_BOPER;            // G1 + G2
-constexpr int OZ_MAXB = 256 / OZ_BN2;              // diagonal blocks per MMA (N <= 256)
+constexpr int OZ_MAXCB = 32;                       // widest probe tile (complex columns)
 static_assert(OZ_EPT == 8, "thread mapping assumes 8 entries per thread");
 
-// shared memory map (bytes)
-constexpr int SM_A = 0;
-constexpr int SM_B = SM_A + OZ_NST * OZ_ASTAGE;
-constexpr int SM_PD = SM_B + OZ_NST * OZ_BSTAGE;   // double2 (x, y) [KD]
-constexpr int SM_PZ = SM_PD + OZ_KD * 16;          // double z [KD]
-constexpr int SM_PF = SM_PZ + OZ_KD * 8;           // float4 local (x, y, z, 0) [KD]
-constexpr int SM_S = SM_PF + OZ_KD * 16;           // int S_row [2][128]
-constexpr int SM_T = SM_S + 2 * OZ_BM * 4;         // int T [NCB]
-constexpr int SM_MIN = SM_T + OZ_NCB * 4;          // uint min d2 bits [128]
-constexpr int SM_TAB = SM_MIN + OZ_BM * 4;         // double2 sin/cos table [256]
-constexpr int SM_BOX = SM_TAB + 256 * 16;          // float4 sub-box bounds [32][2]
-constexpr int SM_CNT = SM_BOX + 64 * 16;           // uint stage arrival counters [NST]
-constexpr int SM_BAR = SM_CNT + 16;                // mbarriers
-constexpr int NBAR = 2 * OZ_NST + 1;
-constexpr int SM_TMEM = SM_BAR + NBAR * 8;
-constexpr int SM_TOTAL = SM_TMEM + 16;
-static_assert(SM_TOTAL <= 232448, "shared memory budget");
+constexpr int pow2_ceil(int x) { return x <= 32 ? 32 : x <= 64 ? 64 : x <= 128 ? 128 : x <= 256 ? 256 : 512; }
+
+// Per-stage MMA schedule.  Plane h (0: A_re x G1, 1: A_im x G2), slice p,
+// first diagonal block jlo, block count nb (N = BN2 nb <= 256), init (first
+// K-step of a chunk writes instead of accumulating).  Diagonal block j holds
+// e = p + q = j + 5, so slice A_p meets B_q for blocks max(0, p-5)..min(7, p+1)
+// -- a contiguous window of the concatenated B slices.  The initialising MMAs
+// (plane 0: A_6 over blocks 1..7 and A_5 over block 0) come first and cover
+// the 8 blocks disjointly.   packed: h | p << 1 | jlo << 4 | nb << 8 | init << 13
+struct OzSched {
+  uint32_t code[64];
+  int n;
+};
+constexpr uint32_t mma_code(int h, int p, int jlo, int nb, int init) {
+  return (uint32_t)(h | (p << 1) | (jlo << 4) | (nb << 8) | (init << 13));
+}
+constexpr OzSched make_sched(int maxb) {
+  OzSched sc{};
+  sc.n = 0;
+  for (int h = 0; h < 2; ++h) {
+    const int init = h == 0 ? 1 : 0;
+    for (int j = 1; j <= 7; j += maxb) sc.code[sc.n++] = mma_code(h, 6, j, (8 - j) < maxb ? 8 - j : maxb, init);
+    sc.code[sc.n++] = mma_code(h, 5, 0, 1, init);
+    for (int j = 1; j <= 6; j += maxb) sc.code[sc.n++] = mma_code(h, 5, j, (7 - j) < maxb ? 7 - j : maxb, 0);
+    for (int p = 4; p >= 0; --p)
+      for (int j = 0; j <= p + 1; j += maxb) sc.code[sc.n++] = mma_code(h, p, j, (p + 2 - j) < maxb ? p + 2 - j : maxb, 0);
+  }
+  return sc;
+}
+
+// NCB-dependent sizes and the shared-memory map (bytes)
+template <int NCB_>
+struct OzT {
+  static constexpr int NCB = NCB_;                   // complex probe columns per tile
+  static constexpr int BN2 = 2 * NCB;                // N-rows per B slice ([re | im])
+  static constexpr int TMEM_COLS = pow2_ceil(OZ_NDIAG * BN2);
+  static constexpr int BROWS = OZ_NSL * BN2;         // N-rows per B operand
+  static constexpr int BOPER = BROWS * OZ_KS;        // G1 or G2 image
+  static constexpr int BSTAGE = 2 * BOPER;           // G1 + G2
+  static constexpr int MAXB = 256 / BN2 < OZ_NDIAG ? 256 / BN2 : OZ_NDIAG;  // blocks per MMA
+  static constexpr int DC = NCB / 2;                 // drained columns per thread
+  static constexpr int SM_A = 0;
+  static constexpr int SM_B = SM_A + OZ_NST * OZ_ASTAGE;
+  static constexpr int SM_PD = SM_B + OZ_NST * BSTAGE;  // double2 (x, y) [KD]
+  static constexpr int SM_PZ = SM_PD + OZ_KD * 16;      // double z [KD]
+  static constexpr int SM_PF = SM_PZ + OZ_KD * 8;       // float4 local (x, y, z, 0) [KD]
+  static constexpr int SM_S = SM_PF + OZ_KD * 16;       // int S_row [2][128]
+  static constexpr int SM_T = SM_S + 2 * OZ_BM * 4;     // int T [NCB]
+  static constexpr int SM_MIN = SM_T + OZ_MAXCB * 4;    // uint min d2 bits [128]
+  static constexpr int SM_TAB = SM_MIN + OZ_BM * 4;     // double2 sin/cos table [256]
+  static constexpr int SM_BOX = SM_TAB + 256 * 16;      // float4 sub-box bounds [32][2]
+  static constexpr int SM_CNT = SM_BOX + 64 * 16;       // uint stage arrival counters [NST]
+  static constexpr int SM_BAR = SM_CNT + 16;            // mbarriers
+  static constexpr int NBAR = 2 * OZ_NST + 1;
+  static constexpr int SM_TMEM = SM_BAR + NBAR * 8;
+  static constexpr int SM_TOTAL = SM_TMEM + 16;
+  static_assert(SM_TOTAL <= 232448, "shared memory budget");
+  static_assert(NCB % 8 == 0 && NCB <= OZ_MAXCB, "tile width");
+};
 
 struct OzItem {
   int64_t row0, rows;   // input point range
@@ -98,21 +133,6 @@ struct OzItem {
   int64_t bstage0;      // first B stage image of this item
   int32_t ncols, pad_;
 };
-
-// Per-stage MMA schedule.  Plane h (0: A_re x G1, 1: A_im x G2), slice p,
-// first diagonal block jlo, block count nb (N = 64 nb <= 256), init (first
-// K-step of a chunk writes instead of accumulating).  The initialising MMAs
-// (plane 0) come first and cover the 8 diagonal blocks disjointly.
-//   packed: h | p << 1 | jlo << 4 | nb << 7 | init << 10
-constexpr uint32_t mma_code(int h, int p, int jlo, int nb, int init) {
-  return (uint32_t)(h | (p << 1) | (jlo << 4) | (nb << 7) | (init << 10));
-}
-#define OZ_PLANE_LIST(h, I)                                                                                    \
-  mma_code(h, 6, 1, 4, I), mma_code(h, 6, 5, 3, I), mma_code(h, 5, 0, 1, I), mma_code(h, 5, 1, 4, 0),          \
-      mma_code(h, 5, 5, 2, 0), mma_code(h, 4, 0, 4, 0), mma_code(h, 4, 4, 2, 0), mma_code(h, 3, 0, 4, 0),      \
-      mma_code(h, 3, 4, 1, 0), mma_code(h, 2, 0, 4, 0), mma_code(h, 1, 0, 3, 0), mma_code(h, 0, 0, 2, 0)
-constexpr int OZ_NMMA = 24;
-static_assert(OZ_MAXB == 4, "schedule assumes 64-column diagonal blocks");
 
 // ------------------------------------------------------------ PTX helpers
 __device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
@@ -175,6 +195,11 @@ __device__ __forceinline__ void tmem_ld16(uint32_t addr, uint32_t (&v)[16]) {
       : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]), "=r"(v[8]),
         "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15])
       : "r"(addr));
+}
+__device__ __forceinline__ void tmem_ld4(uint32_t addr, uint32_t (&v)[4]) {
+  asm volatile("tcgen05.ld.sync.aligned.32x32b.x4.b32 {%0,%1,%2,%3}, [%4];"
+               : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3])
+               : "r"(addr));
 }
 // wait with back-off: the MMA thread shares its scheduler with evaluation warps
 __device__ __forceinline__ void mbar_wait_sleep(uint32_t bar, uint32_t parity) {
@@ -262,7 +287,7 @@ __global__ void oz_colscale_kernel(const double2* __restrict__ X, const OzItem* 
   if (threadIdx.x == 0) {
     const double mx = red[0];
     // zero or non-finite columns: scale 0 (non-finite values trip the slice check)
-    T[blockIdx.y * OZ_NCB + c] = (mx > 0.0 && mx < 1e300) ? 49 - ilogb(mx) : 0;
+    T[blockIdx.y * OZ_MAXCB + c] = (mx > 0.0 && mx < 1e300) ? 49 - ilogb(mx) : 0;
   }
 }
 
@@ -281,38 +306,40 @@ __device__ __forceinline__ void digits7(double x, int (&d)[OZ_NSL]) {
 // into the canonical K-major images of the item's stage k/32:
 //   G1 N-row q*64 + c:      Re x      G1 N-row q*64 + 32 + c:  Im x
 //   G2 N-row q*64 + c:     -Im x      G2 N-row q*64 + 32 + c:  Re x
+template <int NCB>
 __global__ void oz_slice_kernel(const double2* __restrict__ X, const OzItem* __restrict__ items,
                                 const int32_t* __restrict__ T, uint8_t* __restrict__ img, int* __restrict__ flag) {
+  using Z = OzT<NCB>;
   const OzItem it = items[blockIdx.y];
   const int64_t kpad = ceil_div(it.rows, (int64_t)OZ_KS) * OZ_KS;
   const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (t >= kpad * OZ_NCB) return;
-  const int c = (int)(t % OZ_NCB);
-  const int64_t k = t / OZ_NCB;
+  if (t >= kpad * NCB) return;
+  const int c = (int)(t % NCB);
+  const int64_t k = t / NCB;
   double2 v = make_double2(0.0, 0.0);
   if (c < it.ncols && k < it.rows) v = X[it.x_off + k + (int64_t)c * it.ldx];
-  const double sc = pow2(T[blockIdx.y * OZ_NCB + c]);
+  const double sc = pow2(T[blockIdx.y * OZ_MAXCB + c]);
   const double xr = v.x * sc, xi = v.y * sc;
   if (!(fabs(xr) < 1125899906842624.0 && fabs(xi) < 1125899906842624.0)) {  // 2^50; NaN fails too
     atomicOr(flag, 1);
     return;
   }
-  uint8_t* g1 = img + (it.bstage0 + k / OZ_KS) * (int64_t)OZ_BSTAGE;
-  uint8_t* g2 = g1 + OZ_BOPER;
+  uint8_t* g1 = img + (it.bstage0 + k / OZ_KS) * (int64_t)Z::BSTAGE;
+  uint8_t* g2 = g1 + Z::BOPER;
   const int kk = (int)(k % OZ_KS);
   int dr[OZ_NSL], di[OZ_NSL], dn[OZ_NSL];
   digits7(xr, dr);
   digits7(xi, di);
   digits7(-xi, dn);
   auto put = [&](uint8_t* base, int nrow, int d) {
-    base[((kk >> 4) * (OZ_BROWS / 8) + (nrow >> 3)) * 128 + (nrow & 7) * 16 + (kk & 15)] = (uint8_t)(d & 0xFF);
+    base[((kk >> 4) * (Z::BROWS / 8) + (nrow >> 3)) * 128 + (nrow & 7) * 16 + (kk & 15)] = (uint8_t)(d & 0xFF);
   };
 #pragma unroll
   for (int s = 0; s < OZ_NSL; ++s) {
-    put(g1, s * OZ_BN2 + c, dr[s]);
-    put(g1, s * OZ_BN2 + OZ_NCB + c, di[s]);
-    put(g2, s * OZ_BN2 + c, dn[s]);
-    put(g2, s * OZ_BN2 + OZ_NCB + c, dr[s]);
+    put(g1, s * Z::BN2 + c, dr[s]);
+    put(g1, s * Z::BN2 + NCB + c, di[s]);
+    put(g2, s * Z::BN2 + c, dn[s]);
+    put(g2, s * Z::BN2 + NCB + c, dr[s]);
   }
 }
 
@@ -325,11 +352,12 @@ __global__ void oz_slice_kernel(const double2* __restrict__ X, const OzItem* __r
 // d, so the issuer of that stage knows TMEM is free.  tcgen05 MMAs of a CTA
 // execute in issue order, so acc_full (committed by the last stage's
 // issuer) covers the whole chunk.
-template <int KIND, int MODE>
+template <int KIND, int MODE, int NCB>
 __global__ void __launch_bounds__(OZ_THREADS, 1)
     matvec_oz_kernel(Points outp, Points inp, double kappa, int64_t m_out, const uint8_t* __restrict__ bimg,
                      const int32_t* __restrict__ Tg, double2* __restrict__ Y, int64_t ldy,
                      const OzItem* __restrict__ items, int64_t rows_per_split, int64_t pstride, int* __restrict__ flag) {
+  using Z = OzT<NCB>;
   extern __shared__ __align__(1024) uint8_t smem[];
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   OZT_BEGIN(t5)
@@ -340,22 +368,22 @@ __global__ void __launch_bounds__(OZ_THREADS, 1)
   const int64_t nk = ke > kb ? ke - kb : 0;
   const int nchunks = (int)ceil_div(nk, (int64_t)OZ_KD);
 
-  double2* PD = reinterpret_cast<double2*>(smem + SM_PD);
-  double* PZ = reinterpret_cast<double*>(smem + SM_PZ);
-  float4* PF = reinterpret_cast<float4*>(smem + SM_PF);
-  int* Srow = reinterpret_cast<int*>(smem + SM_S);
-  int* Ts = reinterpret_cast<int*>(smem + SM_T);
-  unsigned* Smin = reinterpret_cast<unsigned*>(smem + SM_MIN);
-  unsigned* cnt = reinterpret_cast<unsigned*>(smem + SM_CNT);
-  const uint32_t bar0 = smem_u32(smem + SM_BAR);
+  double2* PD = reinterpret_cast<double2*>(smem + Z::SM_PD);
+  double* PZ = reinterpret_cast<double*>(smem + Z::SM_PZ);
+  float4* PF = reinterpret_cast<float4*>(smem + Z::SM_PF);
+  int* Srow = reinterpret_cast<int*>(smem + Z::SM_S);
+  int* Ts = reinterpret_cast<int*>(smem + Z::SM_T);
+  unsigned* Smin = reinterpret_cast<unsigned*>(smem + Z::SM_MIN);
+  unsigned* cnt = reinterpret_cast<unsigned*>(smem + Z::SM_CNT);
+  const uint32_t bar0 = smem_u32(smem + Z::SM_BAR);
   auto fullB = [&](int s) { return bar0 + 8u * s; };
   auto empty = [&](int s) { return bar0 + 8u * (OZ_NST + s); };
   const uint32_t acc_full = bar0 + 8u * (2 * OZ_NST);
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + SM_TMEM);
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + Z::SM_TMEM);
 
   if (warp == 0) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
-                 "n"(OZ_TMEM_COLS));
+                 "n"(Z::TMEM_COLS));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
   }
   if (tid == 32) {
@@ -367,8 +395,8 @@ __global__ void __launch_bounds__(OZ_THREADS, 1)
     mbar_init(acc_full, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
-  if (tid < OZ_NCB) Ts[tid] = Tg[blockIdx.y * OZ_NCB + tid];
-  double2* tab = reinterpret_cast<double2*>(smem + SM_TAB);
+  if (tid < NCB) Ts[tid] = Tg[blockIdx.y * OZ_MAXCB + tid];
+  double2* tab = reinterpret_cast<double2*>(smem + Z::SM_TAB);
   if (tid < 256) {
     double s_, c_;
     sincospi(tid / 128.0, &s_, &c_);
@@ -378,7 +406,7 @@ __global__ void __launch_bounds__(OZ_THREADS, 1)
   __syncthreads();
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
   const uint32_t tmem = *tmem_slot;
-  const uint32_t sA = smem_u32(smem + SM_A), sB = smem_u32(smem + SM_B);
+  const uint32_t sA = smem_u32(smem + Z::SM_A), sB = smem_u32(smem + Z::SM_B);
 
   // evaluation: row (warp & 7) * 16 + lane / 2, entries kofs .. kofs + 7 of each stage
   const int erow = (warp & 7) * 16 + (lane >> 1);
@@ -391,9 +419,10 @@ __global__ void __launch_bounds__(OZ_THREADS, 1)
   // (0, 1: Re y columns 0-15 / 16-31; 2, 3: Im y columns 0-15 / 16-31)
   const int drow = (warp & 3) * 32 + lane;
   const int dq = warp >> 2;
-  double yacc[16];
+  constexpr int DC = Z::DC;
+  double yacc[DC];
 #pragma unroll
-  for (int c = 0; c < 16; ++c) yacc[c] = 0.0;
+  for (int c = 0; c < DC; ++c) yacc[c] = 0.0;
   uint32_t amp_hi = 0;  // max high word of the scaled amplitudes
 
   auto drain = [&](int d) {
@@ -401,40 +430,51 @@ __global__ void __launch_bounds__(OZ_THREADS, 1)
     mbar_wait(acc_full, (uint32_t)d & 1u);
     if (lane == 0) { OZT_END(t4, 4) }
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-    double t[16];
+    double t[DC];
 #pragma unroll
     for (int j = OZ_NDIAG - 1; j >= 0; --j) {
-      uint32_t v[16];
-      tmem_ld16(tmem + ((uint32_t)((warp & 3) * 32) << 16) + j * OZ_BN2 + dq * 16, v);
+      const uint32_t base = tmem + ((uint32_t)((warp & 3) * 32) << 16) + j * Z::BN2 + dq * DC;
+      uint32_t v[DC];
+      if constexpr (DC == 16) {
+        tmem_ld16(base, v);
+      } else {
+#pragma unroll
+        for (int q = 0; q < DC / 4; ++q) {
+          uint32_t w[4];
+          tmem_ld4(base + 4 * q, w);
+#pragma unroll
+          for (int u = 0; u < 4; ++u) v[4 * q + u] = w[u];
+        }
+      }
       asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 #pragma unroll
-      for (int c = 0; c < 16; ++c) t[c] = (j == OZ_NDIAG - 1) ? i2d(v[c]) : fma(t[c], 256.0, i2d(v[c]));
+      for (int c = 0; c < DC; ++c) t[c] = (j == OZ_NDIAG - 1) ? i2d(v[c]) : fma(t[c], 256.0, i2d(v[c]));
     }
     const int S = Srow[(d & 1) * OZ_BM + drow];
-    const int c0 = (dq & 1) * 16;
+    const int c0 = (dq & 1) * DC;
 #pragma unroll
-    for (int c = 0; c < 16; ++c) yacc[c] = fma(t[c], pow2(40 - S - Ts[c0 + c]), yacc[c]);
+    for (int c = 0; c < DC; ++c) yacc[c] = fma(t[c], pow2(40 - S - Ts[c0 + c]), yacc[c]);
   };
 
   // One MMA of a stage (index i < OZ_NMMA of the fixed schedule kMmaList)
   auto issue_mma = [&](int i, uint32_t a0, uint32_t b0, int s) {
-    constexpr uint32_t kList[OZ_NMMA] = {OZ_PLANE_LIST(0, 1), OZ_PLANE_LIST(1, 0)};
-    const uint32_t e = kList[i];
-    const int h = e & 1, p = (e >> 1) & 7, jlo = (e >> 4) & 7, nb = (e >> 7) & 7;
-    const bool init = (e >> 10) & 1;
+    constexpr OzSched kS = make_sched(Z::MAXB);
+    const uint32_t e = kS.code[i];
+    const int h = e & 1, p = (e >> 1) & 7, jlo = (e >> 4) & 15, nb = (e >> 8) & 31;
+    const bool init = (e >> 13) & 1;
     const uint64_t da = smem_desc(a0 + h * OZ_APLANE + p * OZ_ASLICE, (OZ_BM / 8) * 128, 128);
     const int q0 = jlo + 5 - p;
-    const uint64_t db = smem_desc(b0 + h * OZ_BOPER + q0 * OZ_BN2 * 16, (OZ_BROWS / 8) * 128, 128);
-    mma_i8(tmem + jlo * OZ_BN2, da, db, idesc_i8(128, nb * OZ_BN2, p == OZ_NSL - 1, true),
+    const uint64_t db = smem_desc(b0 + h * Z::BOPER + q0 * Z::BN2 * 16, (Z::BROWS / 8) * 128, 128);
+    mma_i8(tmem + jlo * Z::BN2, da, db, idesc_i8(128, nb * Z::BN2, p == OZ_NSL - 1, true),
            (init && s == 0) ? 0u : 1u);
   };
   // all MMAs of a stage (called by the last-arriving warp's lane 0)
   auto issue_stage = [&](int slot, uint32_t ph, int s, int nst) {
     mbar_wait(fullB(slot), ph);
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-    const uint32_t a0 = sA + slot * OZ_ASTAGE, b0 = sB + slot * OZ_BSTAGE;
+    const uint32_t a0 = sA + slot * OZ_ASTAGE, b0 = sB + slot * Z::BSTAGE;
 #pragma unroll
-    for (int i = 0; i < OZ_NMMA; ++i) issue_mma(i, a0, b0, s);
+    for (int i = 0; i < make_sched(Z::MAXB).n; ++i) issue_mma(i, a0, b0, s);
     mma_commit(empty(slot));
     if (s == nst - 1) mma_commit(acc_full);
   };
@@ -465,7 +505,7 @@ __global__ void __launch_bounds__(OZ_THREADS, 1)
     __syncthreads();
     if (KIND != KK_NUFFT) {
       // bounding boxes of the 32 sub-boxes of 32 consecutive (tree-ordered) points
-      float4* BX = reinterpret_cast<float4*>(smem + SM_BOX);  // [32][lo, hi]
+      float4* BX = reinterpret_cast<float4*>(smem + Z::SM_BOX);  // [32][lo, hi]
 #pragma unroll
       for (int q = 0; q < 2; ++q) {
         const int sb = warp * 2 + q;
@@ -541,8 +581,8 @@ __global__ void __launch_bounds__(OZ_THREADS, 1)
       if (lane == 0) { OZT_END(t3, 3) }
       const int64_t k0 = c0 + (int64_t)s * OZ_KS;  // item-relative first entry of the stage
       if (tid == 0) {
-        mbar_expect_tx(fullB(slot), OZ_BSTAGE);
-        bulk_g2s(sB + slot * OZ_BSTAGE, bimg + (it.bstage0 + k0 / OZ_KS) * (int64_t)OZ_BSTAGE, OZ_BSTAGE,
+        mbar_expect_tx(fullB(slot), Z::BSTAGE);
+        bulk_g2s(sB + slot * Z::BSTAGE, bimg + (it.bstage0 + k0 / OZ_KS) * (int64_t)Z::BSTAGE, Z::BSTAGE,
                  fullB(slot));
       }
       // ---- evaluate 8 entries, scale, round (magic-number: low word = low
@@ -565,7 +605,7 @@ __global__ void __launch_bounds__(OZ_THREADS, 1)
         hi_i[e] = (uint32_t)__double2hiint(ti) - 0x43380000u;
       }
       // ---- byte slices -> canonical K-major A images (4x4 byte transposes)
-      uint8_t* a0 = smem + SM_A + slot * OZ_ASTAGE;
+      uint8_t* a0 = smem + Z::SM_A + slot * OZ_ASTAGE;
       const int off = ((kofs >> 4) * (OZ_BM / 8) + (erow >> 3)) * 128 + (erow & 7) * 16 + (kofs & 15);
 #pragma unroll
       for (int h = 0; h < 2; ++h) {
@@ -601,13 +641,13 @@ __global__ void __launch_bounds__(OZ_THREADS, 1)
   // |v| < 2^50 <=> high word of the scaled amplitude < 0x43100000 (NaN / inf fail)
   if (KIND != KK_NUFFT && amp_hi >= 0x43100000u) atomicOr(flag, 2);
 
-  // ---- store: thread owns row drow, columns (dq & 1) * 16 + c of Re (dq < 2) or Im y
+  // ---- store: thread owns row drow, columns (dq & 1) * DC + c of Re (dq < 2) or Im y
   const int64_t go = i0 + drow;
   if (go < m_out) {
     double* Yb = reinterpret_cast<double*>(Y + it.ybase + (int64_t)blockIdx.z * pstride);
-    const int cb = (dq & 1) * 16, comp = dq >> 1;
+    const int cb = (dq & 1) * DC, comp = dq >> 1;
 #pragma unroll
-    for (int c = 0; c < 16; ++c)
+    for (int c = 0; c < DC; ++c)
       if (cb + c < it.ncols) Yb[2 * (go + (it.ycol + cb + c) * ldy) + comp] = yacc[c];
   }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
@@ -615,7 +655,7 @@ __global__ void __launch_bounds__(OZ_THREADS, 1)
   if (tid == 0) { OZT_END(t5, 5) }
   if (warp == 0) {
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(OZ_TMEM_COLS));
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(Z::TMEM_COLS));
   }
 }
 
@@ -635,9 +675,10 @@ __global__ void oz_reduce_kernel(const double2* __restrict__ P, int64_t pstride,
   }
 }
 
-template <int KIND, int MODE>
+template <int KIND, int MODE, int NCB>
 bool run_oz(Ctx* c, Points outp, Points inp, double kappa, int64_t m_out, const double2* X, double2* Y, int64_t ldy,
             const MatvecSeg* segs, int nseg) {
+  using Z = OzT<NCB>;
   std::vector<OzItem> items;
   std::vector<const MatvecSeg*> item_seg;
   int64_t max_rows = 0, max_col = 0, nstages = 0;
@@ -649,14 +690,14 @@ bool run_oz(Ctx* c, Points outp, Points inp, double kappa, int64_t m_out, const 
                                   c->stream));
       continue;
     }
-    for (int tc = 0; tc < g.ncols; tc += OZ_NCB) {
+    for (int tc = 0; tc < g.ncols; tc += NCB) {
       OzItem it{};
       it.row0 = g.row0;
       it.rows = g.rows;
       it.x_off = g.x_off + (int64_t)tc * g.ldx;
       it.ldx = g.ldx;
       it.ycol = g.col0 + tc;
-      it.ncols = std::min(OZ_NCB, g.ncols - tc);
+      it.ncols = std::min(NCB, g.ncols - tc);
       it.bstage0 = nstages;
       nstages += ceil_div(g.rows, (int64_t)OZ_KS);
       items.push_back(it);
@@ -678,8 +719,8 @@ bool run_oz(Ctx* c, Points outp, Points inp, double kappa, int64_t m_out, const 
 
   DBuf<OzItem> ditems(c, items.size());
   ditems.upload(items.data(), items.size());
-  DBuf<int32_t> T(c, items.size() * OZ_NCB);
-  DBuf<uint8_t> img(c, (size_t)(nstages * OZ_BSTAGE));
+  DBuf<int32_t> T(c, items.size() * OZ_MAXCB);
+  DBuf<uint8_t> img(c, (size_t)(nstages * Z::BSTAGE));
   DBuf<int> flag(c, 1);
   flag.zero();
   double kflops = 0, kbytes = 0;
@@ -688,16 +729,16 @@ bool run_oz(Ctx* c, Points outp, Points inp, double kappa, int64_t m_out, const 
     kbytes += 16.0 * ((double)it.rows + (double)m_out) * (double)it.ncols;
   }
   {
-    KTimer timer(c, "oz_prep", 0.0, (double)nstages * OZ_BSTAGE);
-    oz_colscale_kernel<<<dim3(OZ_NCB, (unsigned)items.size()), 256, 0, c->stream>>>(X, ditems.p, T.p);
+    KTimer timer(c, "oz_prep", 0.0, (double)nstages * Z::BSTAGE);
+    oz_colscale_kernel<<<dim3(NCB, (unsigned)items.size()), 256, 0, c->stream>>>(X, ditems.p, T.p);
     BFLY_LAUNCH_CHECK("oz_colscale");
-    const int64_t per_item = ceil_div(max_rows, (int64_t)OZ_KS) * OZ_KS * OZ_NCB;
-    oz_slice_kernel<<<dim3((unsigned)ceil_div(per_item, (int64_t)256), (unsigned)items.size()), 256, 0, c->stream>>>(
+    const int64_t per_item = ceil_div(max_rows, (int64_t)OZ_KS) * OZ_KS * NCB;
+    oz_slice_kernel<NCB><<<dim3((unsigned)ceil_div(per_item, (int64_t)256), (unsigned)items.size()), 256, 0, c->stream>>>(
         X, ditems.p, T.p, img.p, flag.p);
     BFLY_LAUNCH_CHECK("oz_slice");
   }
-  auto kern = matvec_oz_kernel<KIND, MODE>;
-  BFLY_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, SM_TOTAL));
+  auto kern = matvec_oz_kernel<KIND, MODE, NCB>;
+  BFLY_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Z::SM_TOTAL));
   dim3 grid((unsigned)gx, (unsigned)items.size(), (unsigned)nsplit);
   DBuf<double2> part;
   int64_t pstride = 0;
@@ -709,7 +750,7 @@ bool run_oz(Ctx* c, Points outp, Points inp, double kappa, int64_t m_out, const 
   }
   {
     KTimer timer(c, "kernel_matvec", kflops, kbytes);
-    kern<<<grid, OZ_THREADS, SM_TOTAL, c->stream>>>(outp, inp, kappa, m_out, img.p, T.p, Yt, ldy, ditems.p,
+    kern<<<grid, OZ_THREADS, Z::SM_TOTAL, c->stream>>>(outp, inp, kappa, m_out, img.p, T.p, Yt, ldy, ditems.p,
                                                     rows_per_split, pstride, flag.p);
     BFLY_LAUNCH_CHECK("kernel_matvec_oz");
   }
@@ -741,12 +782,25 @@ bool run_oz(Ctx* c, Points outp, Points inp, double kappa, int64_t m_out, const 
   return hflag == 0;
 }
 
+template <int KIND, int MODE>
+bool run_oz_width(Ctx* c, Points outp, Points inp, double kappa, int64_t m_out, const double2* X, double2* Y,
+                  int64_t ldy, const MatvecSeg* segs, int nseg) {
+  // tile width = the widest column tile of the launch (tiles of <= 32 columns):
+  // narrow probe blocks (leaf rounds) do proportionally less tensor work
+  int w = 0;
+  for (int s = 0; s < nseg; ++s) w = std::max(w, std::min(segs[s].ncols, OZ_MAXCB));
+  if (w <= 8) return run_oz<KIND, MODE, 8>(c, outp, inp, kappa, m_out, X, Y, ldy, segs, nseg);
+  if (w <= 16) return run_oz<KIND, MODE, 16>(c, outp, inp, kappa, m_out, X, Y, ldy, segs, nseg);
+  if (w <= 24) return run_oz<KIND, MODE, 24>(c, outp, inp, kappa, m_out, X, Y, ldy, segs, nseg);
+  return run_oz<KIND, MODE, 32>(c, outp, inp, kappa, m_out, X, Y, ldy, segs, nseg);
+}
+
 template <int KIND>
 bool dispatch_oz_mode(Ctx* c, int mode, Points outp, Points inp, double kappa, int64_t m_out, const double2* X,
                       double2* Y, int64_t ldy, const MatvecSeg* segs, int nseg) {
-  if (mode == OP_N) return run_oz<KIND, OP_N>(c, outp, inp, kappa, m_out, X, Y, ldy, segs, nseg);
-  if (mode == OP_T) return run_oz<KIND, OP_T>(c, outp, inp, kappa, m_out, X, Y, ldy, segs, nseg);
-  return run_oz<KIND, OP_H>(c, outp, inp, kappa, m_out, X, Y, ldy, segs, nseg);
+  if (mode == OP_N) return run_oz_width<KIND, OP_N>(c, outp, inp, kappa, m_out, X, Y, ldy, segs, nseg);
+  if (mode == OP_T) return run_oz_width<KIND, OP_T>(c, outp, inp, kappa, m_out, X, Y, ldy, segs, nseg);
+  return run_oz_width<KIND, OP_H>(c, outp, inp, kappa, m_out, X, Y, ldy, segs, nseg);
 }
 
 }  // namespace
