@@ -748,8 +748,21 @@ bool run_oz(Ctx* c, Points outp, Points inp, double kappa, int64_t m_out, const 
     part.reset(c, (size_t)(pstride * nsplit));
     Yt = part.p;
   }
+  // tensor work actually executed (int8 ops = 2 per MAC): per stage of 128
+  // rows x 32 entries, 2 planes x (sum of MMA N) x 128 x 32 MACs
+  double stages = 0;
+  for (const auto& it : items)
+    for (int z = 0; z < nsplit; ++z) {
+      const int64_t k0 = (int64_t)z * rows_per_split, k1 = std::min(it.rows, k0 + rows_per_split);
+      if (k1 > k0) stages += (double)ceil_div(k1 - k0, (int64_t)OZ_KS);
+    }
+  constexpr OzSched sch = make_sched(Z::MAXB);
+  double nsum = 0;
+  for (int i = 0; i < sch.n; ++i) nsum += (double)(((sch.code[i] >> 8) & 31) * Z::BN2);
+  const double int8_ops = 2.0 * stages * (double)gx * nsum * OZ_BM * OZ_KS;
   {
     KTimer timer(c, "kernel_matvec", kflops, kbytes);
+    KTimer timer8(c, "kernel_matvec.int8_ops", int8_ops, 0.0);
     kern<<<grid, OZ_THREADS, Z::SM_TOTAL, c->stream>>>(outp, inp, kappa, m_out, img.p, T.p, Yt, ldy, ditems.p,
                                                     rows_per_split, pstride, flag.p);
     BFLY_LAUNCH_CHECK("kernel_matvec_oz");
