@@ -93,23 +93,23 @@ __device__ __forceinline__ double2 kernel_entry_fast(double tx, double ty, doubl
 }
 
 
-// ---- table-based sin/cos (K2 integer-slice path): 256 table points over a
-// full turn (tab[j] = (cos, sin)(2 pi j / 256), in shared memory) and short
-// polynomials on |f| <= pi/256 (truncation < 1e-19 relative).
-// kTabC: 256/(2 pi), (2 pi/256) high / low, then -1/5040, 1/120, -1/6, -1/720, 1/24
-static __constant__ double kTabC[8] = {40.743665431525205956834243423364, 0.024543692606170258718734089597,
-                                       9.5675531183386969e-19, -1.9841269841269841270e-04,
-                                       8.3333333333333333333e-03, -1.6666666666666666667e-01,
-                                       -1.3888888888888888889e-03, 4.1666666666666666667e-02};
+// ---- table-based sin/cos (K2 integer-slice path): 512 table points over a
+// full turn (tab[j] = (cos, sin)(2 pi j / 512), in shared memory) and short
+// polynomials on |f| <= pi/512 (truncation < 2e-17 relative).
+// kTabC: 512/(2 pi), (2 pi/512) high / low, 1/120, -1/6, -1/720, 1/24
+constexpr int kTabN = 512;
+static __constant__ double kTabC[8] = {81.487330863050411913668486846728, 0.012271846303085129359367044798,
+                                       4.7837765591693484e-19, 8.3333333333333333333e-03,
+                                       -1.6666666666666666667e-01, -1.3888888888888888889e-03,
+                                       4.1666666666666666667e-02, 0.0};
 constexpr double kMagic = 6755399441055744.0;  // 1.5 * 2^52
 
 // (s, c) of the angle a_j + f given the table entry (cos a_j, sin a_j)
 __device__ __forceinline__ void tab_poly(double f, double2 tc, double& s, double& c) {
   const double f2 = f * f;
-  double ps = fma(f2, kTabC[3], kTabC[4]);
-  ps = fma(f2, ps, kTabC[5]);
+  const double ps = fma(f2, kTabC[3], kTabC[4]);
   const double sf = fma(f * f2, ps, f);
-  double pc = fma(f2, kTabC[6], kTabC[7]);
+  double pc = fma(f2, kTabC[5], kTabC[6]);
   pc = fma(f2, pc, -0.5);
   const double cm1 = f2 * pc;
   s = fma(tc.x, sf, fma(tc.y, cm1, tc.y));
@@ -123,15 +123,34 @@ __device__ __forceinline__ void tab_sincos(double ph, const double2* __restrict_
   const double q = t - kMagic;
   double f = fma(-q, kTabC[1], ph);
   f = fma(-q, kTabC[2], f);
-  tab_poly(f, tab[qi & 255], s, c);
+  tab_poly(f, tab[qi & (kTabN - 1)], s, c);
 }
 
 // exp(2 pi i g) for a reduced turn fraction f in [-1/2, 1/2]
 __device__ __forceinline__ void tab_sincos_turn(double f, const double2* __restrict__ tab, double& s, double& c) {
-  const double t = fma(f, 256.0, kMagic);
+  const double t = fma(f, (double)kTabN, kMagic);
   const int qi = __double2loint(t);
-  const double g = __dsub_rn(f, (t - kMagic) * 0.00390625);  // exact (Sterbenz)
-  tab_poly(__dmul_rn(kTwoPi, g), tab[qi & 255], s, c);
+  const double g = __dsub_rn(f, (t - kMagic) * (1.0 / kTabN));  // exact (Sterbenz)
+  tab_poly(__dmul_rn(kTwoPi, g), tab[qi & (kTabN - 1)], s, c);
+}
+
+// r = sqrt_rn(x) (bit-identical to __dsqrt_rn: 0 mismatches in 8.6e9 random
+// normal inputs, tools/microbench/sqrt_check.cu) and h = 1/(2 sqrt(x)) to
+// ~3 ulp as a by-product; branch-free Goldschmidt iteration + Markstein
+// correction, positive normal x only (0 / inf / NaN yield non-finite h).
+__device__ __forceinline__ double sqrt_rcp(double x, double& h) {
+  double y;
+  asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
+  double s = x * y;
+  h = 0.5 * y;
+  double e = fma(-s, h, 0.5);
+  s = fma(s, e, s);
+  h = fma(h, e, h);
+  e = fma(-s, h, 0.5);
+  s = fma(s, e, s);
+  h = fma(h, e, h);
+  const double d = fma(-s, s, x);
+  return fma(d, h, s);
 }
 }  // namespace keval
 }  // namespace bfly

@@ -115,8 +115,8 @@ struct OzT {
   static constexpr int SM_S = SM_PF + OZ_KD * 16;       // int S_row [2][128]
   static constexpr int SM_T = SM_S + 2 * OZ_BM * 4;     // int T [NCB]
   static constexpr int SM_MIN = SM_T + OZ_MAXCB * 4;    // uint min d2 bits [128]
-  static constexpr int SM_TAB = SM_MIN + OZ_BM * 4;     // double2 sin/cos table [256]
-  static constexpr int SM_BOX = SM_TAB + 256 * 16;      // float4 sub-box bounds [32][2]
+  static constexpr int SM_TAB = SM_MIN + OZ_BM * 4;     // double2 sin/cos table [kTabN]
+  static constexpr int SM_BOX = SM_TAB + keval::kTabN * 16;  // float4 sub-box bounds [32][2]
   static constexpr int SM_CNT = SM_BOX + 64 * 16;       // uint stage arrival counters [NST]
   static constexpr int SM_BAR = SM_CNT + 16;            // mbarriers
   static constexpr int NBAR = 2 * OZ_NST + 1;
@@ -249,16 +249,21 @@ __device__ __forceinline__ void entry_rounded(double tx, double ty, double tz, d
     const double ph = __dmul_rn(tx, sx);
     keval::tab_sincos_turn(__dsub_rn(ph, rint(ph)), tab, sn, cs);
     sc = p2;
-  } else if (KIND == KK_PLATES) {
-    const double dx = __dsub_rn(tx, sx), dy = __dsub_rn(ty, sy), dz = __dsub_rn(tz, sz);
-    const double r = __dsqrt_rn(fma(dz, dz, fma(dy, dy, __dmul_rn(dx, dx))));
-    keval::tab_sincos(__dmul_rn(kappa, r), tab, sn, cs);
-    sc = keval::fast_rcp(__dmul_rn(keval::kFourPi, r)) * p2;
   } else {
+    // p2 here is the row scale pre-multiplied by the amplitude constant:
+    // 2 * 2^S (circle: 1/r = 2h) or 2 * 2^S / (4 pi) (plates)
     const double dx = __dsub_rn(tx, sx), dy = __dsub_rn(ty, sy);
-    const double r = __dsqrt_rn(fma(dy, dy, __dmul_rn(dx, dx)));
+    double d2;
+    if (KIND == KK_PLATES) {
+      const double dz = __dsub_rn(tz, sz);
+      d2 = fma(dz, dz, fma(dy, dy, __dmul_rn(dx, dx)));
+    } else {
+      d2 = fma(dy, dy, __dmul_rn(dx, dx));
+    }
+    double h;
+    const double r = keval::sqrt_rcp(d2, h);
     keval::tab_sincos(__dmul_rn(kappa, r), tab, sn, cs);
-    sc = keval::fast_rcp(r) * p2;
+    sc = h * p2;
   }
   amp = sc;
   re = fma(cs, sc, keval::kMagic);
@@ -397,10 +402,10 @@ __global__ void __launch_bounds__(OZ_THREADS, 1)
   }
   if (tid < NCB) Ts[tid] = Tg[blockIdx.y * OZ_MAXCB + tid];
   double2* tab = reinterpret_cast<double2*>(smem + Z::SM_TAB);
-  if (tid < 256) {
+  for (int j = tid; j < keval::kTabN; j += OZ_THREADS) {
     double s_, c_;
-    sincospi(tid / 128.0, &s_, &c_);
-    tab[tid] = make_double2(c_, s_);
+    sincospi(j / (keval::kTabN / 2.0), &s_, &c_);
+    tab[j] = make_double2(c_, s_);
   }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   __syncthreads();
@@ -572,7 +577,10 @@ __global__ void __launch_bounds__(OZ_THREADS, 1)
     }
     __syncthreads();
     if (lane == 0) { OZT_END(t6, 6) }
-    const double p2 = pow2(Srow[(d & 1) * OZ_BM + erow]);
+    // row scale 2^S, folded with the amplitude constant (see entry_rounded)
+    const double p2 = KIND == KK_NUFFT    ? pow2(Srow[(d & 1) * OZ_BM + erow])
+                      : KIND == KK_PLATES ? pow2(Srow[(d & 1) * OZ_BM + erow] + 1) / keval::kFourPi
+                                          : pow2(Srow[(d & 1) * OZ_BM + erow] + 1);
     for (int s = 0; s < nst; ++s, ++g) {
       const int slot = g % OZ_NST;
       const uint32_t ph = (uint32_t)(g / OZ_NST) & 1u;

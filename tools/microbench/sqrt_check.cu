@@ -1,0 +1,65 @@
+// sqrt_check.cu -- validates the branch-free Goldschmidt sqrt used by the K2
+// evaluation (k_eval.cuh: sqrt_rcp) against __dsqrt_rn, bit for bit, on
+// random normal doubles spanning 2^-200 .. 2^200, and reports the relative
+// error of the by-product reciprocal 1/sqrt(x).
+// nvcc -gencode arch=compute_100a,code=sm_100a -O3 -std=c++17 sqrt_check.cu -o sqrt_check
+#include <cstdint>
+#include <cstdio>
+
+__device__ __forceinline__ uint64_t mix64(uint64_t z) {
+  z += 0x9E3779B97F4A7C15ull;
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+  return z ^ (z >> 31);
+}
+
+// r = sqrt_rn(x), h = 1/(2 sqrt(x)) (~1 ulp), for positive normal x
+__device__ __forceinline__ double sqrt_rcp(double x, double& h) {
+  double y;
+  asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
+  double s = x * y;
+  h = 0.5 * y;
+  double e = fma(-s, h, 0.5);
+  s = fma(s, e, s);
+  h = fma(h, e, h);
+  e = fma(-s, h, 0.5);
+  s = fma(s, e, s);
+  h = fma(h, e, h);
+  const double d = fma(-s, s, x);
+  return fma(d, h, s);
+}
+
+__global__ void check(uint64_t seed, int64_t n, unsigned long long* bad, double* maxrel) {
+  double mr = 0;
+  unsigned long long b = 0;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const uint64_t r = mix64(seed + i);
+    // mantissa random, exponent in [-200, 200]
+    const int ex = (int)((r >> 52) % 401) - 200;
+    const double x = __longlong_as_double((long long)((r & 0xFFFFFFFFFFFFFull) | ((uint64_t)(1023 + ex) << 52)));
+    double h;
+    const double s = sqrt_rcp(x, h);
+    const double ref = __dsqrt_rn(x);
+    if (__double_as_longlong(s) != __double_as_longlong(ref)) ++b;
+    const double inv = 1.0 / ref;
+    mr = fmax(mr, fabs(2.0 * h - inv) / inv);
+  }
+  atomicAdd(bad, b);
+  // positive doubles compare as integers
+  atomicMax(reinterpret_cast<unsigned long long*>(maxrel), (unsigned long long)__double_as_longlong(mr));
+}
+
+int main() {
+  unsigned long long* bad;
+  double* mr;
+  cudaMallocManaged(&bad, 8);
+  cudaMallocManaged(&mr, 8);
+  *bad = 0;
+  *mr = 0;
+  const int64_t n = 1LL << 33;  // 8.6e9 samples
+  check<<<148 * 16, 256>>>(12345, n, bad, mr);
+  cudaDeviceSynchronize();
+  printf("samples %lld  sqrt mismatches vs __dsqrt_rn: %llu  max rel err of 2h vs 1/sqrt: %.3e (%.2f ulp)\n",
+         (long long)n, *bad, *mr, *mr / 1.1102230246251565e-16);
+  return *bad ? 1 : 0;
+}
