@@ -583,24 +583,24 @@ void DevButterfly<R>::apply_n(const cx<R>* xt, int64_t ldx, cx<R>* yt, int64_t l
   int st = 0;
   const int kk = (int)k;
   launch_bgemm<R>(c, OP_H, PV(0), (int)vleaf.ld, 1, vleaf.data.p, vleaf.ld, xt, ldx, cur, NB * PV(0),
-                  plan_n_.stages[st++].p, (int)NB, kk, false, kk);
+                  plan_n_.stages[st++].p, (int)NB, kk, false, kk, true);
   for (int l = 1; l <= lm; ++l) {
     const Level<R>& wl = w[l - 1];
     launch_bgemm<R>(c, OP_H, PV(l), 2 * PV(l - 1), 1, wl.data.p, wl.ld, cur, NB * PV(l - 1), nxt, NB * PV(l),
-                    plan_n_.stages[st++].p, (int)NB, kk, false, kk);
+                    plan_n_.stages[st++].p, (int)NB, kk, false, kk, true);
     std::swap(cur, nxt);
   }
   launch_bgemm<R>(c, OP_N, PU(lm), PV(lm), 1, b.data.p, b.ld, cur, NB * PV(lm), nxt, NB * PU(lm),
-                  plan_n_.stages[st++].p, (int)NB, kk, false, kk);
+                  plan_n_.stages[st++].p, (int)NB, kk, false, kk, true);
   std::swap(cur, nxt);
   for (int l = lm; l < L; ++l) {
     const Level<R>& rl = r[l - lm];
     launch_bgemm<R>(c, OP_N, PU(l + 1), PU(l), 2, rl.data.p, rl.ld, cur, NB * PU(l), nxt, NB * PU(l + 1),
-                    plan_n_.stages[st++].p, (int)NB, kk, false, kk);
+                    plan_n_.stages[st++].p, (int)NB, kk, false, kk, true);
     std::swap(cur, nxt);
   }
   launch_bgemm<R>(c, OP_N, (int)uleaf.ld, PU(L), 1, uleaf.data.p, uleaf.ld, cur, NB * PU(L), yt, ldy,
-                  plan_n_.stages[st++].p, (int)NB, kk, false, kk);
+                  plan_n_.stages[st++].p, (int)NB, kk, false, kk, true);
 }
 
 template <typename R>
@@ -657,24 +657,24 @@ void DevButterfly<R>::apply_h(const cx<R>* yt, int64_t ldy, cx<R>* xt, int64_t l
   int st = 0;
   const int kk = (int)k;
   launch_bgemm<R>(c, OP_H, PU(L), (int)uleaf.ld, 1, uleaf.data.p, uleaf.ld, yt, ldy, cur, NB * PU(L),
-                  plan_h_.stages[st++].p, (int)NB, kk, false, kk);
+                  plan_h_.stages[st++].p, (int)NB, kk, false, kk, true);
   for (int l = L - 1; l >= lm; --l) {
     const Level<R>& rl = r[l - lm];
     launch_bgemm<R>(c, OP_H, PU(l), PU(l + 1), 2, rl.data.p, rl.ld, cur, NB * PU(l + 1), nxt, NB * PU(l),
-                    plan_h_.stages[st++].p, (int)NB, kk, false, kk);
+                    plan_h_.stages[st++].p, (int)NB, kk, false, kk, true);
     std::swap(cur, nxt);
   }
   launch_bgemm<R>(c, OP_H, PV(lm), PU(lm), 1, b.data.p, b.ld, cur, NB * PU(lm), nxt, NB * PV(lm),
-                  plan_h_.stages[st++].p, (int)NB, kk, false, kk);
+                  plan_h_.stages[st++].p, (int)NB, kk, false, kk, true);
   std::swap(cur, nxt);
   for (int l = lm; l >= 1; --l) {
     const Level<R>& wl = w[l - 1];
     launch_bgemm<R>(c, OP_N, PV(l - 1), PV(l), 2, wl.data.p, wl.ld, cur, NB * PV(l), nxt, NB * PV(l - 1),
-                    plan_h_.stages[st++].p, (int)NB, kk, false, kk);
+                    plan_h_.stages[st++].p, (int)NB, kk, false, kk, true);
     std::swap(cur, nxt);
   }
   launch_bgemm<R>(c, OP_N, (int)vleaf.ld, PV(0), 1, vleaf.data.p, vleaf.ld, cur, NB * PV(0), xt, ldx,
-                  plan_h_.stages[st++].p, (int)NB, kk, false, kk);
+                  plan_h_.stages[st++].p, (int)NB, kk, false, kk, true);
 }
 
 // ------------------------------------------------------- host <-> device

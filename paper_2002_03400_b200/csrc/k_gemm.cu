@@ -118,10 +118,12 @@ __global__ void __launch_bounds__(128) bgemm_small_kernel(const cx<R>* __restric
   const int Me = min(M, e.mrows), Ke = min(K, e.krows);
   const int SMA = M + 1;
   V* Bs = As + S * K * SMA;                // [S][ncols][K]
+  // A (a fixed factor level when launched with programmatic dependent launch,
+  // see launch_bgemm's pdl flag) is staged first; B, the previous stage's
+  // output, only after griddepcontrol.wait (a no-op for ordinary launches).
 #pragma unroll
   for (int s = 0; s < S; ++s) {
     const V* Ab = A + (s == 0 ? e.a0 : e.a1);
-    const V* Bb = B + (s == 0 ? e.b0 : e.b1);
     V* as = As + s * K * SMA;
     if (OP == OP_N) {
       for (int idx = threadIdx.x; idx < M * K; idx += 128) {
@@ -136,6 +138,11 @@ __global__ void __launch_bounds__(128) bgemm_small_kernel(const cx<R>* __restric
         as[m + kk * SMA] = v;
       }
     }
+  }
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+#pragma unroll
+  for (int s = 0; s < S; ++s) {
+    const V* Bb = B + (s == 0 ? e.b0 : e.b1);
     V* bs = Bs + s * ncols * K;
     for (int idx = threadIdx.x; idx < K * ncols; idx += 128) {
       const int kk = idx % K, cc = idx / K;
@@ -143,6 +150,7 @@ __global__ void __launch_bounds__(128) bgemm_small_kernel(const cx<R>* __restric
     }
   }
   __syncthreads();
+  asm volatile("griddepcontrol.launch_dependents;");
   V* Cb = C + e.c;
   for (int idx = threadIdx.x; idx < Me * ncols; idx += 128) {
     const int m = idx % Me, cc = idx / Me;
@@ -285,7 +293,7 @@ __global__ void __launch_bounds__(256) bgemm_dmma_kernel(const double2* __restri
 template <typename R>
 void launch_bgemm(Ctx* c, int op, int M, int K, int S, const cx<R>* A, int64_t lda, const cx<R>* B, int64_t ldb,
                   cx<R>* C, int64_t ldc, const GemmEnt* ents, int nent, int max_ncols, bool accumulate,
-                  int ncols_all) {
+                  int ncols_all, bool pdl) {
   if (nent <= 0 || M <= 0 || max_ncols <= 0) return;
   const int kcols = ncols_all > 0 ? ncols_all : max_ncols;
   const size_t small_smem = sizeof(cx<R>) * (size_t)S * ((size_t)K * (M + 1) + (size_t)K * kcols);
@@ -300,7 +308,21 @@ void launch_bgemm(Ctx* c, int op, int M, int K, int S, const cx<R>* A, int64_t l
       BFLY_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024));           \
       attr_bytes = 96 * 1024;                                                                                  \
     }                                                                                                          \
-    kern<<<nent, 128, small_smem, c->stream>>>(A, lda, B, ldb, C, ldc, M, K, ents, accumulate, ncols_all);     \
+    if (pdl) {                                                                                                 \
+      cudaLaunchConfig_t cfg = {};                                                                             \
+      cudaLaunchAttribute at[1];                                                                               \
+      at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;                                          \
+      at[0].val.programmaticStreamSerializationAllowed = 1;                                                    \
+      cfg.gridDim = dim3(nent);                                                                                \
+      cfg.blockDim = dim3(128);                                                                                \
+      cfg.dynamicSmemBytes = small_smem;                                                                       \
+      cfg.stream = c->stream;                                                                                  \
+      cfg.attrs = at;                                                                                          \
+      cfg.numAttrs = 1;                                                                                        \
+      BFLY_CUDA(cudaLaunchKernelEx(&cfg, kern, A, lda, B, ldb, C, ldc, M, K, ents, (int)accumulate, ncols_all)); \
+    } else {                                                                                                   \
+      kern<<<nent, 128, small_smem, c->stream>>>(A, lda, B, ldb, C, ldc, M, K, ents, accumulate, ncols_all);   \
+    }                                                                                                          \
   } while (0)
     if (S == 1) {
       if (op == OP_N) BGS(OP_N, 1);
@@ -369,8 +391,8 @@ void launch_bgemm(Ctx* c, int op, int M, int K, int S, const cx<R>* A, int64_t l
 }
 
 template void launch_bgemm<double>(Ctx*, int, int, int, int, const double2*, int64_t, const double2*, int64_t, double2*,
-                                   int64_t, const GemmEnt*, int, int, bool, int);
+                                   int64_t, const GemmEnt*, int, int, bool, int, bool);
 template void launch_bgemm<float>(Ctx*, int, int, int, int, const float2*, int64_t, const float2*, int64_t, float2*,
-                                  int64_t, const GemmEnt*, int, int, bool, int);
+                                  int64_t, const GemmEnt*, int, int, bool, int, bool);
 
 }  // namespace bfly

@@ -163,12 +163,14 @@ __device__ __forceinline__ void mbar_expect_tx(uint32_t bar, uint32_t bytes) {
                : "memory");
 }
 __device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
+  // suspend-time hint: a waiting warp sleeps until the phase completes
+  // instead of spinning on issue slots the MMA-issuing warp needs
   asm volatile(
       "{\n\t.reg .pred done;\n\t"
       "WAIT_%=:\n\t"
-      "mbarrier.try_wait.parity.acquire.cta.shared::cta.b64 done, [%0], %1;\n\t"
+      "mbarrier.try_wait.parity.acquire.cta.shared::cta.b64 done, [%0], %1, %2;\n\t"
       "@!done bra WAIT_%=;\n\t}\n" ::"r"(bar),
-      "r"(parity)
+      "r"(parity), "r"(1000000u)
       : "memory");
 }
 __device__ __forceinline__ void mma_commit(uint32_t bar) {

@@ -60,7 +60,10 @@ struct GemmEnt {
 template <typename R>
 void launch_bgemm(Ctx* c, int op, int M, int K, int S, const cx<R>* A, int64_t lda, const cx<R>* B, int64_t ldb,
                   cx<R>* C, int64_t ldc, const GemmEnt* ents_dev, int nent, int max_ncols, bool accumulate,
-                  int ncols_all = 0);
+                  int ncols_all = 0, bool pdl = false);
+// pdl: programmatic dependent launch for chains whose A operand is NOT written
+// by the preceding kernel (butterfly apply stages): A is staged before the
+// dependency wait, overlapping the previous stage's tail.
 
 // ------------------------------------------ K5: batched truncated CPQR
 // Compact input rows: [0, r1) from src, [r1, r1+r2) from src + src_gap.
