@@ -93,6 +93,7 @@ def _ctx(ctx):
 
 
 # --------------------------------------------------------------------- trees
+
 class PartitionTree:
     """Complete bisection tree (tree.hpp:66-216)."""
 
@@ -495,15 +496,29 @@ class HybridButterfly(_Applicable):
         lib().bfly_rank_profile(self.h, _vp(out))
         return out.reshape(self.levels + 2, 1 << self.levels)
 
-    def serialize(self) -> bytearray:
-        """.bfh container bytes (reference format, serialize.hpp:103-127)."""
+    def serialized_size(self) -> int:
         n = lib().bfly_serialize(self.h, None)
         if n < 0:
             check(6)
-        buf = bytearray(n)
-        if lib().bfly_serialize(self.h, (C.c_uint8 * n).from_buffer(buf)) < 0:
+        return int(n)
+
+    def serialize(self, out=None):
+        """.bfh container bytes (reference format, serialize.hpp:103-127).
+
+        Factor blocks are packed into the file layout on the GPU and read back
+        with one device-to-host copy.  ``out``: optional writable buffer of at
+        least ``serialized_size()`` bytes (e.g. a reused pinned host buffer --
+        filling fresh pageable memory costs more than the export itself);
+        returns a memoryview of the written bytes.  Without ``out`` a new
+        bytearray is returned."""
+        n = self.serialized_size()
+        buf = bytearray(n) if out is None else out
+        view = (C.c_uint8 * n).from_buffer(buf)
+        rc = lib().bfly_serialize(self.h, view)
+        del view
+        if rc < 0:
             check(6)
-        return buf
+        return buf if out is None else memoryview(buf).cast("B")[:n]
 
     @staticmethod
     def deserialize(data: bytes, scalar=COMPLEX128, ctx=None) -> "HybridButterfly":

@@ -836,6 +836,49 @@ struct ByteSink {
   void u32(uint32_t v) { put(&v, 4); }
   void u64(uint64_t v) { put(&v, 8); }
 };
+
+// One level's blocks in .bfh layout (serialize.hpp:103-127): per block the
+// u64 row and column counts, then the compact column-major payload (rows
+// [0, r1) and [gap, gap + r2) of every column) as f64 (real) or c128.
+// Byte-granular stores: the payload's file offset has no alignment.
+struct PackBlk {
+  int64_t off;      // byte offset of the block header in the output
+  int32_t r1, r2, cols, pad_;
+};
+template <typename R>
+__global__ void pack_level_kernel(const cx<R>* __restrict__ data, int64_t ld, int64_t stride, int64_t gap,
+                                  const PackBlk* __restrict__ blks, int nb, int real, uint8_t* __restrict__ out) {
+  for (int i = blockIdx.x; i < nb; i += gridDim.x) {
+    const PackBlk b = blks[i];
+    const int64_t rows = b.r1 + b.r2;
+    uint8_t* dst = out + b.off;
+    if (threadIdx.x < 16) {
+      const uint64_t v = threadIdx.x < 8 ? (uint64_t)rows : (uint64_t)b.cols;
+      dst[threadIdx.x] = (uint8_t)(v >> (8 * (threadIdx.x & 7)));
+    }
+    dst += 16;
+    const cx<R>* blk = data + (int64_t)i * stride;
+    const int64_t n = rows * b.cols;
+    for (int64_t e = threadIdx.x; e < n; e += blockDim.x) {
+      const int64_t c = e / rows, q = e - c * rows;
+      const cx<R> v = blk[c * ld + (q < b.r1 ? q : gap + (q - b.r1))];
+      if (real) {
+        const double x = (double)v.x;
+        const uint64_t u = (uint64_t)__double_as_longlong(x);
+#pragma unroll
+        for (int t = 0; t < 8; ++t) dst[8 * e + t] = (uint8_t)(u >> (8 * t));
+      } else {
+        const uint64_t u0 = (uint64_t)__double_as_longlong((double)v.x);
+        const uint64_t u1 = (uint64_t)__double_as_longlong((double)v.y);
+#pragma unroll
+        for (int t = 0; t < 8; ++t) {
+          dst[16 * e + t] = (uint8_t)(u0 >> (8 * t));
+          dst[16 * e + 8 + t] = (uint8_t)(u1 >> (8 * t));
+        }
+      }
+    }
+  }
+}
 }  // namespace
 
 template <typename R>
@@ -859,47 +902,30 @@ int64_t DevButterfly<R>::serialize(int tag, uint8_t* out) const {
     bs.put(t->perm.data(), sizeof(int64_t) * t->perm.size());
     for (const auto& lv : t->ranges) bs.put(lv.data(), sizeof(int64_t) * lv.size());
   }
-  cx<R>* stage = nullptr;
-  // one level: rows/gap per block given by row_split(i) -> (r1, r2)
+  // levels: block headers + payloads, packed on the device into one buffer
+  // (exact file layout) and copied to the host once
+  const int64_t body0 = bs.pos;
+  const int64_t esz = real ? 8 : 16;
+  struct LevelJob {
+    const Level<R>* lv;
+    std::vector<PackBlk> blks;
+  };
+  std::vector<LevelJob> jobs;
+  int64_t pos = 0;  // relative to body0
   auto emit = [&](const Level<R>& lv, auto rows_of) {
-    if (out) {
-      size_t n = (size_t)(NB * lv.stride());
-      stage = static_cast<cx<R>*>(lv.data.ctx->pinned(n * sizeof(cx<R>)));
-      lv.data.download(stage, n);
-      BFLY_CUDA(cudaStreamSynchronize(lv.data.ctx->stream));
-    }
+    LevelJob j{&lv, std::vector<PackBlk>((size_t)NB)};
     for (int64_t i = 0; i < NB; ++i) {
       int64_t r1, r2;
       rows_of(i, r1, r2);
-      const int64_t cols = lv.ranks[i], rows = r1 + r2;
-      bs.u64((uint64_t)rows);
-      bs.u64((uint64_t)cols);
-      if (!out) {
-        bs.pos += rows * cols * (real ? 8 : 16);
-        continue;
-      }
-      const cx<R>* blk = stage + i * lv.stride();
-      for (int64_t c = 0; c < cols; ++c) {
-        const cx<R>* col = blk + c * lv.ld;
-        for (int part = 0; part < 2; ++part) {
-          const cx<R>* src = part == 0 ? col : col + lv.gap;
-          const int64_t cnt = part == 0 ? r1 : r2;
-          if (real) {
-            for (int64_t q = 0; q < cnt; ++q) {
-              double v = (double)src[q].x;
-              bs.put(&v, 8);
-            }
-          } else if (sizeof(R) == 8) {
-            bs.put(src, (size_t)cnt * 16);
-          } else {
-            for (int64_t q = 0; q < cnt; ++q) {
-              double v[2] = {(double)src[q].x, (double)src[q].y};
-              bs.put(v, 16);
-            }
-          }
-        }
-      }
+      PackBlk& b = j.blks[(size_t)i];
+      b.off = pos;
+      b.r1 = (int32_t)r1;
+      b.r2 = (int32_t)r2;
+      b.cols = lv.ranks[i];
+      b.pad_ = 0;
+      pos += 16 + (r1 + r2) * (int64_t)b.cols * esz;
     }
+    jobs.push_back(std::move(j));
   };
   emit(uleaf, [&](int64_t i, int64_t& r1, int64_t& r2) { r1 = rt.size(L, i); r2 = 0; });
   for (int l = lm; l < L; ++l)
@@ -916,7 +942,20 @@ int64_t DevButterfly<R>::serialize(int tag, uint8_t* out) const {
       r2 = v_rank(l - 1, tau / 2, 2 * nu + 1);
     });
   emit(vleaf, [&](int64_t i, int64_t& r1, int64_t& r2) { r1 = ct.size(L, i); r2 = 0; });
-  return bs.pos;
+  if (out && pos > 0) {
+    Ctx* c = ctx;
+    DBuf<uint8_t> body(c, (size_t)pos);
+    for (const LevelJob& j : jobs) {
+      DBuf<PackBlk> db = to_device(c, j.blks);
+      const unsigned grid = (unsigned)std::min<int64_t>(NB, (int64_t)c->sm_count * 16);
+      pack_level_kernel<R><<<grid, 256, 0, c->stream>>>(j.lv->data.p, j.lv->ld, j.lv->stride(), j.lv->gap, db.p,
+                                                        (int)NB, real ? 1 : 0, body.p);
+      BFLY_LAUNCH_CHECK("pack_level");
+    }
+    BFLY_CUDA(cudaMemcpyAsync(out + body0, body.p, (size_t)pos, cudaMemcpyDeviceToHost, c->stream));
+    BFLY_CUDA(cudaStreamSynchronize(c->stream));
+  }
+  return body0 + pos;
 }
 
 template struct Level<double>;

@@ -531,14 +531,46 @@ int bfly_factorize(bfly_ctx* ctx, bfly_op* op, const bfly_tree* rt, const bfly_t
     auto h = std::make_unique<bfly_bf>();
     h->ctx = ctx;
     h->scalar = op->scalar;
-    if (op->z) {
-      Factorizer<double> f(C_(ctx), op->z.get(), rt->t, ct->t, *cfg);
-      f.run();
-      h->z = f.take(log);
-    } else {
-      Factorizer<float> f(C_(ctx), op->c.get(), rt->t, ct->t, *cfg);
-      f.run();
-      h->c = f.take(log);
+    Ctx* c = C_(ctx);
+    auto run_once = [&] {
+      if (op->z) {
+        Factorizer<double> f(c, op->z.get(), rt->t, ct->t, *cfg);
+        f.run();
+        h->z = f.take(log);
+      } else {
+        Factorizer<float> f(c, op->c.get(), rt->t, ct->t, *cfg);
+        f.run();
+        h->c = f.take(log);
+      }
+    };
+    // K2 range checks are deferred to the end of the factorization (no host
+    // sync per black-box product); on an out-of-range entry the whole
+    // factorization is recomputed on the FP64 path, operator counters restored
+    auto counters = [&](int64_t* v, double* w, bool save) {
+      if (op->z) {
+        if (save) { v[0] = op->z->fwd; v[1] = op->z->tr; w[0] = op->z->flops; w[1] = op->z->evals; }
+        else { op->z->fwd = v[0]; op->z->tr = v[1]; op->z->flops = w[0]; op->z->evals = w[1]; }
+      } else {
+        if (save) { v[0] = op->c->fwd; v[1] = op->c->tr; w[0] = op->c->flops; w[1] = op->c->evals; }
+        else { op->c->fwd = v[0]; op->c->tr = v[1]; op->c->flops = w[0]; op->c->evals = w[1]; }
+      }
+    };
+    int64_t cv[2];
+    double cw[2];
+    counters(cv, cw, true);
+    struct Reset {
+      Ctx* c;
+      ~Reset() { c->oz_deferred = c->force_fp64 = false; }
+    } reset{c};
+    c->oz_deferred = true;
+    run_once();
+    c->oz_deferred = false;
+    if (c->take_oz_overflow()) {
+      counters(cv, cw, false);
+      h->z.reset();
+      h->c.reset();
+      c->force_fp64 = true;
+      run_once();
     }
     *out = h.release();
   });

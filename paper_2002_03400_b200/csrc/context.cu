@@ -1,5 +1,6 @@
 // context.cu -- per-GPU context implementation.
 #include "context.h"
+#include "comm.h"
 
 namespace bfly {
 
@@ -30,6 +31,7 @@ Ctx::~Ctx() {
     cudaStreamDestroy(stream);
   }
   if (pinned_p) cudaFreeHost(pinned_p);
+  if (oz_flag) cudaFree(oz_flag);
 }
 
 void* Ctx::alloc(size_t bytes) {
@@ -45,6 +47,7 @@ void Ctx::release(void* p) { cudaFreeAsync(p, stream); }
 void* Ctx::pinned(size_t bytes) {
   if (bytes > pinned_n) {
     if (pinned_p) cudaFreeHost(pinned_p);
+  if (oz_flag) cudaFree(oz_flag);
     pinned_p = nullptr;
     pinned_n = 0;
     BFLY_CUDA(cudaMallocHost(&pinned_p, bytes));
@@ -76,6 +79,24 @@ void Ctx::resolve_records() {
     s->bytes += r.bytes;
   }
   records.clear();
+}
+
+int* Ctx::oz_flag_dev() {
+  if (!oz_flag) {
+    BFLY_CUDA(cudaMalloc(&oz_flag, sizeof(int)));
+    BFLY_CUDA(cudaMemsetAsync(oz_flag, 0, sizeof(int), stream));
+  }
+  return oz_flag;
+}
+
+bool Ctx::take_oz_overflow() {
+  if (!oz_flag) return false;
+  if (world > 1 && comm) comm_allreduce_max_i32(this, oz_flag, 1);
+  int h = 0;
+  BFLY_CUDA(cudaMemcpyAsync(&h, oz_flag, sizeof(int), cudaMemcpyDeviceToHost, stream));
+  BFLY_CUDA(cudaStreamSynchronize(stream));
+  if (h) BFLY_CUDA(cudaMemsetAsync(oz_flag, 0, sizeof(int), stream));
+  return h != 0;
 }
 
 }  // namespace bfly

@@ -50,6 +50,13 @@ struct Ctx {
   size_t pinned_n = 0;
   void release(void* p);
   void sync();
+  // K2 int8-slice path range flag (k_matvec_oz.cu).  oz_deferred: launches OR
+  // into one persistent device flag that is checked once per factorization
+  // (no per-launch host sync); force_fp64: recompute on the FP64 DMMA path.
+  bool oz_deferred = false, force_fp64 = false;
+  int* oz_flag = nullptr;
+  int* oz_flag_dev();
+  bool take_oz_overflow();  // all ranks agree; resets the flag
 };
 
 // The context kernels are currently being launched for (set by the C ABI

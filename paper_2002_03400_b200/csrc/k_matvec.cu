@@ -535,7 +535,8 @@ void launch_kernel_matvec(Ctx* c, int kind, int mode, Points outp, Points inp, d
                           const cx<R>* X, cx<R>* Y, int64_t ldy, const MatvecSeg* segs, int nseg) {
   if (m_out <= 0 || nseg <= 0) return;
   if constexpr (std::is_same<R, double>::value) {
-    if (matvec_oz_enabled() && launch_kernel_matvec_oz(c, kind, mode, outp, inp, kappa, m_out, X, Y, ldy, segs, nseg))
+    if (!c->force_fp64 && matvec_oz_enabled() &&
+        launch_kernel_matvec_oz(c, kind, mode, outp, inp, kappa, m_out, X, Y, ldy, segs, nseg))
       return;
   }
   if (kind == KK_NUFFT) dispatch_mode<R, KK_NUFFT>(c, mode, outp, inp, kappa, m_out, X, Y, ldy, segs, nseg);

@@ -731,8 +731,13 @@ bool run_oz(Ctx* c, Points outp, Points inp, double kappa, int64_t m_out, const 
   ditems.upload(items.data(), items.size());
   DBuf<int32_t> T(c, items.size() * OZ_MAXCB);
   DBuf<uint8_t> img(c, (size_t)(nstages * Z::BSTAGE));
-  DBuf<int> flag(c, 1);
-  flag.zero();
+  DBuf<int> local_flag;
+  int* flag = c->oz_deferred ? c->oz_flag_dev() : nullptr;
+  if (!flag) {
+    local_flag.reset(c, 1);
+    local_flag.zero();
+    flag = local_flag.p;
+  }
   double kflops = 0, kbytes = 0;
   for (const auto& it : items) {
     kflops += 8.0 * (double)m_out * (double)it.rows * (double)it.ncols;
@@ -744,7 +749,7 @@ bool run_oz(Ctx* c, Points outp, Points inp, double kappa, int64_t m_out, const 
     BFLY_LAUNCH_CHECK("oz_colscale");
     const int64_t per_item = ceil_div(max_rows, (int64_t)OZ_KS) * OZ_KS * NCB;
     oz_slice_kernel<NCB><<<dim3((unsigned)ceil_div(per_item, (int64_t)256), (unsigned)items.size()), 256, 0, c->stream>>>(
-        X, ditems.p, T.p, img.p, flag.p);
+        X, ditems.p, T.p, img.p, flag);
     BFLY_LAUNCH_CHECK("oz_slice");
   }
   auto kern = matvec_oz_kernel<KIND, MODE, NCB>;
@@ -774,7 +779,7 @@ bool run_oz(Ctx* c, Points outp, Points inp, double kappa, int64_t m_out, const 
     KTimer timer(c, "kernel_matvec", kflops, kbytes);
     KTimer timer8(c, "kernel_matvec.int8_ops", int8_ops, 0.0);
     kern<<<grid, OZ_THREADS, Z::SM_TOTAL, c->stream>>>(outp, inp, kappa, m_out, img.p, T.p, Yt, ldy, ditems.p,
-                                                    rows_per_split, pstride, flag.p);
+                                                    rows_per_split, pstride, flag);
     BFLY_LAUNCH_CHECK("kernel_matvec_oz");
   }
   if (nsplit > 1) {
@@ -799,8 +804,11 @@ bool run_oz(Ctx* c, Points outp, Points inp, double kappa, int64_t m_out, const 
     BFLY_CUDA(cudaMemcpyToSymbol(g_oz_trace, z, sizeof(z)));
   }
 #endif
+  if (std::getenv("BFLY_OZ_TEST_OVERFLOW"))  // test hook: exercise the FP64 recompute path
+    BFLY_CUDA(cudaMemsetAsync(flag, 0xFF, sizeof(int), c->stream));
+  if (c->oz_deferred) return true;  // checked once per factorization (Ctx::take_oz_overflow)
   int hflag = 0;
-  flag.download(&hflag, 1);
+  local_flag.download(&hflag, 1);
   c->sync();
   return hflag == 0;
 }

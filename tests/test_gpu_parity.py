@@ -341,3 +341,22 @@ def test_cpp_adapter_drop_in():
     print(r.stdout)
     assert r.returncode == 0, r.stdout + r.stderr
     assert "ADAPTER PARITY OK" in r.stdout
+
+
+def test_int8_range_fallback_recomputes_on_fp64(B, oracle_threads, monkeypatch):
+    """K2's integer-slice path defers its range check to the end of a
+    factorization; a flagged launch makes the whole factorization rerun on the
+    FP64 DMMA path with the operator counters restored (forced here through
+    the BFLY_OZ_TEST_OVERFLOW hook).  Results and bookkeeping must still be
+    the oracle's, and the public apply path must recompute as well."""
+    op_o, rt_o, ct_o, cfg = oracle_config(2, 1024)
+    bf_o, log_o = O.factorize(op_o, rt_o, ct_o, dict(cfg, threads=oracle_threads))
+    w = B.configs.build(2, 1024)
+    monkeypatch.setenv("BFLY_OZ_TEST_OVERFLOW", "1")
+    bf_g, log_g = B.factorize(w.op, w.row_tree, w.col_tree, w.recon)
+    assert log_g.forward_columns() + log_g.transpose_columns() == w.op.total_columns()
+    _compare(bf_g, log_g, bf_o, log_o, w.op.rows, w.op.cols)
+    x = O.gaussian_matrix(w.op.cols, 3, 9)
+    assert rel_err(w.op.apply(x), op_o.apply(x)) < 1e-12
+    monkeypatch.delenv("BFLY_OZ_TEST_OVERFLOW")
+    assert rel_err(w.op.apply(x), op_o.apply(x)) < 1e-12
