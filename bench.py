@@ -34,10 +34,10 @@ sys.path.insert(0, ROOT)
 METRIC = "butterfly construction GFLOP/s at n=65536 complex128 (config 2)"
 FP64_PEAK_TFLOPS = 36.99  # measured DMMA m8n8k4 f64 on this pool (profiles/r01_fp64_peaks.txt)
 INT8_PEAK_TOPS = 4248.7  # measured tcgen05 kind::i8 M128 N256 from shared memory (profiles/r01_tc_i8.txt)
-# dram__bytes_read.sum + dram__bytes_write.sum of one K2 launch (config-2 transfer level, 8 segments x 32
-# columns; profiles/r01_matvec_oz_ncu.txt): 65.2 MB read + 212.4 MB write (= the 268 MB product it writes);
-# its algorithmic traffic (points + probes in, product out) is 302 MB
-K2_DRAM_BYTES_PER_LAUNCH = 277583616
+# dram__bytes_read.sum + dram__bytes_write.sum of one K2 launch (the 9th of a config-2 construction: 32
+# probe segments x 32 columns, profiles/r01_matvec_oz_ncu.txt): 69.2 MB read + 1015.8 MB write (= the
+# 1.07 GB product it writes); its algorithmic traffic (points + probes in, product out) is 1.11 GB
+K2_DRAM_BYTES_PER_LAUNCH = 1085056142
 CFG_ID = 2
 
 
