@@ -486,6 +486,13 @@ __global__ void __launch_bounds__(OZ_THREADS, 1)
     if (s == nst - 1) mma_commit(acc_full);
   };
 
+  // The last warp to finish stage g issues its MMAs only after evaluating its
+  // entries of stage g+1: FP64 and tensor work time-share the datapath, so
+  // the tensor then runs during the integer write phase (transposes, shared
+  // stores) instead of blocking the next evaluation.  Ordering holds: the
+  // issuer writes stage g+1 only after issuing stage g.
+  int pend_slot = -1, pend_s = 0, pend_nst = 0;
+  uint32_t pend_ph = 0;
   int g = 0;
   for (int d = 0; d < nchunks; ++d) {
     const int64_t c0 = kb + (int64_t)d * OZ_KD;
@@ -614,6 +621,10 @@ __global__ void __launch_bounds__(OZ_THREADS, 1)
         lo_i[e] = (uint32_t)__double2loint(ti);
         hi_i[e] = (uint32_t)__double2hiint(ti) - 0x43380000u;
       }
+      if (pend_slot >= 0) {  // lane 0 of last stage's issuing warp
+        issue_stage(pend_slot, pend_ph, pend_s, pend_nst);
+        pend_slot = -1;
+      }
       // ---- byte slices -> canonical K-major A images (4x4 byte transposes)
       uint8_t* a0 = smem + Z::SM_A + slot * OZ_ASTAGE;
       const int off = ((kofs >> 4) * (OZ_BM / 8) + (erow >> 3)) * 128 + (erow & 7) * 16 + (kofs & 15);
@@ -638,15 +649,20 @@ __global__ void __launch_bounds__(OZ_THREADS, 1)
       __syncwarp();
       if (lane == 0) {
         __threadfence_block();
-        if (atomicAdd(&cnt[slot], 1u) == OZ_EWARPS - 1) {  // last warp in: issue the stage
+        if (atomicAdd(&cnt[slot], 1u) == OZ_EWARPS - 1) {  // last warp in: issues the stage (deferred)
           cnt[slot] = 0;
           __threadfence_block();
-          issue_stage(slot, ph, s, nst);
+          pend_slot = slot;
+          pend_ph = ph;
+          pend_s = s;
+          pend_nst = nst;
         }
       }
       __syncwarp();
     }
   }
+  if (pend_slot >= 0) issue_stage(pend_slot, pend_ph, pend_s, pend_nst);
+  __syncwarp();
   if (nchunks > 0) drain(nchunks - 1);
   // |v| < 2^50 <=> high word of the scaled amplitude < 0x43100000 (NaN / inf fail)
   if (KIND != KK_NUFFT && amp_hi >= 0x43100000u) atomicOr(flag, 2);
