@@ -1,4 +1,7 @@
 // context.cu -- per-GPU context implementation.
+#include <algorithm>
+#include <cstdlib>
+
 #include "context.h"
 #include "comm.h"
 
@@ -15,14 +18,23 @@ void note_launch(const char*) {
 Ctx::Ctx(int dev) : device(dev) {
   BFLY_CUDA(cudaSetDevice(dev));
   BFLY_CUDA(cudaStreamCreateWithFlags(&stream, cudaStreamNonBlocking));
-  BFLY_CUDA(cudaDeviceGetDefaultMemPool(&pool, dev));
-  // keep freed blocks cached in the pool: level buffers are re-allocated
-  // every phase and must not go back to the driver each time.
+  // the library's own stream-ordered pool (isolated from other users of the
+  // device's default pool); freed blocks stay cached: level buffers are
+  // re-allocated every phase and must not go back to the driver each time.
+  cudaMemPoolProps props = {};
+  props.allocType = cudaMemAllocationTypePinned;
+  props.handleTypes = cudaMemHandleTypeNone;
+  props.location.type = cudaMemLocationTypeDevice;
+  props.location.id = dev;
+  BFLY_CUDA(cudaMemPoolCreate(&pool, &props));
   uint64_t threshold = UINT64_MAX;
   BFLY_CUDA(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &threshold));
   cudaDeviceProp p;
   BFLY_CUDA(cudaGetDeviceProperties(&p, dev));
   sm_count = p.multiProcessorCount;
+  // explicit up-front reservation (otherwise sized from the previous
+  // factorization's peak, see reserve_pool)
+  if (const char* e = std::getenv("BFLY_POOL_RESERVE_GB")) reserve_pool((size_t)(std::atof(e) * (double)(1ull << 30)));
 }
 
 Ctx::~Ctx() {
@@ -32,6 +44,7 @@ Ctx::~Ctx() {
   }
   if (pinned_p) cudaFreeHost(pinned_p);
   if (oz_flag) cudaFree(oz_flag);
+  if (pool) cudaMemPoolDestroy(pool);
 }
 
 void* Ctx::alloc(size_t bytes) {
@@ -48,6 +61,7 @@ void* Ctx::pinned(size_t bytes) {
   if (bytes > pinned_n) {
     if (pinned_p) cudaFreeHost(pinned_p);
   if (oz_flag) cudaFree(oz_flag);
+  if (pool) cudaMemPoolDestroy(pool);
     pinned_p = nullptr;
     pinned_n = 0;
     BFLY_CUDA(cudaMallocHost(&pinned_p, bytes));
@@ -97,6 +111,32 @@ bool Ctx::take_oz_overflow() {
   BFLY_CUDA(cudaStreamSynchronize(stream));
   if (h) BFLY_CUDA(cudaMemsetAsync(oz_flag, 0, sizeof(int), stream));
   return h != 0;
+}
+
+// One contiguous pool chunk of at least `bytes`: many separately grown
+// chunks fragment, and a multi-GB level buffer that fits none of them maps
+// new physical memory mid-factorization (hundreds of ms to seconds).
+void Ctx::reserve_pool(size_t bytes) {
+  if (bytes <= pool_reserved) return;
+  BFLY_CUDA(cudaStreamSynchronize(stream));
+  BFLY_CUDA(cudaMemPoolTrimTo(pool, 0));
+  void* q = nullptr;
+  if (cudaMallocFromPoolAsync(&q, bytes, pool, stream) == cudaSuccess) {
+    BFLY_CUDA(cudaFreeAsync(q, stream));
+    BFLY_CUDA(cudaStreamSynchronize(stream));
+    pool_reserved = bytes;
+  } else {
+    cudaGetLastError();  // not enough memory for one chunk: keep growing on demand
+  }
+}
+
+// after a factorization: remember its peak pool use for the next one
+void Ctx::note_pool_peak() {
+  uint64_t high = 0;
+  if (cudaMemPoolGetAttribute(pool, cudaMemPoolAttrUsedMemHigh, &high) != cudaSuccess) return;
+  pool_hint = std::max<size_t>(pool_hint, (size_t)(high + high / 16));
+  uint64_t zero = 0;
+  cudaMemPoolSetAttribute(pool, cudaMemPoolAttrUsedMemHigh, &zero);
 }
 
 }  // namespace bfly

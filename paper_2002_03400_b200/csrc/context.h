@@ -57,6 +57,11 @@ struct Ctx {
   int* oz_flag = nullptr;
   int* oz_flag_dev();
   bool take_oz_overflow();  // all ranks agree; resets the flag
+  // pool sizing: a factorization reserves one contiguous chunk sized to the
+  // previous one's peak (see reserve_pool)
+  size_t pool_reserved = 0, pool_hint = 0;
+  void reserve_pool(size_t bytes);
+  void note_pool_peak();
 };
 
 // The context kernels are currently being launched for (set by the C ABI

@@ -177,6 +177,98 @@ __device__ __forceinline__ void dmma884(double& d0, double& d1, double a, double
                : "d"(a), "d"(b));
 }
 
+// Narrow entries (M <= 16 rows, <= 32 columns: the U/V chain projections of
+// one probe, ~10^5 entries per launch): one WARP per entry, m8n8k4 DMMA
+// fragments loaded straight from global memory (L1/L2 resident), no shared
+// memory or block barriers.  Complex MAC = 4 real DMMAs.
+template <int OP, int S>
+__global__ void __launch_bounds__(256) bgemm_dmma_warp_kernel(const double2* __restrict__ A, int64_t lda,
+                                                              const double2* __restrict__ B, int64_t ldb,
+                                                              double2* __restrict__ C, int64_t ldc, int M, int K,
+                                                              const GemmEnt* __restrict__ ents, int nent,
+                                                              int accumulate, int ncols_all) {
+  const int lane = threadIdx.x & 31;
+  const int ei = blockIdx.x * 8 + (threadIdx.x >> 5);
+  if (ei >= nent) return;
+  const GemmEnt e = ents[ei];
+  const int ncols = ncols_all > 0 ? ncols_all : e.ncols;
+  const int Me = min(M, e.mrows), Ke = min(K, e.krows);
+  const int g = lane >> 2, t = lane & 3;
+  double acc[2][4][2][2];  // [m tile][n tile][re|im][2]
+#pragma unroll
+  for (int a = 0; a < 2; ++a)
+#pragma unroll
+    for (int b = 0; b < 4; ++b) acc[a][b][0][0] = acc[a][b][0][1] = acc[a][b][1][0] = acc[a][b][1][1] = 0.0;
+#pragma unroll
+  for (int s = 0; s < S; ++s) {
+    const double2* Ab = A + (s == 0 ? e.a0 : e.a1);
+    const double2* Bb = B + (s == 0 ? e.b0 : e.b1);
+    for (int k0 = 0; k0 < K; k0 += 4) {
+      const int k = k0 + t;
+      double ar[2], ai[2], br[4], bi[4];
+#pragma unroll
+      for (int a = 0; a < 2; ++a) {
+        const int m = a * 8 + g;
+        double2 v = make_double2(0.0, 0.0);
+        if (m < M && k < K) {
+          if (OP == OP_N) v = Ab[m + (int64_t)k * lda];
+          else {
+            v = Ab[k + (int64_t)m * lda];
+            if (OP == OP_H) v.y = -v.y;
+          }
+        }
+        ar[a] = v.x;
+        ai[a] = v.y;
+      }
+#pragma unroll
+      for (int b = 0; b < 4; ++b) {
+        const int n = b * 8 + g;
+        double2 v = make_double2(0.0, 0.0);
+        if (n < ncols && k < Ke) v = Bb[k + (int64_t)n * ldb];
+        br[b] = v.x;
+        bi[b] = v.y;
+      }
+#pragma unroll
+      for (int a = 0; a < 2; ++a)
+#pragma unroll
+        for (int b = 0; b < 4; ++b) {
+          dmma884(acc[a][b][0][0], acc[a][b][0][1], ar[a], br[b]);
+          dmma884(acc[a][b][1][0], acc[a][b][1][1], ar[a], bi[b]);
+        }
+#pragma unroll
+      for (int a = 0; a < 2; ++a) {
+        const double nai = -ai[a];
+#pragma unroll
+        for (int b = 0; b < 4; ++b) {
+          dmma884(acc[a][b][0][0], acc[a][b][0][1], nai, bi[b]);
+          dmma884(acc[a][b][1][0], acc[a][b][1][1], ai[a], br[b]);
+        }
+      }
+    }
+  }
+  double2* Cb = C + e.c;
+#pragma unroll
+  for (int a = 0; a < 2; ++a) {
+    const int m = a * 8 + g;
+    if (m >= Me) continue;
+#pragma unroll
+    for (int b = 0; b < 4; ++b)
+#pragma unroll
+      for (int v = 0; v < 2; ++v) {
+        const int n = b * 8 + 2 * t + v;
+        if (n >= ncols) continue;
+        double2 r = make_double2(acc[a][b][0][v], acc[a][b][1][v]);
+        double2* p = Cb + m + (int64_t)n * ldc;
+        if (accumulate) {
+          const double2 o = *p;
+          r.x += o.x;
+          r.y += o.y;
+        }
+        *p = r;
+      }
+  }
+}
+
 template <int OP, int S, int MT>
 __global__ void __launch_bounds__(256) bgemm_dmma_kernel(const double2* __restrict__ A, int64_t lda,
                                                          const double2* __restrict__ B, int64_t ldb,
@@ -339,6 +431,30 @@ void launch_bgemm(Ctx* c, int op, int M, int K, int S, const cx<R>* A, int64_t l
   }
   if constexpr (std::is_same<R, double>::value) {
     static const bool no_dmma = std::getenv("BFLY_NO_DMMA_GEMM") != nullptr;
+    static const bool no_warp = std::getenv("BFLY_NO_WARP_GEMM") != nullptr;
+    if (!no_dmma && !no_warp && kcols > 16 && max_ncols <= 32 && M <= 16 && K > 0) {
+      static const char* wnames[3][2] = {{"bgemm_warp_N1", "bgemm_warp_N2"},
+                                         {"bgemm_warp_T1", "bgemm_warp_T2"},
+                                         {"bgemm_warp_H1", "bgemm_warp_H2"}};
+      KTimer timer(c, wnames[op][S - 1], 8.0 * M * K * S * (double)nent * kcols,
+                   sizeof(cx<R>) * ((double)nent * S * (M * (double)K + K * kcols) + (double)nent * M * kcols));
+      const unsigned grid = (unsigned)ceil_div((int64_t)nent, (int64_t)8);
+#define BW(OPV, SV)                                                                                          \
+  bgemm_dmma_warp_kernel<OPV, SV><<<grid, 256, 0, c->stream>>>(A, lda, B, ldb, C, ldc, M, K, ents, nent,      \
+                                                               accumulate, ncols_all)
+      if (S == 1) {
+        if (op == OP_N) BW(OP_N, 1);
+        else if (op == OP_T) BW(OP_T, 1);
+        else BW(OP_H, 1);
+      } else {
+        if (op == OP_N) BW(OP_N, 2);
+        else if (op == OP_T) BW(OP_T, 2);
+        else BW(OP_H, 2);
+      }
+#undef BW
+      BFLY_LAUNCH_CHECK("bgemm_warp");
+      return;
+    }
     if (!no_dmma && kcols > 16 && M <= 64 && K > 0) {
       const unsigned gy = (unsigned)ceil_div(max_ncols, 64);
       if (gy > 65535) fail(PRECONDITION, "bgemm: grid too large");

@@ -26,6 +26,9 @@ def main():
                 w.op.ctx.profile(-1)
                 w.op.ctx.profile(1)
             bf, log = B.factorize(w.op, w.row_tree, w.col_tree, w.recon)
+            if a.reps > 1:
+                worst = max(log.phases, key=lambda p: p.seconds)
+                print(f"   rep {r}: construct {log.total_seconds:.4f}s (slowest phase {worst.name} {worst.seconds*1e3:.1f} ms)")
         if a.profile:
             for k, v in sorted(w.op.ctx.profile_report().items(), key=lambda kv: -kv[1]["ms"]):
                 print(f"   kernel {k:22s} launches {v['launches']:5d} ms {v['ms']:9.2f} "
