@@ -54,7 +54,9 @@ namespace {
 constexpr int OZ_NSL = 7;                         // slices per operand
 constexpr int OZ_NDIAG = 8;                       // kept diagonals e = 5..12
 constexpr int OZ_KS = 32;                         // input entries per stage (MMA K)
-constexpr int OZ_KD = 1024;                       // entries per drain / scale chunk
+// drain / scale chunk: 2048 entries (int32 diagonal sums stay < 2^30); the 3D
+// kernel keeps 1024 (its z coordinates must fit shared memory too)
+constexpr int oz_kd(int kind) { return kind == KK_PLATES ? 1024 : 2048; }
 constexpr int OZ_NST = 2;                         // ring depth
 constexpr int OZ_BM = 128;                        // output rows per CTA (= TMEM lanes)
 constexpr int OZ_EWARPS = 16;
@@ -97,9 +99,11 @@ constexpr OzSched make_sched(int maxb) {
 }
 
 // NCB-dependent sizes and the shared-memory map (bytes)
-template <int NCB_>
+template <int NCB_, int KD_, bool HASZ_>
 struct OzT {
   static constexpr int NCB = NCB_;                   // complex probe columns per tile
+  static constexpr int KD = KD_;                     // entries per drain / scale chunk
+  static constexpr int NBOX = KD / 32;               // sub-boxes of 32 points per chunk
   static constexpr int BN2 = 2 * NCB;                // N-rows per B slice ([re | im])
   static constexpr int TMEM_COLS = pow2_ceil(OZ_NDIAG * BN2);
   static constexpr int BROWS = OZ_NSL * BN2;         // N-rows per B operand
@@ -110,14 +114,13 @@ struct OzT {
   static constexpr int SM_A = 0;
   static constexpr int SM_B = SM_A + OZ_NST * OZ_ASTAGE;
   static constexpr int SM_PD = SM_B + OZ_NST * BSTAGE;  // double2 (x, y) [KD]
-  static constexpr int SM_PZ = SM_PD + OZ_KD * 16;      // double z [KD]
-  static constexpr int SM_PF = SM_PZ + OZ_KD * 8;       // float4 local (x, y, z, 0) [KD]
-  static constexpr int SM_S = SM_PF + OZ_KD * 16;       // int S_row [2][128]
+  static constexpr int SM_PZ = SM_PD + KD * 16;         // double z [KD] (3D kernels only)
+  static constexpr int SM_S = SM_PZ + (HASZ_ ? KD * 8 : 0);  // int S_row [2][128]
   static constexpr int SM_T = SM_S + 2 * OZ_BM * 4;     // int T [NCB]
   static constexpr int SM_MIN = SM_T + OZ_MAXCB * 4;    // uint min d2 bits [128]
   static constexpr int SM_TAB = SM_MIN + OZ_BM * 4;     // double2 sin/cos table [kTabN]
-  static constexpr int SM_BOX = SM_TAB + keval::kTabN * 16;  // float4 sub-box bounds [32][2]
-  static constexpr int SM_CNT = SM_BOX + 64 * 16;       // uint stage arrival counters [NST]
+  static constexpr int SM_BOX = SM_TAB + keval::kTabN * 16;  // float4 sub-box bounds [NBOX][2]
+  static constexpr int SM_CNT = SM_BOX + NBOX * 32;     // uint stage arrival counters [NST]
   static constexpr int SM_BAR = SM_CNT + 16;            // mbarriers
   static constexpr int NBAR = 2 * OZ_NST + 1;
   static constexpr int SM_TMEM = SM_BAR + NBAR * 8;
@@ -316,7 +319,7 @@ __device__ __forceinline__ void digits7(double x, int (&d)[OZ_NSL]) {
 template <int NCB>
 __global__ void oz_slice_kernel(const double2* __restrict__ X, const OzItem* __restrict__ items,
                                 const int32_t* __restrict__ T, uint8_t* __restrict__ img, int* __restrict__ flag) {
-  using Z = OzT<NCB>;
+  using Z = OzT<NCB, 1024, false>;  // B image geometry only (independent of KD)
   const OzItem it = items[blockIdx.y];
   const int64_t kpad = ceil_div(it.rows, (int64_t)OZ_KS) * OZ_KS;
   const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -364,7 +367,7 @@ __global__ void __launch_bounds__(OZ_THREADS, 1)
     matvec_oz_kernel(Points outp, Points inp, double kappa, int64_t m_out, const uint8_t* __restrict__ bimg,
                      const int32_t* __restrict__ Tg, double2* __restrict__ Y, int64_t ldy,
                      const OzItem* __restrict__ items, int64_t rows_per_split, int64_t pstride, int* __restrict__ flag) {
-  using Z = OzT<NCB>;
+  using Z = OzT<NCB, oz_kd(KIND), KIND == KK_PLATES>;
   extern __shared__ __align__(1024) uint8_t smem[];
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   OZT_BEGIN(t5)
@@ -373,11 +376,10 @@ __global__ void __launch_bounds__(OZ_THREADS, 1)
   const int64_t kb = (int64_t)blockIdx.z * rows_per_split;
   const int64_t ke = min(it.rows, kb + rows_per_split);
   const int64_t nk = ke > kb ? ke - kb : 0;
-  const int nchunks = (int)ceil_div(nk, (int64_t)OZ_KD);
+  const int nchunks = (int)ceil_div(nk, (int64_t)Z::KD);
 
   double2* PD = reinterpret_cast<double2*>(smem + Z::SM_PD);
   double* PZ = reinterpret_cast<double*>(smem + Z::SM_PZ);
-  float4* PF = reinterpret_cast<float4*>(smem + Z::SM_PF);
   int* Srow = reinterpret_cast<int*>(smem + Z::SM_S);
   int* Ts = reinterpret_cast<int*>(smem + Z::SM_T);
   unsigned* Smin = reinterpret_cast<unsigned*>(smem + Z::SM_MIN);
@@ -495,8 +497,8 @@ __global__ void __launch_bounds__(OZ_THREADS, 1)
   uint32_t pend_ph = 0;
   int g = 0;
   for (int d = 0; d < nchunks; ++d) {
-    const int64_t c0 = kb + (int64_t)d * OZ_KD;
-    const int npts = (int)min((int64_t)OZ_KD, ke - c0);
+    const int64_t c0 = kb + (int64_t)d * Z::KD;
+    const int npts = (int)min((int64_t)Z::KD, ke - c0);
     const int nst = (int)ceil_div((int64_t)npts, (int64_t)OZ_KS);
     // ---- chunk setup: input points, per-row scale S (bound on |a| over the chunk)
     OZT_BEGIN(t6)
@@ -513,18 +515,21 @@ __global__ void __launch_bounds__(OZ_THREADS, 1)
       const double z = KIND == KK_PLATES ? inp.z[pk] : 0.0;
       PD[k] = make_double2(x, y);
       if (KIND == KK_PLATES) PZ[k] = z;
-      PF[k] = make_float4((float)(x - bx), (float)(y - by), (float)(z - bz), 0.f);
     }
     if (tid < OZ_BM) Smin[tid] = 0x7F7FFFFFu;  // FLT_MAX bits
     __syncthreads();
     if (KIND != KK_NUFFT) {
-      // bounding boxes of the 32 sub-boxes of 32 consecutive (tree-ordered) points
-      float4* BX = reinterpret_cast<float4*>(smem + Z::SM_BOX);  // [32][lo, hi]
+      // bounding boxes of the sub-boxes of 32 consecutive (tree-ordered) points,
+      // in float coordinates local to the chunk's first point
+      float4* BX = reinterpret_cast<float4*>(smem + Z::SM_BOX);  // [NBOX][lo, hi]
 #pragma unroll
-      for (int q = 0; q < 2; ++q) {
-        const int sb = warp * 2 + q;
-        const float4 pt = PF[min(sb * 32 + lane, OZ_KD - 1)];
-        float lx = pt.x, ly = pt.y, lz = pt.z, hx = pt.x, hy = pt.y, hz = pt.z;
+      for (int q = 0; q < Z::NBOX / OZ_EWARPS; ++q) {
+        const int sb = warp * (Z::NBOX / OZ_EWARPS) + q;
+        const int k = min(sb * 32 + lane, Z::KD - 1);
+        const double2 pd = PD[k];
+        const float px = (float)(pd.x - bx), py = (float)(pd.y - by);
+        const float pz = KIND == KK_PLATES ? (float)(PZ[k] - bz) : 0.f;
+        float lx = px, ly = py, lz = pz, hx = px, hy = py, hz = pz;
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) {
           lx = fminf(lx, __shfl_xor_sync(0xffffffffu, lx, o));
@@ -558,11 +563,11 @@ __global__ void __launch_bounds__(OZ_THREADS, 1)
         if (d2 == 0.f) {
           d2 = 3.0e38f;
           for (int k = b * 32; k < b * 32 + 32; ++k) {
-            const float4 p = PF[k];
-            const float ex = lx - p.x, ey = ly - p.y;
+            const double2 pd = PD[k];
+            const float ex = lx - (float)(pd.x - bx), ey = ly - (float)(pd.y - by);
             float e2 = fmaf(ex, ex, ey * ey);
             if (KIND == KK_PLATES) {
-              const float ez = lz - p.z;
+              const float ez = lz - (float)(PZ[k] - bz);
               e2 = fmaf(ez, ez, e2);
             }
             d2 = fminf(d2, e2);
@@ -704,7 +709,7 @@ __global__ void oz_reduce_kernel(const double2* __restrict__ P, int64_t pstride,
 template <int KIND, int MODE, int NCB>
 bool run_oz(Ctx* c, Points outp, Points inp, double kappa, int64_t m_out, const double2* X, double2* Y, int64_t ldy,
             const MatvecSeg* segs, int nseg) {
-  using Z = OzT<NCB>;
+  using Z = OzT<NCB, oz_kd(KIND), KIND == KK_PLATES>;
   std::vector<OzItem> items;
   std::vector<const MatvecSeg*> item_seg;
   int64_t max_rows = 0, max_col = 0, nstages = 0;
@@ -738,9 +743,9 @@ bool run_oz(Ctx* c, Points outp, Points inp, double kappa, int64_t m_out, const 
   // split long segments so the grid covers every SM a few times (1 CTA / SM)
   const int64_t target = (int64_t)c->sm_count * 4;
   int nsplit = 1;
-  if (base_ctas < target) nsplit = (int)std::min<int64_t>(ceil_div(target, base_ctas), ceil_div(max_rows, OZ_KD));
+  if (base_ctas < target) nsplit = (int)std::min<int64_t>(ceil_div(target, base_ctas), ceil_div(max_rows, (int64_t)Z::KD));
   nsplit = std::max(1, std::min(nsplit, 64));
-  const int64_t rows_per_split = ceil_div(ceil_div(max_rows, (int64_t)nsplit), (int64_t)OZ_KD) * OZ_KD;
+  const int64_t rows_per_split = ceil_div(ceil_div(max_rows, (int64_t)nsplit), (int64_t)Z::KD) * Z::KD;
   nsplit = (int)ceil_div(max_rows, rows_per_split);
 
   DBuf<OzItem> ditems(c, items.size());
