@@ -360,3 +360,29 @@ def test_int8_range_fallback_recomputes_on_fp64(B, oracle_threads, monkeypatch):
     assert rel_err(w.op.apply(x), op_o.apply(x)) < 1e-12
     monkeypatch.delenv("BFLY_OZ_TEST_OVERFLOW")
     assert rel_err(w.op.apply(x), op_o.apply(x)) < 1e-12
+
+
+@pytest.mark.parametrize("real", [False, True])
+def test_serialize_into_caller_buffer_matches_oracle_layout(B, real):
+    """The .bfh export is packed on the GPU straight into the file layout
+    (serialize.hpp:103-127); writing into a caller-provided (reused, pinned)
+    buffer gives the same bytes as the default allocation, and both parse in
+    the oracle into the same container."""
+    import torch
+
+    scalar = B.REAL64 if real else B.COMPLEX128
+    bf = B.synth_butterfly(5, 3, 17, scalar=scalar)
+    op = B.ButterflyOperator(bf)
+    t = B.PartitionTree.build(np.arange(256, dtype=float), 5)
+    a, _ = B.factorize(op, t, t, B.ReconstructionConfig(levels=5, tolerance=1e-10, seed=5))
+    ref = bytes(a.serialize())
+    n = a.serialized_size()
+    assert n == len(ref)
+    host = torch.empty(n + 4096, dtype=torch.uint8, pin_memory=True)
+    for _ in range(2):  # reuse
+        view = a.serialize(out=host.numpy())
+        assert len(view) == n and bytes(view) == ref
+    o = O.HybridButterfly.deserialize(ref)
+    assert bytes(o.serialize()) == ref
+    x = O.gaussian_matrix(256, 3, 4, real=real)
+    assert rel_err(a.apply(x), o.apply(x)) < 1e-13
