@@ -192,7 +192,7 @@ def run_ours(args):
     ctx.profile(-1)
     ctx.profile(1)
     launches0 = ctx.launches
-    total_ms, flops, logs = 0.0, 0.0, []
+    total_ms, flops, logs, step_ms = 0.0, 0.0, [], []
     for _ in range(args.steps):
         l2_flush()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -200,7 +200,8 @@ def run_ours(args):
         bf, log = B.factorize(op, rt, ct, rc)
         e1.record(stream)
         e1.synchronize()
-        total_ms += e0.elapsed_time(e1)
+        step_ms.append(e0.elapsed_time(e1))
+        total_ms += step_ms[-1]
         flops += log.flops
         logs.append(log)
     launches = ctx.launches - launches0
@@ -308,6 +309,10 @@ def run_ours(args):
                                        else f"replicas{world}" if world > 1 else "single"),
                        "l2": "flushed before every step (256 MB write); probe products 0.1-1 GB > L2"},
             "construct_seconds": round(ms_per_step / 1e3, 4),
+            "construct_seconds_median": round(statistics.median(step_ms) / 1e3, 4),
+            # per-phase wall times (PhaseStat names), median over the timed steps
+            "phases_ms": {p.name: round(statistics.median(lg.phases[i].seconds for lg in logs) * 1e3, 3)
+                          for i, p in enumerate(logs[0].phases)},
             "flops_per_step": fl.item() / args.steps, "kernel_evals_per_step": logs[0].kernel_evals,
             "max_rank": bf.max_rank(), "nnz": bf.nnz(),
             "roofline": roofline,

@@ -122,6 +122,10 @@ class RefButterfly:
         n = lib().ref_log(self.h, _vp(cols), _vp(rounds), _vp(widths), C.byref(tot))
         return [(int(cols[2 * i]), int(cols[2 * i + 1]), int(rounds[i]), int(widths[i])) for i in range(n)], tot.value
 
+    def estimate_error(self, k=16, seed=0):
+        """estimate_error(op, bf, k, seed) of the reference (reconstruct.hpp:423-434)."""
+        return float(lib().ref_estimate_error(self.op.h, self.h, k, seed))
+
     def serialize(self):
         n = lib().ref_serialize(self.h, None)
         buf = np.zeros(n, np.uint8)

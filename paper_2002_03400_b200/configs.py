@@ -78,10 +78,16 @@ def nufft_points(n, op_seed):
     return x, xi
 
 
-def build(cfg_id: int, n: int | None = None, scalar=api.COMPLEX128, ctx=None, seed: int = 0) -> Workload:
+def build(cfg_id: int, n: int | None = None, scalar=api.COMPLEX128, ctx=None, seed: int = 0,
+          levels: int | None = None) -> Workload:
+    """``levels`` overrides the tree depth (default: depth_for(n, leaf)),
+    like the reference CLI's --L (tools/bfly_cli.cpp:351)."""
     n = n or FULL_N[cfg_id]
+
+    def depth(nn, leaf):
+        return levels if levels else api.PartitionTree.depth_for(nn, leaf)
     if cfg_id == 0:
-        L = api.PartitionTree.depth_for(n, 32)
+        L = depth(n, 32)
         x, xi = nufft_points(n, 0)
         x, rt = tree_order(x, L, 1)
         xi, ct = tree_order(xi, L, 1)
@@ -91,7 +97,7 @@ def build(cfg_id: int, n: int | None = None, scalar=api.COMPLEX128, ctx=None, se
     if cfg_id == 1:
         side = int(round(math.sqrt(n)))
         assert side * side == n, "plates need a square point count"
-        L = api.PartitionTree.depth_for(n, 32)
+        L = depth(n, 32)
         h = 1.0 / side
         kappa = 2.0 * math.pi / (10.0 * h)
         t, rt = tree_order(points_plate(side, 0.0), L, 3)
@@ -100,7 +106,7 @@ def build(cfg_id: int, n: int | None = None, scalar=api.COMPLEX128, ctx=None, se
         rc = api.ReconstructionConfig(tolerance=1e-6, rank_guess=16, levels=L, seed=seed)
         return Workload(1, n, op, rt, ct, rc, f"helmholtz_plates_n{n}", dict(leaf=32, kappa=kappa))
     if cfg_id == 2:
-        L = api.PartitionTree.depth_for(n, 32)
+        L = depth(n, 32)
         kappa = 2.0 * n / 10.0
         t, rt = tree_order(points_half_circle(n, True), L, 2)
         s, ct = tree_order(points_half_circle(n, False), L, 2)
@@ -108,7 +114,7 @@ def build(cfg_id: int, n: int | None = None, scalar=api.COMPLEX128, ctx=None, se
         rc = api.ReconstructionConfig(tolerance=1e-6, rank_guess=4, levels=L, seed=seed)
         return Workload(2, n, op, rt, ct, rc, f"helmholtz_circle_n{n}", dict(leaf=32, kappa=kappa))
     if cfg_id == 3:
-        L = api.PartitionTree.depth_for(n, 32)
+        L = depth(n, 32)
         x1, xi1 = nufft_points(n, 1)
         x2, xi2 = nufft_points(n, 2)
         x2, rt = tree_order(x2, L, 1)      # rows of A = F2's targets
@@ -120,7 +126,7 @@ def build(cfg_id: int, n: int | None = None, scalar=api.COMPLEX128, ctx=None, se
         return Workload(3, n, op, rt, ct, rc, f"nufft_composition_n{n}", dict(leaf=32))
     if cfg_id == 4:
         leaf, rank = 64, 32
-        L = api.PartitionTree.depth_for(n, leaf)
+        L = depth(n, leaf)
         bf = api.synth_butterfly(L, rank, 0, leaf=leaf, scalar=scalar, perturb=1e-8, ctx=ctx)
         rt = api.PartitionTree.build(np.arange(n, dtype=np.float64), L)
         op = api.ButterflyOperator(bf, ctx=ctx)

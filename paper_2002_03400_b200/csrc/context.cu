@@ -125,6 +125,9 @@ void Ctx::reserve_pool(size_t bytes) {
     BFLY_CUDA(cudaFreeAsync(q, stream));
     BFLY_CUDA(cudaStreamSynchronize(stream));
     pool_reserved = bytes;
+    // the reservation itself must not count as a factorization's peak
+    uint64_t zero = 0;
+    cudaMemPoolSetAttribute(pool, cudaMemPoolAttrUsedMemHigh, &zero);
   } else {
     cudaGetLastError();  // not enough memory for one chunk: keep growing on demand
   }
@@ -134,7 +137,8 @@ void Ctx::reserve_pool(size_t bytes) {
 void Ctx::note_pool_peak() {
   uint64_t high = 0;
   if (cudaMemPoolGetAttribute(pool, cudaMemPoolAttrUsedMemHigh, &high) != cudaSuccess) return;
-  pool_hint = std::max<size_t>(pool_hint, (size_t)(high + high / 16));
+  // grow the hint only when the peak really exceeds the reservation
+  if ((size_t)high > pool_reserved) pool_hint = std::max<size_t>(pool_hint, (size_t)(high + high / 16));
   uint64_t zero = 0;
   cudaMemPoolSetAttribute(pool, cudaMemPoolAttrUsedMemHigh, &zero);
 }

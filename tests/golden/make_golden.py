@@ -14,11 +14,13 @@ on the generators staying unchanged.
 Files
   rng.npz      seed_mix (core.hpp:78-88) and gaussian_matrix (linalg.hpp:16-25)
                known answers, complex and real streams
+  probe_kat.npz  first 64 Gaussians of every probe-seed family (leaf, W, R,
+               error probe) of config 2
   cpqr.npz     pivoted_qr_truncate (linalg.hpp:63-80): ranks and bases
   cfg_*.npz    factorize (reconstruct.hpp:412-419) on small BASELINE configs and
                the reference's synthetic butterfly: rank profile of every
                block, per-phase bookkeeping, butterfly apply / adjoint apply
-               outputs on reference-generated probes
+               outputs on reference-generated probes, estimate_error
 """
 import os
 import sys
@@ -54,6 +56,35 @@ def make_rng():
         d[f"gz_{tag}_seed"] = np.uint64(seed)
         d[f"gd_{tag}"] = R.gaussian_matrix(rows, cols, seed, complex_=False)
     np.savez_compressed(os.path.join(HERE, "rng.npz"), **d)
+
+
+def make_probe_kats():
+    """First 64 Gaussians of every probe-seed family of config 2 (reconstruct.hpp
+    seeds: leaf seed_mix(seed, tag, round) :370-372, W seed_mix(seed, 3, l, tau)
+    :219, R seed_mix(seed, 4, l, nu) :275, error probe seed_mix(seed, 5) :428),
+    drawn through gaussian_matrix (column-major fill, so any probe's first
+    entries are these)."""
+    seeds, words = [], []
+    for tag in (1, 2):
+        for rnd in range(3):
+            words.append((0, tag, rnd))
+    for l in (1, 3, 5):
+        for node in (0, 1, (1 << l) - 1):
+            words.append((0, 3, l, node))
+            words.append((0, 4, l, node))
+    words.append((0, 5))
+    kat = np.zeros((len(words), 64), np.complex128)
+    for i, w in enumerate(words):
+        s = R.seed_mix(*w)
+        seeds.append(s)
+        kat[i] = R.gaussian_matrix(64, 1, s)[:, 0]
+    wa = np.zeros((len(words), 4), np.uint64)
+    nw = np.zeros(len(words), np.int32)
+    for i, w in enumerate(words):
+        wa[i, : len(w)] = w
+        nw[i] = len(w)
+    np.savez_compressed(os.path.join(HERE, "probe_kat.npz"), words=wa, nwords=nw, seeds=np.array(seeds, np.uint64),
+                        first64=kat)
 
 
 def make_cpqr():
@@ -120,7 +151,7 @@ def save_factorization(name, inp, op, bf, L, seed):
     d = dict(inp)
     d.update(seed=seed, rank_profile=bf.rank_profile(L), phases=np.array(phases, np.int64),
              probe_x=x, probe_y=y, apply_n=bf.apply(np.asfortranarray(x), 0),
-             apply_h=bf.apply(np.asfortranarray(y), 2))
+             apply_h=bf.apply(np.asfortranarray(y), 2), estimate_error=bf.estimate_error(16, 3))
     np.savez_compressed(os.path.join(HERE, f"{name}.npz"), **d)
     print(name, "ranks", int(d["rank_profile"].max()), "phases", len(phases))
 
@@ -141,5 +172,6 @@ def make_configs():
 if __name__ == "__main__":
     assert R.available(), "build oracle/_ref first (make -C oracle/ref)"
     make_rng()
+    make_probe_kats()
     make_cpqr()
     make_configs()

@@ -51,6 +51,20 @@ def test_oracle_gaussian_golden_bit_exact(tag):
     np.testing.assert_array_equal(O.gaussian_matrix(rows, cols, seed, real=True), gd)
 
 
+def _probe_kats():
+    g = _load("probe_kat.npz")
+    for words, nw, seed, first in zip(g["words"], g["nwords"], g["seeds"], g["first64"]):
+        yield [int(x) for x in words[:nw]], int(seed), first
+
+
+def test_oracle_probe_seed_kats_bit_exact():
+    """Every probe-seed family (leaf, W, R, error probe): the seed and the
+    first 64 Gaussians of the probe equal the reference's bit for bit."""
+    for words, seed, first in _probe_kats():
+        assert O.seed_mix(*words) == seed, words
+        np.testing.assert_array_equal(O.gaussian_matrix(64, 1, seed)[:, 0], first)
+
+
 def test_oracle_cpqr_golden():
     g = _load("cpqr.npz")
     for name in g["names"]:
@@ -95,6 +109,8 @@ def test_oracle_factorization_golden(path, oracle_threads):
     assert got == _phase_tuples(d["phases"])
     assert rel_err(bf.apply(d["probe_x"]), d["apply_n"]) < APPLY_TOL
     assert rel_err(bf.apply_adjoint(d["probe_y"]), d["apply_h"]) < APPLY_TOL
+    est = O.estimate_error(op, bf, 16, 3)
+    assert abs(est - float(d["estimate_error"])) <= 1e-5 * float(d["estimate_error"]) + 1e-14
 
 
 # --------------------------------------------------------------------- GPU --
@@ -118,6 +134,14 @@ def test_gpu_rng_golden(B):
         assert np.max(np.abs(B.gaussian_matrix(rows, cols, seed) - gz)) <= 4e-15 * max(1.0, np.abs(gz).max())
         assert np.max(np.abs(B.gaussian_matrix(rows, cols, seed, scalar=B.REAL64) - gd)) <= 4e-15 * max(
             1.0, np.abs(gd).max())
+
+
+@pytest.mark.gpu
+def test_gpu_probe_seed_kats(B):
+    for words, seed, first in _probe_kats():
+        assert B.seed_mix(*words) == seed
+        g = B.gaussian_matrix(64, 1, seed)[:, 0]
+        assert np.max(np.abs(g - first)) <= 4e-15 * max(1.0, np.abs(first).max())
 
 
 @pytest.mark.gpu
@@ -166,3 +190,5 @@ def test_gpu_factorization_golden(B, path):
     assert got == _phase_tuples(d["phases"])
     assert rel_err(bf.apply(d["probe_x"]), d["apply_n"]) < APPLY_TOL
     assert rel_err(bf.apply_adjoint(d["probe_y"]), d["apply_h"]) < APPLY_TOL
+    est = B.estimate_error(op, bf, 16, 3)
+    assert abs(est - float(d["estimate_error"])) <= 1e-5 * float(d["estimate_error"]) + 1e-14
