@@ -197,6 +197,16 @@ BFLY_API void bfly_factorizer_destroy(bfly_factorizer* f);
 /* estimate_error (reconstruct.hpp:423-434) */
 BFLY_API int bfly_estimate_error(bfly_op* op, bfly_bf* bf, int64_t k, uint64_t seed, double* err);
 
+/* Level-wise residual sums of bf against a dense copy of op (desk scale: the
+ * operator is densified on the GPU), reconstruct.hpp:443-503 u_side_residual /
+ * v_side_residual / center_residual:
+ *   u_res[L - l]  for l = L .. l_m   sum_b ||K_b - U U^H K_b||_F^2
+ *   v_res[l]      for l = 0 .. l_m   sum_b ||K_b - K_b V V^H||_F^2
+ *   *center                          sum_b ||K_b - U (U^H K_b V) V^H||_F^2
+ *   *knorm2                          ||K||_F^2
+ * (the error-bound check of Theorems 5.1-5.3, tools/bfly_cli.cpp:208-235) */
+BFLY_API int bfly_residuals(bfly_op* op, bfly_bf* bf, double* u_res, double* v_res, double* center, double* knorm2);
+
 /* ---------------------------------------------------------------- butterfly */
 /* HybridButterfly::apply / apply_transpose / apply_adjoint (butterfly.hpp:71-193) */
 BFLY_API int bfly_apply(bfly_bf* bf, int trans, const void* x, int64_t ldx, void* y, int64_t ldy, int64_t k,

@@ -292,6 +292,19 @@ int64_t ref_serialize(const ref_bf* b, uint8_t* buf) {
 
 void ref_bf_free(ref_bf* b) { delete b; }
 
+// u_side_residual / v_side_residual / center_residual (reconstruct.hpp:443-503)
+// against densify(op) (operators.hpp), as run_verify does (bfly_cli.cpp:208-235)
+int ref_residuals(ref_op* h, const ref_bf* b, double* u, double* v, double* center, double* knorm2) {
+  return guard([&] {
+    Matrix<cplx> dense = densify(*h->op);
+    *knorm2 = dense.squaredNorm();
+    const int L = b->bf.levels, lm = b->bf.center;
+    for (int l = L; l >= lm; --l) u[L - l] = u_side_residual(dense, b->bf, l);
+    for (int l = 0; l <= lm; ++l) v[l] = v_side_residual(dense, b->bf, l);
+    *center = center_residual(dense, b->bf);
+  });
+}
+
 // ---- primitives for the golden vectors (tests/golden/make_golden.py)
 // seed_mix(seed, words...) core.hpp:78-88 (up to 4 words)
 uint64_t ref_seed_mix(uint64_t seed, int nw, const uint64_t* w) {

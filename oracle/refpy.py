@@ -40,6 +40,7 @@ def lib():
             "ref_seed_mix": (u64, [u64, i32, p]),
             "ref_gaussian": (i32, [i32, i64, i64, u64, p]),
             "ref_cpqr": (i64, [i64, i64, p, dbl, p]),
+            "ref_residuals": (i32, [p, p, p, p, p, p]),
         }
         for k, (r, a) in sig.items():
             f = getattr(L, k)
@@ -125,6 +126,14 @@ class RefButterfly:
     def estimate_error(self, k=16, seed=0):
         """estimate_error(op, bf, k, seed) of the reference (reconstruct.hpp:423-434)."""
         return float(lib().ref_estimate_error(self.op.h, self.h, k, seed))
+
+    def residuals(self, levels, center):
+        """(u[l=L..lm], v[l=0..lm], center, ||K||^2) of the reference."""
+        u = np.zeros(levels - center + 1)
+        v = np.zeros(center + 1)
+        cen, kn = C.c_double(), C.c_double()
+        _check(lib().ref_residuals(self.op.h, self.h, _vp(u), _vp(v), C.byref(cen), C.byref(kn)))
+        return u, v, cen.value, kn.value
 
     def serialize(self):
         n = lib().ref_serialize(self.h, None)

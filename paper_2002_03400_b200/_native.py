@@ -127,6 +127,7 @@ def lib():
         "bfly_factorizer_take": (i32, [p, pp, C.POINTER(Log)]),
         "bfly_factorizer_destroy": (None, [p]),
         "bfly_estimate_error": (i32, [p, p, i64, u64, C.POINTER(C.c_double)]),
+        "bfly_residuals": (i32, [p, p, p, p, C.POINTER(C.c_double), C.POINTER(C.c_double)]),
         "bfly_apply": (i32, [p, i32, p, i64, p, i64, i64, i32]),
         "bfly_bf_info": (i32, [p, C.POINTER(C.c_int), C.POINTER(C.c_int), C.POINTER(C.c_int64),
                                C.POINTER(C.c_int64), C.POINTER(C.c_int64), C.POINTER(C.c_int64),

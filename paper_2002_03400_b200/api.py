@@ -607,6 +607,18 @@ def estimate_error(op: BlackBoxOperator, bf: HybridButterfly, k: int = 16, seed:
     return e.value
 
 
+def residuals(op: BlackBoxOperator, bf: HybridButterfly) -> dict:
+    """Level-wise residual sums against a dense copy of ``op`` (desk scale),
+    reconstruct.hpp:443-503: ``u`` (l = L..l_m, u_side_residual), ``v``
+    (l = 0..l_m, v_side_residual), ``center`` (center_residual) and
+    ``knorm2`` = ||K||_F^2.  The operator is densified on the GPU."""
+    u = np.zeros(bf.levels - bf.center + 1)
+    v = np.zeros(bf.center + 1)
+    cen, kn = C.c_double(), C.c_double()
+    check(lib().bfly_residuals(op.h, bf.h, _vp(u), _vp(v), C.byref(cen), C.byref(kn)))
+    return {"u": u, "v": v, "center": cen.value, "knorm2": kn.value}
+
+
 def synth_butterfly(levels: int, rank: int, seed: int, leaf: int = 8, scalar=COMPLEX128, perturb: float = 0.0,
                     ctx=None) -> HybridButterfly:
     """synth_butterfly (operators.hpp:131-178), generalised to leaf b."""
@@ -649,7 +661,7 @@ def pinv_solve(m, tol: float = 1e-12, ctx=None):
 
 
 __all__ = [
-    "BflyError", "PreconditionError", "DimensionError", "SequencingError", "FormatError", "ConditioningError",
+    "residuals", "BflyError", "PreconditionError", "DimensionError", "SequencingError", "FormatError", "ConditioningError",
     "CudaError", "NcclError", "Context", "PartitionTree", "BlackBoxOperator", "apply_adjoint", "NufftOperator",
     "HelmholtzPlatesOperator", "HelmholtzCircleOperator", "CompositionOperator", "DenseOperator",
     "ButterflyOperator", "CallbackOperator", "KernelOperator", "ReconstructionConfig", "PhaseStat",

@@ -4,6 +4,7 @@ Mirrors the reference CLI (tools/bfly_cli.cpp) for the subcommands on the
 hot path:
 
   python -m paper_2002_03400_b200.cli [common options] factorize --config cfg.json
+  python -m paper_2002_03400_b200.cli [common options] verify --config cfg.json [--check-eps e]
   python -m paper_2002_03400_b200.cli [common options] synth --levels L --rank r
 
 Common options are the reference's (bfly_cli.cpp:345-354): --out, --csv,
@@ -110,6 +111,43 @@ def cmd_factorize(opts) -> int:
     return 0
 
 
+def cmd_verify(opts) -> int:
+    """run_verify (bfly_cli.cpp:203-235): factorize, then check the level-wise
+    error bounds of Theorems 5.1-5.3 against a dense copy of the operator:
+    column-basis sum at row level l <= (L - l + 1) e^2 ||K||^2 (l = L..l_m),
+    row-basis sum <= (l + 1) e^2 ||K||^2 (l = 0..l_m), combined at l_m <=
+    (L + 2) e^2 ||K||^2, e = --check-eps (default --eps).  Exit 0 iff all pass."""
+    if not opts.config:
+        raise api.PreconditionError("verify: --config is required")
+    with open(opts.config) as f:
+        cfg = json.load(f)
+    kind, op, rt, ct, levels, _ = build_operator(cfg, opts)
+    if op.rows * op.cols > opts.dense_cap * opts.dense_cap:
+        raise api.PreconditionError("verify: operator exceeds the dense extraction cap")
+    rc = api.ReconstructionConfig(tolerance=opts.eps, rank_guess=opts.r0, oversampling=opts.oversample,
+                                  levels=levels, seed=opts.seed)
+    bf, log = api.factorize(op, rt, ct, rc)
+    res = api.residuals(op, bf)
+    check_eps = opts.check_eps if opts.check_eps > 0 else opts.eps
+    e2, kf2 = check_eps * check_eps, res["knorm2"]
+    L, lm = bf.levels, bf.center
+    ok = True
+
+    def report(name, level, residual, bound):
+        nonlocal ok
+        passed = residual <= bound
+        ok = ok and passed
+        print(f"{name} level {level}: residual {residual:g} bound {bound:g}{'  pass' if passed else '  FAIL'}")
+
+    for i, l in enumerate(range(L, lm - 1, -1)):
+        report("column-basis bound", l, res["u"][i], (L - l + 1) * e2 * kf2)
+    for l in range(0, lm + 1):
+        report("row-basis bound", l, res["v"][l], (l + 1) * e2 * kf2)
+    report("combined bound", lm, res["center"], (L + 2) * e2 * kf2)
+    print(f"relative apply error: {api.estimate_error(op, bf, 16, opts.seed):g}")
+    return 0 if ok else 1
+
+
 def cmd_synth(opts) -> int:
     """bfly_cli.cpp:150-170: a ground-truth synthetic butterfly + manifest."""
     bf = api.synth_butterfly(opts.levels, opts.rank, opts.seed, scalar=api.REAL64)
@@ -136,9 +174,14 @@ def parser() -> argparse.ArgumentParser:
     ap.add_argument("--L", type=int, default=-1, help="tree depth override")
     ap.add_argument("--r0", type=int, default=4, help="initial rank guess")
     ap.add_argument("--oversample", type=int, default=2, help="oversampling columns")
+    ap.add_argument("--dense-cap", dest="dense_cap", type=int, default=4096, help="dense-oracle size cap")
     sub = ap.add_subparsers(dest="cmd", required=True)
     f = sub.add_parser("factorize", help="reconstruct a butterfly from black-box products")
     f.add_argument("--config", dest="config_sub", default="")
+    v = sub.add_parser("verify", help="check the level-wise error bounds densely")
+    v.add_argument("--config", dest="config_sub", default="")
+    v.add_argument("--check-eps", dest="check_eps", type=float, default=-1.0,
+                   help="bound-evaluation tolerance (default: --eps)")
     s = sub.add_parser("synth", help="generate a ground-truth butterfly")
     s.add_argument("--levels", type=int, default=4)
     s.add_argument("--rank", type=int, default=4)
@@ -152,6 +195,8 @@ def main(argv=None) -> int:
     try:
         if opts.cmd == "factorize":
             return cmd_factorize(opts)
+        if opts.cmd == "verify":
+            return cmd_verify(opts)
         return cmd_synth(opts)
     except api.BflyError as e:  # the reference prints the error and exits non-zero
         print(f"error: {e}", file=sys.stderr)

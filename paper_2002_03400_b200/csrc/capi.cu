@@ -8,6 +8,7 @@
 #include "butterfly.h"
 #include "comm.h"
 #include "factorizer.h"
+#include "verify.h"
 #include "operators.h"
 
 using namespace bfly;
@@ -581,6 +582,18 @@ int bfly_estimate_error(bfly_op* op, bfly_bf* bf, int64_t k, uint64_t seed, doub
     if (op->scalar != bf->scalar) fail(PRECONDITION, "estimate_error: scalar types differ");
     if (op->z) *err = estimate_error_t<double>(C_(op->ctx), op->z.get(), bf->z.get(), k, seed);
     else *err = estimate_error_t<float>(C_(op->ctx), op->c.get(), bf->c.get(), k, seed);
+  });
+}
+
+int bfly_residuals(bfly_op* op, bfly_bf* bf, double* u_res, double* v_res, double* center, double* knorm2) {
+  return guard(C_(op->ctx), [&] {
+    if (op->scalar != bf->scalar) fail(PRECONDITION, "residuals: scalar types differ");
+    Residuals r = op->z ? compute_residuals<double>(C_(op->ctx), op->z.get(), *bf->z)
+                        : compute_residuals<float>(C_(op->ctx), op->c.get(), *bf->c);
+    for (size_t i = 0; i < r.u.size(); ++i) u_res[i] = r.u[i];
+    for (size_t i = 0; i < r.v.size(); ++i) v_res[i] = r.v[i];
+    *center = r.center;
+    *knorm2 = r.knorm2;
   });
 }
 

@@ -20,7 +20,8 @@ Files
   cfg_*.npz    factorize (reconstruct.hpp:412-419) on small BASELINE configs and
                the reference's synthetic butterfly: rank profile of every
                block, per-phase bookkeeping, butterfly apply / adjoint apply
-               outputs on reference-generated probes, estimate_error
+               outputs on reference-generated probes, estimate_error, and the level-wise
+               residual sums of the error-bound check (reconstruct.hpp:443-503)
 """
 import os
 import sys
@@ -152,6 +153,8 @@ def save_factorization(name, inp, op, bf, L, seed):
     d.update(seed=seed, rank_profile=bf.rank_profile(L), phases=np.array(phases, np.int64),
              probe_x=x, probe_y=y, apply_n=bf.apply(np.asfortranarray(x), 0),
              apply_h=bf.apply(np.asfortranarray(y), 2), estimate_error=bf.estimate_error(16, 3))
+    u, v, cen, kn = bf.residuals(L, L // 2)
+    d.update(res_u=u, res_v=v, res_center=cen, res_knorm2=kn)
     np.savez_compressed(os.path.join(HERE, f"{name}.npz"), **d)
     print(name, "ranks", int(d["rank_profile"].max()), "phases", len(phases))
 

@@ -72,3 +72,21 @@ def test_cli_synth_container_is_the_references_generator(tmp_path):
     assert np.abs(got.to_dense() - ref.to_dense()).max() <= 1e-13 * np.abs(ref.to_dense()).max()
     m = json.load(open(tmp_path / "manifest.json"))
     assert (m["n"], m["levels"], m["rank"], m["seed"], m["scalar"]) == (128, 4, 3, 7, "real64")
+
+
+@pytest.mark.gpu
+def test_cli_verify_passes_the_theorem_bounds(tmp_path, capsys):
+    from paper_2002_03400_b200 import cli
+
+    cfgp = tmp_path / "cfg.json"
+    cfgp.write_text(json.dumps({"operator": "nufft1d", "n": 1024}))
+    rc = cli.main(["--eps", "1e-6", "--r0", "16", "verify", "--config", str(cfgp)])
+    out = capsys.readouterr().out
+    assert rc == 0, out
+    lines = out.splitlines()
+    L, lm = 5, 2
+    assert sum(l.startswith("column-basis bound") for l in lines) == L - lm + 1
+    assert sum(l.startswith("row-basis bound") for l in lines) == lm + 1
+    assert any(l.startswith("combined bound") for l in lines) and "FAIL" not in out
+    assert lines[-1].startswith("relative apply error:")
+

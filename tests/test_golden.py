@@ -192,3 +192,25 @@ def test_gpu_factorization_golden(B, path):
     assert rel_err(bf.apply_adjoint(d["probe_y"]), d["apply_h"]) < APPLY_TOL
     est = B.estimate_error(op, bf, 16, 3)
     assert abs(est - float(d["estimate_error"])) <= 1e-5 * float(d["estimate_error"]) + 1e-14
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("path", CFG_FILES, ids=[os.path.basename(p)[:-4] for p in CFG_FILES])
+def test_gpu_residual_sums_match_reference(B, path):
+    """Level-wise residual sums of the error-bound check (reconstruct.hpp:
+    443-503), computed on the GPU against its own dense copy of the operator,
+    equal the reference's on its factorization of the same problem (identical
+    ranks; the residuals are truncation-dominated, round-off far below)."""
+    d = np.load(path)
+    op, rt, ct = _gpu_problem(B, d)
+    rc = B.ReconstructionConfig(tolerance=float(d["tol"]), rank_guess=int(d["r0"]), levels=int(d["L"]),
+                                seed=int(d["seed"]))
+    bf, _ = B.factorize(op, rt, ct, rc)
+    r = B.residuals(op, bf)
+    kn = float(d["res_knorm2"])
+    assert abs(r["knorm2"] - kn) <= 1e-12 * kn
+    floor = 1e-20 * kn  # exact recoveries: residuals at round-off
+    np.testing.assert_allclose(r["u"], d["res_u"], rtol=1e-3, atol=floor)
+    np.testing.assert_allclose(r["v"], d["res_v"], rtol=1e-3, atol=floor)
+    assert abs(r["center"] - float(d["res_center"])) <= 1e-3 * float(d["res_center"]) + floor
+
