@@ -133,14 +133,21 @@ void Ctx::reserve_pool(size_t bytes) {
   }
 }
 
-// after a factorization: remember its peak pool use for the next one
+// start of a factorization: its working set is measured from here
+void Ctx::mark_pool_start() {
+  uint64_t used = 0, zero = 0;
+  cudaMemPoolGetAttribute(pool, cudaMemPoolAttrUsedMemCurrent, &used);
+  pool_used_start = (size_t)used;
+  cudaMemPoolSetAttribute(pool, cudaMemPoolAttrUsedMemHigh, &zero);
+}
+
+// after a factorization: remember its working set (peak minus what was
+// already in use -- earlier results the caller keeps are not part of it)
 void Ctx::note_pool_peak() {
   uint64_t high = 0;
   if (cudaMemPoolGetAttribute(pool, cudaMemPoolAttrUsedMemHigh, &high) != cudaSuccess) return;
-  // grow the hint only when the peak really exceeds the reservation
-  if ((size_t)high > pool_reserved) pool_hint = std::max<size_t>(pool_hint, (size_t)(high + high / 16));
-  uint64_t zero = 0;
-  cudaMemPoolSetAttribute(pool, cudaMemPoolAttrUsedMemHigh, &zero);
+  const size_t ws = (size_t)high > pool_used_start ? (size_t)high - pool_used_start : 0;
+  pool_hint = std::max<size_t>(pool_hint, ws + ws / 16);
 }
 
 }  // namespace bfly

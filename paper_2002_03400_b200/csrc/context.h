@@ -59,8 +59,9 @@ struct Ctx {
   bool take_oz_overflow();  // all ranks agree; resets the flag
   // pool sizing: a factorization reserves one contiguous chunk sized to the
   // previous one's peak (see reserve_pool)
-  size_t pool_reserved = 0, pool_hint = 0;
+  size_t pool_reserved = 0, pool_hint = 0, pool_used_start = 0;
   void reserve_pool(size_t bytes);
+  void mark_pool_start();
   void note_pool_peak();
 };
 
