@@ -528,153 +528,178 @@ GemmEnt ent(int64_t a0, int64_t a1, int64_t b0, int64_t b1, int64_t c, int mrows
   e.ncols = 0; e.mrows = mrows; e.krows = krows; e.pad_ = 0;
   return e;
 }
+// the used prefix (ld x cols) of every block of a factor level
+template <typename R>
+L2Prefetch l2pf(const Level<R>& lv, int cols) {
+  L2Prefetch p;
+  p.base = lv.data.p;
+  p.stride = lv.stride() * (int64_t)sizeof(cx<R>);
+  p.len = std::min<int64_t>(lv.stride(), lv.ld * (int64_t)std::max(cols, 1)) * (int64_t)sizeof(cx<R>);
+  return p;
+}
 }  // namespace
 
+// Stage plans (butterfly.hpp:71-193): K x = U_L R_{L-1} .. R_lm B W_lm .. W_1 V_0^H x.
+// Entry e of a stage computes C[c_e] = sum_s op(A[a_s]) B[b_s]; pad_ carries
+// the stage index (BFLY_STAGE_TRACE instrumentation only).
 template <typename R>
-void DevButterfly<R>::apply_n(const cx<R>* xt, int64_t ldx, cx<R>* yt, int64_t ldy, int64_t k, cx<R>* buf0,
-                               cx<R>* buf1) {
-  Ctx* c = ctx;
+void DevButterfly<R>::build_plan_n() {
+  Plan& pl = plan_n_;
+  pl = Plan();
   const int64_t NB = nb();
   const int BIG = 1 << 30;
-  if (!have_n_) {
-    plan_n_ = Plan();
-    std::vector<GemmEnt> e;
+  auto add = [&](int op, int M, int K, int S, const Level<R>& lv, int64_t ld_out, int pfcols) -> StageDesc& {
+    pl.st.emplace_back();
+    StageDesc& d = pl.st.back();
+    d.op = op; d.M = M; d.K = K; d.S = S; d.A = lv.data.p; d.lda = lv.ld; d.ld_out = ld_out;
+    d.pf = l2pf(lv, pfcols);
+    return d;
+  };
+  {
+    StageDesc& d = add(OP_H, PV(0), (int)vleaf.ld, 1, vleaf, NB * PV(0), PV(0));
     for (int64_t nu = 0; nu < NB; ++nu)
-      e.push_back(ent(nu * vleaf.stride(), 0, ct.begin(L, nu), 0, nu * PV(0), BIG, (int)ct.size(L, nu)));
-    plan_n_.stages.push_back(to_device(c, e));
-    for (int l = 1; l <= lm; ++l) {
-      e.clear();
-      const Level<R>& wl = w[l - 1];
-      for (int64_t tau = 0; tau < (int64_t(1) << l); ++tau)
-        for (int64_t nu = 0; nu < (int64_t(1) << (L - l)); ++nu) {
-          int64_t i = bidx(L, l, tau, nu);
-          e.push_back(ent(i * wl.stride(), 0, bidx(L, l - 1, tau / 2, 2 * nu) * PV(l - 1), 0, i * PV(l), BIG, BIG));
-        }
-      plan_n_.stages.push_back(to_device(c, e));
-    }
-    e.clear();
-    for (int64_t i = 0; i < NB; ++i) e.push_back(ent(i * b.stride(), 0, i * PV(lm), 0, i * PU(lm), BIG, BIG));
-    plan_n_.stages.push_back(to_device(c, e));
-    for (int l = lm; l < L; ++l) {
-      e.clear();
-      const Level<R>& rl = r[l - lm];
-      for (int64_t tp = 0; tp < (int64_t(1) << (l + 1)); ++tp)
-        for (int64_t np = 0; np < (int64_t(1) << (L - l - 1)); ++np) {
-          int64_t tau = tp >> 1, h = tp & 1;
-          int64_t i0 = bidx(L, l, tau, 2 * np), i1 = bidx(L, l, tau, 2 * np + 1);
-          e.push_back(ent(i0 * rl.stride() + h * rl.gap, i1 * rl.stride() + h * rl.gap, i0 * PU(l), i1 * PU(l),
-                          bidx(L, l + 1, tp, np) * PU(l + 1), BIG, BIG));
-        }
-      plan_n_.stages.push_back(to_device(c, e));
-    }
-    e.clear();
-    for (int64_t tau = 0; tau < NB; ++tau)
-      e.push_back(ent(tau * uleaf.stride(), 0, tau * PU(L), 0, rt.begin(L, tau), (int)rt.size(L, tau), BIG));
-    plan_n_.stages.push_back(to_device(c, e));
-    have_n_ = true;
+      d.h.push_back(ent(nu * vleaf.stride(), 0, ct.begin(L, nu), 0, nu * PV(0), BIG, (int)ct.size(L, nu)));
   }
+  for (int l = 1; l <= lm; ++l) {
+    const Level<R>& wl = w[l - 1];
+    StageDesc& d = add(OP_H, PV(l), 2 * PV(l - 1), 1, wl, NB * PV(l), PV(l));
+    for (int64_t tau = 0; tau < (int64_t(1) << l); ++tau)
+      for (int64_t nu = 0; nu < (int64_t(1) << (L - l)); ++nu) {
+        int64_t i = bidx(L, l, tau, nu);
+        d.h.push_back(ent(i * wl.stride(), 0, bidx(L, l - 1, tau / 2, 2 * nu) * PV(l - 1), 0, i * PV(l), BIG, BIG));
+      }
+  }
+  {
+    StageDesc& d = add(OP_N, PU(lm), PV(lm), 1, b, NB * PU(lm), PV(lm));
+    for (int64_t i = 0; i < NB; ++i) d.h.push_back(ent(i * b.stride(), 0, i * PV(lm), 0, i * PU(lm), BIG, BIG));
+  }
+  for (int l = lm; l < L; ++l) {
+    const Level<R>& rl = r[l - lm];
+    StageDesc& d = add(OP_N, PU(l + 1), PU(l), 2, rl, NB * PU(l + 1), PU(l));
+    for (int64_t tp = 0; tp < (int64_t(1) << (l + 1)); ++tp)
+      for (int64_t np = 0; np < (int64_t(1) << (L - l - 1)); ++np) {
+        int64_t tau = tp >> 1, h = tp & 1;
+        int64_t i0 = bidx(L, l, tau, 2 * np), i1 = bidx(L, l, tau, 2 * np + 1);
+        d.h.push_back(ent(i0 * rl.stride() + h * rl.gap, i1 * rl.stride() + h * rl.gap, i0 * PU(l), i1 * PU(l),
+                          bidx(L, l + 1, tp, np) * PU(l + 1), BIG, BIG));
+      }
+  }
+  {
+    StageDesc& d = add(OP_N, (int)uleaf.ld, PU(L), 1, uleaf, 0, PU(L));
+    for (int64_t tau = 0; tau < NB; ++tau)
+      d.h.push_back(ent(tau * uleaf.stride(), 0, tau * PU(L), 0, rt.begin(L, tau), (int)rt.size(L, tau), BIG));
+  }
+  upload_plan(pl);
+}
+
+template <typename R>
+void DevButterfly<R>::build_plan_h() {
+  Plan& pl = plan_h_;
+  pl = Plan();
+  const int64_t NB = nb();
+  const int BIG = 1 << 30;
+  auto add = [&](int op, int M, int K, int S, const Level<R>& lv, int64_t ld_out, int pfcols) -> StageDesc& {
+    pl.st.emplace_back();
+    StageDesc& d = pl.st.back();
+    d.op = op; d.M = M; d.K = K; d.S = S; d.A = lv.data.p; d.lda = lv.ld; d.ld_out = ld_out;
+    d.pf = l2pf(lv, pfcols);
+    return d;
+  };
+  {
+    StageDesc& d = add(OP_H, PU(L), (int)uleaf.ld, 1, uleaf, NB * PU(L), PU(L));
+    for (int64_t tau = 0; tau < NB; ++tau)
+      d.h.push_back(ent(tau * uleaf.stride(), 0, rt.begin(L, tau), 0, tau * PU(L), BIG, (int)rt.size(L, tau)));
+  }
+  for (int l = L - 1; l >= lm; --l) {
+    const Level<R>& rl = r[l - lm];
+    StageDesc& d = add(OP_H, PU(l), PU(l + 1), 2, rl, NB * PU(l), PU(l));
+    for (int64_t tau = 0; tau < (int64_t(1) << l); ++tau)
+      for (int64_t nu = 0; nu < (int64_t(1) << (L - l)); ++nu) {
+        int64_t i = bidx(L, l, tau, nu);
+        d.h.push_back(ent(i * rl.stride(), i * rl.stride() + rl.gap, bidx(L, l + 1, 2 * tau, nu / 2) * PU(l + 1),
+                          bidx(L, l + 1, 2 * tau + 1, nu / 2) * PU(l + 1), i * PU(l), BIG, BIG));
+      }
+  }
+  {
+    StageDesc& d = add(OP_H, PV(lm), PU(lm), 1, b, NB * PV(lm), PV(lm));
+    for (int64_t i = 0; i < NB; ++i) d.h.push_back(ent(i * b.stride(), 0, i * PU(lm), 0, i * PV(lm), BIG, BIG));
+  }
+  for (int l = lm; l >= 1; --l) {
+    const Level<R>& wl = w[l - 1];
+    StageDesc& d = add(OP_N, PV(l - 1), PV(l), 2, wl, NB * PV(l - 1), PV(l));
+    for (int64_t tp = 0; tp < (int64_t(1) << (l - 1)); ++tp)
+      for (int64_t npp = 0; npp < (int64_t(1) << (L - l + 1)); ++npp) {
+        int64_t nu = npp >> 1, h = npp & 1;
+        int64_t i0 = bidx(L, l, 2 * tp, nu), i1 = bidx(L, l, 2 * tp + 1, nu);
+        d.h.push_back(ent(i0 * wl.stride() + h * wl.gap, i1 * wl.stride() + h * wl.gap, i0 * PV(l), i1 * PV(l),
+                          bidx(L, l - 1, tp, npp) * PV(l - 1), BIG, BIG));
+      }
+  }
+  {
+    StageDesc& d = add(OP_N, (int)vleaf.ld, PV(0), 1, vleaf, 0, PV(0));
+    for (int64_t nu = 0; nu < NB; ++nu)
+      d.h.push_back(ent(nu * vleaf.stride(), 0, nu * PV(0), 0, ct.begin(L, nu), (int)ct.size(L, nu), BIG));
+  }
+  upload_plan(pl);
+}
+
+template <typename R>
+void DevButterfly<R>::upload_plan(Plan& pl) {
+  for (size_t i = 0; i < pl.st.size(); ++i) {
+    for (auto& e : pl.st[i].h) e.pad_ = (int32_t)i;
+    pl.st[i].d = to_device(ctx, pl.st[i].h);
+  }
+}
+
+// One launch per stage, ping-ponging the coefficient vector between buf0 and
+// buf1; every stage is a programmatic dependent launch that prefetches the
+// next stage's factor level into L2 (see bgemm_stage_kernel).
+template <typename R>
+void DevButterfly<R>::run_plan(Plan& pl, const cx<R>* x, int64_t ldx, cx<R>* y, int64_t ldy, int64_t k,
+                               cx<R>* buf0, cx<R>* buf1) {
+  Ctx* c = ctx;
+  const int64_t NB = nb();
   DBuf<cx<R>> b0, b1;
   if (!buf0) {
     b0.reset(c, (size_t)(NB * max_p() * k));
     b1.reset(c, (size_t)(NB * max_p() * k));
+    buf0 = b0.p;
+    buf1 = b1.p;
   }
-  cx<R>* cur = buf0 ? buf0 : b0.p;
-  cx<R>* nxt = buf1 ? buf1 : b1.p;
-  int st = 0;
-  const int kk = (int)k;
-  launch_bgemm<R>(c, OP_H, PV(0), (int)vleaf.ld, 1, vleaf.data.p, vleaf.ld, xt, ldx, cur, NB * PV(0),
-                  plan_n_.stages[st++].p, (int)NB, kk, false, kk, true);
-  for (int l = 1; l <= lm; ++l) {
-    const Level<R>& wl = w[l - 1];
-    launch_bgemm<R>(c, OP_H, PV(l), 2 * PV(l - 1), 1, wl.data.p, wl.ld, cur, NB * PV(l - 1), nxt, NB * PV(l),
-                    plan_n_.stages[st++].p, (int)NB, kk, false, kk, true);
-    std::swap(cur, nxt);
+  cx<R>* bufs[2] = {buf0, buf1};
+  const int n = (int)pl.st.size();
+  const cx<R>* in = x;
+  int64_t ldin = ldx;
+  for (int i = 0; i < n; ++i) {
+    const StageDesc& d = pl.st[i];
+    const bool final = i == n - 1;
+    cx<R>* out = final ? y : bufs[i % 2];
+    const int64_t ldout = final ? ldy : d.ld_out;
+    launch_bgemm<R>(c, d.op, d.M, d.K, d.S, d.A, d.lda, in, ldin, out, ldout, d.d.p, (int)d.h.size(), (int)k, false,
+                    (int)k, true, final ? L2Prefetch() : pl.st[i + 1].pf);
+    in = out;
+    ldin = ldout;
   }
-  launch_bgemm<R>(c, OP_N, PU(lm), PV(lm), 1, b.data.p, b.ld, cur, NB * PV(lm), nxt, NB * PU(lm),
-                  plan_n_.stages[st++].p, (int)NB, kk, false, kk, true);
-  std::swap(cur, nxt);
-  for (int l = lm; l < L; ++l) {
-    const Level<R>& rl = r[l - lm];
-    launch_bgemm<R>(c, OP_N, PU(l + 1), PU(l), 2, rl.data.p, rl.ld, cur, NB * PU(l), nxt, NB * PU(l + 1),
-                    plan_n_.stages[st++].p, (int)NB, kk, false, kk, true);
-    std::swap(cur, nxt);
+}
+
+template <typename R>
+void DevButterfly<R>::apply_n(const cx<R>* xt, int64_t ldx, cx<R>* yt, int64_t ldy, int64_t k, cx<R>* buf0,
+                               cx<R>* buf1) {
+  if (!have_n_) {
+    build_plan_n();
+    have_n_ = true;
   }
-  launch_bgemm<R>(c, OP_N, (int)uleaf.ld, PU(L), 1, uleaf.data.p, uleaf.ld, cur, NB * PU(L), yt, ldy,
-                  plan_n_.stages[st++].p, (int)NB, kk, false, kk, true);
+  run_plan(plan_n_, xt, ldx, yt, ldy, k, buf0, buf1);
 }
 
 template <typename R>
 void DevButterfly<R>::apply_h(const cx<R>* yt, int64_t ldy, cx<R>* xt, int64_t ldx, int64_t k, cx<R>* buf0,
                                cx<R>* buf1) {
-  Ctx* c = ctx;
-  const int64_t NB = nb();
-  const int BIG = 1 << 30;
   if (!have_h_) {
-    plan_h_ = Plan();
-    std::vector<GemmEnt> e;
-    for (int64_t tau = 0; tau < NB; ++tau)
-      e.push_back(ent(tau * uleaf.stride(), 0, rt.begin(L, tau), 0, tau * PU(L), BIG, (int)rt.size(L, tau)));
-    plan_h_.stages.push_back(to_device(c, e));
-    for (int l = L - 1; l >= lm; --l) {
-      e.clear();
-      const Level<R>& rl = r[l - lm];
-      for (int64_t tau = 0; tau < (int64_t(1) << l); ++tau)
-        for (int64_t nu = 0; nu < (int64_t(1) << (L - l)); ++nu) {
-          int64_t i = bidx(L, l, tau, nu);
-          e.push_back(ent(i * rl.stride(), i * rl.stride() + rl.gap, bidx(L, l + 1, 2 * tau, nu / 2) * PU(l + 1),
-                          bidx(L, l + 1, 2 * tau + 1, nu / 2) * PU(l + 1), i * PU(l), BIG, BIG));
-        }
-      plan_h_.stages.push_back(to_device(c, e));
-    }
-    e.clear();
-    for (int64_t i = 0; i < NB; ++i) e.push_back(ent(i * b.stride(), 0, i * PU(lm), 0, i * PV(lm), BIG, BIG));
-    plan_h_.stages.push_back(to_device(c, e));
-    for (int l = lm; l >= 1; --l) {
-      e.clear();
-      const Level<R>& wl = w[l - 1];
-      for (int64_t tp = 0; tp < (int64_t(1) << (l - 1)); ++tp)
-        for (int64_t npp = 0; npp < (int64_t(1) << (L - l + 1)); ++npp) {
-          int64_t nu = npp >> 1, h = npp & 1;
-          int64_t i0 = bidx(L, l, 2 * tp, nu), i1 = bidx(L, l, 2 * tp + 1, nu);
-          e.push_back(ent(i0 * wl.stride() + h * wl.gap, i1 * wl.stride() + h * wl.gap, i0 * PV(l), i1 * PV(l),
-                          bidx(L, l - 1, tp, npp) * PV(l - 1), BIG, BIG));
-        }
-      plan_h_.stages.push_back(to_device(c, e));
-    }
-    e.clear();
-    for (int64_t nu = 0; nu < NB; ++nu)
-      e.push_back(ent(nu * vleaf.stride(), 0, nu * PV(0), 0, ct.begin(L, nu), (int)ct.size(L, nu), BIG));
-    plan_h_.stages.push_back(to_device(c, e));
+    build_plan_h();
     have_h_ = true;
   }
-  DBuf<cx<R>> b0, b1;
-  if (!buf0) {
-    b0.reset(c, (size_t)(NB * max_p() * k));
-    b1.reset(c, (size_t)(NB * max_p() * k));
-  }
-  cx<R>* cur = buf0 ? buf0 : b0.p;
-  cx<R>* nxt = buf1 ? buf1 : b1.p;
-  int st = 0;
-  const int kk = (int)k;
-  launch_bgemm<R>(c, OP_H, PU(L), (int)uleaf.ld, 1, uleaf.data.p, uleaf.ld, yt, ldy, cur, NB * PU(L),
-                  plan_h_.stages[st++].p, (int)NB, kk, false, kk, true);
-  for (int l = L - 1; l >= lm; --l) {
-    const Level<R>& rl = r[l - lm];
-    launch_bgemm<R>(c, OP_H, PU(l), PU(l + 1), 2, rl.data.p, rl.ld, cur, NB * PU(l + 1), nxt, NB * PU(l),
-                    plan_h_.stages[st++].p, (int)NB, kk, false, kk, true);
-    std::swap(cur, nxt);
-  }
-  launch_bgemm<R>(c, OP_H, PV(lm), PU(lm), 1, b.data.p, b.ld, cur, NB * PU(lm), nxt, NB * PV(lm),
-                  plan_h_.stages[st++].p, (int)NB, kk, false, kk, true);
-  std::swap(cur, nxt);
-  for (int l = lm; l >= 1; --l) {
-    const Level<R>& wl = w[l - 1];
-    launch_bgemm<R>(c, OP_N, PV(l - 1), PV(l), 2, wl.data.p, wl.ld, cur, NB * PV(l), nxt, NB * PV(l - 1),
-                    plan_h_.stages[st++].p, (int)NB, kk, false, kk, true);
-    std::swap(cur, nxt);
-  }
-  launch_bgemm<R>(c, OP_N, (int)vleaf.ld, PV(0), 1, vleaf.data.p, vleaf.ld, cur, NB * PV(0), xt, ldx,
-                  plan_h_.stages[st++].p, (int)NB, kk, false, kk, true);
+  run_plan(plan_h_, yt, ldy, xt, ldx, k, buf0, buf1);
 }
 
 // ------------------------------------------------------- host <-> device

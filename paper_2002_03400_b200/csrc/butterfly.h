@@ -119,12 +119,26 @@ struct DevButterfly {
   static std::unique_ptr<DevButterfly> from_host(Ctx* c, const HostButterfly& h);
 
  private:
+  // One stage of the apply chain: C_e = sum_s op(A_s) B_s over its entries.
+  struct StageDesc {
+    int op = 0, M = 0, K = 0, S = 1;
+    const cx<R>* A = nullptr;
+    int64_t lda = 0;
+    int64_t ld_out = 0;  // ld of its coefficient output (NB * M); 0 for the last stage
+    std::vector<GemmEnt> h;
+    DBuf<GemmEnt> d;
+    L2Prefetch pf;  // its factor level, prefetched into L2 by the kernel before it
+  };
   struct Plan {
-    std::vector<DBuf<GemmEnt>> stages;
-    std::vector<int> nent;
+    std::vector<StageDesc> st;
   };
   Plan plan_n_, plan_h_;
   bool have_n_ = false, have_h_ = false;
+  void build_plan_n();
+  void build_plan_h();
+  void upload_plan(Plan& plan);
+  void run_plan(Plan& plan, const cx<R>* x, int64_t ldx, cx<R>* y, int64_t ldy, int64_t k, cx<R>* buf0,
+                cx<R>* buf1);
   // buf0/buf1: level coefficient buffers (NB*maxP*k each); null -> allocate
   void apply_n(const cx<R>* xt, int64_t ldx, cx<R>* yt, int64_t ldy, int64_t k, cx<R>* buf0 = nullptr,
                cx<R>* buf1 = nullptr);

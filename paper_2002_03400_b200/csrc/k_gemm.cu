@@ -166,6 +166,220 @@ __global__ void __launch_bounds__(128) bgemm_small_kernel(const cx<R>* __restric
   }
 }
 
+// Butterfly apply stages (programmatic dependent launch chains, k <= 16).
+// WPE warps own one output block (a CTA holds up to 4 single-warp groups), so a k = 1
+// stage grid needs ~14 warps per SM and three to four consecutive stage grids
+// fit on the GPU at once.  Each grid triggers its dependents on entry; a
+// launched-but-waiting grid queues its factor blocks (never written by the
+// chain) as cp.async global->shared copies -- no register round trip, so a
+// warp has its whole share of the block in flight at once -- and only then
+// parks at griddepcontrol.wait.  The factor traffic of the next stages thus
+// streams from HBM while this stage computes; the per-stage critical path is
+// the previous stage's output (L2 resident) plus the small GEMV, which splits
+// K over Q lanes per output (shuffle reduction) when the block has few
+// outputs.  griddepcontrol.wait returns only once the prerequisite grid has
+// completed and flushed, which transitively orders every earlier stage.
+template <typename V>
+__device__ __forceinline__ void cp_async_elem(V* dst, const V* src) {
+  const uint32_t d = (uint32_t)__cvta_generic_to_shared(dst);
+  if constexpr (sizeof(V) == 16)
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(d), "l"(src) : "memory");
+  else
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(d), "l"(src) : "memory");
+}
+
+#ifdef BFLY_STAGE_TRACE
+// per stage: [0] first group start, [1] last group start, [2] first wait return,
+// [3] last wait return, [4] last group end (%globaltimer ns)
+__device__ unsigned long long g_stage_trace[64][10];
+__device__ __forceinline__ unsigned long long gtime() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+#define STAGE_TRACE(slot, v)                                                  \
+  do {                                                                          \
+    if (t == 0 && (ei & 31) == 0) {                                           \
+      const unsigned long long now = gtime();                                   \
+      if (v & 1) atomicMax(&g_stage_trace[slot][v >> 1], now);                  \
+      else atomicMin(&g_stage_trace[slot][v >> 1], now);                        \
+    }                                                                           \
+  } while (0)
+#else
+#define STAGE_TRACE(slot, v) \
+  do {                       \
+  } while (0)
+#endif
+
+__device__ __forceinline__ void st_mbar_wait(uint32_t bar, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred done;\n\t"
+      "WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.acquire.cta.shared::cta.b64 done, [%0], %1, %2;\n\t"
+      "@!done bra WAIT_%=;\n\t}\n" ::"r"(bar),
+      "r"(parity), "r"(1000000u)
+      : "memory");
+}
+
+// Shared-memory image of one output block: per s, op(A_s) in the stored
+// orientation -- OP_N: column kk of A_s (M entries) at kk*(M+1), lanes then
+// read consecutive rows; OP_T/OP_H: stored column m (K entries) at m*P with
+// an ODD pitch P (K+1 or K+2), so lanes reading one kk of different m hit
+// distinct 16-byte bank groups -- then the K x ncols input slices; an
+// mbarrier heads the group's region.
+__host__ __device__ __forceinline__ int stage_pitch(int op, int M, int K) {
+  return op == OP_N ? M + 1 : K + 1 + (K & 1);
+}
+__host__ __device__ __forceinline__ int64_t stage_group_elems(int op, int M, int K, int S, int ncols) {
+  return (int64_t)S * ((int64_t)(op == OP_N ? K : M) * stage_pitch(op, M, K) + (int64_t)K * ncols);
+}
+
+template <typename R, int OP, int S>
+__global__ void __launch_bounds__(256) bgemm_stage_kernel(const cx<R>* __restrict__ A, int64_t lda,
+                                                          const cx<R>* __restrict__ B, int64_t ldb,
+                                                          cx<R>* __restrict__ C, int64_t ldc, int M, int K,
+                                                          const GemmEnt* __restrict__ ents, int nent, int accumulate,
+                                                          int ncols, int wpe, L2Prefetch pf) {
+  using V = cx<R>;
+  constexpr bool kBulk = sizeof(V) == 16;  // TMA bulk copies need 16-byte granules
+  asm volatile("griddepcontrol.launch_dependents;");
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  const int gthreads = 32 * wpe;
+  const int grp = threadIdx.x / gthreads, t = threadIdx.x % gthreads;
+  const int64_t ei = (int64_t)blockIdx.x * (blockDim.x / gthreads) + grp;
+  if (ei >= nent) return;
+  const int64_t gbytes = 16 + stage_group_elems(OP, M, K, S, ncols) * (int64_t)sizeof(V);
+  unsigned char* gbase = smem_raw + grp * gbytes;
+  const uint32_t bar = (uint32_t)__cvta_generic_to_shared(gbase);
+  V* As = reinterpret_cast<V*>(gbase + 16);
+  const int cpitch = stage_pitch(OP, M, K);
+  const int64_t aelems = (int64_t)(OP == OP_N ? K : M) * cpitch;
+  V* Bs = As + S * aelems;  // [S][ncols][K]
+  const GemmEnt e = ents[ei];
+  const int Me = min(M, e.mrows), Ke = min(K, e.krows);
+  if (pf.base != nullptr && pf.len >= 16 && t == 0) {
+    const char* p = static_cast<const char*>(pf.base) + ei * pf.stride;
+    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p), "r"((uint32_t)(pf.len & ~int64_t(15)))
+                 : "memory");
+  }
+  const int slot = e.pad_ & 63;
+  STAGE_TRACE(slot, 0);
+  STAGE_TRACE(slot, 3);
+  // op(A_s) columns: OP_N copies the K stored columns (M entries each), the
+  // transposed ops the M stored columns (K entries each)
+  const int ncopy = OP == OP_N ? K : M, clen = OP == OP_N ? M : K;
+  if constexpr (kBulk) {
+    // the tensor-memory-access engine moves the factor block, so the load/
+    // store pipe stays free for the running stage's GEMV
+    if (t == 0) {
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(bar));
+      asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+      asm volatile("mbarrier.arrive.expect_tx.release.cta.shared::cta.b64 _, [%0], %1;" ::"r"(bar),
+                   "r"((uint32_t)(S * ncopy * clen * sizeof(V)))
+                   : "memory");
+    }
+    if (wpe == 1) __syncwarp();
+    else __syncthreads();
+    for (int c = t; c < S * ncopy; c += gthreads) {
+      const int s = c >= ncopy, j = c - s * ncopy;
+      const V* src = A + (s == 0 ? e.a0 : e.a1) + (int64_t)j * lda;
+      const uint32_t dst = (uint32_t)__cvta_generic_to_shared(As + s * aelems + (int64_t)j * cpitch);
+      asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                       dst),
+                   "l"(src), "r"((uint32_t)(clen * sizeof(V))), "r"(bar)
+                   : "memory");
+    }
+  } else {
+#pragma unroll
+    for (int s = 0; s < S; ++s) {
+      const V* Ab = A + (s == 0 ? e.a0 : e.a1);
+      V* as = As + s * aelems;
+      for (int idx = t; idx < ncopy * clen; idx += gthreads) {
+        const int i = idx % clen, j = idx / clen;
+        cp_async_elem(as + i + j * cpitch, Ab + i + (int64_t)j * lda);
+      }
+    }
+    asm volatile("cp.async.commit_group;" ::: "memory");
+  }
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  STAGE_TRACE(slot, 4);
+  STAGE_TRACE(slot, 7);
+#pragma unroll
+  for (int s = 0; s < S; ++s) {
+    const V* Bb = B + (s == 0 ? e.b0 : e.b1);
+    V* bs = Bs + s * ncols * K;
+    for (int idx = t; idx < K * ncols; idx += gthreads) {
+      const int kk = idx % K, cc = idx / K;
+      if (kk < Ke) cp_async_elem(bs + kk + cc * K, Bb + kk + (int64_t)cc * ldb);
+      else bs[kk + cc * K] = mkc<R>(0, 0);
+    }
+  }
+  asm volatile("cp.async.commit_group;" ::: "memory");
+  asm volatile("cp.async.wait_all;" ::: "memory");
+  if constexpr (kBulk) st_mbar_wait(bar, 0);
+  if (wpe == 1) __syncwarp();
+  else __syncthreads();  // multi-warp groups run one per CTA
+  STAGE_TRACE(slot, 11);
+  STAGE_TRACE(slot, 12);
+  // Q lanes per output (power of two, Q * outputs <= threads of the group)
+  const int nout = Me * ncols;
+  int Q = 1;
+  while (Q < 32 && 2 * Q * nout <= gthreads) Q *= 2;
+  const int part = t % Q;
+  // element (m, kk) of op(A_s): stride along kk
+  const int ks = OP == OP_N ? M + 1 : 1;
+  V* Cb = C + e.c;
+  for (int o0 = 0; o0 < nout; o0 += gthreads / Q) {
+    const int o = o0 + t / Q;
+    // four independent partial sums: the FP64 dependent-issue latency, not
+    // throughput, bounds this loop
+    V acc = mkc<R>(0, 0), acc1 = acc, acc2 = acc, acc3 = acc;
+    if (o < nout) {
+      const int m = o % Me, cc = o / Me;
+#pragma unroll
+      for (int s = 0; s < S; ++s) {
+        const V* as = As + s * aelems + (OP == OP_N ? m : m * cpitch);
+        const V* bs = Bs + s * ncols * K + cc * K;
+        int kk = part;
+        for (; kk + 3 * Q < K; kk += 4 * Q) {
+          const V a0 = as[kk * ks], a1 = as[(kk + Q) * ks], a2 = as[(kk + 2 * Q) * ks], a3 = as[(kk + 3 * Q) * ks];
+          const V b0 = bs[kk], b1 = bs[kk + Q], b2 = bs[kk + 2 * Q], b3 = bs[kk + 3 * Q];
+          if (OP == OP_H) {
+            cfma_conj(acc, a0, b0);
+            cfma_conj(acc1, a1, b1);
+            cfma_conj(acc2, a2, b2);
+            cfma_conj(acc3, a3, b3);
+          } else {
+            cfma(acc, a0, b0);
+            cfma(acc1, a1, b1);
+            cfma(acc2, a2, b2);
+            cfma(acc3, a3, b3);
+          }
+        }
+        for (; kk < K; kk += Q) {
+          if (OP == OP_H) cfma_conj(acc, as[kk * ks], bs[kk]);
+          else cfma(acc, as[kk * ks], bs[kk]);
+        }
+      }
+      acc = cadd(cadd(acc, acc1), cadd(acc2, acc3));
+    }
+    for (int q = 1; q < Q; q *= 2) {
+      acc.x += __shfl_xor_sync(0xffffffffu, acc.x, q);
+      acc.y += __shfl_xor_sync(0xffffffffu, acc.y, q);
+    }
+    if (o0 == 0) {
+      STAGE_TRACE(slot, 17);
+      STAGE_TRACE(slot, 18);
+    }
+    if (o < nout && part == 0) {
+      const int m = o % Me, cc = o / Me;
+      V* p = Cb + m + (int64_t)cc * ldc;
+      *p = accumulate ? cadd(*p, acc) : acc;
+    }
+  }
+  STAGE_TRACE(slot, 9);
+}
+
 // Large-k complex128 path on DMMA (mma.sync m8n8k4 f64): one CTA = 8 warps
 // (4 along rows x 2 along columns) computes all M <= 64 rows of one output
 // block for a 64-column slab; op(A_s) and B_s chunks of 16 along K are staged
@@ -187,10 +401,15 @@ __global__ void __launch_bounds__(256) bgemm_dmma_warp_kernel(const double2* __r
                                                               double2* __restrict__ C, int64_t ldc, int M, int K,
                                                               const GemmEnt* __restrict__ ents, int nent,
                                                               int accumulate, int ncols_all) {
+  // programmatic dependent launch (apply stages): dependents may start at
+  // once; B and C are touched only after the prerequisite grid has completed
+  // (both are no-ops for ordinary launches)
+  asm volatile("griddepcontrol.launch_dependents;");
   const int lane = threadIdx.x & 31;
   const int ei = blockIdx.x * 8 + (threadIdx.x >> 5);
   if (ei >= nent) return;
   const GemmEnt e = ents[ei];
+  asm volatile("griddepcontrol.wait;" ::: "memory");
   const int ncols = ncols_all > 0 ? ncols_all : e.ncols;
   const int Me = min(M, e.mrows), Ke = min(K, e.krows);
   const int g = lane >> 2, t = lane & 3;
@@ -277,7 +496,9 @@ __global__ void __launch_bounds__(256) bgemm_dmma_kernel(const double2* __restri
                                                          int ncols_all) {
   constexpr int BM = 32 * MT, BN = 64, BK = 16, SA = BM + 8, SB = BK + 4, NT = 4;
   __shared__ __align__(16) double Are[BK * SA], Aim[BK * SA], Bre[BN * SB], Bim[BN * SB];
+  asm volatile("griddepcontrol.launch_dependents;");  // see bgemm_dmma_warp_kernel
   const GemmEnt e = ents[blockIdx.x];
+  asm volatile("griddepcontrol.wait;" ::: "memory");
   const int ncols = ncols_all > 0 ? ncols_all : e.ncols;
   const int Me = min(M, e.mrows), Ke = min(K, e.krows);
   const int n0 = blockIdx.y * BN;
@@ -380,16 +601,77 @@ __global__ void __launch_bounds__(256) bgemm_dmma_kernel(const double2* __restri
   }
 }
 
+// kernel launch with the programmatic-stream-serialization attribute when pdl
+template <typename... KArgs, typename... Args>
+void launch_pdl(void (*kern)(KArgs...), dim3 grid, int block, cudaStream_t stream, bool pdl, Args... args) {
+  cudaLaunchConfig_t cfg = {};
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.gridDim = grid;
+  cfg.blockDim = dim3(block);
+  cfg.dynamicSmemBytes = 0;
+  cfg.stream = stream;
+  cfg.attrs = pdl ? at : nullptr;
+  cfg.numAttrs = pdl ? 1 : 0;
+  BFLY_CUDA(cudaLaunchKernelEx(&cfg, kern, static_cast<KArgs>(args)...));
+}
 }  // namespace
 
 template <typename R>
 void launch_bgemm(Ctx* c, int op, int M, int K, int S, const cx<R>* A, int64_t lda, const cx<R>* B, int64_t ldb,
                   cx<R>* C, int64_t ldc, const GemmEnt* ents, int nent, int max_ncols, bool accumulate,
-                  int ncols_all, bool pdl) {
+                  int ncols_all, bool pdl, L2Prefetch pf) {
   if (nent <= 0 || M <= 0 || max_ncols <= 0) return;
   const int kcols = ncols_all > 0 ? ncols_all : max_ncols;
   const size_t small_smem = sizeof(cx<R>) * (size_t)S * ((size_t)K * (M + 1) + (size_t)K * kcols);
-  if (kcols <= 16 && K > 0 && small_smem <= 96 * 1024 && nent <= 0x7fffffff) {
+  static const bool no_stage = std::getenv("BFLY_NO_STAGE_GEMM") != nullptr;
+  const size_t stage_smem = 16 + sizeof(cx<R>) * (size_t)stage_group_elems(op, M, K, S, kcols);
+  static const int dmma_mink = std::getenv("BFLY_DMMA_MINK") ? std::atoi(std::getenv("BFLY_DMMA_MINK")) : 8;
+  const bool dmma_cols = std::is_same<R, double>::value && kcols >= dmma_mink;
+  if (pdl && !no_stage && !dmma_cols && ncols_all > 0 && kcols <= 16 && K > 0 && stage_smem <= 96 * 1024) {
+    KTimer timer(c, "bgemm_stage", 8.0 * M * K * S * (double)nent * kcols,
+                 sizeof(cx<R>) * ((double)nent * S * (M * (double)K + K * kcols) + (double)nent * M * kcols));
+    static const int wpe_env = std::getenv("BFLY_STAGE_WPE") ? std::atoi(std::getenv("BFLY_STAGE_WPE")) : 0;
+    const int wpe = wpe_env > 0 ? std::min(wpe_env, 8) : kcols <= 2 ? 1 : kcols <= 8 ? 2 : 4;
+    const size_t grp_smem = stage_smem;
+    static const int epb_env = std::getenv("BFLY_STAGE_EPB") ? std::atoi(std::getenv("BFLY_STAGE_EPB")) : 0;
+    int epb = wpe == 1 ? (epb_env > 0 ? std::min(epb_env, 8) : 4) : 1;
+    while (epb > 1 && epb * grp_smem > 200 * 1024) epb /= 2;
+    cudaLaunchConfig_t cfg = {};
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.gridDim = dim3((unsigned)ceil_div((int64_t)nent, (int64_t)epb));
+    cfg.blockDim = dim3(32 * wpe * epb);
+    cfg.dynamicSmemBytes = epb * grp_smem;
+    cfg.stream = c->stream;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+#define BST(OPV, SV)                                                                                        \
+  do {                                                                                                      \
+    auto kern = bgemm_stage_kernel<R, OPV, SV>;                                                             \
+    static bool attr_set = false; /* first use is eager (never inside graph capture) */                    \
+    if (!attr_set) {                                                                                        \
+      BFLY_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024));        \
+      attr_set = true;                                                                                      \
+    }                                                                                                       \
+    BFLY_CUDA(cudaLaunchKernelEx(&cfg, kern, A, lda, B, ldb, C, ldc, M, K, ents, nent, (int)accumulate, kcols, wpe, pf)); \
+  } while (0)
+    if (S == 1) {
+      if (op == OP_N) BST(OP_N, 1);
+      else if (op == OP_T) BST(OP_T, 1);
+      else BST(OP_H, 1);
+    } else {
+      if (op == OP_N) BST(OP_N, 2);
+      else if (op == OP_T) BST(OP_T, 2);
+      else BST(OP_H, 2);
+    }
+#undef BST
+    BFLY_LAUNCH_CHECK("bgemm_stage");
+    return;
+  }
+  if (!dmma_cols && kcols <= 16 && K > 0 && small_smem <= 96 * 1024 && nent <= 0x7fffffff) {
     KTimer timer(c, "bgemm_small", 8.0 * M * K * S * (double)nent * kcols,
                  sizeof(cx<R>) * ((double)nent * S * (M * (double)K + K * kcols) + (double)nent * M * kcols));
 #define BGS(OPV, SV)                                                                                           \
@@ -432,7 +714,7 @@ void launch_bgemm(Ctx* c, int op, int M, int K, int S, const cx<R>* A, int64_t l
   if constexpr (std::is_same<R, double>::value) {
     static const bool no_dmma = std::getenv("BFLY_NO_DMMA_GEMM") != nullptr;
     static const bool no_warp = std::getenv("BFLY_NO_WARP_GEMM") != nullptr;
-    if (!no_dmma && !no_warp && kcols > 16 && max_ncols <= 32 && M <= 16 && K > 0) {
+    if (!no_dmma && !no_warp && dmma_cols && max_ncols <= 32 && M <= 16 && K > 0) {
       static const char* wnames[3][2] = {{"bgemm_warp_N1", "bgemm_warp_N2"},
                                          {"bgemm_warp_T1", "bgemm_warp_T2"},
                                          {"bgemm_warp_H1", "bgemm_warp_H2"}};
@@ -440,7 +722,7 @@ void launch_bgemm(Ctx* c, int op, int M, int K, int S, const cx<R>* A, int64_t l
                    sizeof(cx<R>) * ((double)nent * S * (M * (double)K + K * kcols) + (double)nent * M * kcols));
       const unsigned grid = (unsigned)ceil_div((int64_t)nent, (int64_t)8);
 #define BW(OPV, SV)                                                                                          \
-  bgemm_dmma_warp_kernel<OPV, SV><<<grid, 256, 0, c->stream>>>(A, lda, B, ldb, C, ldc, M, K, ents, nent,      \
+  launch_pdl(bgemm_dmma_warp_kernel<OPV, SV>, dim3(grid), 256, c->stream, pdl, A, lda, B, ldb, C, ldc, M, K, ents, nent, \
                                                                accumulate, ncols_all)
       if (S == 1) {
         if (op == OP_N) BW(OP_N, 1);
@@ -455,7 +737,7 @@ void launch_bgemm(Ctx* c, int op, int M, int K, int S, const cx<R>* A, int64_t l
       BFLY_LAUNCH_CHECK("bgemm_warp");
       return;
     }
-    if (!no_dmma && kcols > 16 && M <= 64 && K > 0) {
+    if (!no_dmma && dmma_cols && M <= 64 && K > 0) {
       const unsigned gy = (unsigned)ceil_div(max_ncols, 64);
       if (gy > 65535) fail(PRECONDITION, "bgemm: grid too large");
       dim3 grid(nent, gy);
@@ -465,7 +747,7 @@ void launch_bgemm(Ctx* c, int op, int M, int K, int S, const cx<R>* A, int64_t l
       KTimer timer(c, names[op][S - 1][M > 32], 8.0 * M * K * S * (double)nent * kcols,
                    sizeof(cx<R>) * ((double)nent * S * (M * (double)K + K * kcols) + (double)nent * M * kcols));
 #define BD(OPV, SV, MTV)                                                                                  \
-  bgemm_dmma_kernel<OPV, SV, MTV><<<grid, 256, 0, c->stream>>>(A, lda, B, ldb, C, ldc, M, K, ents, accumulate, \
+  launch_pdl(bgemm_dmma_kernel<OPV, SV, MTV>, grid, 256, c->stream, pdl, A, lda, B, ldb, C, ldc, M, K, ents, accumulate, \
                                                                  ncols_all)
 #define BD_OP(SV, MTV)                   \
   do {                                   \
@@ -507,8 +789,21 @@ void launch_bgemm(Ctx* c, int op, int M, int K, int S, const cx<R>* A, int64_t l
 }
 
 template void launch_bgemm<double>(Ctx*, int, int, int, int, const double2*, int64_t, const double2*, int64_t, double2*,
-                                   int64_t, const GemmEnt*, int, int, bool, int, bool);
+                                   int64_t, const GemmEnt*, int, int, bool, int, bool, L2Prefetch);
 template void launch_bgemm<float>(Ctx*, int, int, int, int, const float2*, int64_t, const float2*, int64_t, float2*,
-                                  int64_t, const GemmEnt*, int, int, bool, int, bool);
+                                  int64_t, const GemmEnt*, int, int, bool, int, bool, L2Prefetch);
 
+#ifdef BFLY_STAGE_TRACE
+extern "C" __attribute__((visibility("default"))) int bfly_debug_stage_trace(unsigned long long* out, int reset) {
+  if (reset) {
+    unsigned long long init[64][10];
+    for (auto& r : init) {
+      r[0] = r[2] = r[6] = r[9] = ~0ull;
+      r[1] = r[3] = r[4] = r[5] = r[7] = r[8] = 0;
+    }
+    return (int)cudaMemcpyToSymbol(g_stage_trace, init, sizeof(init));
+  }
+  return (int)cudaMemcpyFromSymbol(out, g_stage_trace, sizeof(g_stage_trace));
+}
+#endif
 }  // namespace bfly

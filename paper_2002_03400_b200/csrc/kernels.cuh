@@ -57,10 +57,16 @@ struct GemmEnt {
   int64_t a0, a1, b0, b1, c;
   int32_t ncols, mrows, krows, pad_;
 };
+// L2 prefetch of the NEXT chain stage's factor level: entry e of this launch
+// prefetches [base + e*stride, +len) bytes (stage kernel only)
+struct L2Prefetch {
+  const void* base = nullptr;
+  int64_t stride = 0, len = 0;
+};
 template <typename R>
 void launch_bgemm(Ctx* c, int op, int M, int K, int S, const cx<R>* A, int64_t lda, const cx<R>* B, int64_t ldb,
                   cx<R>* C, int64_t ldc, const GemmEnt* ents_dev, int nent, int max_ncols, bool accumulate,
-                  int ncols_all = 0, bool pdl = false);
+                  int ncols_all = 0, bool pdl = false, L2Prefetch pf = L2Prefetch());
 // pdl: programmatic dependent launch for chains whose A operand is NOT written
 // by the preceding kernel (butterfly apply stages): A is staged before the
 // dependency wait, overlapping the previous stage's tail.
