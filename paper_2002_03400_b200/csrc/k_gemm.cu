@@ -321,16 +321,21 @@ __global__ void __launch_bounds__(256) bgemm_stage_kernel(const cx<R>* __restric
   else __syncthreads();  // multi-warp groups run one per CTA
   STAGE_TRACE(slot, 11);
   STAGE_TRACE(slot, 12);
-  // Q lanes per output (power of two, Q * outputs <= threads of the group)
+  // Q lanes per output (power of two, Q * outputs <= threads of the group).
+  // The K split is across the HIGH lane bits (part = lane / (32/Q)), so a
+  // quarter-warp reads 8 consecutive outputs of one kk: distinct bank groups
+  // for every image pitch (a low-bit split costs 2-way conflicts, measured
+  // 1.5x on tools/microbench/gemv_lat.cu).
   const int nout = Me * ncols;
   int Q = 1;
   while (Q < 32 && 2 * Q * nout <= gthreads) Q *= 2;
-  const int part = t % Q;
+  const int opw = 32 / Q;  // outputs per warp and pass
+  const int lane = t & 31, part = lane / opw;
   // element (m, kk) of op(A_s): stride along kk
   const int ks = OP == OP_N ? M + 1 : 1;
   V* Cb = C + e.c;
   for (int o0 = 0; o0 < nout; o0 += gthreads / Q) {
-    const int o = o0 + t / Q;
+    const int o = o0 + (t >> 5) * opw + lane % opw;
     // four independent partial sums: the FP64 dependent-issue latency, not
     // throughput, bounds this loop
     V acc = mkc<R>(0, 0), acc1 = acc, acc2 = acc, acc3 = acc;
@@ -363,7 +368,7 @@ __global__ void __launch_bounds__(256) bgemm_stage_kernel(const cx<R>* __restric
       }
       acc = cadd(cadd(acc, acc1), cadd(acc2, acc3));
     }
-    for (int q = 1; q < Q; q *= 2) {
+    for (int q = opw; q < 32; q *= 2) {
       acc.x += __shfl_xor_sync(0xffffffffu, acc.x, q);
       acc.y += __shfl_xor_sync(0xffffffffu, acc.y, q);
     }
