@@ -211,6 +211,26 @@ BFLY_API int bfly_residuals(bfly_op* op, bfly_bf* bf, double* u_res, double* v_r
 /* HybridButterfly::apply / apply_transpose / apply_adjoint (butterfly.hpp:71-193) */
 BFLY_API int bfly_apply(bfly_bf* bf, int trans, const void* x, int64_t ldx, void* y, int64_t ldy, int64_t k,
                int on_device);
+/* Process layouts of the apply (inc/layout.hpp).  kind: 0 column, 1 row,
+ * 2 hybrid; processes a power of two <= 2^L.
+ * bfly_comm_cost: closed-form CommCostReport (comm_cost, layout.hpp:70-88)
+ *   out[4] = exchange volume, exchange messages, all-to-all volume,
+ *   all-to-all messages (scalars per input column and process).
+ * bfly_layout_owners: assign_ownership (layout.hpp:139-188) without a
+ *   butterfly; out[(L+3) 2^L] = u leaves, v leaves, R levels center..L-1,
+ *   W levels 1..center, centre cores (flat block index tau*2^(L-l)+nu);
+ *   returns the length (out == NULL: length only) or -status.
+ * bfly_apply_layout: the apply (trans N or H) executed over the layout: with
+ *   a communicator (bfly_ctx_set_comm) one process per GPU exchanging
+ *   coefficient blocks by NCCL send/recv, else `processes` virtual processes
+ *   in turn on this GPU; x full input, y full output on every process.
+ *   report[6] = the four simulated_parallel_apply tallies
+ *   (layout.hpp:190-261), then the measured scalars per column received by
+ *   the busiest process and in total. */
+BFLY_API int bfly_comm_cost(int kind, int levels, int64_t rank, int64_t processes, double* out);
+BFLY_API int64_t bfly_layout_owners(int kind, int levels, int center, int64_t processes, int32_t* out);
+BFLY_API int bfly_apply_layout(bfly_bf* bf, int trans, int kind, int64_t processes, const void* x, int64_t ldx, void* y,
+                               int64_t ldy, int64_t k, int on_device, double* report);
 BFLY_API int bfly_bf_info(const bfly_bf* bf, int* levels, int* center, int64_t* m, int64_t* n, int64_t* nnz,
                  int64_t* max_rank, int* scalar);
 /* u ranks for levels center..L, then v ranks for levels 0..center (2^L each,

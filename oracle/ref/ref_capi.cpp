@@ -14,6 +14,7 @@
 #include <sstream>
 #include <string>
 
+#include "bfly/layout.hpp"
 #include "bfly/reconstruct.hpp"
 #include "bfly/serialize.hpp"
 
@@ -157,6 +158,35 @@ int guard(F&& f) {
   }
 }
 
+}  // namespace
+
+namespace {
+template <typename BF>
+void layout_of(const BF& bf, int kind, int64_t p, double* out, int32_t* owners) {
+  LayoutSpec ls;
+  ls.kind = (layout_kind)kind;
+  ls.levels = bf.levels;
+  ls.rank = 1;
+  ls.processes = p;
+  auto map = assign_ownership(bf, ls);
+  Matrix<cplx> x = gaussian_matrix<cplx>(bf.cols(), 1, 2);
+  auto res = simulated_parallel_apply(bf, x, ls);
+  const auto& r = res.second;
+  out[0] = r.exchange_volume;
+  out[1] = (double)r.exchange_msgs;
+  out[2] = r.alltoall_volume;
+  out[3] = (double)r.alltoall_msgs;
+  if (owners) {
+    int32_t* o = owners;
+    for (int v : map.u_leaf) *o++ = v;
+    for (int v : map.v_leaf) *o++ = v;
+    for (const auto& lv : map.r_owner)
+      for (int v : lv) *o++ = v;
+    for (const auto& lv : map.w_owner)
+      for (int v : lv) *o++ = v;
+    for (int v : map.b_owner) *o++ = v;
+  }
+}
 }  // namespace
 
 extern "C" {
@@ -360,6 +390,40 @@ double ref_probe_sample(ref_op* h, int level, int probes, int64_t width, uint64_
     secs = omp_get_wtime() - t0;
   });
   return secs;
+}
+
+// ---- process layouts (layout.hpp): closed-form model, ownership maps and
+// the simulated sweep's tallies.  owners: (L+3) 2^L = u leaves, v leaves,
+// R levels center..L-1, W levels 1..center, centre cores.
+int ref_comm_cost(int kind, int levels, int64_t rank, int64_t p, double* out) {
+  return guard([&] {
+    LayoutSpec ls;
+    ls.kind = (layout_kind)kind;
+    ls.levels = levels;
+    ls.rank = rank;
+    ls.processes = p;
+    auto r = comm_cost(ls);
+    out[0] = r.exchange_volume;
+    out[1] = (double)r.exchange_msgs;
+    out[2] = r.alltoall_volume;
+    out[3] = (double)r.alltoall_msgs;
+  });
+}
+
+
+int ref_layout_synth(int levels, int64_t rank, uint64_t seed, int kind, int64_t p, double* out, int32_t* owners) {
+  return guard([&] {
+    SyntheticButterflySpec spec;
+    spec.levels = levels;
+    spec.rank = rank;
+    spec.seed = seed;
+    auto bf = synth_butterfly<cplx>(spec);
+    layout_of(bf, kind, p, out, owners);
+  });
+}
+
+int ref_layout_bf(const ref_bf* b, int kind, int64_t p, double* out, int32_t* owners) {
+  return guard([&] { layout_of(b->bf, kind, p, out, owners); });
 }
 
 }  // extern "C"

@@ -41,6 +41,9 @@ def lib():
             "ref_gaussian": (i32, [i32, i64, i64, u64, p]),
             "ref_cpqr": (i64, [i64, i64, p, dbl, p]),
             "ref_residuals": (i32, [p, p, p, p, p, p]),
+            "ref_comm_cost": (i32, [i32, i32, i64, i64, p]),
+            "ref_layout_synth": (i32, [i32, i64, u64, i32, i64, p, p]),
+            "ref_layout_bf": (i32, [p, i32, i64, p, p]),
         }
         for k, (r, a) in sig.items():
             f = getattr(L, k)
@@ -135,6 +138,13 @@ class RefButterfly:
         _check(lib().ref_residuals(self.op.h, self.h, _vp(u), _vp(v), C.byref(cen), C.byref(kn)))
         return u, v, cen.value, kn.value
 
+    def layout(self, levels, kind, p):
+        """(simulated_parallel_apply tallies[4], owners[(L+3) 2^L]) (layout.hpp:139-261)."""
+        out = np.zeros(4)
+        own = np.zeros((levels + 3) << levels, np.int32)
+        _check(lib().ref_layout_bf(self.h, kind, p, _vp(out), _vp(own)))
+        return out, own
+
     def serialize(self):
         n = lib().ref_serialize(self.h, None)
         buf = np.zeros(n, np.uint8)
@@ -176,3 +186,18 @@ def pivoted_qr_truncate(w, eps):
         raise RuntimeError(lib().ref_last_error().decode())
     k = max(rank, 0)
     return rank, q[:k].T.copy()
+
+
+def comm_cost(kind, levels, rank, p):
+    """comm_cost (layout.hpp:70-88) -> [exchange_volume, exchange_msgs, alltoall_volume, alltoall_msgs]."""
+    out = np.zeros(4)
+    _check(lib().ref_comm_cost(kind, levels, rank, p, _vp(out)))
+    return out
+
+
+def layout_synth(levels, rank, seed, kind, p):
+    """The reference's synthetic butterfly through assign_ownership + simulated_parallel_apply."""
+    out = np.zeros(4)
+    own = np.zeros((levels + 3) << levels, np.int32)
+    _check(lib().ref_layout_synth(levels, rank, seed, kind, p, _vp(out), _vp(own)))
+    return out, own

@@ -129,6 +129,9 @@ def lib():
         "bfly_estimate_error": (i32, [p, p, i64, u64, C.POINTER(C.c_double)]),
         "bfly_residuals": (i32, [p, p, p, p, C.POINTER(C.c_double), C.POINTER(C.c_double)]),
         "bfly_apply": (i32, [p, i32, p, i64, p, i64, i64, i32]),
+        "bfly_apply_layout": (i32, [p, i32, i32, i64, p, i64, p, i64, i64, i32, C.POINTER(C.c_double)]),
+        "bfly_comm_cost": (i32, [i32, i32, i64, i64, C.POINTER(C.c_double)]),
+        "bfly_layout_owners": (i64, [i32, i32, i32, i64, p]),
         "bfly_bf_info": (i32, [p, C.POINTER(C.c_int), C.POINTER(C.c_int), C.POINTER(C.c_int64),
                                C.POINTER(C.c_int64), C.POINTER(C.c_int64), C.POINTER(C.c_int64),
                                C.POINTER(C.c_int)]),

@@ -10,7 +10,9 @@ and out inside the call, torch CUDA tensors are used in place.
 """
 from __future__ import annotations
 
+import atexit
 import ctypes as C
+from dataclasses import dataclass
 import dataclasses
 from typing import Optional
 
@@ -27,6 +29,18 @@ OP_DENSE, OP_NUFFT, OP_PLATES, OP_CIRCLE, OP_COMPOSE, OP_BUTTERFLY, OP_CALLBACK 
 
 def _vp(a):
     return a.ctypes.data_as(C.c_void_p)
+
+
+# Native handles are released by __del__ while the interpreter runs; at exit
+# the process teardown reclaims them instead (finalizers of objects kept alive
+# until shutdown -- e.g. by a stored traceback -- run in no particular order,
+# so a butterfly could otherwise be destroyed after its context).
+_FINALIZING = [False]
+atexit.register(lambda: _FINALIZING.__setitem__(0, True))
+
+
+def _live() -> bool:
+    return not _FINALIZING[0]
 
 
 # ------------------------------------------------------------------ context
@@ -82,6 +96,8 @@ class Context:
 
     def __del__(self):
         try:
+            if not _live():
+                return
             if getattr(self, "h", None):
                 lib().bfly_ctx_destroy(self.h)
         except Exception:
@@ -156,6 +172,8 @@ class PartitionTree:
 
     def __del__(self):
         try:
+            if not _live():
+                return
             lib().bfly_tree_destroy(self.h)
         except Exception:
             pass
@@ -259,6 +277,8 @@ class BlackBoxOperator(_Applicable):
 
     def __del__(self):
         try:
+            if not _live():
+                return
             if getattr(self, "h", None):
                 lib().bfly_op_destroy(self.h)
         except Exception:
@@ -480,6 +500,29 @@ class HybridButterfly(_Applicable):
     def apply_transpose(self, y, out=None):
         return self._call(T, y, out)
 
+    def apply_layout(self, x, spec: "LayoutSpec", trans: int = N):
+        """The apply executed over a process layout (inc/layout.hpp:139-261).
+        With a communicator on the context (one process per GPU) the
+        coefficient blocks move by NCCL send/recv; otherwise
+        ``spec.processes`` virtual processes run in turn on this GPU.  Returns
+        (y, measured CommCostReport, {"max_recv": ..., "total_recv": ...} --
+        scalars per column actually moved)."""
+        if spec.levels != self.levels:
+            raise DimensionError("apply_layout: spec level count does not match the butterfly")
+        rep = (C.c_double * 6)()
+
+        def fn(trans_, x_, ldx, y_, ldy, k, dev):
+            return lib().bfly_apply_layout(self.h, trans_, spec.kind_id, spec.processes, x_, ldx, y_, ldy, k, dev,
+                                           rep)
+
+        self._apply_fn = fn  # instance override for this call only
+        try:
+            y = self._call(trans, x)
+        finally:
+            del self._apply_fn
+        measured = CommCostReport(rep[0], int(rep[1]), rep[2], int(rep[3]))
+        return y, measured, {"max_recv": rep[4], "total_recv": rep[5]}
+
     def nnz(self) -> int:
         return self._nnz
 
@@ -548,6 +591,8 @@ class HybridButterfly(_Applicable):
 
     def __del__(self):
         try:
+            if not _live():
+                return
             if getattr(self, "h", None):
                 lib().bfly_bf_destroy(self.h)
         except Exception:
@@ -595,9 +640,106 @@ class Factorizer:
 
     def __del__(self):
         try:
+            if not _live():
+                return
             lib().bfly_factorizer_destroy(self.h)
         except Exception:
             pass
+
+
+# ---------------------------------------------------------------- layouts
+LAYOUT_KINDS = ("column", "row", "hybrid")
+
+
+def layout_name(kind: str) -> str:
+    return kind
+
+
+def layout_from_name(name: str) -> str:
+    """layout_from_name (layout.hpp:20-25)."""
+    if name not in LAYOUT_KINDS:
+        raise PreconditionError("unknown layout kind: " + str(name))
+    return name
+
+
+@dataclass
+class LayoutSpec:
+    """LayoutSpec (layout.hpp:27-49): kind, L, constant model rank r, p."""
+
+    kind: str = "hybrid"
+    levels: int = 4
+    rank: int = 8
+    processes: int = 1
+
+    @property
+    def kind_id(self) -> int:
+        return LAYOUT_KINDS.index(layout_from_name(self.kind))
+
+    def log_p(self) -> int:
+        g = 0
+        while (1 << (g + 1)) <= self.processes:
+            g += 1
+        return g
+
+
+@dataclass
+class CommCostReport:
+    """CommCostReport (layout.hpp:52-66), scalars per input column."""
+
+    exchange_volume: float = 0.0
+    exchange_msgs: int = 0
+    alltoall_volume: float = 0.0
+    alltoall_msgs: int = 0
+
+    def model_time(self, alpha: float, beta: float) -> float:
+        return alpha * (self.exchange_msgs + self.alltoall_msgs) + beta * (self.exchange_volume + self.alltoall_volume)
+
+
+def comm_cost(spec: LayoutSpec) -> CommCostReport:
+    """Closed-form model (layout.hpp:70-88); invalid specs raise PreconditionError."""
+    out = (C.c_double * 4)()
+    check(lib().bfly_comm_cost(spec.kind_id, spec.levels, spec.rank, spec.processes, out))
+    return CommCostReport(out[0], int(out[1]), out[2], int(out[3]))
+
+
+@dataclass
+class OwnershipMap:
+    """OwnershipMap (layout.hpp:113-136): owners by flat block index."""
+
+    processes: int
+    levels: int
+    center: int
+    u_leaf: np.ndarray
+    v_leaf: np.ndarray
+    r_owner: np.ndarray  # [l - center][block]
+    w_owner: np.ndarray  # [l - 1][block]
+    b_owner: np.ndarray
+
+    def r_at(self, level, tau, nu):
+        return int(self.r_owner[level - self.center][tau * (1 << (self.levels - level)) + nu])
+
+    def w_at(self, level, tau, nu):
+        return int(self.w_owner[level - 1][tau * (1 << (self.levels - level)) + nu])
+
+    def b_at(self, tau, nu):
+        return int(self.b_owner[tau * (1 << (self.levels - self.center)) + nu])
+
+
+def assign_ownership(bf, spec: LayoutSpec) -> OwnershipMap:
+    """assign_ownership (layout.hpp:139-188).  ``bf`` is a HybridButterfly or
+    a (levels, center) pair (the map depends on nothing else)."""
+    levels, center = (bf.levels, bf.center) if hasattr(bf, "levels") else bf
+    if spec.levels != levels:
+        raise DimensionError("assign_ownership: spec level count does not match the butterfly")
+    n = lib().bfly_layout_owners(spec.kind_id, levels, center, spec.processes, None)
+    if n < 0:
+        check(int(-n))
+    out = np.zeros(n, np.int32)
+    lib().bfly_layout_owners(spec.kind_id, levels, center, spec.processes, _vp(out))
+    nb = 1 << levels
+    o = out.reshape(-1, nb)
+    return OwnershipMap(spec.processes, levels, center, o[0].copy(), o[1].copy(), o[2:2 + levels - center].copy(),
+                        o[2 + levels - center:2 + levels].copy(), o[2 + levels].copy())
 
 
 def estimate_error(op: BlackBoxOperator, bf: HybridButterfly, k: int = 16, seed: int = 0) -> float:

@@ -548,46 +548,57 @@ void DevButterfly<R>::build_plan_n() {
   pl = Plan();
   const int64_t NB = nb();
   const int BIG = 1 << 30;
-  auto add = [&](int op, int M, int K, int S, const Level<R>& lv, int64_t ld_out, int pfcols) -> StageDesc& {
+  auto add = [&](int op, int M, int K, int S, const Level<R>& lv, int64_t ld_out, int pfcols, int side,
+                 int level) -> StageDesc& {
     pl.st.emplace_back();
     StageDesc& d = pl.st.back();
     d.op = op; d.M = M; d.K = K; d.S = S; d.A = lv.data.p; d.lda = lv.ld; d.ld_out = ld_out;
     d.pf = l2pf(lv, pfcols);
+    d.own_side = side;
+    d.own_level = level;
     return d;
   };
+  auto push = [](StageDesc& d, const GemmEnt& e, int64_t tau, int64_t nu) {
+    d.h.push_back(e);
+    d.own_tau.push_back(tau);
+    d.own_nu.push_back(nu);
+  };
   {
-    StageDesc& d = add(OP_H, PV(0), (int)vleaf.ld, 1, vleaf, NB * PV(0), PV(0));
+    StageDesc& d = add(OP_H, PV(0), (int)vleaf.ld, 1, vleaf, NB * PV(0), PV(0), 0, 0);
     for (int64_t nu = 0; nu < NB; ++nu)
-      d.h.push_back(ent(nu * vleaf.stride(), 0, ct.begin(L, nu), 0, nu * PV(0), BIG, (int)ct.size(L, nu)));
+      push(d, ent(nu * vleaf.stride(), 0, ct.begin(L, nu), 0, nu * PV(0), BIG, (int)ct.size(L, nu)), 0, nu);
   }
   for (int l = 1; l <= lm; ++l) {
     const Level<R>& wl = w[l - 1];
-    StageDesc& d = add(OP_H, PV(l), 2 * PV(l - 1), 1, wl, NB * PV(l), PV(l));
+    StageDesc& d = add(OP_H, PV(l), 2 * PV(l - 1), 1, wl, NB * PV(l), PV(l), 0, l);
     for (int64_t tau = 0; tau < (int64_t(1) << l); ++tau)
       for (int64_t nu = 0; nu < (int64_t(1) << (L - l)); ++nu) {
         int64_t i = bidx(L, l, tau, nu);
-        d.h.push_back(ent(i * wl.stride(), 0, bidx(L, l - 1, tau / 2, 2 * nu) * PV(l - 1), 0, i * PV(l), BIG, BIG));
+        push(d, ent(i * wl.stride(), 0, bidx(L, l - 1, tau / 2, 2 * nu) * PV(l - 1), 0, i * PV(l), BIG, BIG), tau,
+             nu);
       }
   }
   {
-    StageDesc& d = add(OP_N, PU(lm), PV(lm), 1, b, NB * PU(lm), PV(lm));
-    for (int64_t i = 0; i < NB; ++i) d.h.push_back(ent(i * b.stride(), 0, i * PV(lm), 0, i * PU(lm), BIG, BIG));
+    StageDesc& d = add(OP_N, PU(lm), PV(lm), 1, b, NB * PU(lm), PV(lm), 0, lm);
+    for (int64_t i = 0; i < NB; ++i)
+      push(d, ent(i * b.stride(), 0, i * PV(lm), 0, i * PU(lm), BIG, BIG), i >> (L - lm),
+           i & ((int64_t(1) << (L - lm)) - 1));
   }
   for (int l = lm; l < L; ++l) {
     const Level<R>& rl = r[l - lm];
-    StageDesc& d = add(OP_N, PU(l + 1), PU(l), 2, rl, NB * PU(l + 1), PU(l));
+    StageDesc& d = add(OP_N, PU(l + 1), PU(l), 2, rl, NB * PU(l + 1), PU(l), 1, l + 1);
     for (int64_t tp = 0; tp < (int64_t(1) << (l + 1)); ++tp)
       for (int64_t np = 0; np < (int64_t(1) << (L - l - 1)); ++np) {
         int64_t tau = tp >> 1, h = tp & 1;
         int64_t i0 = bidx(L, l, tau, 2 * np), i1 = bidx(L, l, tau, 2 * np + 1);
-        d.h.push_back(ent(i0 * rl.stride() + h * rl.gap, i1 * rl.stride() + h * rl.gap, i0 * PU(l), i1 * PU(l),
-                          bidx(L, l + 1, tp, np) * PU(l + 1), BIG, BIG));
+        push(d, ent(i0 * rl.stride() + h * rl.gap, i1 * rl.stride() + h * rl.gap, i0 * PU(l), i1 * PU(l),
+                    bidx(L, l + 1, tp, np) * PU(l + 1), BIG, BIG), tp, np);
       }
   }
   {
-    StageDesc& d = add(OP_N, (int)uleaf.ld, PU(L), 1, uleaf, 0, PU(L));
+    StageDesc& d = add(OP_N, (int)uleaf.ld, PU(L), 1, uleaf, 0, PU(L), 1, L);
     for (int64_t tau = 0; tau < NB; ++tau)
-      d.h.push_back(ent(tau * uleaf.stride(), 0, tau * PU(L), 0, rt.begin(L, tau), (int)rt.size(L, tau), BIG));
+      push(d, ent(tau * uleaf.stride(), 0, tau * PU(L), 0, rt.begin(L, tau), (int)rt.size(L, tau), BIG), tau, 0);
   }
   upload_plan(pl);
 }
@@ -598,47 +609,57 @@ void DevButterfly<R>::build_plan_h() {
   pl = Plan();
   const int64_t NB = nb();
   const int BIG = 1 << 30;
-  auto add = [&](int op, int M, int K, int S, const Level<R>& lv, int64_t ld_out, int pfcols) -> StageDesc& {
+  auto add = [&](int op, int M, int K, int S, const Level<R>& lv, int64_t ld_out, int pfcols, int side,
+                 int level) -> StageDesc& {
     pl.st.emplace_back();
     StageDesc& d = pl.st.back();
     d.op = op; d.M = M; d.K = K; d.S = S; d.A = lv.data.p; d.lda = lv.ld; d.ld_out = ld_out;
     d.pf = l2pf(lv, pfcols);
+    d.own_side = side;
+    d.own_level = level;
     return d;
   };
+  auto push = [](StageDesc& d, const GemmEnt& e, int64_t tau, int64_t nu) {
+    d.h.push_back(e);
+    d.own_tau.push_back(tau);
+    d.own_nu.push_back(nu);
+  };
   {
-    StageDesc& d = add(OP_H, PU(L), (int)uleaf.ld, 1, uleaf, NB * PU(L), PU(L));
+    StageDesc& d = add(OP_H, PU(L), (int)uleaf.ld, 1, uleaf, NB * PU(L), PU(L), 1, L);
     for (int64_t tau = 0; tau < NB; ++tau)
-      d.h.push_back(ent(tau * uleaf.stride(), 0, rt.begin(L, tau), 0, tau * PU(L), BIG, (int)rt.size(L, tau)));
+      push(d, ent(tau * uleaf.stride(), 0, rt.begin(L, tau), 0, tau * PU(L), BIG, (int)rt.size(L, tau)), tau, 0);
   }
   for (int l = L - 1; l >= lm; --l) {
     const Level<R>& rl = r[l - lm];
-    StageDesc& d = add(OP_H, PU(l), PU(l + 1), 2, rl, NB * PU(l), PU(l));
+    StageDesc& d = add(OP_H, PU(l), PU(l + 1), 2, rl, NB * PU(l), PU(l), 1, l);
     for (int64_t tau = 0; tau < (int64_t(1) << l); ++tau)
       for (int64_t nu = 0; nu < (int64_t(1) << (L - l)); ++nu) {
         int64_t i = bidx(L, l, tau, nu);
-        d.h.push_back(ent(i * rl.stride(), i * rl.stride() + rl.gap, bidx(L, l + 1, 2 * tau, nu / 2) * PU(l + 1),
-                          bidx(L, l + 1, 2 * tau + 1, nu / 2) * PU(l + 1), i * PU(l), BIG, BIG));
+        push(d, ent(i * rl.stride(), i * rl.stride() + rl.gap, bidx(L, l + 1, 2 * tau, nu / 2) * PU(l + 1),
+                    bidx(L, l + 1, 2 * tau + 1, nu / 2) * PU(l + 1), i * PU(l), BIG, BIG), tau, nu);
       }
   }
   {
-    StageDesc& d = add(OP_H, PV(lm), PU(lm), 1, b, NB * PV(lm), PV(lm));
-    for (int64_t i = 0; i < NB; ++i) d.h.push_back(ent(i * b.stride(), 0, i * PU(lm), 0, i * PV(lm), BIG, BIG));
+    StageDesc& d = add(OP_H, PV(lm), PU(lm), 1, b, NB * PV(lm), PV(lm), 0, lm);
+    for (int64_t i = 0; i < NB; ++i)
+      push(d, ent(i * b.stride(), 0, i * PU(lm), 0, i * PV(lm), BIG, BIG), i >> (L - lm),
+           i & ((int64_t(1) << (L - lm)) - 1));
   }
   for (int l = lm; l >= 1; --l) {
     const Level<R>& wl = w[l - 1];
-    StageDesc& d = add(OP_N, PV(l - 1), PV(l), 2, wl, NB * PV(l - 1), PV(l));
+    StageDesc& d = add(OP_N, PV(l - 1), PV(l), 2, wl, NB * PV(l - 1), PV(l), 0, l - 1);
     for (int64_t tp = 0; tp < (int64_t(1) << (l - 1)); ++tp)
       for (int64_t npp = 0; npp < (int64_t(1) << (L - l + 1)); ++npp) {
         int64_t nu = npp >> 1, h = npp & 1;
         int64_t i0 = bidx(L, l, 2 * tp, nu), i1 = bidx(L, l, 2 * tp + 1, nu);
-        d.h.push_back(ent(i0 * wl.stride() + h * wl.gap, i1 * wl.stride() + h * wl.gap, i0 * PV(l), i1 * PV(l),
-                          bidx(L, l - 1, tp, npp) * PV(l - 1), BIG, BIG));
+        push(d, ent(i0 * wl.stride() + h * wl.gap, i1 * wl.stride() + h * wl.gap, i0 * PV(l), i1 * PV(l),
+                    bidx(L, l - 1, tp, npp) * PV(l - 1), BIG, BIG), tp, npp);
       }
   }
   {
-    StageDesc& d = add(OP_N, (int)vleaf.ld, PV(0), 1, vleaf, 0, PV(0));
+    StageDesc& d = add(OP_N, (int)vleaf.ld, PV(0), 1, vleaf, 0, PV(0), 0, 0);
     for (int64_t nu = 0; nu < NB; ++nu)
-      d.h.push_back(ent(nu * vleaf.stride(), 0, nu * PV(0), 0, ct.begin(L, nu), (int)ct.size(L, nu), BIG));
+      push(d, ent(nu * vleaf.stride(), 0, nu * PV(0), 0, ct.begin(L, nu), (int)ct.size(L, nu), BIG), 0, nu);
   }
   upload_plan(pl);
 }

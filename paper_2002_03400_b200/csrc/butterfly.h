@@ -128,6 +128,10 @@ struct DevButterfly {
     std::vector<GemmEnt> h;
     DBuf<GemmEnt> d;
     L2Prefetch pf;  // its factor level, prefetched into L2 by the kernel before it
+    // block whose owner runs entry e in a process layout (layout.h):
+    // side (0 V, 1 U), level, and per entry (tau, nu)
+    int own_side = 0, own_level = 0;
+    std::vector<int64_t> own_tau, own_nu;
   };
   struct Plan {
     std::vector<StageDesc> st;
@@ -139,6 +143,36 @@ struct DevButterfly {
   void upload_plan(Plan& plan);
   void run_plan(Plan& plan, const cx<R>* x, int64_t ldx, cx<R>* y, int64_t ldy, int64_t k, cx<R>* buf0,
                 cx<R>* buf1);
+  // per (trans, layout, p): every stage's entries split by owner, and the
+  // block transfers feeding each stage (producer != consumer owner)
+  struct DistXfer {
+    int src = 0, dst = 0;
+    std::vector<int64_t> offs;  // producer output row offsets (M rows each)
+    DBuf<int64_t> d_offs;
+  };
+  struct DistPlan {
+    int trans = 0, kind = 0, p = 1;
+    std::vector<std::vector<std::vector<GemmEnt>>> h;  // [stage][rank]
+    std::vector<std::vector<DBuf<GemmEnt>>> d;         // [stage][rank]
+    std::vector<std::vector<DistXfer>> xfers;          // [stage]
+    double report[6] = {0, 0, 0, 0, 0, 0};
+  };
+  std::vector<std::unique_ptr<DistPlan>> dist_plans_;
+  DistPlan& dist_plan(int trans, int kind, int p);
+
+ public:
+  // Distributed apply over a process layout (dist.cu; reference
+  // inc/layout.hpp:139-261): p = ctx world size (one process per GPU, NCCL
+  // point-to-point exchanges), or p virtual processes run in turn on this GPU
+  // when the context has no communicator.  trans: OP_N or OP_H; x is the full
+  // input on every process, y the full output.  report[6]: exchange volume,
+  // exchange messages, all-to-all volume, all-to-all messages (reference
+  // counting, scalars per column and process), then the measured scalars
+  // per column received by the busiest process and by all processes.
+  void apply_layout(int trans, int kind, int p, const cx<R>* x, int64_t ldx, cx<R>* y, int64_t ldy, int64_t k,
+                    double* report);
+
+ private:
   // buf0/buf1: level coefficient buffers (NB*maxP*k each); null -> allocate
   void apply_n(const cx<R>* xt, int64_t ldx, cx<R>* yt, int64_t ldy, int64_t k, cx<R>* buf0 = nullptr,
                cx<R>* buf1 = nullptr);

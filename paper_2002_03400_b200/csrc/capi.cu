@@ -6,6 +6,7 @@
 
 #include "../../include/bfly_b200.h"
 #include "butterfly.h"
+#include "layout.h"
 #include "comm.h"
 #include "factorizer.h"
 #include "verify.h"
@@ -161,6 +162,25 @@ void bf_apply_t(bfly_bf* bf, DevButterfly<R>* b, int trans, const void* x, int64
   } else {
     d2h<R>(c, bf->scalar, dy.p, nout, k, y, ldy);
   }
+}
+
+template <typename R>
+void bf_apply_layout_t(bfly_bf* bf, DevButterfly<R>* b, int trans, int kind, int64_t p, const void* x, int64_t ldx,
+                       void* y, int64_t ldy, int64_t k, int on_device, double* report) {
+  Ctx* c = C_(bf->ctx);
+  const int64_t nin = trans == BFLY_N ? b->n() : b->m(), nout = trans == BFLY_N ? b->m() : b->n();
+  if (ldx < nin || ldy < nout) fail(DIMENSION, "apply_layout: leading dimension smaller than the row count");
+  if (p < 1 || p > (int64_t(1) << 30)) fail(PRECONDITION, "apply_layout: bad process count");
+  if (on_device) {
+    b->apply_layout(trans, kind, (int)p, static_cast<const cx<R>*>(x), ldx, static_cast<cx<R>*>(y), ldy, k, report);
+    c->sync();
+    return;
+  }
+  DBuf<cx<R>> dx(c, (size_t)(nin * std::max<int64_t>(k, 1))), dy(c, (size_t)(nout * std::max<int64_t>(k, 1)));
+  if (k > 0) h2d<R>(c, bf->scalar, x, ldx, dx.p, nin, k);
+  b->apply_layout(trans, kind, (int)p, dx.p, nin, dy.p, nout, k, report);
+  if (k > 0) d2h<R>(c, bf->scalar, dy.p, nout, k, y, ldy);
+  c->sync();
 }
 
 template <typename R>
@@ -604,6 +624,50 @@ int bfly_apply(bfly_bf* bf, int trans, const void* x, int64_t ldx, void* y, int6
     if (bf->z) bf_apply_t<double>(bf, bf->z.get(), trans, x, ldx, y, ldy, k, on_device);
     else bf_apply_t<float>(bf, bf->c.get(), trans, x, ldx, y, ldy, k, on_device);
   });
+}
+
+int bfly_apply_layout(bfly_bf* bf, int trans, int kind, int64_t processes, const void* x, int64_t ldx, void* y,
+                      int64_t ldy, int64_t k, int on_device, double* report) {
+  return guard(C_(bf->ctx), [&] {
+    if (bf->z) bf_apply_layout_t<double>(bf, bf->z.get(), trans, kind, processes, x, ldx, y, ldy, k, on_device, report);
+    else bf_apply_layout_t<float>(bf, bf->c.get(), trans, kind, processes, x, ldx, y, ldy, k, on_device, report);
+  });
+}
+
+int bfly_comm_cost(int kind, int levels, int64_t rank, int64_t processes, double* out) {
+  if (!layout_valid(kind, levels, rank, processes)) {
+    g_err = "comm_cost: invalid LayoutSpec (kind, levels >= 1, rank >= 1, power-of-two p <= 2^L)";
+    return BFLY_PRECONDITION;
+  }
+  const CommReport r = comm_cost(kind, levels, rank, processes);
+  if (out) {
+    out[0] = r.exchange_volume;
+    out[1] = (double)r.exchange_msgs;
+    out[2] = r.alltoall_volume;
+    out[3] = (double)r.alltoall_msgs;
+  }
+  return BFLY_OK;
+}
+
+int64_t bfly_layout_owners(int kind, int levels, int center, int64_t processes, int32_t* out) {
+  if (!layout_valid(kind, levels, 1, processes) || center < 0 || center > levels) {
+    g_err = "layout_owners: invalid layout";
+    return -BFLY_PRECONDITION;
+  }
+  const int L = levels, g = layout_log_p(processes);
+  const int64_t nb = int64_t(1) << L;
+  const int64_t len = (int64_t)(L + 3) * nb;
+  if (!out) return len;
+  int32_t* o = out;
+  for (int64_t tau = 0; tau < nb; ++tau) *o++ = layout_owner(kind, L, g, 1, L, tau, 0);  // u leaves
+  for (int64_t nu = 0; nu < nb; ++nu) *o++ = layout_owner(kind, L, g, 0, 0, 0, nu);      // v leaves
+  for (int l = center; l < L; ++l)                                                       // R levels
+    for (int64_t i = 0; i < nb; ++i) *o++ = layout_owner(kind, L, g, 1, l, i >> (L - l), i & ((int64_t(1) << (L - l)) - 1));
+  for (int l = 1; l <= center; ++l)                                                      // W levels
+    for (int64_t i = 0; i < nb; ++i) *o++ = layout_owner(kind, L, g, 0, l, i >> (L - l), i & ((int64_t(1) << (L - l)) - 1));
+  for (int64_t i = 0; i < nb; ++i)                                                       // centre cores
+    *o++ = layout_owner(kind, L, g, 0, center, i >> (L - center), i & ((int64_t(1) << (L - center)) - 1));
+  return len;
 }
 
 int bfly_bf_info(const bfly_bf* bf, int* levels, int* center, int64_t* m, int64_t* n, int64_t* nnz, int64_t* max_rank,

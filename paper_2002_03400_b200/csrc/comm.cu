@@ -21,6 +21,10 @@ struct NcclApi {
   ncclResult_t (*CommDestroy)(ncclComm_t) = nullptr;
   ncclResult_t (*AllGather)(const void*, void*, size_t, ncclDataType_t, ncclComm_t, cudaStream_t) = nullptr;
   ncclResult_t (*AllReduce)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*Send)(const void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*Recv)(void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*GroupStart)() = nullptr;
+  ncclResult_t (*GroupEnd)() = nullptr;
   const char* (*GetErrorString)(ncclResult_t) = nullptr;
 };
 
@@ -40,6 +44,10 @@ const NcclApi& nccl() {
   api.CommDestroy = reinterpret_cast<decltype(api.CommDestroy)>(sym("ncclCommDestroy"));
   api.AllGather = reinterpret_cast<decltype(api.AllGather)>(sym("ncclAllGather"));
   api.AllReduce = reinterpret_cast<decltype(api.AllReduce)>(sym("ncclAllReduce"));
+  api.Send = reinterpret_cast<decltype(api.Send)>(sym("ncclSend"));
+  api.Recv = reinterpret_cast<decltype(api.Recv)>(sym("ncclRecv"));
+  api.GroupStart = reinterpret_cast<decltype(api.GroupStart)>(sym("ncclGroupStart"));
+  api.GroupEnd = reinterpret_cast<decltype(api.GroupEnd)>(sym("ncclGroupEnd"));
   api.GetErrorString = reinterpret_cast<decltype(api.GetErrorString)>(sym("ncclGetErrorString"));
   loaded = true;
   return api;
@@ -94,6 +102,21 @@ void comm_allreduce_max_i32(Ctx* c, int32_t* buf, size_t count) {
 void comm_allreduce_sum_f64(Ctx* c, double* buf, size_t count) {
   if (c->world == 1 || !c->comm) return;
   nccl_check(nccl().AllReduce(buf, buf, count, ncclFloat64, ncclSum, c->comm, c->stream), "ncclAllReduce");
+}
+
+void comm_allreduce_sum_f32(Ctx* c, float* buf, size_t count) {
+  if (c->world == 1 || !c->comm) return;
+  nccl_check(nccl().AllReduce(buf, buf, count, ncclFloat32, ncclSum, c->comm, c->stream), "ncclAllReduce");
+}
+
+void comm_group_start() { nccl_check(nccl().GroupStart(), "ncclGroupStart"); }
+void comm_group_end() { nccl_check(nccl().GroupEnd(), "ncclGroupEnd"); }
+
+void comm_send(Ctx* c, const void* buf, size_t bytes, int peer) {
+  nccl_check(nccl().Send(buf, bytes, ncclUint8, peer, c->comm, c->stream), "ncclSend");
+}
+void comm_recv(Ctx* c, void* buf, size_t bytes, int peer) {
+  nccl_check(nccl().Recv(buf, bytes, ncclUint8, peer, c->comm, c->stream), "ncclRecv");
 }
 
 void comm_barrier(Ctx* c) {

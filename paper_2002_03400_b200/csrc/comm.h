@@ -16,6 +16,12 @@ void comm_destroy(Ctx* c);
 void comm_allgather_bytes(Ctx* c, const void* send, void* recv, size_t bytes_per_rank);
 void comm_allreduce_max_i32(Ctx* c, int32_t* buf, size_t count);
 void comm_allreduce_sum_f64(Ctx* c, double* buf, size_t count);
+void comm_allreduce_sum_f32(Ctx* c, float* buf, size_t count);
+// point-to-point (distributed apply exchanges), grouped between start/end
+void comm_group_start();
+void comm_group_end();
+void comm_send(Ctx* c, const void* buf, size_t bytes, int peer);
+void comm_recv(Ctx* c, void* buf, size_t bytes, int peer);
 void comm_barrier(Ctx* c);
 
 }  // namespace bfly

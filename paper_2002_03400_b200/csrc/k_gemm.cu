@@ -642,7 +642,7 @@ void launch_bgemm(Ctx* c, int op, int M, int K, int S, const cx<R>* A, int64_t l
     const size_t grp_smem = stage_smem;
     static const int epb_env = std::getenv("BFLY_STAGE_EPB") ? std::atoi(std::getenv("BFLY_STAGE_EPB")) : 0;
     int epb = wpe == 1 ? (epb_env > 0 ? std::min(epb_env, 8) : 4) : 1;
-    while (epb > 1 && epb * grp_smem > 200 * 1024) epb /= 2;
+    while (epb > 1 && epb * grp_smem > 100 * 1024) epb /= 2;
     cudaLaunchConfig_t cfg = {};
     cudaLaunchAttribute at[1];
     at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
@@ -658,7 +658,7 @@ void launch_bgemm(Ctx* c, int op, int M, int K, int S, const cx<R>* A, int64_t l
     auto kern = bgemm_stage_kernel<R, OPV, SV>;                                                             \
     static bool attr_set = false; /* first use is eager (never inside graph capture) */                    \
     if (!attr_set) {                                                                                        \
-      BFLY_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024));        \
+      BFLY_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));        \
       attr_set = true;                                                                                      \
     }                                                                                                       \
     BFLY_CUDA(cudaLaunchKernelEx(&cfg, kern, A, lda, B, ldb, C, ldc, M, K, ents, nent, (int)accumulate, kcols, wpe, pf)); \

@@ -17,6 +17,11 @@ Files
   probe_kat.npz  first 64 Gaussians of every probe-seed family (leaf, W, R,
                error probe) of config 2
   cpqr.npz     pivoted_qr_truncate (linalg.hpp:63-80): ranks and bases
+  layout.npz   process layouts (layout.hpp): comm_cost over a (kind, L, r, p)
+               grid + rejected specs; assign_ownership maps and
+               simulated_parallel_apply tallies on the reference's synthetic
+               butterflies (L=4, 6; r=8, seed=L as acceptance criterion 6) and
+               on the config-0 n=1024 factorization
   cfg_*.npz    factorize (reconstruct.hpp:412-419) on small BASELINE configs and
                the reference's synthetic butterfly: rank profile of every
                block, per-phase bookkeeping, butterfly apply / adjoint apply
@@ -172,9 +177,55 @@ def make_configs():
         save_factorization(f"synth_L{L}_r{r}_s{seed}", inp, op, bf, L, seed + 1000)
 
 
+def make_layout():
+    d = {}
+    grid, vals, bad = [], [], []
+    for kind in (0, 1, 2):
+        for L in range(1, 7):
+            for r in (1, 2, 8):
+                for p in [1 << g for g in range(L + 1)] + [3, 1 << (L + 1)]:
+                    try:
+                        v = R.comm_cost(kind, L, r, p)
+                    except RuntimeError:
+                        bad.append((kind, L, r, p))
+                        continue
+                    grid.append((kind, L, r, p))
+                    vals.append(v)
+    d["cc_spec"] = np.array(grid, np.int64)
+    d["cc_val"] = np.array(vals)
+    d["cc_bad"] = np.array(bad, np.int64)
+    for L in (4, 6):
+        specs, tall, own = [], [], []
+        for kind in (0, 1, 2):
+            for g in range(L + 1):
+                t, o = R.layout_synth(L, 8, L, kind, 1 << g)
+                specs.append((kind, 1 << g))
+                tall.append(t)
+                own.append(o)
+        d[f"synth{L}_spec"] = np.array(specs, np.int64)
+        d[f"synth{L}_tally"] = np.array(tall)
+        d[f"synth{L}_owners"] = np.array(own, np.int32)
+    inp, op = config_inputs(0, 1024)
+    bf = R.factorize(op, inp["tol"], inp["r0"], inp["L"], seed=0, threads=8)
+    specs, tall, own = [], [], []
+    for kind in (0, 1, 2):
+        for g in range(inp["L"] + 1):
+            t, o = bf.layout(inp["L"], kind, 1 << g)
+            specs.append((kind, 1 << g))
+            tall.append(t)
+            own.append(o)
+    d["cfg0_spec"] = np.array(specs, np.int64)
+    d["cfg0_tally"] = np.array(tall)
+    d["cfg0_owners"] = np.array(own, np.int32)
+    d["cfg0_L"] = inp["L"]
+    np.savez_compressed(os.path.join(HERE, "layout.npz"), **d)
+    print("layout", len(grid), "comm_cost cells,", len(bad), "rejected")
+
+
 if __name__ == "__main__":
     assert R.available(), "build oracle/_ref first (make -C oracle/ref)"
     make_rng()
     make_probe_kats()
     make_cpqr()
     make_configs()
+    make_layout()

@@ -190,6 +190,9 @@ def test_gpu_factorization_golden(B, path):
     assert got == _phase_tuples(d["phases"])
     assert rel_err(bf.apply(d["probe_x"]), d["apply_n"]) < APPLY_TOL
     assert rel_err(bf.apply_adjoint(d["probe_y"]), d["apply_h"]) < APPLY_TOL
+    for k in (1, 2):  # narrow column counts take the per-stage kernel with several blocks per CTA
+        assert rel_err(bf.apply(d["probe_x"][:, :k]), d["apply_n"][:, :k]) < APPLY_TOL
+        assert rel_err(bf.apply_adjoint(d["probe_y"][:, :k]), d["apply_h"][:, :k]) < APPLY_TOL
     est = B.estimate_error(op, bf, 16, 3)
     assert abs(est - float(d["estimate_error"])) <= 1e-5 * float(d["estimate_error"]) + 1e-14
 
