@@ -35,9 +35,9 @@ METRIC = "butterfly construction GFLOP/s at n=65536 complex128 (config 2)"
 FP64_PEAK_TFLOPS = 36.99  # measured DMMA m8n8k4 f64 on this pool (profiles/r01_fp64_peaks.txt)
 INT8_PEAK_TOPS = 4248.7  # measured tcgen05 kind::i8 M128 N256 from shared memory (profiles/r01_tc_i8.txt)
 # dram__bytes_read.sum + dram__bytes_write.sum of one K2 launch (the 9th of a config-2 construction: 32
-# probe segments x 32 columns, profiles/r01_matvec_oz_ncu.txt): 69.2 MB read + 1015.8 MB write (= the
+# probe segments x 32 columns, profiles/r01_matvec_oz_ncu.txt): 65.7 MB read + 1015.6 MB write (= the
 # 1.07 GB product it writes); its algorithmic traffic (points + probes in, product out) is 1.11 GB
-K2_DRAM_BYTES_PER_LAUNCH = 1085056142
+K2_DRAM_BYTES_PER_LAUNCH = 1081262992
 CFG_ID = 2
 
 
@@ -254,16 +254,22 @@ def run_ours(args):
     host_out = torch.empty(bf.serialized_size() + (1 << 20), dtype=torch.uint8, pin_memory=True)
     barrier()
     te0 = time.perf_counter()
+    e2e_split = []
     for _ in range(e2e_steps):
+        t0 = time.perf_counter()
         h = C.c_void_p()
         B.api.check(B.api.lib().bfly_op_kernel(ctx.h, B.api.OP_CIRCLE, op.rows, op.cols,
                                                C.c_void_p(pts_t.data_ptr()), C.c_void_p(pts_s.data_ptr()), kappa,
                                                B.api.COMPLEX128, C.byref(h)))
         op_e = B.api.BlackBoxOperator(h, ctx, B.api.COMPLEX128)
         bf_e, log_e = B.factorize(op_e, rt, ct, rc)
+        t1 = time.perf_counter()
         if rank == 0 or not sharded:
             blob = bf_e.serialize(out=host_out.numpy())  # every factor block back on the host
             d2h = len(blob)
+        t2 = time.perf_counter()
+        e2e_split.append((round(t1 - t0, 4), round(t2 - t1, 4)))
+        del bf_e, op_e  # the result now lives on the host; free its device copy before the next job
     barrier()
     te = (time.perf_counter() - te0) / e2e_steps
     e2e_val = (fl.item() / args.steps) / te / 1e9  # whole-job flops of one construction
@@ -320,7 +326,8 @@ def run_ours(args):
             "kernels": {k: {"launches": v["launches"], "ms_per_step": round(v["ms"] / args.steps, 3)}
                         for k, v in kernels.items()},
             "e2e": {"value": round(e2e_val, 3), "unit": "GFLOP/s", "h2d_bytes_per_step": int(h2d),
-                    "d2h_bytes_per_step": int(d2h), "seconds_per_step": round(te, 4)},
+                    "d2h_bytes_per_step": int(d2h), "seconds_per_step": round(te, 4),
+                    "steps_s": e2e_split},
             "gpu_launches": int(launches),
             "clocks": clk,
         }

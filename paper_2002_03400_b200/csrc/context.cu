@@ -117,9 +117,14 @@ bool Ctx::take_oz_overflow() {
 // chunks fragment, and a multi-GB level buffer that fits none of them maps
 // new physical memory mid-factorization (hundreds of ms to seconds).
 void Ctx::reserve_pool(size_t bytes) {
-  if (bytes <= pool_reserved) return;
+  // enough free reserved memory already (results the caller still holds
+  // count as used, so a kept butterfly does not eat the next one's room)
+  uint64_t used = 0, reserved = 0;
+  cudaMemPoolGetAttribute(pool, cudaMemPoolAttrUsedMemCurrent, &used);
+  cudaMemPoolGetAttribute(pool, cudaMemPoolAttrReservedMemCurrent, &reserved);
+  if (bytes == 0 || reserved >= used + bytes) return;
   BFLY_CUDA(cudaStreamSynchronize(stream));
-  BFLY_CUDA(cudaMemPoolTrimTo(pool, 0));
+  BFLY_CUDA(cudaMemPoolTrimTo(pool, 0));  // drop free chunks; live allocations stay
   void* q = nullptr;
   if (cudaMallocFromPoolAsync(&q, bytes, pool, stream) == cudaSuccess) {
     BFLY_CUDA(cudaFreeAsync(q, stream));
