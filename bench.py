@@ -220,7 +220,7 @@ def run_ours(args):
 
     # ----------------------------------------------- apply bandwidth (device)
     apply = {}
-    for k in ((1, 16) if rank == 0 else ()):
+    for k in ((1, 2, 16) if rank == 0 else ()):
         x = torch.randn((k, op.cols), dtype=torch.complex128, device="cuda").t()
         y = torch.empty((k, op.rows), dtype=torch.complex128, device="cuda").t()
         for _ in range(3):
