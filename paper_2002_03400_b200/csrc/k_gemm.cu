@@ -4,6 +4,7 @@
 // Every output block is C_e = sum_{s<S} op(A_s) B_s with uniform padded
 // shapes per launch (zero padding contributes exact zeros).  One CTA computes
 // a 32 x 32 tile of one block; A and B tiles are staged through shared memory.
+#include <climits>
 #include <cstdlib>
 #include <type_traits>
 
@@ -385,11 +386,7 @@ __global__ void __launch_bounds__(256) bgemm_stage_kernel(const cx<R>* __restric
   STAGE_TRACE(slot, 9);
 }
 
-// Large-k complex128 path on DMMA (mma.sync m8n8k4 f64): one CTA = 8 warps
-// (4 along rows x 2 along columns) computes all M <= 64 rows of one output
-// block for a 64-column slab; op(A_s) and B_s chunks of 16 along K are staged
-// in shared memory (A k-major planes, stride 8*MT*4+8; B column-major planes,
-// stride 20 -> conflict-free fragments).  Complex MAC = 4 real DMMAs.
+// DMMA fragment helper (mma.sync m8n8k4 f64).
 __device__ __forceinline__ void dmma884(double& d0, double& d1, double a, double b) {
   asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
                : "+d"(d0), "+d"(d1)
@@ -493,14 +490,29 @@ __global__ void __launch_bounds__(256) bgemm_dmma_warp_kernel(const double2* __r
   }
 }
 
-template <int OP, int S, int MT>
-__global__ void __launch_bounds__(256) bgemm_dmma_kernel(const double2* __restrict__ A, int64_t lda,
-                                                         const double2* __restrict__ B, int64_t ldb,
-                                                         double2* __restrict__ C, int64_t ldc, int M, int K,
-                                                         const GemmEnt* __restrict__ ents, int accumulate,
-                                                         int ncols_all) {
-  constexpr int BM = 32 * MT, BN = 64, BK = 16, SA = BM + 8, SB = BK + 4, NT = 4;
-  __shared__ __align__(16) double Are[BK * SA], Aim[BK * SA], Bre[BN * SB], Bim[BN * SB];
+// Large-k complex128 path on DMMA (mma.sync m8n8k4 f64): one CTA = 4 x WN
+// warps computes all M <= 32 MT rows of one output block for a column slab of
+// BN = 8 NT WN columns (picked per launch to minimise padded columns: 66
+// probe columns run as one 72-wide slab).  op(A_s) and B_s chunks of 16
+// along K stream through a 2-stage cp.async ring as raw complex values
+// (16-byte granules, zero-filled out of range), the next chunk in flight
+// while the current one feeds the DMMAs.  Shared layouts keep fragment reads
+// conflict-free: OP_N A [k][m] with pitch = 2 mod 8 granules, OP_T/H A [m][k]
+// and B [col][k] with pitch = 4 mod 8.  Complex MAC = 4 real DMMAs.
+template <int OP, int S, int MT, int WN, int NT>
+__global__ void __launch_bounds__(128 * WN) bgemm_dmma_kernel(const double2* __restrict__ A, int64_t lda,
+                                                              const double2* __restrict__ B, int64_t ldb,
+                                                              double2* __restrict__ C, int64_t ldc, int M, int K,
+                                                              const GemmEnt* __restrict__ ents, int accumulate,
+                                                              int ncols_all) {
+  constexpr int BM = 32 * MT, BN = 8 * NT * WN, BK = 16, NTHR = 128 * WN;
+  constexpr int PA = OP == OP_N ? BM + 2 : BK + 4;  // A pitch (granules)
+  constexpr int AEL = OP == OP_N ? BK * PA : BM * PA;
+  constexpr int PB = BK + 4;
+  constexpr int BEL = BN * PB;
+  extern __shared__ __align__(16) double2 dsm_[];
+  double2(*As)[AEL] = reinterpret_cast<double2(*)[AEL]>(dsm_);
+  double2(*Bs)[BEL] = reinterpret_cast<double2(*)[BEL]>(dsm_ + 2 * AEL);
   asm volatile("griddepcontrol.launch_dependents;");  // see bgemm_dmma_warp_kernel
   const GemmEnt e = ents[blockIdx.x];
   asm volatile("griddepcontrol.wait;" ::: "memory");
@@ -510,82 +522,89 @@ __global__ void __launch_bounds__(256) bgemm_dmma_kernel(const double2* __restri
   if (n0 >= ncols) return;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int g = lane >> 2, t = lane & 3;
-  const int wm = warp & 3, wn = warp >> 2;  // 4 x 2 warps
+  const int wm = warp & 3, wn = warp >> 2;  // 4 x WN warps
+  const int kch = (K + BK - 1) / BK, nch = S * kch;
+  auto cp16 = [](double2* dst, const double2* src, bool ok) {
+    const uint32_t d = (uint32_t)__cvta_generic_to_shared(dst);
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(d), "l"(src), "r"(ok ? 16 : 0) : "memory");
+  };
+  auto load_chunk = [&](int c, int buf) {
+    const int s = c / kch, k0 = (c % kch) * BK;
+    const double2* Ab = A + (s == 0 ? e.a0 : e.a1);
+    const double2* Bb = B + (s == 0 ? e.b0 : e.b1);
+    for (int idx = tid; idx < BM * BK; idx += NTHR) {
+      int m, kk;
+      if (OP == OP_N) {
+        m = idx % BM;
+        kk = idx / BM;
+      } else {
+        kk = idx % BK;
+        m = idx / BK;
+      }
+      const int gk = k0 + kk;
+      const bool ok = m < M && gk < K;
+      const double2* src = ok ? (OP == OP_N ? Ab + m + (int64_t)gk * lda : Ab + gk + (int64_t)m * lda) : Ab;
+      cp16(&As[buf][OP == OP_N ? kk * PA + m : m * PA + kk], src, ok);
+    }
+    for (int idx = tid; idx < BK * BN; idx += NTHR) {
+      const int kk = idx % BK, cc = idx / BK;
+      const int gk = k0 + kk, gc = n0 + cc;
+      const bool ok = gk < Ke && gc < ncols;
+      cp16(&Bs[buf][cc * PB + kk], ok ? Bb + gk + (int64_t)gc * ldb : Bb, ok);
+    }
+    asm volatile("cp.async.commit_group;" ::: "memory");
+  };
   double acc[MT][NT][2][2];
 #pragma unroll
   for (int a = 0; a < MT; ++a)
 #pragma unroll
     for (int b = 0; b < NT; ++b) acc[a][b][0][0] = acc[a][b][0][1] = acc[a][b][1][0] = acc[a][b][1][1] = 0.0;
+  load_chunk(0, 0);
+  for (int c = 0; c < nch; ++c) {
+    const int buf = c & 1;
+    if (c + 1 < nch) {
+      load_chunk(c + 1, buf ^ 1);
+      asm volatile("cp.async.wait_group 1;" ::: "memory");
+    } else {
+      asm volatile("cp.async.wait_group 0;" ::: "memory");
+    }
+    __syncthreads();
+    const double2* as = As[buf];
+    const double2* bs = Bs[buf];
 #pragma unroll
-  for (int s = 0; s < S; ++s) {
-    const double2* Ab = A + (s == 0 ? e.a0 : e.a1);
-    const double2* Bb = B + (s == 0 ? e.b0 : e.b1);
-    for (int k0 = 0; k0 < K; k0 += BK) {
-      // op(A) chunk: rows m < BM, k in [k0, k0+BK)
-      for (int idx = tid; idx < BM * BK; idx += 256) {
-        int m, kk;
-        if (OP == OP_N) {
-          m = idx % BM;
-          kk = idx / BM;
-        } else {
-          kk = idx % BK;
-          m = idx / BK;
-        }
-        double2 v = make_double2(0.0, 0.0);
-        const int gk = k0 + kk;
-        if (m < M && gk < K) {
-          if (OP == OP_N) v = Ab[m + (int64_t)gk * lda];
-          else {
-            v = Ab[gk + (int64_t)m * lda];
-            if (OP == OP_H) v.y = -v.y;
-          }
-        }
-        Are[kk * SA + m] = v.x;
-        Aim[kk * SA + m] = v.y;
+    for (int ks = 0; ks < BK; ks += 4) {
+      double ar[MT], ai[MT], br[NT], bi[NT];
+#pragma unroll
+      for (int a = 0; a < MT; ++a) {
+        const int row = wm * 8 * MT + a * 8 + g;
+        const double2 v = OP == OP_N ? as[(ks + t) * PA + row] : as[row * PA + ks + t];
+        ar[a] = v.x;
+        ai[a] = OP == OP_H ? -v.y : v.y;
       }
-      for (int idx = tid; idx < BK * BN; idx += 256) {
-        const int kk = idx % BK, cc = idx / BK;
-        const int gk = k0 + kk, gc = n0 + cc;
-        double2 v = make_double2(0.0, 0.0);
-        if (gk < Ke && gc < ncols) v = Bb[gk + (int64_t)gc * ldb];
-        Bre[cc * SB + kk] = v.x;
-        Bim[cc * SB + kk] = v.y;
+#pragma unroll
+      for (int b = 0; b < NT; ++b) {
+        const double2 v = bs[(wn * 8 * NT + b * 8 + g) * PB + ks + t];
+        br[b] = v.x;
+        bi[b] = v.y;
       }
-      __syncthreads();
 #pragma unroll
-      for (int ks = 0; ks < BK; ks += 4) {
-        double ar[MT], ai[MT], br[NT], bi[NT];
-#pragma unroll
-        for (int a = 0; a < MT; ++a) {
-          const int row = wm * 8 * MT + a * 8 + g;
-          ar[a] = Are[(ks + t) * SA + row];
-          ai[a] = Aim[(ks + t) * SA + row];
-        }
+      for (int a = 0; a < MT; ++a)
 #pragma unroll
         for (int b = 0; b < NT; ++b) {
-          const int col = wn * 32 + b * 8 + g;
-          br[b] = Bre[col * SB + ks + t];
-          bi[b] = Bim[col * SB + ks + t];
+          dmma884(acc[a][b][0][0], acc[a][b][0][1], ar[a], br[b]);
+          dmma884(acc[a][b][1][0], acc[a][b][1][1], ar[a], bi[b]);
         }
 #pragma unroll
-        for (int a = 0; a < MT; ++a)
+      for (int a = 0; a < MT; ++a) {
+        const double nai = -ai[a];
 #pragma unroll
-          for (int b = 0; b < NT; ++b) {
-            dmma884(acc[a][b][0][0], acc[a][b][0][1], ar[a], br[b]);
-            dmma884(acc[a][b][1][0], acc[a][b][1][1], ar[a], bi[b]);
-          }
-#pragma unroll
-        for (int a = 0; a < MT; ++a) {
-          const double nai = -ai[a];
-#pragma unroll
-          for (int b = 0; b < NT; ++b) {
-            dmma884(acc[a][b][0][0], acc[a][b][0][1], nai, bi[b]);
-            dmma884(acc[a][b][1][0], acc[a][b][1][1], ai[a], br[b]);
-          }
+        for (int b = 0; b < NT; ++b) {
+          dmma884(acc[a][b][0][0], acc[a][b][0][1], nai, bi[b]);
+          dmma884(acc[a][b][1][0], acc[a][b][1][1], ai[a], br[b]);
         }
       }
-      __syncthreads();
     }
+    __syncthreads();  // the buffer is refilled by the next iteration's prefetch
   }
   double2* Cb = C + e.c;
 #pragma unroll
@@ -596,7 +615,7 @@ __global__ void __launch_bounds__(256) bgemm_dmma_kernel(const double2* __restri
     for (int b = 0; b < NT; ++b)
 #pragma unroll
       for (int v = 0; v < 2; ++v) {
-        const int gc = n0 + wn * 32 + b * 8 + 2 * t + v;
+        const int gc = n0 + wn * 8 * NT + b * 8 + 2 * t + v;
         if (gc >= ncols) continue;
         double2* p = Cb + m + (int64_t)gc * ldc;
         double2 r = make_double2(acc[a][b][0][v], acc[a][b][1][v]);
@@ -604,6 +623,28 @@ __global__ void __launch_bounds__(256) bgemm_dmma_kernel(const double2* __restri
         *p = r;
       }
   }
+}
+
+// dynamic shared memory of bgemm_dmma_kernel: 2-stage A and B rings
+constexpr size_t dmma_smem_bytes(int op, int mt, int wn, int nt) {
+  return 16 * 2 *
+         ((size_t)(op == OP_N ? 16 * (32 * mt + 2) : 32 * mt * 20) + (size_t)8 * nt * wn * 20);
+}
+
+template <typename... KArgs, typename... Args>
+void launch_pdl_smem(void (*kern)(KArgs...), dim3 grid, int block, int smem, cudaStream_t stream, bool pdl,
+                     Args... args) {
+  cudaLaunchConfig_t cfg = {};
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.gridDim = grid;
+  cfg.blockDim = dim3(block);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = stream;
+  cfg.attrs = pdl ? at : nullptr;
+  cfg.numAttrs = pdl ? 1 : 0;
+  BFLY_CUDA(cudaLaunchKernelEx(&cfg, kern, static_cast<KArgs>(args)...));
 }
 
 // kernel launch with the programmatic-stream-serialization attribute when pdl
@@ -743,7 +784,20 @@ void launch_bgemm(Ctx* c, int op, int M, int K, int S, const cx<R>* A, int64_t l
       return;
     }
     if (!no_dmma && dmma_cols && M <= 64 && K > 0) {
-      const unsigned gy = (unsigned)ceil_div(max_ncols, 64);
+      // column slab: the (WN, NT) shape with the fewest padded columns
+      static const int shapes[4][2] = {{2, 4}, {3, 3}, {2, 3}, {3, 4}};
+      int best = 0;
+      int64_t best_cols = INT64_MAX;
+      for (int i = 0; i < 4; ++i) {
+        const int bn = 8 * shapes[i][0] * shapes[i][1];
+        const int64_t cols = ceil_div((int64_t)max_ncols, (int64_t)bn) * bn;
+        if (cols < best_cols || (cols == best_cols && bn > 8 * shapes[best][0] * shapes[best][1])) {
+          best = i;
+          best_cols = cols;
+        }
+      }
+      const int WNv = shapes[best][0], NTv = shapes[best][1], BNv = 8 * WNv * NTv;
+      const unsigned gy = (unsigned)ceil_div(max_ncols, BNv);
       if (gy > 65535) fail(PRECONDITION, "bgemm: grid too large");
       dim3 grid(nent, gy);
       static const char* names[3][2][2] = {{{"bgemm_dmma_N1_m32", "bgemm_dmma_N1_m64"}, {"bgemm_dmma_N2_m32", "bgemm_dmma_N2_m64"}},
@@ -751,9 +805,27 @@ void launch_bgemm(Ctx* c, int op, int M, int K, int S, const cx<R>* A, int64_t l
                                            {{"bgemm_dmma_H1_m32", "bgemm_dmma_H1_m64"}, {"bgemm_dmma_H2_m32", "bgemm_dmma_H2_m64"}}};
       KTimer timer(c, names[op][S - 1][M > 32], 8.0 * M * K * S * (double)nent * kcols,
                    sizeof(cx<R>) * ((double)nent * S * (M * (double)K + K * kcols) + (double)nent * M * kcols));
-#define BD(OPV, SV, MTV)                                                                                  \
-  launch_pdl(bgemm_dmma_kernel<OPV, SV, MTV>, grid, 256, c->stream, pdl, A, lda, B, ldb, C, ldc, M, K, ents, accumulate, \
-                                                                 ncols_all)
+#define BDS(OPV, SV, MTV, WNV, NTV)                                                                             \
+  do {                                                                                                          \
+    auto kern = bgemm_dmma_kernel<OPV, SV, MTV, WNV, NTV>;                                                      \
+    const int smem = (int)dmma_smem_bytes(OPV, MTV, WNV, NTV);                                                  \
+    static bool attr_set = false; /* first use is eager (never inside graph capture) */                        \
+    if (!attr_set) {                                                                                            \
+      BFLY_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));                  \
+      attr_set = true;                                                                                          \
+    }                                                                                                           \
+    launch_pdl_smem(kern, grid, 128 * WNV, smem, c->stream, pdl, A, lda, B, ldb, C, ldc, M, K, ents, accumulate, \
+                    ncols_all);                                                                                 \
+  } while (0)
+#define BD(OPV, SV, MTV)                         \
+  do {                                           \
+    switch (best) {                              \
+      case 0: BDS(OPV, SV, MTV, 2, 4); break;    \
+      case 1: BDS(OPV, SV, MTV, 3, 3); break;    \
+      case 2: BDS(OPV, SV, MTV, 2, 3); break;    \
+      default: BDS(OPV, SV, MTV, 3, 4); break;   \
+    }                                            \
+  } while (0)
 #define BD_OP(SV, MTV)                   \
   do {                                   \
     if (op == OP_N) BD(OP_N, SV, MTV);   \
@@ -769,6 +841,7 @@ void launch_bgemm(Ctx* c, int op, int M, int K, int S, const cx<R>* A, int64_t l
       }
 #undef BD_OP
 #undef BD
+#undef BDS
       BFLY_LAUNCH_CHECK("bgemm_dmma");
       return;
     }
