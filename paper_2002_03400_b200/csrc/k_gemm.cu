@@ -235,7 +235,17 @@ __host__ __device__ __forceinline__ int64_t stage_group_elems(int op, int M, int
   return (int64_t)S * ((int64_t)(op == OP_N ? K : M) * stage_pitch(op, M, K) + (int64_t)K * ncols);
 }
 
-template <typename R, int OP, int S>
+__device__ __forceinline__ void dmma884(double& d0, double& d1, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+               : "+d"(d0), "+d"(d1)
+               : "d"(a), "d"(b));
+}
+
+// DM = true (complex128, 8..32 columns): after the same staging, the warps of
+// the group tile the output block in 8 x 8 DMMA tiles (m8n8k4 f64 fragments
+// read from the shared-memory image; complex MAC = 4 real DMMAs, two
+// interleaved accumulator sets per tile).
+template <typename R, int OP, int S, bool DM = false>
 __global__ void __launch_bounds__(256) bgemm_stage_kernel(const cx<R>* __restrict__ A, int64_t lda,
                                                           const cx<R>* __restrict__ B, int64_t ldb,
                                                           cx<R>* __restrict__ C, int64_t ldc, int M, int K,
@@ -249,7 +259,8 @@ __global__ void __launch_bounds__(256) bgemm_stage_kernel(const cx<R>* __restric
   const int grp = threadIdx.x / gthreads, t = threadIdx.x % gthreads;
   const int64_t ei = (int64_t)blockIdx.x * (blockDim.x / gthreads) + grp;
   if (ei >= nent) return;
-  const int64_t gbytes = 16 + stage_group_elems(OP, M, K, S, ncols) * (int64_t)sizeof(V);
+  // DM groups stage only the factor image (B fragments go to registers)
+  const int64_t gbytes = 16 + stage_group_elems(OP, M, K, S, DM ? 0 : ncols) * (int64_t)sizeof(V);
   unsigned char* gbase = smem_raw + grp * gbytes;
   const uint32_t bar = (uint32_t)__cvta_generic_to_shared(gbase);
   V* As = reinterpret_cast<V*>(gbase + 16);
@@ -306,7 +317,7 @@ __global__ void __launch_bounds__(256) bgemm_stage_kernel(const cx<R>* __restric
   STAGE_TRACE(slot, 4);
   STAGE_TRACE(slot, 7);
 #pragma unroll
-  for (int s = 0; s < S; ++s) {
+  for (int s = 0; s < (DM ? 0 : S); ++s) {
     const V* Bb = B + (s == 0 ? e.b0 : e.b1);
     V* bs = Bs + s * ncols * K;
     for (int idx = t; idx < K * ncols; idx += gthreads) {
@@ -322,6 +333,57 @@ __global__ void __launch_bounds__(256) bgemm_stage_kernel(const cx<R>* __restric
   else __syncthreads();  // multi-warp groups run one per CTA
   STAGE_TRACE(slot, 11);
   STAGE_TRACE(slot, 12);
+  if constexpr (DM) {
+    // B fragments straight from L2 (the previous stage's output; .cg: never a
+    // stale L1 line), 8 k-steps per batch of loads
+    const int lane = t & 31, gq = lane >> 2, tq = lane & 3;
+    const int mt = (Me + 7) / 8, ntiles = mt * ((ncols + 7) / 8);
+    for (int tile = t >> 5; tile < ntiles; tile += gthreads >> 5) {
+      const int m = (tile % mt) * 8 + gq, n = (tile / mt) * 8 + gq;
+      double acc[2][2][2] = {};  // [set][re|im][2]
+#pragma unroll
+      for (int s = 0; s < S; ++s) {
+        const V* as = As + s * aelems;
+        const V* Bb = B + (s == 0 ? e.b0 : e.b1) + (int64_t)n * ldb;
+        for (int kc = 0; kc < K; kc += 32) {
+          V bf[8];
+#pragma unroll
+          for (int u = 0; u < 8; ++u) {
+            const int k = kc + 4 * u + tq;
+            bf[u] = (n < ncols && k < Ke) ? __ldcg(Bb + k) : mkc<R>(0, 0);
+          }
+#pragma unroll
+          for (int u = 0; u < 8; ++u) {
+            const int k = kc + 4 * u + tq;
+            if (kc + 4 * u >= K) break;
+            V a = mkc<R>(0, 0);
+            if (m < M && k < K) {
+              a = OP == OP_N ? as[k * cpitch + m] : as[m * cpitch + k];
+              if (OP == OP_H) a.y = -a.y;
+            }
+            const V b = bf[u];
+            const int st = u & 1;
+            dmma884(acc[st][0][0], acc[st][0][1], a.x, b.x);
+            dmma884(acc[st][1][0], acc[st][1][1], a.x, b.y);
+            dmma884(acc[st][0][0], acc[st][0][1], -a.y, b.y);
+            dmma884(acc[st][1][0], acc[st][1][1], a.y, b.x);
+          }
+        }
+      }
+      if (m < Me) {
+#pragma unroll
+        for (int v = 0; v < 2; ++v) {
+          const int col = (tile / mt) * 8 + 2 * tq + v;
+          if (col >= ncols) continue;
+          V r = mkc<R>(acc[0][0][v] + acc[1][0][v], acc[0][1][v] + acc[1][1][v]);
+          V* p = C + e.c + m + (int64_t)col * ldc;
+          *p = accumulate ? cadd(*p, r) : r;
+        }
+      }
+    }
+    STAGE_TRACE(slot, 9);
+    return;
+  }
   // Q lanes per output (power of two, Q * outputs <= threads of the group).
   // The K split is across the HIGH lane bits (part = lane / (32/Q)), so a
   // quarter-warp reads 8 consecutive outputs of one kk: distinct bank groups
@@ -386,12 +448,6 @@ __global__ void __launch_bounds__(256) bgemm_stage_kernel(const cx<R>* __restric
   STAGE_TRACE(slot, 9);
 }
 
-// DMMA fragment helper (mma.sync m8n8k4 f64).
-__device__ __forceinline__ void dmma884(double& d0, double& d1, double a, double b) {
-  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
-               : "+d"(d0), "+d"(d1)
-               : "d"(a), "d"(b));
-}
 
 // Narrow entries (M <= 16 rows, <= 32 columns: the U/V chain projections of
 // one probe, ~10^5 entries per launch): one WARP per entry, m8n8k4 DMMA
@@ -672,14 +728,22 @@ void launch_bgemm(Ctx* c, int op, int M, int K, int S, const cx<R>* A, int64_t l
   const int kcols = ncols_all > 0 ? ncols_all : max_ncols;
   const size_t small_smem = sizeof(cx<R>) * (size_t)S * ((size_t)K * (M + 1) + (size_t)K * kcols);
   static const bool no_stage = std::getenv("BFLY_NO_STAGE_GEMM") != nullptr;
-  const size_t stage_smem = 16 + sizeof(cx<R>) * (size_t)stage_group_elems(op, M, K, S, kcols);
   static const int dmma_mink = std::getenv("BFLY_DMMA_MINK") ? std::atoi(std::getenv("BFLY_DMMA_MINK")) : 8;
   const bool dmma_cols = std::is_same<R, double>::value && kcols >= dmma_mink;
-  if (pdl && !no_stage && !dmma_cols && ncols_all > 0 && kcols <= 16 && K > 0 && stage_smem <= 96 * 1024) {
+  // complex128 with 8..32 columns: the same staged kernel with DMMA tiles
+  // (factor image only in shared memory)
+  const bool stage_dm = dmma_cols && kcols <= 32;
+  const size_t stage_smem = 16 + sizeof(cx<R>) * (size_t)stage_group_elems(op, M, K, S, stage_dm ? 0 : kcols);
+  if (pdl && !no_stage && (dmma_cols ? stage_dm : kcols <= 16) && ncols_all > 0 && K > 0 &&
+      stage_smem <= 96 * 1024) {
     KTimer timer(c, "bgemm_stage", 8.0 * M * K * S * (double)nent * kcols,
                  sizeof(cx<R>) * ((double)nent * S * (M * (double)K + K * kcols) + (double)nent * M * kcols));
     static const int wpe_env = std::getenv("BFLY_STAGE_WPE") ? std::atoi(std::getenv("BFLY_STAGE_WPE")) : 0;
-    const int wpe = wpe_env > 0 ? std::min(wpe_env, 8) : kcols <= 2 ? 1 : kcols <= 8 ? 2 : 4;
+    // DMMA groups: 2 warps up to 16 columns, 4 beyond (measured on the
+    // config-2 apply: fewer threads per entry keep ~2 stage grids resident)
+    const int wpe = wpe_env > 0 ? std::min(wpe_env, 8)
+                    : stage_dm ? (kcols <= 16 ? 2 : 4)
+                    : kcols <= 2 ? 1 : kcols <= 8 ? 2 : 4;
     const size_t grp_smem = stage_smem;
     static const int epb_env = std::getenv("BFLY_STAGE_EPB") ? std::atoi(std::getenv("BFLY_STAGE_EPB")) : 0;
     int epb = wpe == 1 ? (epb_env > 0 ? std::min(epb_env, 8) : 4) : 1;
@@ -696,11 +760,13 @@ void launch_bgemm(Ctx* c, int op, int M, int K, int S, const cx<R>* A, int64_t l
     cfg.numAttrs = 1;
 #define BST(OPV, SV)                                                                                        \
   do {                                                                                                      \
-    auto kern = bgemm_stage_kernel<R, OPV, SV>;                                                             \
-    static bool attr_set = false; /* first use is eager (never inside graph capture) */                    \
-    if (!attr_set) {                                                                                        \
+    auto kern = bgemm_stage_kernel<R, OPV, SV, false>;                                                      \
+    if constexpr (std::is_same<R, double>::value)                                                           \
+      if (stage_dm) kern = bgemm_stage_kernel<R, OPV, SV, true>;                                            \
+    static bool attr_set[2] = {false, false}; /* first use is eager (never inside graph capture) */        \
+    if (!attr_set[stage_dm]) {                                                                              \
       BFLY_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));        \
-      attr_set = true;                                                                                      \
+      attr_set[stage_dm] = true;                                                                            \
     }                                                                                                       \
     BFLY_CUDA(cudaLaunchKernelEx(&cfg, kern, A, lda, B, ldb, C, ldc, M, K, ents, nent, (int)accumulate, kcols, wpe, pf)); \
   } while (0)
