@@ -17,6 +17,7 @@
 
 #include "../../include/bfly_b200.h"
 #include "butterfly.h"
+#include "shard.h"
 #include "operators.h"
 
 namespace bfly {
@@ -55,13 +56,18 @@ class Factorizer {
   void end_phase(bfly_phase& st, clock::time_point t0, int64_t f0, int64_t tr0);
   void note_probe_bytes(double scalars, int64_t probes);
   void run_leaf_phase(const char* name, bool row_side);
+  // orange[p]: output rows probe p needs ([o0, o1) in tree order of the
+  // output side); counted[p]: its columns go into the operator counters (a
+  // probe split across ranks is counted by the rank holding its first piece)
   void probe_products(int mode, const Tree& probe_tree, int level, const std::vector<int64_t>& nodes,
                       const std::vector<int>& widths, const std::vector<int64_t>& col0, const std::vector<int64_t>& goff,
-                      const V* G, int64_t wtot, DBuf<V>& Y);
-  // W level: probes tau in [t0, t1)
-  void w_probes(int l, const std::vector<int>& width, int64_t t0, int64_t t1, int maxw);
-  // R level: probes nu in [n0, n1)
-  void r_probes(int l, const std::vector<int>& width, int64_t n0, int64_t n1, int maxw, int32_t* err_flag);
+                      const V* G, int64_t wtot, DBuf<V>& Y, const std::vector<std::pair<int64_t, int64_t>>& orange,
+                      const std::vector<char>& counted);
+  // W level: probe pieces (tau, partner nodes nu in [p0, p1)) of one rank
+  void w_probes(int l, const std::vector<int>& width, const std::vector<ProbePiece>& pieces, int maxw);
+  // R level: probe pieces (nu, partner nodes tau in [p0, p1)) of one rank
+  void r_probes(int l, const std::vector<int>& width, const std::vector<ProbePiece>& pieces, int maxw,
+                int32_t* err_flag);
   // in-place all-gather of `per_rank` consecutive blocks per rank (+ ranks)
   void gather_inplace(Level<R>& lv, int64_t per_rank);
   // pack/all-gather/unpack of block index lists (one list per rank)

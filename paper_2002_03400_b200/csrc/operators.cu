@@ -26,6 +26,7 @@ template <typename R>
 struct KernelOp : DevOp<R> {
   DBuf<double> tx, ty, tz, sx, sy, sz;
   double kappa = 0;
+  bool restricts_rows() const override { return true; }
   void do_apply(int mode, const cx<R>* X, const std::vector<MatvecSeg>& segs, cx<R>* Y, int64_t ldy, int64_t o0,
                 int64_t o1) override {
     Points tp{tx.p, ty.p, tz.p}, sp{sx.p, sy.p, sz.p};
@@ -47,6 +48,7 @@ struct KernelOp : DevOp<R> {
 template <typename R>
 struct DenseOp : DevOp<R> {
   DBuf<cx<R>> a;  // m x n column major
+  bool restricts_rows() const override { return true; }
   void do_apply(int mode, const cx<R>* X, const std::vector<MatvecSeg>& segs, cx<R>* Y, int64_t ldy, int64_t o0,
                 int64_t o1) override {
     Ctx* c = this->ctx;

@@ -32,6 +32,9 @@ struct DevOp {
   double flops = 0, evals = 0;  // algorithmic work of every product so far
 
   virtual ~DevOp() = default;
+  // true when do_apply computes only the requested output rows (work and
+  // counted flops proportional to them)
+  virtual bool restricts_rows() const { return false; }
   int64_t in_dim(int mode) const { return mode == OP_N ? n : m; }
   int64_t out_dim(int mode) const { return mode == OP_N ? m : n; }
 
@@ -39,10 +42,12 @@ struct DevOp {
   // adjoint, derived exactly as apply_adjoint in the reference).
   // [o0, o1) restricts the output rows that must be produced (the rank's
   // leaves in a sharded leaf phase); kinds that cannot restrict compute all.
+  // count_cols >= 0 overrides the columns added to the counters
   void apply_segs(int mode, const cx<R>* X, const std::vector<MatvecSeg>& segs, cx<R>* Y, int64_t ldy,
-                  int64_t o0 = 0, int64_t o1 = -1) {
+                  int64_t o0 = 0, int64_t o1 = -1, int64_t count_cols = -1) {
     int64_t cols = 0;
     for (const auto& s : segs) cols += s.ncols;
+    if (count_cols >= 0) cols = count_cols;
     if (mode == OP_N) fwd += cols;
     else tr += cols;
     if (o1 < 0) o1 = out_dim(mode);

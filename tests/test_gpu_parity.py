@@ -264,11 +264,13 @@ def _torch_apply(at, trans, x, ldx, y, ldy, k, stream):
     return 0
 
 
-@pytest.mark.parametrize("cfg_id,n,vr", [(0, 2048, 2), (0, 2048, 3), (2, 4096, 8), (4, 4096, 4), (1, 1024, 5)])
+@pytest.mark.parametrize("cfg_id,n,vr", [(0, 2048, 2), (0, 2048, 3), (2, 4096, 8), (4, 4096, 4), (1, 1024, 5),
+                                        (3, 1024, 4), (2, 4096, 6)])
 def test_virtual_ranks_match_single_gpu(B, cfg_id, n, vr):
-    """The rank-sharded schedule (leaf rows, W probes in place, R/B blocks
-    packed -> gathered -> unpacked) executed for `vr` ranks in one process
-    reproduces the single-GPU factorization."""
+    """The rank-sharded schedule (leaf rows, W blocks in place, R/B blocks
+    packed -> gathered -> unpacked; levels with fewer probes than ranks split
+    a probe's partner nodes, i.e. its output rows) executed for `vr` ranks in
+    one process reproduces the single-GPU factorization."""
     import dataclasses
 
     w = B.configs.build(cfg_id, n)

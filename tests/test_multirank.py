@@ -5,7 +5,9 @@ host-only entry points) which blocks they produce at every level, exchange
 the lists over torch.distributed, and check the properties the device-side
 exchange relies on: the per-rank lists partition every level exactly once,
 leaf/W chunks are contiguous and start at rank * per_rank (the in-place
-ncclAllGather layout), and R chunks are whole column probes.  The same plan
+ncclAllGather layout), and R chunks are contiguous ranges of the nu-major
+block order -- equal chunks at every level, so a level with fewer probes
+than ranks splits a probe's partner nodes instead of idling ranks.  The same plan
 drives tests/test_gpu_parity.py::test_virtual_ranks_match_single_gpu.
 """
 import os
@@ -54,19 +56,22 @@ def _worker(rank, world, port, L, q):
             flat = [b for g in gathered for b in g]
             if sorted(flat) != list(range(nb)):
                 errors.append(f"level {l} side {side}: not a partition")
-            units = nb if side == 0 else (1 << l if side == 1 else 1 << (L - l))
-            per_unit = 1 if side == 0 else (nb // units)
-            per_rank = -(-units // world) * per_unit
+            # every level: equal contiguous chunks of the 2^L blocks (levels with
+            # fewer probes than ranks split a probe's partner nodes)
+            per_rank = -(-nb // world)
             if side in (0, 1):
                 for r, g in enumerate(gathered):
                     if g and (g != list(range(r * per_rank, r * per_rank + len(g)))):
                         errors.append(f"level {l} side {side} rank {r}: chunk not contiguous at r*per_rank")
             else:
-                nnu = 1 << (L - l)
+                # nu-major order u = nu * 2^l + tau: contiguous unit ranges
+                nnu, ntau = 1 << (L - l), 1 << l
                 for r, g in enumerate(gathered):
-                    cols = {b % nnu for b in g}
-                    if len(g) != len(cols) * (nb // nnu):
-                        errors.append(f"level {l} rank {r}: R chunk is not whole column probes")
+                    units = [(b % nnu) * ntau + b // nnu for b in g]
+                    if g and units != list(range(r * per_rank, r * per_rank + len(g))):
+                        errors.append(f"level {l} rank {r}: R chunk is not a nu-major unit range")
+            if max(len(g) for g in gathered) - min(len(g) for g in gathered) > per_rank:
+                errors.append(f"level {l} side {side}: unbalanced chunks")
         # the all-gather itself: every rank ends with every rank's blocks
         import torch
 
