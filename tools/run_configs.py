@@ -16,10 +16,11 @@ def main():
     ap.add_argument("--n", type=int, default=0)
     ap.add_argument("--reps", type=int, default=2)
     ap.add_argument("--profile", action="store_true")
+    ap.add_argument("--c64", action="store_true", help="complex64 operators")
     a = ap.parse_args()
     for c in a.cfg:
         t0 = time.time()
-        w = B.configs.build(c, a.n or None)
+        w = B.configs.build(c, a.n or None, scalar=B.COMPLEX64 if a.c64 else B.COMPLEX128)
         t1 = time.time()
         for r in range(a.reps):
             if a.profile and r == a.reps - 1:
