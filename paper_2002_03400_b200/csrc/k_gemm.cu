@@ -681,6 +681,119 @@ __global__ void __launch_bounds__(128 * WN) bgemm_dmma_kernel(const double2* __r
   }
 }
 
+// complex64 batched GEMM on the FP32 pipe (the recompression at complex64):
+// CTA tile 16 TI x 16 TJ complex outputs (TI, TJ in {2, 4}, picked per launch
+// for the least padding), 256 threads with TI x TJ outputs each
+// (rows ty + 16 i, columns tx + 16 j: broadcast A reads, conflict-free B
+// reads), K chunks of 16 through a 2-stage cp.async ring of raw complex
+// values (8-byte granules, zero-filled out of range; op(A) conjugated in
+// registers).  Complex MAC = 4 FFMA.
+template <int OP, int S, int TI, int TJ>
+__global__ void __launch_bounds__(256) bgemm_f32_kernel(const float2* __restrict__ A, int64_t lda,
+                                                        const float2* __restrict__ B, int64_t ldb,
+                                                        float2* __restrict__ C, int64_t ldc, int M, int K,
+                                                        const GemmEnt* __restrict__ ents, int accumulate,
+                                                        int ncols_all) {
+  constexpr int BM = 16 * TI, BN = 16 * TJ, BK = 16;
+  // +1 pitch: the transposed 8-byte fills (consecutive k in consecutive
+  // threads) land in distinct banks
+  __shared__ __align__(16) float2 As[2][BK][BM + 1], Bs[2][BK][BN + 1];
+  const GemmEnt e = ents[blockIdx.x];
+  const int ncols = ncols_all > 0 ? ncols_all : e.ncols;
+  const int Me = min(M, e.mrows), Ke = min(K, e.krows);
+  const int n0 = blockIdx.y * BN, m0 = blockIdx.z * BM;
+  if (n0 >= ncols || m0 >= Me) return;
+  const int tid = threadIdx.x, tx = tid & 15, ty = tid >> 4;
+  const int kch = (K + BK - 1) / BK, nch = S * kch;
+  auto cp8 = [](float2* dst, const float2* src, bool ok) {
+    const uint32_t d = (uint32_t)__cvta_generic_to_shared(dst);
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;" ::"r"(d), "l"(src), "r"(ok ? 8 : 0) : "memory");
+  };
+  auto load_chunk = [&](int c, int buf) {
+    const int s = c / kch, k0 = (c % kch) * BK;
+    const float2* Ab = A + (s == 0 ? e.a0 : e.a1);
+    const float2* Bb = B + (s == 0 ? e.b0 : e.b1);
+#pragma unroll
+    for (int q = 0; q < (BM * BK + 255) / 256; ++q) {
+      const int idx = tid + q * 256;
+      if (idx >= BM * BK) break;
+      int m, kk;
+      if (OP == OP_N) {
+        m = idx % BM;
+        kk = idx / BM;
+      } else {
+        kk = idx % BK;
+        m = idx / BK;
+      }
+      const int gm = m0 + m, gk = k0 + kk;
+      const bool ok = gm < M && gk < K;
+      cp8(&As[buf][kk][m], ok ? (OP == OP_N ? Ab + gm + (int64_t)gk * lda : Ab + gk + (int64_t)gm * lda) : Ab, ok);
+    }
+#pragma unroll
+    for (int q = 0; q < (BK * BN + 255) / 256; ++q) {
+      const int idx = tid + q * 256;
+      if (idx >= BK * BN) break;
+      const int kk = idx % BK, cc = idx / BK;
+      const int gk = k0 + kk, gc = n0 + cc;
+      const bool ok = gk < Ke && gc < ncols;
+      cp8(&Bs[buf][kk][cc], ok ? Bb + gk + (int64_t)gc * ldb : Bb, ok);
+    }
+    asm volatile("cp.async.commit_group;" ::: "memory");
+  };
+  float acc[TI][TJ][2];
+#pragma unroll
+  for (int i = 0; i < TI; ++i)
+#pragma unroll
+    for (int j = 0; j < TJ; ++j) acc[i][j][0] = acc[i][j][1] = 0.f;
+  load_chunk(0, 0);
+  for (int c = 0; c < nch; ++c) {
+    const int buf = c & 1;
+    if (c + 1 < nch) {
+      load_chunk(c + 1, buf ^ 1);
+      asm volatile("cp.async.wait_group 1;" ::: "memory");
+    } else {
+      asm volatile("cp.async.wait_group 0;" ::: "memory");
+    }
+    __syncthreads();
+#pragma unroll
+    for (int kk = 0; kk < BK; ++kk) {
+      float2 a[TI], b[TJ];
+#pragma unroll
+      for (int i = 0; i < TI; ++i) {
+        a[i] = As[buf][kk][ty + 16 * i];
+        if (OP == OP_H) a[i].y = -a[i].y;
+      }
+#pragma unroll
+      for (int j = 0; j < TJ; ++j) b[j] = Bs[buf][kk][tx + 16 * j];
+#pragma unroll
+      for (int i = 0; i < TI; ++i)
+#pragma unroll
+        for (int j = 0; j < TJ; ++j) {
+          acc[i][j][0] = fmaf(a[i].x, b[j].x, acc[i][j][0]);
+          acc[i][j][0] = fmaf(-a[i].y, b[j].y, acc[i][j][0]);
+          acc[i][j][1] = fmaf(a[i].x, b[j].y, acc[i][j][1]);
+          acc[i][j][1] = fmaf(a[i].y, b[j].x, acc[i][j][1]);
+        }
+    }
+    __syncthreads();  // the buffer is refilled by the next iteration's prefetch
+  }
+  float2* Cb = C + e.c;
+#pragma unroll
+  for (int i = 0; i < TI; ++i) {
+    const int m = m0 + ty + 16 * i;
+    if (m >= Me) continue;
+#pragma unroll
+    for (int j = 0; j < TJ; ++j) {
+      const int gc = n0 + tx + 16 * j;
+      if (gc >= ncols) continue;
+      float2* p = Cb + m + (int64_t)gc * ldc;
+      float2 r = make_float2(acc[i][j][0], acc[i][j][1]);
+      if (accumulate) r = make_float2(p->x + r.x, p->y + r.y);
+      *p = r;
+    }
+  }
+}
+
 // dynamic shared memory of bgemm_dmma_kernel: 2-stage A and B rings
 constexpr size_t dmma_smem_bytes(int op, int mt, int wn, int nt) {
   return 16 * 2 *
@@ -909,6 +1022,55 @@ void launch_bgemm(Ctx* c, int op, int M, int K, int S, const cx<R>* A, int64_t l
 #undef BD
 #undef BDS
       BFLY_LAUNCH_CHECK("bgemm_dmma");
+      return;
+    }
+  }
+  if constexpr (std::is_same<R, float>::value) {
+    static const bool no_f32 = std::getenv("BFLY_NO_F32_GEMM") != nullptr;
+    if (!no_f32 && K > 0) {
+      // tile shape with the least padded output area (ties: the larger tile)
+      static const int f32_env = std::getenv("BFLY_F32_TILE") ? std::atoi(std::getenv("BFLY_F32_TILE")) : -1;
+      int best = 0;
+      int64_t best_area = INT64_MAX;
+      for (int i = 0; i < 4; ++i) {
+        const int bm = 32 << (i >> 1), bn = 32 << (i & 1);
+        const int64_t area = ceil_div((int64_t)M, (int64_t)bm) * bm * ceil_div((int64_t)max_ncols, (int64_t)bn) * bn;
+        if (area < best_area || (area == best_area)) {
+          best = i;
+          best_area = area;
+        }
+      }
+      if (f32_env >= 0 && f32_env < 4) best = f32_env;
+      const int BMv = 32 << (best >> 1), BNv = 32 << (best & 1);
+      dim3 grid(nent, (unsigned)ceil_div(max_ncols, BNv), (unsigned)ceil_div(M, BMv));
+      if (grid.y > 65535 || grid.z > 65535) fail(PRECONDITION, "bgemm: grid too large");
+      const double nc = ncols_all > 0 ? ncols_all : max_ncols;
+      KTimer timer(c, "bgemm_f32", 8.0 * M * K * S * (double)nent * nc,
+                   sizeof(cx<R>) * ((double)nent * S * (M * (double)K + K * nc) + (double)nent * M * nc));
+#define BFT(OPV, SV, TIV, TJV)                                                                          \
+  bgemm_f32_kernel<OPV, SV, TIV, TJV><<<grid, 256, 0, c->stream>>>(A, lda, B, ldb, C, ldc, M, K, ents, \
+                                                                   (int)accumulate, ncols_all)
+#define BF(OPV, SV)                          \
+  do {                                       \
+    switch (best) {                          \
+      case 0: BFT(OPV, SV, 2, 2); break;     \
+      case 1: BFT(OPV, SV, 2, 4); break;     \
+      case 2: BFT(OPV, SV, 4, 2); break;     \
+      default: BFT(OPV, SV, 4, 4); break;    \
+    }                                        \
+  } while (0)
+      if (S == 1) {
+        if (op == OP_N) BF(OP_N, 1);
+        else if (op == OP_T) BF(OP_T, 1);
+        else BF(OP_H, 1);
+      } else {
+        if (op == OP_N) BF(OP_N, 2);
+        else if (op == OP_T) BF(OP_T, 2);
+        else BF(OP_H, 2);
+      }
+#undef BF
+#undef BFT
+      BFLY_LAUNCH_CHECK("bgemm_f32");
       return;
     }
   }
