@@ -76,3 +76,25 @@ def oracle_config(cfg_id, n, seed=0):
 
 def rel_err(a, b):
     return float(np.linalg.norm(a - b) / max(np.linalg.norm(b), 1e-300))
+
+
+def oracle_points(cfg_id, n):
+    """Tree-ordered (targets, sources, kernel kind, kappa) of a kernel config,
+    through the oracle's generators (configs 0-2)."""
+    if cfg_id == 0:
+        L = O.depth_for(n, 32)
+        x, _ = _tree_order(_uniform(n, 0, 1, 0.0, 1.0), L, 1)
+        xi, _ = _tree_order(_uniform(n, 0, 2, -n / 2.0, n / 2.0), L, 1)
+        return x, xi, O.OP_NUFFT, 0.0
+    if cfg_id == 1:
+        side = int(round(math.sqrt(n)))
+        L = O.depth_for(n, 32)
+        t, _ = _tree_order(_plate(side, 0.0), L, 3)
+        s, _ = _tree_order(_plate(side, 2.0), L, 3)
+        return t, s, O.OP_PLATES, 2.0 * math.pi / (10.0 * (1.0 / side))
+    if cfg_id == 2:
+        L = O.depth_for(n, 32)
+        t, _ = _tree_order(_half_circle(n, True), L, 2)
+        s, _ = _tree_order(_half_circle(n, False), L, 2)
+        return t, s, O.OP_CIRCLE, 2.0 * n / 10.0
+    raise ValueError(cfg_id)
