@@ -38,6 +38,9 @@ INT8_PEAK_TOPS = 4248.7  # measured tcgen05 kind::i8 M128 N256 from shared memor
 # probe segments x 32 columns, profiles/r01_matvec_oz_ncu.txt): 65.7 MB read + 1015.6 MB write (= the
 # 1.07 GB product it writes); its algorithmic traffic (points + probes in, product out) is 1.11 GB
 K2_DRAM_BYTES_PER_LAUNCH = 1081262992
+# the same capture: FP64 pipe 37.4 % + int8 tensor pipe 37.9 % busy; on B200 both run on one shared
+# datapath (sm__pipe_shared_cycles_active 75.3 %), the utilisation that bounds K2
+K2_PIPES = {"fp64": 0.374, "tensor_int8": 0.379, "shared_datapath": 0.753}
 CFG_ID = 2
 
 
@@ -302,6 +305,10 @@ def run_ours(args):
         roofline["int8"] = {"achieved_tops": round(tops, 1), "peak_tops": INT8_PEAK_TOPS,
                             "frac": round(tops / INT8_PEAK_TOPS, 4),
                             "peak_source": "measured tcgen05 kind::i8 M128 N256 (tools/microbench/tc_i8.cu)"}
+    roofline["pipes_busy"] = dict(K2_PIPES, source="ncu --set full sm__pipe_*_cycles_active, one config-2 "
+                                                   "transfer-level launch (profiles/r01_matvec_oz_ncu.txt); FP64 "
+                                                   "and int8 tensor ops time-share one datapath "
+                                                   "(profiles/r01_tc_i8.txt overlap test)")
 
     if rank == 0:
         line = {
