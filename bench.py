@@ -339,7 +339,8 @@ def run_ours(args):
             "clocks": clk,
         }
         if world == 1 and not args.no_cpu:
-            v, dt, threads, kind, sample = cpu_sample(probes=args.ref_probes)
+            # a bounded sample of ~10-30 s of CPU work (two reference-arm steps)
+            v, dt, threads, kind, sample = cpu_sample(probes=2 * args.ref_probes)
             line["cpu_baseline"] = {"value": round(v, 3), "unit": "GFLOP/s", "cores": threads, "kind": kind,
                                     "sample": sample, "seconds": round(dt, 2)}
         print(json.dumps(line), flush=True)
