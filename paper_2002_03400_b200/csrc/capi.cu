@@ -64,7 +64,6 @@ Ctx* C_(bfly_ctx* c) { return c ? c->c.get() : nullptr; }
 void check_scalar(int s) {
   if (s != BFLY_Z && s != BFLY_C && s != BFLY_D) fail(PRECONDITION, "unknown scalar type");
 }
-size_t host_elem(int scalar) { return scalar == BFLY_Z ? 16 : (scalar == BFLY_C ? 8 : 8); }
 
 // host (user scalar layout) <-> device (internal storage) column-major copies
 template <typename R>

@@ -274,7 +274,8 @@ __global__ void __launch_bounds__(256) bgemm_stage_kernel(const cx<R>* __restric
     asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p), "r"((uint32_t)(pf.len & ~int64_t(15)))
                  : "memory");
   }
-  const int slot = e.pad_ & 63;
+  const int slot = e.pad_ & 63;  // stage index (BFLY_STAGE_TRACE instrumentation)
+  (void)slot;
   STAGE_TRACE(slot, 0);
   STAGE_TRACE(slot, 3);
   // op(A_s) columns: OP_N copies the K stored columns (M entries each), the

@@ -158,9 +158,6 @@ __device__ __forceinline__ void mma_i8(uint32_t d, uint64_t da, uint64_t db, uin
 __device__ __forceinline__ void mbar_init(uint32_t bar, uint32_t count) {
   asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(bar), "r"(count));
 }
-__device__ __forceinline__ void mbar_arrive(uint32_t bar) {
-  asm volatile("mbarrier.arrive.release.cta.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");
-}
 __device__ __forceinline__ void mbar_expect_tx(uint32_t bar, uint32_t bytes) {
   asm volatile("mbarrier.arrive.expect_tx.release.cta.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes)
                : "memory");
@@ -192,7 +189,6 @@ __device__ unsigned long long g_oz_trace[8];
 #define OZT_BEGIN(v)
 #define OZT_END(v, slot)
 #endif
-__device__ __forceinline__ void eval_bar() { asm volatile("bar.sync 1, %0;" ::"n"(OZ_EWARPS * 32) : "memory"); }
 
 __device__ __forceinline__ void tmem_ld16(uint32_t addr, uint32_t (&v)[16]) {
   asm volatile(
@@ -206,22 +202,6 @@ __device__ __forceinline__ void tmem_ld4(uint32_t addr, uint32_t (&v)[4]) {
                : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3])
                : "r"(addr));
 }
-// wait with back-off: the MMA thread shares its scheduler with evaluation warps
-__device__ __forceinline__ void mbar_wait_sleep(uint32_t bar, uint32_t parity) {
-  uint32_t done = 0;
-  while (true) {
-    asm volatile(
-        "{\n\t.reg .pred p;\n\t"
-        "mbarrier.try_wait.parity.acquire.cta.shared::cta.b64 p, [%1], %2;\n\t"
-        "selp.u32 %0, 1, 0, p;\n\t}\n"
-        : "=r"(done)
-        : "r"(bar), "r"(parity)
-        : "memory");
-    if (done) return;
-    __nanosleep(100);
-  }
-}
-
 // exact int32 -> double (magic-number bias: one LOP + one DADD)
 __device__ __forceinline__ double i2d(uint32_t v) {
   return __hiloint2double(0x43300000, (int)(v ^ 0x80000000u)) - 4503601774854144.0;  // 2^52 + 2^31

@@ -252,7 +252,7 @@ __global__ void __launch_bounds__(QR_THREADS) core_fit_kernel(const cx<R>* __res
   using V = cx<R>;
   const CoreEnt e = ents[blockIdx.x];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int ku = e.ku, kv = e.kv, w = e.w, r = e.r1 + e.r2;
+  const int ku = e.ku, kv = e.kv, w = e.w;
   V* out = B + e.b;
   // zero the whole block first (padding stays zero)
   for (int64_t i = threadIdx.x; i < ldb * bcap; i += QR_THREADS) out[i] = mkc<R>(0, 0);
