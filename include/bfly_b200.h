@@ -252,6 +252,11 @@ BFLY_API void bfly_bf_destroy(bfly_bf* bf);
  * 1 W level (row probes), 2 R level (column probes)); returns the count. */
 BFLY_API int bfly_shard_chunk(int64_t n, int world, int rank, int64_t* begin, int64_t* end);
 BFLY_API int64_t bfly_shard_blocks(int levels, int level, int side, int world, int rank, int64_t* out);
+/* Diagnostics for a scaling projection: device milliseconds of every rank's
+ * share of every phase of the last factorization run with virtual_ranks > 1
+ * and BFLY_VRANK_TIMING=1 (row-major, virtual_ranks entries per phase, phases
+ * in log order); returns the entry count, copies up to cap entries. */
+BFLY_API int64_t bfly_vrank_times(double* out, int64_t cap);
 
 /* ------------------------------------------------------------- dense helpers */
 /* gaussian_matrix (linalg.hpp:16-25) generated on the device, copied to host */

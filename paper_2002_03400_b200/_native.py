@@ -145,6 +145,7 @@ def lib():
         "bfly_seed_mix": (u64, [u64, i32, p]),
         "bfly_cpqr_truncate": (i32, [p, i64, i64, p, dbl, p, C.POINTER(C.c_int64)]),
         "bfly_pinv": (i32, [p, i64, i64, p, dbl, p]),
+        "bfly_vrank_times": (i64, [p, i64]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(L, name)

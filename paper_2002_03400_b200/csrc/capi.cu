@@ -865,4 +865,9 @@ int64_t bfly_shard_blocks(int levels, int level, int side, int world, int rank, 
   if (out) std::copy(v.begin(), v.end(), out);
   return (int64_t)v.size();
 }
+int64_t bfly_vrank_times(double* out, int64_t cap) {
+  const std::vector<double>& t = vrank_table();
+  if (out) std::copy(t.begin(), t.begin() + std::min<int64_t>(cap, (int64_t)t.size()), out);
+  return (int64_t)t.size();
+}
 }

@@ -22,6 +22,10 @@
 
 namespace bfly {
 
+// per-(phase, rank) device milliseconds of the last virtual-rank factorization
+// run with BFLY_VRANK_TIMING=1 (row-major, world entries per phase)
+std::vector<double>& vrank_table();
+
 template <typename R>
 class Factorizer {
  public:
@@ -49,6 +53,21 @@ class Factorizer {
   // sharding
   int world_ = 1, rank_ = 0;
   bool virtual_ = false;
+
+  // per-(phase, virtual rank) device time of each rank's share
+  // (BFLY_VRANK_TIMING=1 with virtual ranks; diagnostics for a scaling
+  // projection, see vrank_table())
+  bool vr_timing_ = false;
+  struct VrTimer {
+    Factorizer* f;
+    int rank;
+    cudaEvent_t a = nullptr, b = nullptr;
+    VrTimer(Factorizer* f_, int r);
+    ~VrTimer();
+  };
+  std::vector<std::pair<cudaEvent_t, cudaEvent_t>> vr_events_;
+  std::vector<int> vr_rank_;
+  void vr_flush(int phase);  // accumulate the phase's rank timings into the table
 
   std::vector<int> my_ranks() const;
   static std::pair<int64_t, int64_t> chunk(int64_t n, int world, int r);
