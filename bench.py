@@ -244,6 +244,24 @@ def run_ours(args):
         apply[f"k{k}"] = {"ms": round(ms, 4), "GB/s": round(nbytes / (ms / 1e3) / 1e9, 1),
                           "frac_of_hbm": round(nbytes / (ms / 1e3) / 1e9 / 6554.9, 3)}
 
+    # ------------------------------- the other full-size configs (info only)
+    # config 4 (recompression, n = 262144: the north-star scaling config) and
+    # config 1 (3D plates, n = 16384): one warm-up + median of 3 constructions
+    other = {}
+    if rank == 0 and world == 1 and not args.no_extra:
+        for cid in (4, 1):
+            wx = B.configs.build(cid, ctx=ctx)
+            ts_x = []
+            for i in range(4):
+                l2_flush()
+                bx, lx = B.factorize(wx.op, wx.row_tree, wx.col_tree, wx.recon)
+                if i:
+                    ts_x.append(lx.total_seconds)
+            med = statistics.median(ts_x)
+            other[wx.name] = {"construct_s": round(med, 4), "GFLOP/s": round(lx.flops / med / 1e9, 1),
+                              "max_rank": bx.max_rank(), "nnz": bx.nnz()}
+            del bx, wx
+
     # --------------------------------------------------- e2e (host buffers)
     import ctypes as C
 
@@ -330,6 +348,7 @@ def run_ours(args):
             "max_rank": bf.max_rank(), "nnz": bf.nnz(),
             "roofline": roofline,
             "apply": apply,
+            "other_configs": other,
             "kernels": {k: {"launches": v["launches"], "ms_per_step": round(v["ms"] / args.steps, 3)}
                         for k, v in kernels.items()},
             "e2e": {"value": round(e2e_val, 3), "unit": "GFLOP/s", "h2d_bytes_per_step": int(h2d),
@@ -359,6 +378,7 @@ def main():
     ap.add_argument("--n", type=int, default=0, help="override n (testing only)")
     ap.add_argument("--ref-probes", type=int, default=8)
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-extra", action="store_true", help="skip the other full-size configs (info only)")
     ap.add_argument("--mode", default="shard", choices=["shard", "replica"], help="N > 1 schedule")
     args = ap.parse_args()
     if args.impl == "reference":
