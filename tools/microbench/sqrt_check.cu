@@ -49,6 +49,22 @@ __device__ __forceinline__ double sqrt_rcp_k2(double x, double& h) {
   return r;
 }
 
+// candidate (rejected): one coupled step, then an h-only Newton step against s1,
+// Markstein on s1 -- r stays correctly rounded but h inherits s1's 2^-40 error
+__device__ __forceinline__ double sqrt_rcp_h2(double x, double& h) {
+  double y;
+  asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
+  double s = x * y;
+  h = 0.5 * y;
+  double e = fma(-s, h, 0.5);
+  s = fma(s, e, s);
+  h = fma(h, e, h);
+  e = fma(-s, h, 0.5);
+  h = fma(h, e + e, h);
+  const double d = fma(-s, s, x);
+  return fma(d, h, s);
+}
+
 template <int ITERS>
 __global__ void check(uint64_t seed, int64_t n, unsigned long long* bad, double* maxrel, double* seedrel) {
   double mr = 0, sr = 0;
@@ -59,7 +75,7 @@ __global__ void check(uint64_t seed, int64_t n, unsigned long long* bad, double*
     const int ex = (int)((r >> 52) % 401) - 200;
     const double x = __longlong_as_double((long long)((r & 0xFFFFFFFFFFFFFull) | ((uint64_t)(1023 + ex) << 52)));
     double h;
-    const double s = ITERS == 0 ? sqrt_rcp_k2(x, h) : sqrt_rcp<ITERS>(x, h);
+    const double s = ITERS == 0 ? sqrt_rcp_k2(x, h) : ITERS < 0 ? sqrt_rcp_h2(x, h) : sqrt_rcp<ITERS>(x, h);
     const double ref = __dsqrt_rn(x);
     if (__double_as_longlong(s) != __double_as_longlong(ref)) ++b;
     const double inv = 1.0 / ref;
@@ -96,6 +112,7 @@ int main() {
   const int64_t n = 1LL << 33;  // 8.6e9 samples
   const int b2 = run<2>(n);
   run<1>(n);
-  run<0>(n);  // "iters 0" = the 1-step + Markstein + h-refine variant
+  run<0>(n);   // "iters 0" = the 1-step + Markstein + h-refine variant
+  run<-1>(n);  // "iters -1" = coupled step + h-only Newton step (e doubled) + Markstein
   return b2;
 }
