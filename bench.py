@@ -35,12 +35,12 @@ METRIC = "butterfly construction GFLOP/s at n=65536 complex128 (config 2)"
 FP64_PEAK_TFLOPS = 36.99  # measured DMMA m8n8k4 f64 on this pool (profiles/r01_fp64_peaks.txt)
 INT8_PEAK_TOPS = 4248.7  # measured tcgen05 kind::i8 M128 N256 from shared memory (profiles/r01_tc_i8.txt)
 # dram__bytes_read.sum + dram__bytes_write.sum of one K2 launch (the 9th of a config-2 construction: 32
-# probe segments x 32 columns, profiles/r01_matvec_oz_ncu.txt): 65.7 MB read + 1015.6 MB write (= the
+# probe segments x 32 columns, profiles/r01_matvec_oz_ncu.txt): 64.9 MB read + 1018.2 MB write (= the
 # 1.07 GB product it writes); its algorithmic traffic (points + probes in, product out) is 1.11 GB
-K2_DRAM_BYTES_PER_LAUNCH = 1081262992
-# the same capture: FP64 pipe 37.4 % + int8 tensor pipe 37.9 % busy; on B200 both run on one shared
-# datapath (sm__pipe_shared_cycles_active 75.3 %), the utilisation that bounds K2
-K2_PIPES = {"fp64": 0.374, "tensor_int8": 0.379, "shared_datapath": 0.753}
+K2_DRAM_BYTES_PER_LAUNCH = 1083077840
+# the same capture: FP64 pipe 36.7 % + int8 tensor pipe 38.3 % busy; on B200 both run on one shared
+# datapath (sm__pipe_shared_cycles_active 75.1 %), the utilisation that bounds K2
+K2_PIPES = {"fp64": 0.367, "tensor_int8": 0.383, "shared_datapath": 0.751}
 CFG_ID = 2
 
 
