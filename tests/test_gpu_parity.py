@@ -388,3 +388,33 @@ def test_serialize_into_caller_buffer_matches_oracle_layout(B, real):
     assert bytes(o.serialize()) == ref
     x = O.gaussian_matrix(256, 3, 4, real=real)
     assert rel_err(a.apply(x), o.apply(x)) < 1e-13
+
+
+def test_rank_cap_and_rectangular_operator(B, oracle_threads):
+    """Edge cases of the adaptive loop against the oracle: a hard rank cap that
+    stops the leaf doubling (reconstruct.hpp:389-393, rank_capped set) and a
+    rectangular operator (m != n, row and column trees of different sizes)."""
+    m, n = 768, 1024
+    x = np.zeros((m, 3))
+    xi = np.zeros((n, 3))
+    O.lib().bo_points_uniform(m, 7, 1, 0.0, 1.0, O._ptr(x))
+    O.lib().bo_points_uniform(n, 7, 2, -n / 2.0, n / 2.0, O._ptr(xi))
+    L = 4
+    for cap in (-1, 8):
+        rt_o = O.PartitionTree.build(x[:, :1], L)
+        ct_o = O.PartitionTree.build(xi[:, :1], L)
+        op_o = O.kernel_operator(O.OP_NUFFT, x, xi)
+        cfg = dict(levels=L, tolerance=1e-6, rank_guess=4, oversampling=2, seed=3, hard_cap=cap,
+                   threads=oracle_threads)
+        bf_o, log_o = O.factorize(op_o, rt_o, ct_o, cfg)
+        op = B.NufftOperator(x, xi)
+        rt = B.PartitionTree.build(x[:, :1], L, 1)
+        ct = B.PartitionTree.build(xi[:, :1], L, 1)
+        rc = B.ReconstructionConfig(tolerance=1e-6, rank_guess=4, levels=L, seed=3, hard_cap=cap)
+        bf, log = B.factorize(op, rt, ct, rc)
+        assert (bf.rows, bf.cols) == (m, n)
+        _compare(bf, log, bf_o, log_o, m, n)
+        assert log.rank_capped == (1 if cap > 0 else 0)
+        if cap > 0:
+            # the cap stops the leaf doubling: leaf bases from the round with r = cap
+            assert log.phase("leaf_v").probe_width == cap + 2
