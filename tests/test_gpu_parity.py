@@ -418,3 +418,10 @@ def test_rank_cap_and_rectangular_operator(B, oracle_threads):
         if cap > 0:
             # the cap stops the leaf doubling: leaf bases from the round with r = cap
             assert log.phase("leaf_v").probe_width == cap + 2
+        # the sharded schedule with non-identity trees (column-split leaf products)
+        import dataclasses
+
+        bv, _ = B.factorize(op, rt, ct, dataclasses.replace(rc, virtual_ranks=3))
+        np.testing.assert_array_equal(bv.rank_profile(), bf.rank_profile())
+        xv = O.gaussian_matrix(n, 4, 77)
+        assert rel_err(bv.apply(xv), bf.apply(xv)) < 1e-12
