@@ -21,8 +21,9 @@ namespace bfly {
 
 namespace {
 
-constexpr int QR_THREADS = 256;
-constexpr int QR_WARPS = QR_THREADS / 32;
+// threads per block: 256 for butterfly-sized blocks; 512 for saturated ones
+// (more warps on the per-column work; 64 registers then spill a little)
+constexpr int QR_SMALL = 256, QR_BIG = 512;
 
 template <typename T> __device__ __forceinline__ T warp_sum(T v) {
 #pragma unroll
@@ -42,7 +43,7 @@ template <> struct QrTraits<float> {
   static constexpr float jacobi_tol = 1e-7f;
 };
 
-template <typename R>
+template <typename R, int QR_THREADS>
 __global__ void __launch_bounds__(QR_THREADS) cpqr_kernel(const cx<R>* __restrict__ src, int64_t ld_src,
                                                           cx<R>* __restrict__ dst, int64_t ld_dst, int cap,
                                                           const QrEnt* __restrict__ ents, int32_t* ranks, double eps_t,
@@ -75,7 +76,7 @@ __global__ void __launch_bounds__(QR_THREADS) cpqr_kernel(const cx<R>* __restric
     Z[i + c * zld] = i < e.r1 ? s[i] : s[e.src_gap + (i - e.r1)];
   }
   __syncthreads();
-  for (int c = warp; c < w; c += QR_WARPS) {
+  for (int c = warp; c < w; c += (QR_THREADS / 32)) {
     R s = 0;
     for (int i = lane; i < r; i += 32) s += cabs2(Z[i + c * zld]);
     s = warp_sum(s);
@@ -163,7 +164,7 @@ __global__ void __launch_bounds__(QR_THREADS) cpqr_kernel(const cx<R>* __restric
     }
     // ---- apply H_j = I - tau v v^H to the trailing columns; downdate norms
     const V tj = tau[j];
-    for (int c = j + 1 + warp; c < w; c += QR_WARPS) {
+    for (int c = j + 1 + warp; c < w; c += (QR_THREADS / 32)) {
       V dot = mkc<R>(0, 0);
       for (int i = j + 1 + lane; i < r; i += 32) cfma_conj(dot, Z[i + j * zld], Z[i + c * zld]);
       dot.x = warp_sum(dot.x);
@@ -206,7 +207,7 @@ __global__ void __launch_bounds__(QR_THREADS) cpqr_kernel(const cx<R>* __restric
   // ---- form Q(:, 0:k) in place: Q = H_0 ... H_{k-1} [I_k; 0], H_i = I - conj(tau_i) v v^H
   for (int i = k - 1; i >= 0; --i) {
     const V tq = cconj(tau[i]);
-    for (int c = i + 1 + warp; c < k; c += QR_WARPS) {
+    for (int c = i + 1 + warp; c < k; c += (QR_THREADS / 32)) {
       V dot = Z[i + c * zld];  // v_i = 1
       V part = mkc<R>(0, 0);
       for (int q = i + 1 + lane; q < r; q += 32) cfma_conj(part, Z[q + i * zld], Z[q + c * zld]);
@@ -242,7 +243,7 @@ __global__ void __launch_bounds__(QR_THREADS) cpqr_kernel(const cx<R>* __restric
 }
 
 // --------------------------------------------------------------- core fit
-template <typename R>
+template <typename R, int QR_THREADS>
 __global__ void __launch_bounds__(QR_THREADS) core_fit_kernel(const cx<R>* __restrict__ Q, int64_t ldq,
                                                               const cx<R>* __restrict__ Zg, int64_t ldz,
                                                               const cx<R>* __restrict__ Cf, int64_t ldc,
@@ -302,7 +303,7 @@ __global__ void __launch_bounds__(QR_THREADS) core_fit_kernel(const cx<R>* __res
     if (threadIdx.x == 0) s_rot = 0;
     __syncthreads();
     for (int round = 0; round < kvp - 1; ++round) {
-      for (int pi = warp; pi < npair; pi += QR_WARPS) {
+      for (int pi = warp; pi < npair; pi += (QR_THREADS / 32)) {
         // round-robin tournament: position 0 fixed, others rotate
         int a = (pi == 0) ? 0 : 1 + (pi - 1 + round) % (kvp - 1);
         int b = 1 + (kvp - 2 - pi + round) % (kvp - 1);
@@ -347,7 +348,7 @@ __global__ void __launch_bounds__(QR_THREADS) core_fit_kernel(const cx<R>* __res
     __syncthreads();
   }
   // singular values and cutoff
-  for (int j = warp; j < kvp; j += QR_WARPS) {
+  for (int j = warp; j < kvp; j += (QR_THREADS / 32)) {
     R s = 0;
     for (int i = lane; i < w; i += 32) s += cabs2(A[i + (int64_t)j * w]);
     s = warp_sum(s);
@@ -397,11 +398,13 @@ void launch_cpqr(Ctx* c, const cx<R>* src, int64_t ld_src, cx<R>* dst, int64_t l
   int zld = max_rows > 0 ? max_rows : 1;
   const size_t aux = 2 * sizeof(R) * max_cols + sizeof(cx<R>) * max_cols + 64;
   size_t smem = sizeof(cx<R>) * (size_t)zld * max_cols + aux;
-  auto kern = cpqr_kernel<R>;
+  const bool big = (int64_t)max_rows * max_cols >= 128 * 128;
+  auto kern = big ? cpqr_kernel<R, QR_BIG> : cpqr_kernel<R, QR_SMALL>;
+  const int nt = big ? QR_BIG : QR_SMALL;
   KTimer timer(c, "cpqr", 0.0, (double)sizeof(cx<R>) * nent * ((double)max_rows * max_cols + (double)ld_dst * cap));
   if (smem <= 200 * 1024) {
     BFLY_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    kern<<<nent, QR_THREADS, smem, c->stream>>>(src, ld_src, dst, ld_dst, cap, ents, ranks, eps, zld, nullptr, 0);
+    kern<<<nent, nt, smem, c->stream>>>(src, ld_src, dst, ld_dst, cap, ents, ranks, eps, zld, nullptr, 0);
     BFLY_LAUNCH_CHECK("cpqr");
     return;
   }
@@ -413,7 +416,7 @@ void launch_cpqr(Ctx* c, const cx<R>* src, int64_t ld_src, cx<R>* dst, int64_t l
   DBuf<cx<R>> zbuf(c, (size_t)(chunk * zstride));
   for (int64_t e0 = 0; e0 < nent; e0 += chunk) {
     int n = (int)std::min<int64_t>(chunk, nent - e0);
-    kern<<<n, QR_THREADS, aux, c->stream>>>(src, ld_src, dst, ld_dst, cap, ents + e0, ranks, eps, zld, zbuf.p, zstride);
+    kern<<<n, nt, aux, c->stream>>>(src, ld_src, dst, ld_dst, cap, ents + e0, ranks, eps, zld, zbuf.p, zstride);
     BFLY_LAUNCH_CHECK("cpqr");
   }
 }
@@ -427,8 +430,12 @@ void launch_core_fit(Ctx* c, const cx<R>* Q, int64_t ldq, const cx<R>* Z, int64_
   int64_t stride = (int64_t)max_ku * max_w + (int64_t)max_w * kvp + (int64_t)kvp * kvp + (int64_t)max_ku * kvp + kvp + 8;
   DBuf<cx<R>> scratch(c, (size_t)stride * nent);
   KTimer timer(c, "core_fit", 0.0, 0.0);
-  core_fit_kernel<R><<<nent, QR_THREADS, 0, c->stream>>>(Q, ldq, Z, ldz, Cf, ldc, B, ldb, bcap, ents, scratch.p, stride,
-                                                          literal, err_flag);
+  if (max_kv >= 64)
+    core_fit_kernel<R, QR_BIG><<<nent, QR_BIG, 0, c->stream>>>(Q, ldq, Z, ldz, Cf, ldc, B, ldb, bcap, ents, scratch.p,
+                                                                 stride, literal, err_flag);
+  else
+    core_fit_kernel<R, QR_SMALL><<<nent, QR_SMALL, 0, c->stream>>>(Q, ldq, Z, ldz, Cf, ldc, B, ldb, bcap, ents, scratch.p,
+                                                                     stride, literal, err_flag);
   BFLY_LAUNCH_CHECK("core_fit");
 }
 
