@@ -1,6 +1,7 @@
 // context.cu -- per-GPU context implementation.
 #include <algorithm>
 #include <cstdlib>
+#include <cstring>
 
 #include "context.h"
 #include "comm.h"
@@ -42,7 +43,8 @@ Ctx::~Ctx() {
     cudaStreamSynchronize(stream);
     cudaStreamDestroy(stream);
   }
-  if (pinned_p) cudaFreeHost(pinned_p);
+  for (auto& u : stage_uses) cudaEventDestroy(u.done);
+  if (stage_p) cudaFreeHost(stage_p);
   if (oz_flag) cudaFree(oz_flag);
   if (pool) cudaMemPoolDestroy(pool);
 }
@@ -57,20 +59,53 @@ void* Ctx::alloc(size_t bytes) {
 
 void Ctx::release(void* p) { cudaFreeAsync(p, stream); }
 
-void* Ctx::pinned(size_t bytes) {
-  if (bytes > pinned_n) {
-    if (pinned_p) cudaFreeHost(pinned_p);
-  if (oz_flag) cudaFree(oz_flag);
-  if (pool) cudaMemPoolDestroy(pool);
-    pinned_p = nullptr;
-    pinned_n = 0;
-    BFLY_CUDA(cudaMallocHost(&pinned_p, bytes));
-    pinned_n = bytes;
-  }
-  return pinned_p;
-}
-
 void Ctx::sync() { BFLY_CUDA(cudaStreamSynchronize(stream)); }
+
+void Ctx::upload(void* dst, const void* src, size_t bytes) {
+  constexpr size_t kRing = 64ull << 20;
+  if (bytes == 0) return;
+  if (bytes > kRing / 2) {
+    BFLY_CUDA(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, stream));
+    return;
+  }
+  if (!stage_p) {
+    BFLY_CUDA(cudaMallocHost(reinterpret_cast<void**>(&stage_p), kRing));
+    stage_n = kRing;
+  }
+  size_t b = (stage_off + 255) / 256 * 256;
+  if (b + bytes > stage_n) b = 0;  // wrap
+  const size_t e = b + bytes;
+  // wait for earlier copies that read [b, e) and retire them
+  for (size_t i = 0; i < stage_uses.size();) {
+    StageUse& u = stage_uses[i];
+    if (u.begin < e && b < u.end) {
+      BFLY_CUDA(cudaEventSynchronize(u.done));
+      cudaEventDestroy(u.done);
+      stage_uses[i] = stage_uses.back();
+      stage_uses.pop_back();
+    } else {
+      ++i;
+    }
+  }
+  std::memcpy(stage_p + b, src, bytes);
+  BFLY_CUDA(cudaMemcpyAsync(dst, stage_p + b, bytes, cudaMemcpyHostToDevice, stream));
+  cudaEvent_t ev;
+  BFLY_CUDA(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+  BFLY_CUDA(cudaEventRecord(ev, stream));
+  stage_uses.push_back(StageUse{b, e, ev});
+  stage_off = e;
+  // retire finished uses now and then (bounded bookkeeping)
+  if (stage_uses.size() > 256)
+    for (size_t i = 0; i < stage_uses.size();) {
+      if (cudaEventQuery(stage_uses[i].done) == cudaSuccess) {
+        cudaEventDestroy(stage_uses[i].done);
+        stage_uses[i] = stage_uses.back();
+        stage_uses.pop_back();
+      } else {
+        ++i;
+      }
+    }
+}
 
 void Ctx::resolve_records() {
   if (records.empty()) return;

@@ -44,12 +44,21 @@ struct Ctx {
   explicit Ctx(int dev);
   ~Ctx();
   void* alloc(size_t bytes);
-  // pinned host staging buffer (grown on demand, reused across calls)
-  void* pinned(size_t bytes);
-  void* pinned_p = nullptr;
-  size_t pinned_n = 0;
   void release(void* p);
   void sync();
+  // host -> device upload on the library stream that never blocks the host:
+  // the bytes are staged in a pinned ring (a region is reused only after
+  // the copy that read it has executed), so planning of the next launches
+  // overlaps the running kernels; oversized uploads fall back to a pageable
+  // copy.  Not for use during graph capture.
+  void upload(void* dst, const void* src, size_t bytes);
+  struct StageUse {
+    size_t begin, end;
+    cudaEvent_t done;
+  };
+  unsigned char* stage_p = nullptr;
+  size_t stage_n = 0, stage_off = 0;
+  std::vector<StageUse> stage_uses;
   // K2 int8-slice path range flag (k_matvec_oz.cu).  oz_deferred: launches OR
   // into one persistent device flag that is checked once per factorization
   // (no per-launch host sync); force_fp64: recompute on the FP64 DMMA path.
@@ -137,7 +146,7 @@ struct DBuf {
     n = 0;
   }
   void upload(const T* host, size_t count) {
-    if (count) BFLY_CUDA(cudaMemcpyAsync(p, host, count * sizeof(T), cudaMemcpyHostToDevice, ctx->stream));
+    if (count) ctx->upload(p, host, count * sizeof(T));
   }
   void upload(const std::vector<T>& v) {
     if (v.size() > n) reset(ctx, v.size());
