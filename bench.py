@@ -244,24 +244,6 @@ def run_ours(args):
         apply[f"k{k}"] = {"ms": round(ms, 4), "GB/s": round(nbytes / (ms / 1e3) / 1e9, 1),
                           "frac_of_hbm": round(nbytes / (ms / 1e3) / 1e9 / 6554.9, 3)}
 
-    # ------------------------------- the other full-size configs (info only)
-    # config 4 (recompression, n = 262144: the north-star scaling config) and
-    # config 1 (3D plates, n = 16384): one warm-up + median of 3 constructions
-    other = {}
-    if rank == 0 and world == 1 and not args.no_extra:
-        for cid in (4, 1):
-            wx = B.configs.build(cid, ctx=ctx)
-            ts_x = []
-            for i in range(4):
-                l2_flush()
-                bx, lx = B.factorize(wx.op, wx.row_tree, wx.col_tree, wx.recon)
-                if i:
-                    ts_x.append(lx.total_seconds)
-            med = statistics.median(ts_x)
-            other[wx.name] = {"construct_s": round(med, 4), "GFLOP/s": round(lx.flops / med / 1e9, 1),
-                              "max_rank": bx.max_rank(), "nnz": bx.nnz()}
-            del bx, wx
-
     # --------------------------------------------------- e2e (host buffers)
     import ctypes as C
 
@@ -327,6 +309,27 @@ def run_ours(args):
                                                    "transfer-level launch (profiles/r01_matvec_oz_ncu.txt); FP64 "
                                                    "and int8 tensor ops time-share one datapath "
                                                    "(profiles/r01_tc_i8.txt overlap test)")
+
+    # ------------------------------- the other full-size configs (info only)
+    # config 4 (recompression, n = 262144: the north-star scaling config) and
+    # config 1 (3D plates, n = 16384): one warm-up + median of 3 constructions
+    # (own context: its memory pool does not disturb the timed legs above)
+    other = {}
+    if rank == 0 and world == 1 and not args.no_extra:
+        ctx_x = B.Context(local)
+        for cid in (4, 1):
+            wx = B.configs.build(cid, ctx=ctx_x)
+            ts_x = []
+            for i in range(4):
+                l2_flush()
+                bx, lx = B.factorize(wx.op, wx.row_tree, wx.col_tree, wx.recon)
+                if i:
+                    ts_x.append(lx.total_seconds)
+            med = statistics.median(ts_x)
+            other[wx.name] = {"construct_s": round(med, 4), "GFLOP/s": round(lx.flops / med / 1e9, 1),
+                              "max_rank": bx.max_rank(), "nnz": bx.nnz()}
+            del bx, wx
+        del ctx_x
 
     if rank == 0:
         line = {
