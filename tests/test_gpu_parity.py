@@ -425,3 +425,18 @@ def test_rank_cap_and_rectangular_operator(B, oracle_threads):
         np.testing.assert_array_equal(bv.rank_profile(), bf.rank_profile())
         xv = O.gaussian_matrix(n, 4, 77)
         assert rel_err(bv.apply(xv), bf.apply(xv)) < 1e-12
+
+
+def test_repeated_factorizations_identical(B):
+    """Many factorizations on one context (the pinned upload ring wraps
+    several times, pool re-reservations, CUDA-graph applies): every result
+    bit-identical to the first."""
+    w = B.configs.build(2, 8192)
+    bf0, _ = B.factorize(w.op, w.row_tree, w.col_tree, w.recon)
+    x = O.gaussian_matrix(w.op.cols, 2, 5)
+    y0 = bf0.apply(x)
+    prof0 = bf0.rank_profile()
+    for _ in range(12):
+        bf, _ = B.factorize(w.op, w.row_tree, w.col_tree, w.recon)
+        np.testing.assert_array_equal(bf.rank_profile(), prof0)
+        np.testing.assert_array_equal(bf.apply(x), y0)
