@@ -696,8 +696,12 @@ void DevButterfly<R>::run_plan(Plan& pl, const cx<R>* x, int64_t ldx, cx<R>* y, 
     const bool final = i == n - 1;
     cx<R>* out = final ? y : bufs[i % 2];
     const int64_t ldout = final ? ldy : d.ld_out;
+    // L2 prefetch of the next stage's factor level: off by default -- the next
+    // stage's CTAs become resident early (PDL) and stage their factor blocks
+    // by TMA themselves; measured k=1 71.6 -> 68.7 us without the prefetch
+    static const bool l2pf = std::getenv("BFLY_L2PF") && std::atoi(std::getenv("BFLY_L2PF")) != 0;
     launch_bgemm<R>(c, d.op, d.M, d.K, d.S, d.A, d.lda, in, ldin, out, ldout, d.d.p, (int)d.h.size(), (int)k, false,
-                    (int)k, true, final ? L2Prefetch() : pl.st[i + 1].pf);
+                    (int)k, true, (final || !l2pf) ? L2Prefetch() : pl.st[i + 1].pf);
     in = out;
     ldin = ldout;
   }
