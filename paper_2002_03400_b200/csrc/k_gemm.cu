@@ -860,7 +860,9 @@ void launch_bgemm(Ctx* c, int op, int M, int K, int S, const cx<R>* A, int64_t l
                     : kcols <= 2 ? 1 : kcols <= 8 ? 2 : 4;
     const size_t grp_smem = stage_smem;
     static const int epb_env = std::getenv("BFLY_STAGE_EPB") ? std::atoi(std::getenv("BFLY_STAGE_EPB")) : 0;
-    int epb = wpe == 1 ? (epb_env > 0 ? std::min(epb_env, 8) : 4) : 1;
+    // entries per CTA for single-warp groups: measured on the config-2 apply
+    // (k=1: 2 per CTA, k=2: 1 per CTA)
+    int epb = wpe == 1 ? (epb_env > 0 ? std::min(epb_env, 8) : (kcols == 1 ? 2 : 1)) : 1;
     while (epb > 1 && epb * grp_smem > 100 * 1024) epb /= 2;
     cudaLaunchConfig_t cfg = {};
     cudaLaunchAttribute at[1];
