@@ -440,3 +440,16 @@ def test_repeated_factorizations_identical(B):
         bf, _ = B.factorize(w.op, w.row_tree, w.col_tree, w.recon)
         np.testing.assert_array_equal(bf.rank_profile(), prof0)
         np.testing.assert_array_equal(bf.apply(x), y0)
+
+
+@pytest.mark.parametrize("cfg_id,n", [(0, 2048), (2, 4096)])
+def test_complex64_kernel_configs_vs_complex128_oracle(B, oracle_threads, cfg_id, n):
+    """complex64 on the kernel-evaluated operators (B200-only variant):
+    apply within 1e-4 of the complex128 oracle factorization."""
+    op_o, rt_o, ct_o, cfg = oracle_config(cfg_id, n)
+    bf_o, _ = O.factorize(op_o, rt_o, ct_o, dict(cfg, threads=oracle_threads))
+    w = B.configs.build(cfg_id, n, scalar=B.COMPLEX64)
+    bf, _ = B.factorize(w.op, w.row_tree, w.col_tree, w.recon)
+    x = O.gaussian_matrix(w.op.cols, 8, O.seed_mix(5, 5))
+    y = bf.apply(x.astype(np.complex64)).astype(np.complex128)
+    assert rel_err(y, bf_o.apply(x)) < 1e-4
