@@ -453,3 +453,14 @@ def test_complex64_kernel_configs_vs_complex128_oracle(B, oracle_threads, cfg_id
     x = O.gaussian_matrix(w.op.cols, 8, O.seed_mix(5, 5))
     y = bf.apply(x.astype(np.complex64)).astype(np.complex128)
     assert rel_err(y, bf_o.apply(x)) < 1e-4
+
+
+@pytest.mark.parametrize("cfg_id,n,seed", [(0, 1536, 2), (1, 2304, 2), (2, 3000, 1), (4, 2048, 1)])
+def test_other_seeds_and_sizes(B, oracle_threads, cfg_id, n, seed):
+    """Probe seeds != 0 and non-power-of-two sizes (ragged trees): identical
+    rank profiles and apply within 1e-10 of the oracle."""
+    op_o, rt_o, ct_o, cfg = oracle_config(cfg_id, n, seed=seed)
+    bf_o, log_o = O.factorize(op_o, rt_o, ct_o, dict(cfg, threads=oracle_threads))
+    w = B.configs.build(cfg_id, n, seed=seed)
+    bf, log = B.factorize(w.op, w.row_tree, w.col_tree, w.recon)
+    _compare(bf, log, bf_o, log_o, w.op.rows, w.op.cols, seed=seed)
