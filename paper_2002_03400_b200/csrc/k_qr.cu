@@ -21,9 +21,10 @@ namespace bfly {
 
 namespace {
 
-// threads per block: 256 for butterfly-sized blocks; 512 for saturated ones
-// (more warps on the per-column work; 64 registers then spill a little)
-constexpr int QR_SMALL = 256, QR_BIG = 512;
+// threads per block by block size (measured): 128 up to ~32 x 34 (config 2
+// leaves and transfer blocks), 256 for butterfly-sized blocks up to 128 x 128
+// (config 4), 512 for saturated ones (more warps on the per-column work)
+constexpr int QR_TINY = 128, QR_SMALL = 256, QR_BIG = 512;
 
 template <typename T> __device__ __forceinline__ T warp_sum(T v) {
 #pragma unroll
@@ -398,9 +399,10 @@ void launch_cpqr(Ctx* c, const cx<R>* src, int64_t ld_src, cx<R>* dst, int64_t l
   int zld = max_rows > 0 ? max_rows : 1;
   const size_t aux = 2 * sizeof(R) * max_cols + sizeof(cx<R>) * max_cols + 64;
   size_t smem = sizeof(cx<R>) * (size_t)zld * max_cols + aux;
-  const bool big = (int64_t)max_rows * max_cols >= 128 * 128;
-  auto kern = big ? cpqr_kernel<R, QR_BIG> : cpqr_kernel<R, QR_SMALL>;
-  const int nt = big ? QR_BIG : QR_SMALL;
+  const int64_t area = (int64_t)max_rows * max_cols;
+  const bool big = area >= 128 * 128, tiny = area <= 32 * 34;
+  auto kern = big ? cpqr_kernel<R, QR_BIG> : tiny ? cpqr_kernel<R, QR_TINY> : cpqr_kernel<R, QR_SMALL>;
+  const int nt = big ? QR_BIG : tiny ? QR_TINY : QR_SMALL;
   KTimer timer(c, "cpqr", 0.0, (double)sizeof(cx<R>) * nent * ((double)max_rows * max_cols + (double)ld_dst * cap));
   if (smem <= 200 * 1024) {
     BFLY_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
