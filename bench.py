@@ -160,24 +160,44 @@ def run_ours(args):
     import paper_2002_03400_b200 as B
 
     rank, world, local = _env_rank()
+    ndev = torch.cuda.device_count()
+    transport = args.transport
+    if transport == "auto":
+        transport = "nccl" if world <= ndev else "host"
+    if transport == "nccl" and world > ndev:
+        raise SystemExit(f"bench: {world} ranks need {world} GPUs for NCCL, {ndev} visible (use --transport host)")
+    local = local % ndev
     torch.cuda.set_device(local)
     dist = None
     if world > 1:
         import torch.distributed as dist
 
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if transport == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group("gloo")
+    red_dev = "cuda" if transport == "nccl" else "cpu"
 
     def barrier():
         if dist is not None:
             dist.barrier()
         torch.cuda.synchronize()
 
+    def allreduce(v, op):
+        t = torch.tensor([v], dtype=torch.float64, device=red_dev)
+        if dist is not None:
+            dist.all_reduce(t, op=dist.ReduceOp.MAX if op == "max" else dist.ReduceOp.SUM)
+        return t.item()
+
     ctx = B.Context(local)
     sharded = world > 1 and args.mode == "shard"
     if sharded:
-        uid = [B.Context.unique_id() if rank == 0 else None]
-        dist.broadcast_object_list(uid, src=0)
-        ctx.set_comm(rank, world, uid[0])
+        if transport == "nccl":
+            uid = [B.Context.unique_id() if rank == 0 else None]
+            dist.broadcast_object_list(uid, src=0)
+            ctx.set_comm(rank, world, uid[0])
+        else:
+            ctx.set_host_comm()
     stream = torch.cuda.ExternalStream(ctx.stream)
     w = B.configs.build(CFG_ID, args.n or None, ctx=ctx)
     op, rt, ct, rc = w.op, w.row_tree, w.col_tree, w.recon
@@ -212,13 +232,9 @@ def run_ours(args):
     ctx.profile(0)
     barrier()
     clk = clocks.stop()
-    t = torch.tensor([total_ms], dtype=torch.float64, device="cuda")
-    fl = torch.tensor([flops], dtype=torch.float64, device="cuda")
-    if dist is not None:
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        dist.all_reduce(fl, op=dist.ReduceOp.SUM)
-    max_ms = t.item()
-    value = fl.item() / (max_ms / 1e3) / 1e9
+    max_ms = allreduce(total_ms, "max")
+    fl_total = allreduce(flops, "sum")
+    value = fl_total / (max_ms / 1e3) / 1e9
     ms_per_step = max_ms / args.steps
 
     # ----------------------------------------------- apply bandwidth (device)
@@ -275,7 +291,7 @@ def run_ours(args):
         del bf_e, op_e  # the result now lives on the host; free its device copy before the next job
     barrier()
     te = (time.perf_counter() - te0) / e2e_steps
-    e2e_val = (fl.item() / args.steps) / te / 1e9  # whole-job flops of one construction
+    e2e_val = (fl_total / args.steps) / te / 1e9  # whole-job flops of one construction
 
     # ------------------------------------------------------------ roofline
     # K2 (kernel_matvec): kernel entries evaluated on the FP64 pipe, complex128
@@ -339,15 +355,16 @@ def run_ours(args):
             "data": "synthetic",
             "config": {"workload": "config2_helmholtz_circle_n65536", "n": w.n, "levels": rc.levels, "leaf": 32,
                        "tol": rc.tolerance, "r0": rc.rank_guess, "oversampling": rc.oversampling,
-                       "parallelism": (f"probe-sharded x{world} (NCCL all-gather per level)" if sharded
+                       "parallelism": (f"probe-sharded x{world} ({transport} all-gather per level)" if sharded
                                        else f"replicas{world}" if world > 1 else "single"),
+                       "transport": transport if world > 1 else None,
                        "l2": "flushed before every step (256 MB write); probe products 0.1-1 GB > L2"},
             "construct_seconds": round(ms_per_step / 1e3, 4),
             "construct_seconds_median": round(statistics.median(step_ms) / 1e3, 4),
             # per-phase wall times (PhaseStat names), median over the timed steps
             "phases_ms": {p.name: round(statistics.median(lg.phases[i].seconds for lg in logs) * 1e3, 3)
                           for i, p in enumerate(logs[0].phases)},
-            "flops_per_step": fl.item() / args.steps, "kernel_evals_per_step": logs[0].kernel_evals,
+            "flops_per_step": fl_total / args.steps, "kernel_evals_per_step": logs[0].kernel_evals,
             "max_rank": bf.max_rank(), "nnz": bf.nnz(),
             "roofline": roofline,
             "apply": apply,
@@ -372,6 +389,23 @@ def run_ours(args):
     return 0
 
 
+def _free_port():
+    import socket
+
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def self_launch(args, argv):
+    """--gpus N > 1 without a torchrun environment: launch N ranks (one
+    process per GPU) under torch.distributed.run on this node."""
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr", "127.0.0.1", "--master-port", str(_free_port()), os.path.abspath(__file__)] + argv
+    print(f"bench: launching {args.gpus} ranks: {' '.join(cmd[1:])}", file=sys.stderr, flush=True)
+    return subprocess.call(cmd)
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -383,7 +417,25 @@ def main():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-extra", action="store_true", help="skip the other full-size configs (info only)")
     ap.add_argument("--mode", default="shard", choices=["shard", "replica"], help="N > 1 schedule")
-    args = ap.parse_args()
+    ap.add_argument("--transport", default="auto", choices=["auto", "nccl", "host"],
+                    help="N > 1 exchange: NCCL (one GPU per rank) or host-staged over gloo (ranks may share "
+                         "a GPU: a correctness run, not a scaling measurement); auto = NCCL when every rank "
+                         "has its own GPU")
+    ap.add_argument("--dry-launch", action="store_true", help="print rank/world and exit (launcher test)")
+    argv = sys.argv[1:]
+    args = ap.parse_args(argv)
+    if args.gpus < 1:
+        ap.error("--gpus must be >= 1")
+    env_world = os.environ.get("WORLD_SIZE")
+    if env_world is None and args.gpus > 1:
+        return self_launch(args, argv)
+    if env_world is not None and int(env_world) != args.gpus:
+        print(f"bench: refusing to run: --gpus {args.gpus} but WORLD_SIZE={env_world}", file=sys.stderr, flush=True)
+        return 2
+    if args.dry_launch:
+        rank, world, local = _env_rank()
+        print(json.dumps({"rank": rank, "world": world, "local_rank": local}), flush=True)
+        return 0
     if args.impl == "reference":
         return run_reference(args)
     return run_ours(args)

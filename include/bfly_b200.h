@@ -76,6 +76,29 @@ BFLY_API int64_t bfly_ctx_profile_report(bfly_ctx* ctx, char* buf, int64_t len);
  * blocks are all-gathered. */
 BFLY_API int bfly_comm_unique_id(uint8_t* id_out /* 128 bytes */);
 BFLY_API int bfly_ctx_set_comm(bfly_ctx* ctx, int rank, int world, const uint8_t* nccl_id);
+/* Host-staged transport: the same sharded schedule with every exchange staged
+ * through pinned host memory and handed to the caller's collectives (e.g.
+ * torch.distributed over gloo).  For ranks that share one GPU (NCCL rejects
+ * two ranks on one device) or lack peer access; the library synchronizes its
+ * stream before each exchange, so no kernel ever waits on another rank.
+ * Every function is collective (all ranks call it in the same order) and
+ * returns 0 on success.  Host buffers are library-owned, valid for the call.
+ *   allgather: recv (world * bytes) = concat over ranks of send (bytes)
+ *   allreduce: in place on count elements; dtype 0 int32, 1 float64,
+ *              2 float32; op 0 sum, 1 max
+ *   sendrecv:  one group of point-to-point transfers (ncclGroupStart ..
+ *              ncclGroupEnd semantics: all posted, then all completed) */
+typedef struct bfly_host_comm {
+  void* user;
+  int (*allgather)(void* user, const void* send, void* recv, int64_t bytes);
+  int (*allreduce)(void* user, void* buf, int64_t count, int dtype, int op);
+  int (*sendrecv)(void* user, int nsend, const int32_t* send_peer, void* const* send_buf, const int64_t* send_bytes,
+                  int nrecv, const int32_t* recv_peer, void* const* recv_buf, const int64_t* recv_bytes);
+} bfly_host_comm;
+BFLY_API int bfly_ctx_set_host_comm(bfly_ctx* ctx, int rank, int world, const bfly_host_comm* hc);
+/* rank / world of the context's transport (0 / 1 when none); transport 0 none,
+ * 1 NCCL, 2 host-staged */
+BFLY_API int bfly_ctx_comm_info(const bfly_ctx* ctx, int* rank, int* world, int* transport);
 
 /* ------------------------------------------------------------------- trees */
 /* PartitionTree::build (tree.hpp:75-101); coords n x 3 row-major */
@@ -116,6 +139,18 @@ typedef enum {
 typedef int (*bfly_apply_fn)(void* user, int trans, const void* x_dev, int64_t ldx, void* y_dev,
                              int64_t ldy, int64_t k, void* stream);
 
+/* Structured-probe-aware user black box.  Same contract as
+ * bfly_apply_fn plus the probe's nonzero input rows: x_dev is full height in
+ * operator (original) row order and zero outside [nz_row_begin, nz_row_end),
+ * so a reference-style body may ignore the range, while a range-aware body
+ * reads only those rows and skips the zero work (the reference pads the probe
+ * and multiplies the zeros, reconstruct.hpp:72-85, operators.hpp:17-56).  The
+ * library calls it once per structured probe (a contiguous range exists when
+ * the probe side's tree is the identity, i.e. points in tree order; otherwise
+ * the range is [0, rows_in)), and with [0, rows_in) for dense inputs. */
+typedef int (*bfly_apply_range_fn)(void* user, int trans, const void* x_dev, int64_t ldx, void* y_dev,
+                                   int64_t ldy, int64_t k, int64_t nz_row_begin, int64_t nz_row_end, void* stream);
+
 /* tgt (m x 3) and src (n x 3) row-major host points, already in tree order */
 BFLY_API int bfly_op_kernel(bfly_ctx* ctx, int kind, int64_t m, int64_t n, const double* tgt, const double* src,
                    double wavenumber, int scalar, bfly_op** out);
@@ -127,6 +162,8 @@ BFLY_API int bfly_op_dense(bfly_ctx* ctx, int64_t m, int64_t n, const double* a,
 BFLY_API int bfly_op_butterfly(bfly_ctx* ctx, bfly_bf* bf, bfly_op** out);
 BFLY_API int bfly_op_callback(bfly_ctx* ctx, int64_t m, int64_t n, int scalar, bfly_apply_fn fn, void* user,
                      bfly_op** out);
+BFLY_API int bfly_op_callback_ranged(bfly_ctx* ctx, int64_t m, int64_t n, int scalar, bfly_apply_range_fn fn,
+                                     void* user, bfly_op** out);
 BFLY_API int bfly_op_info(const bfly_op* op, int64_t* m, int64_t* n, int* scalar, int* kind);
 /* apply / apply_transpose / apply_adjoint.  on_device = 0: host buffers (copied
  * in and out inside the call); 1: device pointers, stream-ordered. */
@@ -166,6 +203,13 @@ typedef struct bfly_phase {
   double seconds;
   int32_t rounds;
   int64_t probe_width;
+  /* CPQR rank margin at the truncation cut (diagnostic; SURVEY 7 hard part 1):
+   * min over the phase's blocks (leaf phases: the kept round) of
+   * min(|R_{k-1}| / thr - 1, 1 - |R_k| / thr), thr = 0.25 tol |R_00|
+   * (linalg.hpp:74-77, reconstruct.hpp:342-348); +inf when no block was
+   * truncated.  Near 0 = a rank that rounding could flip.  Multi-process:
+   * over this process's blocks. */
+  double rank_margin;
 } bfly_phase;
 
 typedef struct bfly_log {

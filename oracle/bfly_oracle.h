@@ -163,6 +163,9 @@ typedef struct bo_cfg {
 
 void bo_cfg_default(bo_cfg* cfg);
 
+/* CPQR cut margin min(|R_{k-1}|/thr - 1, 1 - |R_k|/thr), thr = eps |R_00| (+inf: zero block) */
+double bo_cut_margin(const double* rdiag, int64_t size, int64_t k, double eps);
+
 #define BO_MAX_PHASES 64
 typedef struct bo_phase {
   char name[32];
@@ -170,6 +173,7 @@ typedef struct bo_phase {
   double seconds;
   int rounds;
   int64_t probe_width;
+  double rank_margin; /* min CPQR cut margin over the phase's blocks (bo_cut_margin) */
 } bo_phase;
 
 typedef struct bo_log {

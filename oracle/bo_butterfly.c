@@ -3,7 +3,8 @@
  *
  * Restates /root/reference/proj/include/bfly/butterfly.hpp:
  *   layout and rank accessors :20-66, apply :71-118, apply_adjoint :122-184,
- *   apply_transpose :187-193, to_dense/expand_* :199-242, validate :290-326,
+ *   apply_transpose :187-193 (block-parallel over a level with OpenMP; each
+ *   output block sums its contributions in the reference's sequential order), to_dense/expand_* :199-242, validate :290-326,
  *   v/u chain coefficients :330-354;
  * and the .bfh container of serialize.hpp:103-177 (format in
  * proj/docs/formats.md:3-54).
@@ -140,6 +141,8 @@ static void apply_n(const bo_bf* bf, const bo_cplx* x, int64_t k, bo_cplx* y) {
   bo_cplx* xt = (bo_cplx*)malloc(sizeof(bo_cplx) * (size_t)(n * k));
   gather_rows(bf->col_tree, x, k, xt);
   bo_mat* coef = (bo_mat*)calloc((size_t)nb, sizeof(bo_mat));
+  const int nt = bo_threads();
+#pragma omp parallel for schedule(static) num_threads(nt)
   for (int64_t nu = 0; nu < nb; ++nu) {
     const bo_mat* v = &bf->v_leaf[nu];
     int64_t b = bo_node_b(bf->col_tree, L, nu);
@@ -148,8 +151,10 @@ static void apply_n(const bo_bf* bf, const bo_cplx* x, int64_t k, bo_cplx* y) {
   }
   for (int l = 1; l <= lm; ++l) {
     bo_mat* next = (bo_mat*)calloc((size_t)nb, sizeof(bo_mat));
-    for (int64_t tau = 0; tau < ((int64_t)1 << l); ++tau)
-      for (int64_t nu = 0; nu < ((int64_t)1 << (L - l)); ++nu) {
+#pragma omp parallel for schedule(static) num_threads(nt)
+    for (int64_t e = 0; e < nb; ++e) {
+      {
+        const int64_t tau = e >> (L - l), nu = e & (((int64_t)1 << (L - l)) - 1);
         bo_mat s = stack2(&coef[bo_bidx(L, l - 1, tau / 2, 2 * nu)], &coef[bo_bidx(L, l - 1, tau / 2, 2 * nu + 1)], k);
         const bo_mat* w = bo_w_block(bf, l, tau, nu);
         bo_mat* o = &next[bo_bidx(L, l, tau, nu)];
@@ -157,10 +162,12 @@ static void apply_n(const bo_bf* bf, const bo_cplx* x, int64_t k, bo_cplx* y) {
         bo_gemm('H', w->cols, k, w->rows, w->a, w->rows, s.a, s.rows, o->a, o->rows, 0);
         bo_mat_free(&s);
       }
+    }
     free_vec(coef, nb);
     coef = next;
   }
   bo_mat* g = (bo_mat*)calloc((size_t)nb, sizeof(bo_mat));
+#pragma omp parallel for schedule(static) num_threads(nt)
   for (int64_t i = 0; i < nb; ++i) {
     const bo_mat* b = &bf->b_blocks[i];
     g[i] = bo_mat_new(b->rows, k);
@@ -173,13 +180,16 @@ static void apply_n(const bo_bf* bf, const bo_cplx* x, int64_t k, bo_cplx* y) {
     for (int64_t tau = 0; tau < ((int64_t)1 << (l + 1)); ++tau)
       for (int64_t nu = 0; nu < wide; ++nu)
         next[bo_bidx(L, l + 1, tau, nu)] = bo_mat_new(bo_u_rank(bf, l + 1, tau, nu), k);
-    for (int64_t tau = 0; tau < ((int64_t)1 << l); ++tau)
-      for (int64_t nu = 0; nu < ((int64_t)1 << (L - l)); ++nu) {
+    /* each (tau, parent nu) pair owns its two outputs; the two children nu
+     * are added in the sequential order (2 pnu, then 2 pnu + 1) */
+#pragma omp parallel for schedule(static) num_threads(nt)
+    for (int64_t e = 0; e < (nb >> 1); ++e) {
+      const int64_t tau = e / wide, pnu = e % wide;
+      for (int64_t nu = 2 * pnu; nu <= 2 * pnu + 1; ++nu) {
         const bo_mat* r = bo_r_block(bf, l, tau, nu);
         bo_mat h = bo_mat_new(r->rows, k);
         const bo_mat* gi = &g[bo_bidx(L, l, tau, nu)];
         bo_gemm('N', r->rows, k, r->cols, r->a, r->rows, gi->a, gi->rows, h.a, h.rows, 0);
-        int64_t pnu = nu / 2;
         bo_mat* t0 = &next[bo_bidx(L, l + 1, 2 * tau, pnu)];
         bo_mat* t1 = &next[bo_bidx(L, l + 1, 2 * tau + 1, pnu)];
         int64_t top = t0->rows;
@@ -189,10 +199,12 @@ static void apply_n(const bo_bf* bf, const bo_cplx* x, int64_t k, bo_cplx* y) {
         }
         bo_mat_free(&h);
       }
+    }
     free_vec(g, nb);
     g = next;
   }
   bo_cplx* yt = (bo_cplx*)calloc((size_t)(m * k), sizeof(bo_cplx));
+#pragma omp parallel for schedule(static) num_threads(nt)
   for (int64_t tau = 0; tau < nb; ++tau) {
     const bo_mat* u = &bf->u_leaf[tau];
     int64_t b = bo_node_b(bf->row_tree, L, tau);
@@ -211,6 +223,8 @@ static void apply_h(const bo_bf* bf, const bo_cplx* y, int64_t k, bo_cplx* x) {
   bo_cplx* yt = (bo_cplx*)malloc(sizeof(bo_cplx) * (size_t)(m * k));
   gather_rows(bf->row_tree, y, k, yt);
   bo_mat* a = (bo_mat*)calloc((size_t)nb, sizeof(bo_mat));
+  const int nt = bo_threads();
+#pragma omp parallel for schedule(static) num_threads(nt)
   for (int64_t tau = 0; tau < nb; ++tau) {
     const bo_mat* u = &bf->u_leaf[tau];
     int64_t b = bo_node_b(bf->row_tree, L, tau);
@@ -219,8 +233,10 @@ static void apply_h(const bo_bf* bf, const bo_cplx* y, int64_t k, bo_cplx* x) {
   }
   for (int l = L - 1; l >= lm; --l) {
     bo_mat* cur = (bo_mat*)calloc((size_t)nb, sizeof(bo_mat));
-    for (int64_t tau = 0; tau < ((int64_t)1 << l); ++tau)
-      for (int64_t nu = 0; nu < ((int64_t)1 << (L - l)); ++nu) {
+#pragma omp parallel for schedule(static) num_threads(nt)
+    for (int64_t e = 0; e < nb; ++e) {
+      {
+        const int64_t tau = e >> (L - l), nu = e & (((int64_t)1 << (L - l)) - 1);
         int64_t pnu = nu / 2;
         bo_mat s = stack2(&a[bo_bidx(L, l + 1, 2 * tau, pnu)], &a[bo_bidx(L, l + 1, 2 * tau + 1, pnu)], k);
         const bo_mat* r = bo_r_block(bf, l, tau, nu);
@@ -229,9 +245,11 @@ static void apply_h(const bo_bf* bf, const bo_cplx* y, int64_t k, bo_cplx* x) {
         bo_gemm('H', r->cols, k, r->rows, r->a, r->rows, s.a, s.rows, o->a, o->rows, 0);
         bo_mat_free(&s);
       }
+    }
     free_vec(a, nb);
     a = cur;
   }
+#pragma omp parallel for schedule(static) num_threads(nt)
   for (int64_t i = 0; i < nb; ++i) {
     const bo_mat* b = &bf->b_blocks[i];
     bo_mat o = bo_mat_new(b->cols, k);
@@ -244,13 +262,17 @@ static void apply_h(const bo_bf* bf, const bo_cplx* y, int64_t k, bo_cplx* x) {
     for (int64_t tau = 0; tau < ((int64_t)1 << (l - 1)); ++tau)
       for (int64_t nu = 0; nu < ((int64_t)1 << (L - l + 1)); ++nu)
         prev[bo_bidx(L, l - 1, tau, nu)] = bo_mat_new(bo_v_rank(bf, l - 1, tau, nu), k);
-    for (int64_t tau = 0; tau < ((int64_t)1 << l); ++tau)
-      for (int64_t nu = 0; nu < ((int64_t)1 << (L - l)); ++nu) {
+    /* each (parent tau, nu) pair owns its two outputs; the two children tau
+     * are added in the sequential order (2 ptau, then 2 ptau + 1) */
+    const int64_t wide = (int64_t)1 << (L - l);
+#pragma omp parallel for schedule(static) num_threads(nt)
+    for (int64_t q = 0; q < (nb >> 1); ++q) {
+      const int64_t ptau = q / wide, nu = q % wide;
+      for (int64_t tau = 2 * ptau; tau <= 2 * ptau + 1; ++tau) {
         const bo_mat* w = bo_w_block(bf, l, tau, nu);
         const bo_mat* ai = &a[bo_bidx(L, l, tau, nu)];
         bo_mat e = bo_mat_new(w->rows, k);
         bo_gemm('N', w->rows, k, w->cols, w->a, w->rows, ai->a, ai->rows, e.a, e.rows, 0);
-        int64_t ptau = tau / 2;
         bo_mat* t0 = &prev[bo_bidx(L, l - 1, ptau, 2 * nu)];
         bo_mat* t1 = &prev[bo_bidx(L, l - 1, ptau, 2 * nu + 1)];
         int64_t top = t0->rows;
@@ -260,10 +282,12 @@ static void apply_h(const bo_bf* bf, const bo_cplx* y, int64_t k, bo_cplx* x) {
         }
         bo_mat_free(&e);
       }
+    }
     free_vec(a, nb);
     a = prev;
   }
   bo_cplx* xt = (bo_cplx*)calloc((size_t)(n * k), sizeof(bo_cplx));
+#pragma omp parallel for schedule(static) num_threads(nt)
   for (int64_t nu = 0; nu < nb; ++nu) {
     const bo_mat* v = &bf->v_leaf[nu];
     int64_t b = bo_node_b(bf->col_tree, L, nu);

@@ -96,20 +96,39 @@ static void note_probe_bytes(bo_factorizer* f, int64_t scalars) {
   if (f->log.peak_concurrent_probes < 1) f->log.peak_concurrent_probes = 1;
 }
 
-/* truncate_basis (reconstruct.hpp:344-348): rank-0 for empty or all-zero input */
+/* Rank margin at the truncation cut (diagnostic, SURVEY 7 hard part 1): how
+ * far the last kept and the first dropped pivot |R_kk| lie from the threshold
+ * eps |R_00| (linalg.hpp:74-77), relative to it:
+ *   min(|R_{k-1}| / thr - 1, 1 - |R_k| / thr);  +inf for a zero block.
+ * A margin near 0 means a rank that rounding could flip. */
+double bo_cut_margin(const double* rd, int64_t size, int64_t k, double eps) {
+  if (k <= 0 || size <= 0 || rd[0] == 0.0) return HUGE_VAL;
+  double thr = eps * rd[0], m = rd[k - 1] / thr - 1.0;
+  if (k < size && 1.0 - rd[k] / thr < m) m = 1.0 - rd[k] / thr;
+  return m;
+}
+
+/* truncate_basis (reconstruct.hpp:344-348): rank-0 for empty or all-zero input;
+ * *margin = the block's cut margin */
 static void truncate_basis(const bo_factorizer* f, int64_t rows, int64_t cols, const bo_cplx* z,
-                           int64_t ldz, bo_mat* out) {
+                           int64_t ldz, bo_mat* out, double* margin) {
   int64_t size = rows < cols ? rows : cols;
+  *margin = HUGE_VAL;
   if (rows == 0 || cols == 0) {
     *out = bo_mat_new(rows, 0);
     return;
   }
   bo_cplx* q = (bo_cplx*)malloc(sizeof(bo_cplx) * (size_t)(rows * size));
+  double* rd = (double*)malloc(sizeof(double) * (size_t)size);
   int64_t k = 0;
-  bo_cpqr_truncate(rows, cols, z, ldz, TRUNCATION_SAFETY * f->cfg.tolerance, q, &k, NULL, NULL);
+  const double eps = TRUNCATION_SAFETY * f->cfg.tolerance;
+  rd[0] = 0.0;
+  bo_cpqr_truncate(rows, cols, z, ldz, eps, q, &k, NULL, rd);
+  *margin = bo_cut_margin(rd, size, k, eps);
   *out = bo_mat_new(rows, k);
   if (k) memcpy(out->a, q, sizeof(bo_cplx) * (size_t)(rows * k));
   free(q);
+  free(rd);
 }
 
 static bo_phase* new_phase(bo_factorizer* f, const char* name) {
@@ -167,17 +186,21 @@ static void leaf_phase(bo_factorizer* f, const char* name, int row_side) {
     bo_cplx* pt = (bo_cplx*)malloc(sizeof(bo_cplx) * (size_t)(out_h * width));
     gather(slice, prod, width, pt);
     int64_t max_rank = 0;
-#pragma omp parallel for schedule(dynamic) num_threads(f->cfg.threads) reduction(max : max_rank)
+    double mg = HUGE_VAL;
+#pragma omp parallel for schedule(dynamic) num_threads(f->cfg.threads) reduction(max : max_rank) reduction(min : mg)
     for (int64_t leaf = 0; leaf < nb; ++leaf) {
       int64_t b = bo_node_b(slice, bf->levels, leaf), e = bo_node_e(slice, bf->levels, leaf);
       bo_mat_free(&out[leaf]);
-      truncate_basis(f, e - b, width, pt + b, out_h, &out[leaf]);
+      double m1;
+      truncate_basis(f, e - b, width, pt + b, out_h, &out[leaf], &m1);
+      if (m1 < mg) mg = m1;
       if (out[leaf].cols > max_rank) max_rank = out[leaf].cols;
     }
     free(omega);
     free(prod);
     free(pt);
     st->rounds = round;
+    st->rank_margin = mg; /* the kept (last) round's blocks */
     if (r > max_rank) break;
     if (r >= hard_cap) {
       f->log.rank_capped = 1;
@@ -230,6 +253,7 @@ int bo_factorizer_transfer_w(bo_factorizer* f, int l) {
   bo_bf* bf = f->bf;
   int L = bf->levels;
   int64_t ntau = (int64_t)1 << l, nnu = (int64_t)1 << (L - l), n = bf->col_tree->n;
+  double mg = HUGE_VAL;
   for (int64_t tau = 0; tau < ntau; ++tau) {
     int64_t bound = 0;
     for (int64_t nu = 0; nu < nnu; ++nu) {
@@ -253,7 +277,7 @@ int bo_factorizer_transfer_w(bo_factorizer* f, int l) {
     note_probe_bytes(f, (he - hb) * width + n * width);
     bo_cplx* xt = (bo_cplx*)malloc(sizeof(bo_cplx) * (size_t)(n * width));
     gather(bf->col_tree, x, width, xt);
-#pragma omp parallel for schedule(dynamic) num_threads(f->cfg.threads)
+#pragma omp parallel for schedule(dynamic) num_threads(f->cfg.threads) reduction(min : mg)
     for (int64_t nu = 0; nu < nnu; ++nu) {
       int cl = L - l + 1;
       int64_t b1 = bo_node_b(bf->col_tree, cl, 2 * nu), b2 = bo_node_b(bf->col_tree, cl, 2 * nu + 1);
@@ -263,13 +287,16 @@ int bo_factorizer_transfer_w(bo_factorizer* f, int l) {
       bo_mat z = stack_mats(&top, &bot, width);
       bo_mat* w = bo_w_block(bf, l, tau, nu);
       bo_mat_free(w);
-      truncate_basis(f, z.rows, z.cols, z.a, z.rows, w);
+      double m1;
+      truncate_basis(f, z.rows, z.cols, z.a, z.rows, w, &m1);
+      if (m1 < mg) mg = m1;
       bo_mat_free(&top); bo_mat_free(&bot); bo_mat_free(&z);
     }
     free(core);
     free(x);
     free(xt);
   }
+  st->rank_margin = mg;
   int64_t f1, tr1;
   bo_op_counters(f->op, &f1, &tr1);
   st->forward_columns = f1 - f0;
@@ -356,6 +383,7 @@ int bo_factorizer_transfer_r(bo_factorizer* f, int l) {
   int at_center = l == bf->center;
   int64_t ntau = (int64_t)1 << l, nnu = (int64_t)1 << (L - l), m = bf->row_tree->n;
   int err = BO_OK;
+  double mg = HUGE_VAL;
   for (int64_t nu = 0; nu < nnu && err == BO_OK; ++nu) {
     int64_t bound = 0;
     for (int64_t tau = 0; tau < ntau; ++tau) {
@@ -385,7 +413,7 @@ int bo_factorizer_transfer_r(bo_factorizer* f, int l) {
     note_probe_bytes(f, (se - sb) * width + m * width);
     bo_cplx* yt = (bo_cplx*)malloc(sizeof(bo_cplx) * (size_t)(m * width));
     gather(bf->row_tree, y, width, yt);
-#pragma omp parallel for schedule(dynamic) num_threads(f->cfg.threads)
+#pragma omp parallel for schedule(dynamic) num_threads(f->cfg.threads) reduction(min : mg)
     for (int64_t tau = 0; tau < ntau; ++tau) {
       int64_t b1 = bo_node_b(bf->row_tree, l + 1, 2 * tau), b2 = bo_node_b(bf->row_tree, l + 1, 2 * tau + 1);
       bo_mat top, bot;
@@ -393,7 +421,9 @@ int bo_factorizer_transfer_r(bo_factorizer* f, int l) {
       bo_u_chain(bf, l + 1, 2 * tau + 1, nu / 2, yt + b2, m, width, &bot);
       bo_mat z = stack_mats(&top, &bot, width);
       bo_mat r;
-      truncate_basis(f, z.rows, z.cols, z.a, z.rows, &r);
+      double m1;
+      truncate_basis(f, z.rows, z.cols, z.a, z.rows, &r, &m1);
+      if (m1 < mg) mg = m1;
       if (at_center) {
         bo_mat coeff;
         bo_v_chain(bf, bf->center, tau, nu, core, se - sb, width, &coeff);
@@ -416,6 +446,7 @@ int bo_factorizer_transfer_r(bo_factorizer* f, int l) {
     free(yt);
   }
   if (err != BO_OK) return err;
+  st->rank_margin = mg;
   int64_t f1, tr1;
   bo_op_counters(f->op, &f1, &tr1);
   st->forward_columns = f1 - f0;

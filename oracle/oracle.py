@@ -379,7 +379,8 @@ class _Cfg(C.Structure):
 
 class _Phase(C.Structure):
     _fields_ = [("name", C.c_char * 32), ("forward_columns", C.c_int64), ("transpose_columns", C.c_int64),
-                ("seconds", C.c_double), ("rounds", C.c_int), ("probe_width", C.c_int64)]
+                ("seconds", C.c_double), ("rounds", C.c_int), ("probe_width", C.c_int64),
+                ("rank_margin", C.c_double)]
 
 
 class _Log(C.Structure):
@@ -401,7 +402,7 @@ def _log_dict(lg: _Log):
         p = lg.phases[i]
         phases.append(dict(name=p.name.decode(), forward_columns=p.forward_columns,
                            transpose_columns=p.transpose_columns, seconds=p.seconds,
-                           rounds=p.rounds, probe_width=p.probe_width))
+                           rounds=p.rounds, probe_width=p.probe_width, rank_margin=p.rank_margin))
     return dict(phases=phases, peak_probe_bytes=lg.peak_probe_bytes,
                 peak_concurrent_probes=lg.peak_concurrent_probes, rank_capped=bool(lg.rank_capped),
                 total_seconds=lg.total_seconds)

@@ -308,6 +308,20 @@ int ref_log(const ref_bf* b, int64_t* cols /* 2 per phase */, int32_t* rounds, i
   return i;
 }
 
+// PhaseStat::seconds / name (reconstruct.hpp:87-120) of every phase; returns the count
+int ref_phase_seconds(const ref_bf* b, double* seconds, char* names /* 32 bytes per phase */) {
+  int i = 0;
+  for (const auto& p : b->log.phases) {
+    if (seconds) seconds[i] = p.seconds;
+    if (names) {
+      std::memset(names + 32 * i, 0, 32);
+      std::strncpy(names + 32 * i, p.name.c_str(), 31);
+    }
+    ++i;
+  }
+  return i;
+}
+
 double ref_estimate_error(ref_op* h, const ref_bf* b, int64_t k, uint64_t seed) {
   double e = -1;
   guard([&] { e = estimate_error<cplx>(*h->op, b->bf, k, seed); });

@@ -34,6 +34,7 @@ def lib():
             "ref_apply": (i32, [p, i32, p, i64, p]),
             "ref_log": (i32, [p, p, p, p, p]),
             "ref_estimate_error": (dbl, [p, p, i64, u64]),
+            "ref_phase_seconds": (i32, [p, p, p]),
             "ref_serialize": (i64, [p, p]),
             "ref_bf_free": (None, [p]),
             "ref_probe_sample": (dbl, [p, i32, i32, i64, u64]),
@@ -125,6 +126,14 @@ class RefButterfly:
         tot = C.c_double()
         n = lib().ref_log(self.h, _vp(cols), _vp(rounds), _vp(widths), C.byref(tot))
         return [(int(cols[2 * i]), int(cols[2 * i + 1]), int(rounds[i]), int(widths[i])) for i in range(n)], tot.value
+
+    def phase_seconds(self):
+        """[(name, seconds)] of the reference's FactorizationLog (reconstruct.hpp:87-120)."""
+        n = lib().ref_phase_seconds(self.h, None, None)
+        sec = np.zeros(n)
+        names = np.zeros(32 * n, np.uint8)
+        lib().ref_phase_seconds(self.h, _vp(sec), _vp(names))
+        return [(bytes(names[32 * i: 32 * i + 32]).split(b"\0")[0].decode(), float(sec[i])) for i in range(n)]
 
     def estimate_error(self, k=16, seed=0):
         """estimate_error(op, bf, k, seed) of the reference (reconstruct.hpp:423-434)."""

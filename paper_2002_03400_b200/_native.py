@@ -63,7 +63,8 @@ class Cfg(C.Structure):
 
 class Phase(C.Structure):
     _fields_ = [("name", C.c_char * 32), ("forward_columns", C.c_int64), ("transpose_columns", C.c_int64),
-                ("seconds", C.c_double), ("rounds", C.c_int32), ("probe_width", C.c_int64)]
+                ("seconds", C.c_double), ("rounds", C.c_int32), ("probe_width", C.c_int64),
+                ("rank_margin", C.c_double)]
 
 
 class Log(C.Structure):
@@ -74,6 +75,21 @@ class Log(C.Structure):
 
 APPLY_FN = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_int, C.c_void_p, C.c_int64, C.c_void_p, C.c_int64, C.c_int64,
                        C.c_void_p)
+APPLY_RANGE_FN = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_int, C.c_void_p, C.c_int64, C.c_void_p, C.c_int64, C.c_int64,
+                             C.c_int64, C.c_int64, C.c_void_p)
+
+
+# bfly_host_comm (include/bfly_b200.h): host-staged collectives supplied by the caller
+HC_ALLGATHER = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_void_p, C.c_void_p, C.c_int64)
+HC_ALLREDUCE = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_void_p, C.c_int64, C.c_int, C.c_int)
+HC_SENDRECV = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_int, C.POINTER(C.c_int32), C.POINTER(C.c_void_p),
+                          C.POINTER(C.c_int64), C.c_int, C.POINTER(C.c_int32), C.POINTER(C.c_void_p),
+                          C.POINTER(C.c_int64))
+
+
+class HostCommFns(C.Structure):
+    _fields_ = [("user", C.c_void_p), ("allgather", HC_ALLGATHER), ("allreduce", HC_ALLREDUCE),
+                ("sendrecv", HC_SENDRECV)]
 
 
 def lib():
@@ -97,6 +113,8 @@ def lib():
         "bfly_ctx_profile_report": (i64, [p, C.c_char_p, i64]),
         "bfly_comm_unique_id": (i32, [p]),
         "bfly_ctx_set_comm": (i32, [p, i32, i32, p]),
+        "bfly_ctx_set_host_comm": (i32, [p, i32, i32, C.POINTER(HostCommFns)]),
+        "bfly_ctx_comm_info": (i32, [p, C.POINTER(C.c_int), C.POINTER(C.c_int), C.POINTER(C.c_int)]),
         "bfly_tree_build": (i32, [i32, i64, p, i32, pp]),
         "bfly_tree_from_table": (i32, [i64, i32, p, p, pp]),
         "bfly_tree_info": (i32, [p, C.POINTER(C.c_int64), C.POINTER(C.c_int)]),
@@ -111,6 +129,7 @@ def lib():
         "bfly_op_dense": (i32, [p, i64, i64, p, i32, pp]),
         "bfly_op_butterfly": (i32, [p, p, pp]),
         "bfly_op_callback": (i32, [p, i64, i64, i32, APPLY_FN, p, pp]),
+        "bfly_op_callback_ranged": (i32, [p, i64, i64, i32, APPLY_RANGE_FN, p, pp]),
         "bfly_op_info": (i32, [p, C.POINTER(C.c_int64), C.POINTER(C.c_int64), C.POINTER(C.c_int), C.POINTER(C.c_int)]),
         "bfly_op_apply": (i32, [p, i32, p, i64, p, i64, i64, i32]),
         "bfly_op_counters": (i32, [p, C.POINTER(C.c_int64), C.POINTER(C.c_int64)]),

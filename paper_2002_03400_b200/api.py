@@ -18,8 +18,8 @@ from typing import Optional
 
 import numpy as np
 
-from ._native import (APPLY_FN, BflyError, ConditioningError, Cfg, CudaError, DimensionError, FormatError, Log,
-                      NcclError, PreconditionError, SequencingError, check, lib)
+from ._native import (APPLY_FN, APPLY_RANGE_FN, BflyError, ConditioningError, Cfg, CudaError, DimensionError,
+                      FormatError, Log, NcclError, PreconditionError, SequencingError, check, lib)
 
 COMPLEX128, COMPLEX64, REAL64 = 0, 1, 2
 _NP = {COMPLEX128: np.complex128, COMPLEX64: np.complex64, REAL64: np.float64}
@@ -87,6 +87,23 @@ class Context:
     def set_comm(self, rank: int, world: int, unique_id: bytes):
         buf = (C.c_uint8 * 128).from_buffer_copy(unique_id.ljust(128, b"\0")[:128])
         check(lib().bfly_ctx_set_comm(self.h, rank, world, buf))
+
+    def set_host_comm(self, group=None):
+        """Join the host-staged transport over an initialized torch.distributed
+        process group (gloo): same sharded schedule as set_comm, every exchange
+        staged through pinned host memory (ranks may share one GPU)."""
+        from .hostcomm import TorchHostComm
+
+        hc = TorchHostComm(group)
+        check(lib().bfly_ctx_set_host_comm(self.h, hc.rank, hc.world, C.byref(hc.fns)))
+        self._host_comm = hc  # the library holds its function pointers
+        return hc
+
+    def comm_info(self):
+        """(rank, world, transport) with transport 'none' | 'nccl' | 'host'."""
+        r, w, t = C.c_int(), C.c_int(), C.c_int()
+        check(lib().bfly_ctx_comm_info(self.h, C.byref(r), C.byref(w), C.byref(t)))
+        return r.value, w.value, ("none", "nccl", "host")[t.value]
 
     @staticmethod
     def unique_id() -> bytes:
@@ -206,15 +223,37 @@ class _Applicable:
         if _is_torch_cuda(x):
             import torch
 
+            # the device kernels read and write the object's own scalar type
+            want = {COMPLEX128: torch.complex128, COMPLEX64: torch.complex64, REAL64: torch.float64}[self.scalar]
             if x.dim() == 1:
                 x = x.reshape(-1, 1)
-            # column-major (ld = rows): a transposed contiguous tensor
-            xt = x.t().contiguous().t() if not (x.stride(0) == 1) else x
-            k = xt.shape[1]
-            y = out if out is not None else torch.empty((k, self._rows_out(trans)), dtype=x.dtype, device=x.device).t()
+            if x.dim() != 2:
+                raise DimensionError(f"apply: X must be 1-D or 2-D, got {x.dim()}-D")
+            if x.shape[0] != self._rows_in(trans):
+                raise DimensionError(f"apply: X row count {x.shape[0]} != {self._rows_in(trans)}")
+            if x.dtype != want:
+                if x.is_complex() and not want.is_complex:
+                    raise PreconditionError(f"apply: complex input for a real ({want}) object")
+                x = x.to(want)
+            k, rows_out = x.shape[1], self._rows_out(trans)
+
+            def ld_of(t):  # column-major leading dimension (a single column may report any stride)
+                return max(t.stride(1), t.shape[0]) if t.shape[1] == 1 else t.stride(1)
+
+            def colmajor(t):
+                return t.stride(0) == 1 and ld_of(t) >= t.shape[0]
+
+            # column-major (ld >= rows): a transposed contiguous tensor
+            xt = x if colmajor(x) else x.t().contiguous().t()
+            if out is not None:
+                if out.dtype != want or tuple(out.shape) != (rows_out, k) or not colmajor(out) or not out.is_cuda:
+                    raise DimensionError(f"apply: out must be a column-major {want} CUDA tensor of shape "
+                                         f"({rows_out}, {k})")
+                y = out
+            else:
+                y = torch.empty((k, rows_out), dtype=want, device=x.device).t()
             torch.cuda.current_stream().synchronize()
-            check(self._apply_fn(trans, C.c_void_p(xt.data_ptr()), xt.stride(1), C.c_void_p(y.data_ptr()),
-                                 y.stride(1), k, 1))
+            check(self._apply_fn(trans, C.c_void_p(xt.data_ptr()), ld_of(xt), C.c_void_p(y.data_ptr()), ld_of(y), k, 1))
             self._ctx().synchronize()
             return y
         a = _host_in(x, self.scalar)
@@ -378,22 +417,38 @@ class ButterflyOperator(BlackBoxOperator):
 
 class CallbackOperator(BlackBoxOperator):
     """User black box: fn(trans, x_ptr, ldx, y_ptr, ldy, k, stream) -> int on
-    device buffers (trans 0 = A x, 1 = A^T y)."""
+    device buffers (trans 0 = A x, 1 = A^T y).  ranged=True: fn(trans, x_ptr,
+    ldx, y_ptr, ldy, k, nz_begin, nz_end, stream), called once per structured
+    probe with its nonzero input rows [nz_begin, nz_end) (bfly_apply_range_fn)."""
 
     kind = OP_CALLBACK
 
-    def __init__(self, m, n, fn, scalar=COMPLEX128, ctx=None):
+    def __init__(self, m, n, fn, scalar=COMPLEX128, ctx=None, ranged=False):
         ctx = _ctx(ctx)
 
-        def tramp(user, trans, x, ldx, y, ldy, k, stream):
-            try:
-                return int(fn(trans, x, ldx, y, ldy, k, stream) or 0)
-            except Exception:  # surfaced as a failed black-box call
-                return 5
+        if ranged:
+            def tramp(user, trans, x, ldx, y, ldy, k, b, e, stream):
+                try:
+                    return int(fn(trans, x, ldx, y, ldy, k, b, e, stream) or 0)
+                except Exception:  # surfaced as a failed black-box call
+                    import traceback
 
-        self._cb = APPLY_FN(tramp)
+                    traceback.print_exc()
+                    return 5
+
+            self._cb = APPLY_RANGE_FN(tramp)
+            register = lib().bfly_op_callback_ranged
+        else:
+            def tramp(user, trans, x, ldx, y, ldy, k, stream):
+                try:
+                    return int(fn(trans, x, ldx, y, ldy, k, stream) or 0)
+                except Exception:  # surfaced as a failed black-box call
+                    return 5
+
+            self._cb = APPLY_FN(tramp)
+            register = lib().bfly_op_callback
         h = C.c_void_p()
-        check(lib().bfly_op_callback(ctx.h, m, n, scalar, self._cb, None, C.byref(h)))
+        check(register(ctx.h, m, n, scalar, self._cb, None, C.byref(h)))
         super().__init__(h, ctx, scalar)
 
 
@@ -434,6 +489,9 @@ class PhaseStat:
     seconds: float
     rounds: int
     probe_width: int
+    # CPQR cut margin (bfly_phase.rank_margin): min over the phase's blocks of
+    # min(|R_{k-1}|/thr - 1, 1 - |R_k|/thr), thr = 0.25 tol |R_00|; inf: none
+    rank_margin: float = float("inf")
 
 
 @dataclasses.dataclass
@@ -450,7 +508,8 @@ class FactorizationLog:
 
     @staticmethod
     def _from(lg: Log) -> "FactorizationLog":
-        ph = [PhaseStat(p.name.decode(), p.forward_columns, p.transpose_columns, p.seconds, p.rounds, p.probe_width)
+        ph = [PhaseStat(p.name.decode(), p.forward_columns, p.transpose_columns, p.seconds, p.rounds, p.probe_width,
+                        p.rank_margin)
               for p in lg.phases[: lg.nphases]]
         return FactorizationLog(ph, lg.peak_probe_bytes, lg.peak_concurrent_probes, bool(lg.rank_capped),
                                 lg.total_seconds, lg.flops, lg.kernel_evals)

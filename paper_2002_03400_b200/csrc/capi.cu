@@ -298,6 +298,17 @@ int bfly_comm_unique_id(uint8_t* id_out) {
 int bfly_ctx_set_comm(bfly_ctx* ctx, int rank, int world, const uint8_t* id) {
   return guard(C_(ctx), [&] { comm_init(C_(ctx), rank, world, id); });
 }
+int bfly_ctx_set_host_comm(bfly_ctx* ctx, int rank, int world, const bfly_host_comm* hc) {
+  return guard(C_(ctx), [&] { comm_init_host(C_(ctx), rank, world, hc); });
+}
+int bfly_ctx_comm_info(const bfly_ctx* ctx, int* rank, int* world, int* transport) {
+  if (!ctx) return BFLY_PRECONDITION;
+  const Ctx* c = ctx->c.get();
+  if (rank) *rank = c->rank;
+  if (world) *world = c->world;
+  if (transport) *transport = c->comm ? 1 : c->host ? 2 : 0;
+  return BFLY_OK;
+}
 
 // ------------------------------------------------------------------ trees
 int bfly_tree_build(int dim, int64_t n, const double* coords, int levels, bfly_tree** out) {
@@ -443,6 +454,20 @@ int bfly_op_callback(bfly_ctx* ctx, int64_t m, int64_t n, int scalar, bfly_apply
   });
 }
 
+int bfly_op_callback_ranged(bfly_ctx* ctx, int64_t m, int64_t n, int scalar, bfly_apply_range_fn fn, void* user,
+                            bfly_op** out) {
+  *out = nullptr;
+  return guard(C_(ctx), [&] {
+    check_scalar(scalar);
+    auto h = std::make_unique<bfly_op>();
+    h->ctx = ctx;
+    h->scalar = scalar;
+    if (scalar == BFLY_C) h->c = make_callback_range_op<float>(C_(ctx), m, n, false, fn, user);
+    else h->z = make_callback_range_op<double>(C_(ctx), m, n, scalar == BFLY_D, fn, user);
+    *out = h.release();
+  });
+}
+
 int bfly_op_info(const bfly_op* op, int64_t* m, int64_t* n, int* scalar, int* kind) {
   if (!op) return BFLY_PRECONDITION;
   if (m) *m = op->m();
@@ -580,8 +605,13 @@ int bfly_factorize(bfly_ctx* ctx, bfly_op* op, const bfly_tree* rt, const bfly_t
     counters(cv, cw, true);
     struct Reset {
       Ctx* c;
-      ~Reset() { c->oz_deferred = c->force_fp64 = false; }
+      ~Reset() {
+        // an exception may leave a flag set by a launch of the failed run
+        if (c->oz_deferred) c->clear_oz_flag();
+        c->oz_deferred = c->force_fp64 = false;
+      }
     } reset{c};
+    c->clear_oz_flag();
     c->oz_deferred = true;
     run_once();
     c->oz_deferred = false;

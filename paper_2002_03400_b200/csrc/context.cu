@@ -130,6 +130,10 @@ void Ctx::resolve_records() {
   records.clear();
 }
 
+void Ctx::clear_oz_flag() {
+  if (oz_flag) BFLY_CUDA(cudaMemsetAsync(oz_flag, 0, sizeof(int), stream));
+}
+
 int* Ctx::oz_flag_dev() {
   if (!oz_flag) {
     BFLY_CUDA(cudaMalloc(&oz_flag, sizeof(int)));
@@ -139,8 +143,11 @@ int* Ctx::oz_flag_dev() {
 }
 
 bool Ctx::take_oz_overflow() {
+  // every rank must join the all-reduce, including a rank that launched no
+  // K2 product (its flag is created here, zero)
+  if (comm_active(this)) oz_flag_dev();
   if (!oz_flag) return false;
-  if (world > 1 && comm) comm_allreduce_max_i32(this, oz_flag, 1);
+  if (comm_active(this)) comm_allreduce_max_i32(this, oz_flag, 1);
   int h = 0;
   BFLY_CUDA(cudaMemcpyAsync(&h, oz_flag, sizeof(int), cudaMemcpyDeviceToHost, stream));
   BFLY_CUDA(cudaStreamSynchronize(stream));

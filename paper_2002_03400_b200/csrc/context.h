@@ -6,14 +6,35 @@
 
 #include <cstdint>
 #include <cstring>
+#include <memory>
 #include <utility>
 #include <vector>
 
+#include "../../include/bfly_b200.h"
 #include "common.cuh"
 
 struct ncclComm;
 
 namespace bfly {
+
+struct Ctx;
+// host-staged transport (bfly_ctx_set_host_comm): the caller's collectives +
+// pinned staging buffers + the point-to-point group being assembled
+struct HostComm {
+  bfly_host_comm fns{};
+  unsigned char* buf[2] = {nullptr, nullptr};
+  size_t cap[2] = {0, 0};
+  struct Xfer {
+    bool send;
+    int peer;
+    void* dev;
+    size_t bytes;
+  };
+  std::vector<Xfer> pending;
+  bool grouped = false;
+  unsigned char* stage(Ctx* c, int slot, size_t bytes);
+  ~HostComm();
+};
 
 // Per-kernel device timing (CUDA events on the library stream) for the
 // roofline numbers; off unless requested, resolved lazily.
@@ -40,6 +61,7 @@ struct Ctx {
   // multi-GPU (rank-sharded probes + NCCL all-gather of each level)
   int rank = 0, world = 1;
   ncclComm* comm = nullptr;
+  std::unique_ptr<HostComm> host;  // host-staged transport (instead of NCCL)
 
   explicit Ctx(int dev);
   ~Ctx();
@@ -66,6 +88,7 @@ struct Ctx {
   int* oz_flag = nullptr;
   int* oz_flag_dev();
   bool take_oz_overflow();  // all ranks agree; resets the flag
+  void clear_oz_flag();     // drop a stale flag (start of a factorization / error path)
   // pool sizing: a factorization reserves one contiguous chunk sized to the
   // previous one's peak (see reserve_pool)
   size_t pool_reserved = 0, pool_hint = 0, pool_used_start = 0;

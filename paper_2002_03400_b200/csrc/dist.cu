@@ -238,7 +238,7 @@ void DevButterfly<R>::apply_layout(int trans, int kind, int p, const cx<R>* x, i
             so += (size_t)cnt;
           }
         }
-        comm_group_start();
+        comm_group_start(c);
         so = 0;
         for (const auto& xf : dp.xfers[s]) {
           const size_t cnt = xf.offs.size() * (size_t)rows * k;
@@ -252,7 +252,7 @@ void DevButterfly<R>::apply_layout(int trans, int kind, int p, const cx<R>* x, i
             ro += cnt;
           }
         }
-        comm_group_end();
+        comm_group_end(c);
         for (const auto& in : ins) {
           const int nblk = (int)in.first->offs.size();
           const int64_t cnt = (int64_t)nblk * rows * k;

@@ -50,6 +50,12 @@ class Factorizer {
   bool v_done_ = false, u_done_ = false, core_done_ = false;
   int next_w_ = 1, next_r_ = 0;
   double flops_ = 0;  // chain + QR + core-fit work (black box counted by the operator)
+  // CPQR cut margin of every block of the current phase (bfly_phase::rank_margin)
+  DBuf<double> margin_;
+  double* margins_reset();
+  // memory guard: probes per launch that fit next to the level (0: no limit)
+  int64_t guard_batch_ = 0;
+  void memory_guard(const std::string& what, double level_bytes, double per_probe_bytes, int64_t nprobes);
   // sharding
   int world_ = 1, rank_ = 0;
   bool virtual_ = false;

@@ -879,10 +879,11 @@ void launch_bgemm(Ctx* c, int op, int M, int K, int S, const cx<R>* A, int64_t l
     auto kern = bgemm_stage_kernel<R, OPV, SV, false>;                                                      \
     if constexpr (std::is_same<R, double>::value)                                                           \
       if (stage_dm) kern = bgemm_stage_kernel<R, OPV, SV, true>;                                            \
-    static bool attr_set[2] = {false, false}; /* first use is eager (never inside graph capture) */        \
-    if (!attr_set[stage_dm]) {                                                                              \
+    /* per device (a process may hold contexts on several GPUs); first use is eager, never in capture */  \
+    static uint64_t attr_set[2] = {0, 0};                                                                   \
+    if (!((attr_set[stage_dm] >> (c->device & 63)) & 1)) {                                                  \
       BFLY_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));        \
-      attr_set[stage_dm] = true;                                                                            \
+      attr_set[stage_dm] |= uint64_t(1) << (c->device & 63);                                                \
     }                                                                                                       \
     BFLY_CUDA(cudaLaunchKernelEx(&cfg, kern, A, lda, B, ldb, C, ldc, M, K, ents, nent, (int)accumulate, kcols, wpe, pf)); \
   } while (0)
@@ -905,10 +906,10 @@ void launch_bgemm(Ctx* c, int op, int M, int K, int S, const cx<R>* A, int64_t l
 #define BGS(OPV, SV)                                                                                           \
   do {                                                                                                         \
     auto kern = bgemm_small_kernel<R, OPV, SV>;                                                                \
-    static size_t attr_bytes = 48 * 1024; /* set once per kernel, never during graph capture */              \
-    if (small_smem > attr_bytes) {                                                                             \
+    static uint64_t attr_96k = 0; /* per device: set once per kernel, never during graph capture */          \
+    if (small_smem > 48 * 1024 && !((attr_96k >> (c->device & 63)) & 1)) {                                     \
       BFLY_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024));           \
-      attr_bytes = 96 * 1024;                                                                                  \
+      attr_96k |= uint64_t(1) << (c->device & 63);                                                             \
     }                                                                                                          \
     if (pdl) {                                                                                                 \
       cudaLaunchConfig_t cfg = {};                                                                             \
@@ -991,10 +992,10 @@ void launch_bgemm(Ctx* c, int op, int M, int K, int S, const cx<R>* A, int64_t l
   do {                                                                                                          \
     auto kern = bgemm_dmma_kernel<OPV, SV, MTV, WNV, NTV>;                                                      \
     const int smem = (int)dmma_smem_bytes(OPV, MTV, WNV, NTV);                                                  \
-    static bool attr_set = false; /* first use is eager (never inside graph capture) */                        \
-    if (!attr_set) {                                                                                            \
+    static uint64_t attr_set = 0; /* per device; first use is eager (never inside graph capture) */           \
+    if (!((attr_set >> (c->device & 63)) & 1)) {                                                                \
       BFLY_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));                  \
-      attr_set = true;                                                                                          \
+      attr_set |= uint64_t(1) << (c->device & 63);                                                              \
     }                                                                                                           \
     launch_pdl_smem(kern, grid, 128 * WNV, smem, c->stream, pdl, A, lda, B, ldb, C, ldc, M, K, ents, accumulate, \
                     ncols_all);                                                                                 \

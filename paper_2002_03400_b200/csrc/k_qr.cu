@@ -48,7 +48,7 @@ template <typename R, int QR_THREADS>
 __global__ void __launch_bounds__(QR_THREADS) cpqr_kernel(const cx<R>* __restrict__ src, int64_t ld_src,
                                                           cx<R>* __restrict__ dst, int64_t ld_dst, int cap,
                                                           const QrEnt* __restrict__ ents, int32_t* ranks, double eps_t,
-                                                          int zld, cx<R>* zglobal, int64_t zstride) {
+                                                          int zld, cx<R>* zglobal, int64_t zstride, double* margins) {
   using V = cx<R>;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const QrEnt e = ents[blockIdx.x];
@@ -67,7 +67,10 @@ __global__ void __launch_bounds__(QR_THREADS) cpqr_kernel(const cx<R>* __restric
   V* out = dst + e.dst;
   if (r == 0 || w == 0) {
     for (int64_t i = threadIdx.x; i < ld_dst * cap; i += QR_THREADS) out[i] = mkc<R>(0, 0);
-    if (threadIdx.x == 0) ranks[e.rank_slot] = 0;
+    if (threadIdx.x == 0) {
+      ranks[e.rank_slot] = 0;
+      if (margins) margins[e.rank_slot] = HUGE_VAL;
+    }
     return;
   }
   // load the compact block
@@ -92,11 +95,14 @@ __global__ void __launch_bounds__(QR_THREADS) cpqr_kernel(const cx<R>* __restric
   __syncthreads();
   if (s_total == R(0)) {  // all-zero input: rank 0 (linalg.hpp:67-71)
     for (int64_t i = threadIdx.x; i < ld_dst * cap; i += QR_THREADS) out[i] = mkc<R>(0, 0);
-    if (threadIdx.x == 0) ranks[e.rank_slot] = 0;
+    if (threadIdx.x == 0) {
+      ranks[e.rank_slot] = 0;
+      if (margins) margins[e.rank_slot] = HUGE_VAL;
+    }
     return;
   }
   const int kmax = min(r, w);
-  R head = 0;
+  R head = 0, last_kept = 0, first_dropped = -1;
   int k = kmax;
   for (int j = 0; j < kmax; ++j) {
     // ---- pivot: first column with the largest updated norm
@@ -161,8 +167,10 @@ __global__ void __launch_bounds__(QR_THREADS) cpqr_kernel(const cx<R>* __restric
     if (j == 0) head = absb;
     if (!(absb > R(eps_t) * head)) {
       k = j;
+      first_dropped = absb;
       break;
     }
+    last_kept = absb;
     // ---- apply H_j = I - tau v v^H to the trailing columns; downdate norms
     const V tj = tau[j];
     for (int c = j + 1 + warp; c < w; c += (QR_THREADS / 32)) {
@@ -202,7 +210,16 @@ __global__ void __launch_bounds__(QR_THREADS) cpqr_kernel(const cx<R>* __restric
     }
     __syncthreads();
   }
-  if (threadIdx.x == 0) s_k = k;
+  if (threadIdx.x == 0) {
+    s_k = k;
+    // rank margin at the cut (diagnostic): min(|R_{k-1}|/thr - 1, 1 - |R_k|/thr), thr = eps |R_00|
+    if (margins) {
+      const double thr = eps_t * (double)head;
+      double m = (double)last_kept / thr - 1.0;
+      if (first_dropped >= R(0)) m = fmin(m, 1.0 - (double)first_dropped / thr);
+      margins[e.rank_slot] = m;
+    }
+  }
   __syncthreads();
   k = s_k;
   // ---- form Q(:, 0:k) in place: Q = H_0 ... H_{k-1} [I_k; 0], H_i = I - conj(tau_i) v v^H
@@ -394,7 +411,7 @@ __global__ void __launch_bounds__(QR_THREADS) core_fit_kernel(const cx<R>* __res
 
 template <typename R>
 void launch_cpqr(Ctx* c, const cx<R>* src, int64_t ld_src, cx<R>* dst, int64_t ld_dst, int cap, const QrEnt* ents,
-                 int nent, int max_rows, int max_cols, int32_t* ranks, double eps) {
+                 int nent, int max_rows, int max_cols, int32_t* ranks, double eps, double* margins) {
   if (nent <= 0) return;
   int zld = max_rows > 0 ? max_rows : 1;
   const size_t aux = 2 * sizeof(R) * max_cols + sizeof(cx<R>) * max_cols + 64;
@@ -406,7 +423,7 @@ void launch_cpqr(Ctx* c, const cx<R>* src, int64_t ld_src, cx<R>* dst, int64_t l
   KTimer timer(c, "cpqr", 0.0, (double)sizeof(cx<R>) * nent * ((double)max_rows * max_cols + (double)ld_dst * cap));
   if (smem <= 200 * 1024) {
     BFLY_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    kern<<<nent, nt, smem, c->stream>>>(src, ld_src, dst, ld_dst, cap, ents, ranks, eps, zld, nullptr, 0);
+    kern<<<nent, nt, smem, c->stream>>>(src, ld_src, dst, ld_dst, cap, ents, ranks, eps, zld, nullptr, 0, margins);
     BFLY_LAUNCH_CHECK("cpqr");
     return;
   }
@@ -418,7 +435,8 @@ void launch_cpqr(Ctx* c, const cx<R>* src, int64_t ld_src, cx<R>* dst, int64_t l
   DBuf<cx<R>> zbuf(c, (size_t)(chunk * zstride));
   for (int64_t e0 = 0; e0 < nent; e0 += chunk) {
     int n = (int)std::min<int64_t>(chunk, nent - e0);
-    kern<<<n, nt, aux, c->stream>>>(src, ld_src, dst, ld_dst, cap, ents + e0, ranks, eps, zld, zbuf.p, zstride);
+    kern<<<n, nt, aux, c->stream>>>(src, ld_src, dst, ld_dst, cap, ents + e0, ranks, eps, zld, zbuf.p, zstride,
+                                    margins);
     BFLY_LAUNCH_CHECK("cpqr");
   }
 }
@@ -442,9 +460,9 @@ void launch_core_fit(Ctx* c, const cx<R>* Q, int64_t ldq, const cx<R>* Z, int64_
 }
 
 template void launch_cpqr<double>(Ctx*, const double2*, int64_t, double2*, int64_t, int, const QrEnt*, int, int, int,
-                                  int32_t*, double);
+                                  int32_t*, double, double*);
 template void launch_cpqr<float>(Ctx*, const float2*, int64_t, float2*, int64_t, int, const QrEnt*, int, int, int,
-                                 int32_t*, double);
+                                 int32_t*, double, double*);
 template void launch_core_fit<double>(Ctx*, const double2*, int64_t, const double2*, int64_t, const double2*, int64_t,
                                       double2*, int64_t, int, const CoreEnt*, int, int, int, int, bool, int32_t*);
 template void launch_core_fit<float>(Ctx*, const float2*, int64_t, const float2*, int64_t, const float2*, int64_t,

@@ -84,7 +84,7 @@ struct QrEnt {
 };
 template <typename R>
 void launch_cpqr(Ctx* c, const cx<R>* src, int64_t ld_src, cx<R>* dst, int64_t ld_dst, int cap, const QrEnt* ents_dev,
-                 int nent, int max_rows, int max_cols, int32_t* ranks, double eps);
+                 int nent, int max_rows, int max_cols, int32_t* ranks, double eps, double* margins = nullptr);
 
 // ------------------------------------------ K6: batched core fit
 // B = (Q^H z) * pinv(coeff) (core_block, reconstruct.hpp:125-138)

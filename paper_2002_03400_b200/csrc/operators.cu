@@ -133,6 +133,30 @@ struct CallbackOp : DevOp<R> {
   }
 };
 
+// structured-probe-aware callback: one call per probe with its nonzero rows
+template <typename R>
+struct CallbackRangeOp : DevOp<R> {
+  bfly_apply_range_fn fn = nullptr;
+  void* user = nullptr;
+  void do_apply(int mode, const cx<R>* X, const std::vector<MatvecSeg>& segs, cx<R>* Y, int64_t ldy, int64_t o0,
+                int64_t o1) override {
+    Ctx* c = this->ctx;
+    int64_t wtot = 0;
+    DBuf<cx<R>> xp = this->pad_probes(mode, X, segs, wtot);
+    if (wtot <= 0) return;
+    const int64_t nin = this->in_dim(mode), nout = this->out_dim(mode);
+    if (mode == OP_H) launch_conj<R>(c, xp.p, nin, wtot, nin);
+    for (const auto& s : segs) {
+      if (s.ncols <= 0) continue;
+      const int64_t b = s.rows > 0 ? s.row0 : 0, e = s.rows > 0 ? s.row0 + s.rows : 0;
+      int rc = fn(user, mode == OP_N ? 0 : 1, xp.p + s.col0 * nin, nin, Y + s.col0 * ldy, ldy, s.ncols, b, e,
+                  (void*)c->stream);
+      if (rc != 0) fail(rc, "black-box callback failed with status " + std::to_string(rc));
+    }
+    if (mode == OP_H) launch_conj<R>(c, Y, nout, wtot, ldy);
+  }
+};
+
 std::vector<double> column(const double* p, int64_t n, int axis) {
   std::vector<double> v(n);
   for (int64_t i = 0; i < n; ++i) v[i] = p[i * 3 + axis];
@@ -216,6 +240,21 @@ std::unique_ptr<DevOp<R>> make_callback_op(Ctx* c, int64_t m, int64_t n, bool is
 }
 
 template <typename R>
+std::unique_ptr<DevOp<R>> make_callback_range_op(Ctx* c, int64_t m, int64_t n, bool is_real, bfly_apply_range_fn fn,
+                                                 void* user) {
+  if (!fn) fail(PRECONDITION, "callback operator: null function");
+  auto op = std::make_unique<CallbackRangeOp<R>>();
+  op->kind = 6;
+  op->m = m;
+  op->n = n;
+  op->ctx = c;
+  op->is_real = is_real;
+  op->fn = fn;
+  op->user = user;
+  return op;
+}
+
+template <typename R>
 DevButterfly<R>* butterfly_of(DevOp<R>* op) {
   auto* b = dynamic_cast<ButterflyOp<R>*>(op);
   return b ? b->bf.get() : nullptr;
@@ -229,6 +268,8 @@ DevButterfly<R>* butterfly_of(DevOp<R>* op) {
   template std::unique_ptr<DevOp<R>> make_compose_op<R>(Ctx*, std::unique_ptr<DevOp<R>>, std::unique_ptr<DevOp<R>>); \
   template std::unique_ptr<DevOp<R>> make_butterfly_op<R>(Ctx*, std::unique_ptr<DevButterfly<R>>);                \
   template std::unique_ptr<DevOp<R>> make_callback_op<R>(Ctx*, int64_t, int64_t, bool, bfly_apply_fn, void*);      \
+  template std::unique_ptr<DevOp<R>> make_callback_range_op<R>(Ctx*, int64_t, int64_t, bool, bfly_apply_range_fn,     \
+                                                               void*);                                            \
   template DevButterfly<R>* butterfly_of<R>(DevOp<R>*);
 INST(double)
 INST(float)

@@ -15,10 +15,7 @@
 #include "context.h"
 #include "kernels.cuh"
 
-extern "C" {
-typedef int (*bfly_apply_fn)(void* user, int trans, const void* x_dev, int64_t ldx, void* y_dev, int64_t ldy, int64_t k,
-                             void* stream);
-}
+#include "../../include/bfly_b200.h"
 
 namespace bfly {
 
@@ -77,6 +74,9 @@ template <typename R>
 std::unique_ptr<DevOp<R>> make_butterfly_op(Ctx* c, std::unique_ptr<DevButterfly<R>> bf);
 template <typename R>
 std::unique_ptr<DevOp<R>> make_callback_op(Ctx* c, int64_t m, int64_t n, bool is_real, bfly_apply_fn fn, void* user);
+template <typename R>
+std::unique_ptr<DevOp<R>> make_callback_range_op(Ctx* c, int64_t m, int64_t n, bool is_real, bfly_apply_range_fn fn,
+                                                 void* user);
 template <typename R>
 DevButterfly<R>* butterfly_of(DevOp<R>* op);
 

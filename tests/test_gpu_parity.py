@@ -464,3 +464,76 @@ def test_other_seeds_and_sizes(B, oracle_threads, cfg_id, n, seed):
     w = B.configs.build(cfg_id, n, seed=seed)
     bf, log = B.factorize(w.op, w.row_tree, w.col_tree, w.recon)
     _compare(bf, log, bf_o, log_o, w.op.rows, w.op.cols, seed=seed)
+
+
+def test_ranged_callback_skips_zero_rows(B, oracle_threads):
+    """bfly_apply_range_fn: a user black box told each structured
+    probe's nonzero input rows multiplies only those (A[:, b:e] X[b:e]); the
+    factorization equals the oracle's (ranks, bookkeeping, apply 1e-10) and the
+    same matrix as a padded reference-style callback, while the transfer-level
+    products touch |node| rows instead of n (reconstruct.hpp:72-85)."""
+    import torch
+
+    n = 1024
+    op_o, rt_o, ct_o, cfg = oracle_config(2, n)
+    a = op_o.apply(np.eye(n, dtype=np.complex128))  # dense K (tree order = identity)
+    at = torch.tensor(a, dtype=torch.complex128, device="cuda")
+    calls = []
+
+    class _CAI:
+        def __init__(self, ptr, shape, strides):
+            self.__cuda_array_interface__ = {"data": (ptr, False), "shape": shape, "typestr": "<c16",
+                                             "strides": strides, "version": 3}
+
+    def ranged(trans, x, ldx, y, ldy, k, b, e, stream):
+        calls.append((trans, k, b, e))
+        with torch.cuda.stream(torch.cuda.ExternalStream(stream)):
+            X = torch.as_tensor(_CAI(x, (n, k), (16, 16 * ldx)), device="cuda")
+            Y = torch.as_tensor(_CAI(y, (n, k), (16, 16 * ldy)), device="cuda")
+            A = at[:, b:e] if trans == 0 else at[b:e, :].t()
+            Y.copy_(A @ X[b:e])
+        return 0
+
+    op = B.CallbackOperator(n, n, ranged, ranged=True)
+    x = O.gaussian_matrix(n, 3, 4)
+    assert rel_err(op.apply(x), a @ x) < 1e-13 and calls[-1] == (0, 3, 0, n)
+    assert rel_err(op.apply_adjoint(x), a.conj().T @ x) < 1e-13
+    calls.clear()
+    L = cfg["levels"]
+    rt = B.PartitionTree.build(np.arange(n, dtype=np.float64)[:, None], L)  # identity trees
+    rc = B.ReconstructionConfig(tolerance=cfg["tolerance"], rank_guess=cfg["rank_guess"], levels=L)
+    bf, log = B.factorize(op, rt, rt, rc)
+    bf_o, log_o = O.factorize(op_o, rt_o, ct_o, dict(cfg, threads=oracle_threads))
+    _compare(bf, log, bf_o, log_o, n, n)
+    dense = B.DenseOperator(a)
+    bf_d, _ = B.factorize(dense, rt, rt, rc)
+    np.testing.assert_array_equal(bf.rank_profile(), bf_d.rank_profile())
+    # one call per structured probe, each with its node's rows only
+    lm = L // 2
+    sizes = sorted({e - b for _, _, b, e in calls})
+    assert sizes[-1] == n  # the leaf rounds' dense Gaussian probes
+    assert all(s in sizes for s in (n >> l for l in range(1, lm + 1)))  # W level l: |T_tau| = n / 2^l
+    rows_used = sum((e - b) * k for _, k, b, e in calls)
+    rows_padded = sum(n * k for _, k, b, e in calls)
+    assert rows_used < 0.6 * rows_padded
+    print(f"ranged callback: {len(calls)} calls, {rows_used / rows_padded:.2f} of the padded rows multiplied")
+
+
+def test_memory_guard_shrinks_batches_then_refuses(B, monkeypatch):
+    """Memory guard (SURVEY 7 hard part 5): before each level allocates, its
+    factor level and per-probe working set are sized from the children's ranks
+    (the width rule of reconstruct.hpp:204-207, 257-260).  With little memory
+    left the probe batch shrinks (results bit-identical); with too little for
+    one probe the factorization is refused up front with the bytes needed."""
+    w = B.configs.build(2, 16384)
+    a, la = B.factorize(w.op, w.row_tree, w.col_tree, w.recon)
+    monkeypatch.setenv("BFLY_MEM_AVAIL_GB", "0.12")
+    b, lb = B.factorize(w.op, w.row_tree, w.col_tree, w.recon)
+    np.testing.assert_array_equal(a.rank_profile(), b.rank_profile())
+    x = O.gaussian_matrix(w.op.cols, 4, 17)
+    np.testing.assert_array_equal(a.apply(x), b.apply(x))
+    assert lb.peak_concurrent_probes < la.peak_concurrent_probes
+    print(f"guarded batch: {lb.peak_concurrent_probes} probes (unguarded {la.peak_concurrent_probes})")
+    monkeypatch.setenv("BFLY_MEM_AVAIL_GB", "0.001")
+    with pytest.raises(B.PreconditionError, match="memory guard"):
+        B.factorize(w.op, w.row_tree, w.col_tree, w.recon)
