@@ -44,6 +44,18 @@ K2_PIPES = {"fp64": 0.367, "tensor_int8": 0.383, "shared_datapath": 0.751}
 CFG_ID = 2
 
 
+def _hbm_peak():
+    """measured copy bandwidth (MEASURED_PEAKS.json, driver-written), else the recipe's fallback"""
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            return float(json.load(f)["hbm_gbs"])
+    except Exception:
+        return 6650.0
+
+
+HBM_PEAK_GBS = _hbm_peak()
+
+
 def _env_rank():
     return int(os.environ.get("RANK", 0)), int(os.environ.get("WORLD_SIZE", 1)), int(os.environ.get("LOCAL_RANK", 0))
 
@@ -89,6 +101,32 @@ def cpu_sample(n=65536, probes=8, width=32, threads=None):
         f"(n={n}, {n >> level} rows x {width} cols each) via the {what}, {threads} threads")
 
 
+# algorithmic flops of one config-2 construction, counted by the library's log; the
+# reference factorization has the identical rank profile and bookkeeping (tests/test_full_parity.py),
+# hence the same count
+CFG2_FLOPS = 14371885543744.0
+SAMPLE_SCOPE = ("a bounded SAMPLE of the construction, not a whole factorize(): the black-box products of "
+                "W-level-5 row probes (the operation carrying > 90 % of the construction's flops), through the "
+                "reference's own probe_with + operator; the whole reference factorize() is under full_construction")
+
+
+def full_reference_construction():
+    """The reference's own full config-2 factorize() (oracle/_ref, all host threads), timed once on the
+    GPU box's host by tests/golden/make_fullsize_golden.py (FactorizationLog.total_seconds,
+    reconstruct.hpp:309-314) -- reported beside the sampled rate, not re-run per bench step (~3 min)."""
+    try:
+        import numpy as np
+
+        d = np.load(os.path.join(ROOT, "tests", "golden", "full_cfg2.npz"))
+        sec = float(d["total_seconds"])
+        return {"seconds": round(sec, 2), "GFLOP/s": round(CFG2_FLOPS / sec / 1e9, 2), "threads": int(d["threads"]),
+                "cpu": str(d["cpu_model"]), "producer": str(d["producer"]),
+                "phases_s": {str(k): round(float(v), 2) for k, v in zip(d["phase_names"], d["phase_seconds"])},
+                "source": "tests/golden/full_cfg2.npz (tests/golden/make_fullsize_golden.py on the GPU box host)"}
+    except Exception as e:  # fixture missing: say so
+        return {"unavailable": str(e)}
+
+
 def run_reference(args):
     rank, world, _ = _env_rank()
     if rank != 0:
@@ -106,7 +144,8 @@ def run_reference(args):
         "scaling": "weak", "vs_baseline": None, "dtype": "complex128", "data": "synthetic",
         "config": {"workload": "config2_helmholtz_circle_n65536", "n": 65536, "sample": sample},
         "cpu_baseline": {"value": round(value, 3), "unit": "GFLOP/s", "cores": threads, "kind": kind,
-                         "sample": sample},
+                         "sample": sample, "scope": SAMPLE_SCOPE,
+                         "full_construction": full_reference_construction()},
         "e2e": {"value": round(value, 3), "unit": "GFLOP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -199,7 +238,7 @@ def run_ours(args):
         else:
             ctx.set_host_comm()
     stream = torch.cuda.ExternalStream(ctx.stream)
-    w = B.configs.build(CFG_ID, args.n or None, ctx=ctx)
+    w = B.configs.build(CFG_ID, args.size or None, ctx=ctx)
     op, rt, ct, rc = w.op, w.row_tree, w.col_tree, w.recon
     flush = torch.empty(64 * 1024 * 1024, dtype=torch.float32, device="cuda")  # 256 MB > L2
 
@@ -238,27 +277,47 @@ def run_ours(args):
     ms_per_step = max_ms / args.steps
 
     # ----------------------------------------------- apply bandwidth (device)
-    apply = {}
-    for k in ((1, 2, 16) if rank == 0 else ()):
-        x = torch.randn((k, op.cols), dtype=torch.complex128, device="cuda").t()
-        y = torch.empty((k, op.rows), dtype=torch.complex128, device="cuda").t()
-        for _ in range(3):
-            B.api.check(B.api.lib().bfly_apply(bf.h, 0, B.api.C.c_void_p(x.data_ptr()), op.cols,
-                                               B.api.C.c_void_p(y.data_ptr()), op.rows, k, 1))
-        ts = []
-        for _ in range(10):
-            l2_flush()
-            a0, a1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            a0.record(stream)
-            B.api.check(B.api.lib().bfly_apply(bf.h, 0, B.api.C.c_void_p(x.data_ptr()), op.cols,
-                                               B.api.C.c_void_p(y.data_ptr()), op.rows, k, 1))
-            a1.record(stream)
-            a1.synchronize()
-            ts.append(a0.elapsed_time(a1))
-        ms = statistics.median(ts)
-        nbytes = 16.0 * (bf.nnz() + (op.rows + op.cols) * k)
-        apply[f"k{k}"] = {"ms": round(ms, 4), "GB/s": round(nbytes / (ms / 1e3) / 1e9, 1),
-                          "frac_of_hbm": round(nbytes / (ms / 1e3) / 1e9 / 6554.9, 3)}
+    def time_apply(bfx, ks, reps=10):
+        """device-resident apply, L2 flushed before every call, CUDA events on the library stream"""
+        out = {}
+        nin, nout = bfx.cols, bfx.rows
+        for k in ks:
+            x = torch.randn((k, nin), dtype=torch.complex128, device="cuda").t()
+            y = torch.empty((k, nout), dtype=torch.complex128, device="cuda").t()
+
+            def call():
+                B.api.check(B.api.lib().bfly_apply(bfx.h, 0, B.api.C.c_void_p(x.data_ptr()), nin,
+                                                   B.api.C.c_void_p(y.data_ptr()), nout, k, 1))
+
+            for _ in range(3):
+                call()
+            ts = []
+            for _ in range(reps):
+                l2_flush()
+                a0, a1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                a0.record(stream)
+                call()
+                a1.record(stream)
+                a1.synchronize()
+                ts.append(a0.elapsed_time(a1))
+            ms = statistics.median(ts)
+            nbytes = 16.0 * (bfx.nnz() + (nin + nout) * k)
+            gbs = nbytes / (ms / 1e3) / 1e9
+            out[f"k{k}"] = {"ms": round(ms, 4), "GB/s": round(gbs, 1), "frac_of_hbm": round(gbs / HBM_PEAK_GBS, 3),
+                            "bytes": nbytes, "tflops": round(8.0 * bfx.nnz() * k / (ms / 1e3) / 1e12, 2)}
+            del x, y
+        return out
+
+    # config 2's factorization (168 MB of factors) and config 4's input
+    # butterfly (n = 262144, leaf 64, rank 32: 1.95 GB -- the HBM-bound case of SURVEY 8d)
+    apply, apply4 = {}, {}
+    if rank == 0:
+        apply = time_apply(bf, (1, 2, 16))
+        if not args.no_extra:
+            bf4 = B.synth_butterfly(12, 32, 0, leaf=64, perturb=1e-8, ctx=ctx)
+            apply4 = time_apply(bf4, (1, 16))
+            apply4["nnz"] = bf4.nnz()
+            del bf4
 
     # --------------------------------------------------- e2e (host buffers)
     import ctypes as C
@@ -368,6 +427,7 @@ def run_ours(args):
             "max_rank": bf.max_rank(), "nnz": bf.nnz(),
             "roofline": roofline,
             "apply": apply,
+            "apply_cfg4": apply4,
             "other_configs": other,
             "kernels": {k: {"launches": v["launches"], "ms_per_step": round(v["ms"] / args.steps, 3)}
                         for k, v in kernels.items()},
@@ -381,7 +441,8 @@ def run_ours(args):
             # a bounded sample of ~10-30 s of CPU work (two reference-arm steps)
             v, dt, threads, kind, sample = cpu_sample(probes=2 * args.ref_probes)
             line["cpu_baseline"] = {"value": round(v, 3), "unit": "GFLOP/s", "cores": threads, "kind": kind,
-                                    "sample": sample, "seconds": round(dt, 2)}
+                                    "sample": sample, "seconds": round(dt, 2), "scope": SAMPLE_SCOPE,
+                                    "full_construction": full_reference_construction()}
         print(json.dumps(line), flush=True)
     if dist is not None:
         dist.barrier()
@@ -412,7 +473,7 @@ def main():
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--n", type=int, default=0, help="override n (testing only)")
+    ap.add_argument("--size", type=int, default=0, help="override n (testing only)")
     ap.add_argument("--ref-probes", type=int, default=8)
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-extra", action="store_true", help="skip the other full-size configs (info only)")

@@ -32,7 +32,7 @@ def probes(n, k, seed):
 def run(B, ctx, a, world, virtual=0):
     import dataclasses
 
-    w = B.configs.build(a.cfg, a.n, ctx=ctx)
+    w = B.configs.build(a.cfg, a.size, ctx=ctx)
     rc = dataclasses.replace(w.recon, virtual_ranks=virtual) if virtual else w.recon
     bf, log = B.factorize(w.op, w.row_tree, w.col_tree, rc)
     x = probes(w.op.cols, 4, 1)
@@ -54,7 +54,7 @@ def run(B, ctx, a, world, virtual=0):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--cfg", type=int, default=2)
-    ap.add_argument("--n", type=int, default=4096)
+    ap.add_argument("--size", type=int, default=4096)
     ap.add_argument("--transport", default="host", choices=["host", "nccl"])
     ap.add_argument("--out", required=True)
     a = ap.parse_args()

@@ -106,7 +106,7 @@ def test_two_processes_one_gpu_host_transport(tmp_path, cfg_id, n):
     out = str(tmp_path / "mp")
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=2", "--master-addr",
            "127.0.0.1", "--master-port", str(_port()), os.path.join(ROOT, "tests", "mp_worker.py"),
-           "--transport", "host", "--cfg", str(cfg_id), "--n", str(n), "--out", out]
+           "--transport", "host", "--cfg", str(cfg_id), "--size", str(n), "--out", out]
     r = subprocess.run(cmd, capture_output=True, text=True, timeout=900, cwd=ROOT)
     print(r.stdout[-3000:], r.stderr[-3000:])
     assert r.returncode == 0
