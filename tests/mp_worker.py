@@ -44,7 +44,7 @@ def run(B, ctx, a, world, virtual=0):
     for kind in B.api.LAYOUT_KINDS:
         spec = B.api.LayoutSpec(kind, bf.levels, 8, world)
         yl, _, mv = bf.apply_layout(x, spec)
-        xl, _, _ = bf.apply_layout(y, spec, trans=B.H)
+        xl, _, _ = bf.apply_layout(y, spec, trans=B.api.H)
         out[f"layout_{kind}_n"] = yl
         out[f"layout_{kind}_h"] = xl
         out[f"layout_{kind}_moved"] = np.array([mv["max_recv"], mv["total_recv"]])
