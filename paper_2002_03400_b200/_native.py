@@ -9,7 +9,8 @@ import ctypes as C
 import os
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "_native", "libbfly_b200.so")
+# BFLY_LIB: an alternative in-tree build of the same library (A/B experiments, tools/)
+LIB_PATH = os.environ.get("BFLY_LIB") or os.path.join(_HERE, "_native", "libbfly_b200.so")
 
 _lib = None
 

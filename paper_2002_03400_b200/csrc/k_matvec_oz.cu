@@ -9,21 +9,23 @@
 // Here the FP64 pipe only evaluates entries; the contraction runs on the
 // int8 tensor cores (4.2 POPS measured, tools/microbench/tc_i8.cu).
 //
-// Arithmetic (per CTA: 128 output rows x 32 complex probe columns):
+// Arithmetic (per CTA: 128 output rows x 32 complex probe columns), with the
+// default 6-slice scheme (BFLY_OZ_SLICES=7 restores the round-1 scheme):
 //  * every kernel entry a (re and im separately) is scaled by 2^S_row and
-//    rounded to a signed integer |v| < 2^50; S_row is per output row and per
-//    1024-entry chunk of the input range, from a bound on |a| over the chunk
+//    rounded to a signed integer |v| < 2^47; S_row is per output row and per
+//    2048-entry chunk of the input range, from a bound on |a| over the chunk
 //    (1 for NUFFT, 1/r_min or 1/(4 pi r_min) for the Helmholtz kernels);
-//  * v's two's-complement bytes ARE its base-256 digits: slices A_0..A_5
-//    unsigned, A_6 signed -- no decomposition work;
-//  * probe entries x are scaled per column by 2^T_c (|x| < 2^50) and split into
-//    balanced signed digits B_0..B_6 (prep kernel, once per launch);
+//  * v's two's-complement bytes ARE its base-256 digits: slices A_0..A_4
+//    unsigned, A_5 signed -- no decomposition work;
+//  * probe entries x are scaled per column by 2^T_c (|x| < 2^46) and split into
+//    balanced signed digits B_0..B_5 (prep kernel, once per launch);
 //  * sum_k v_ik w_kc = sum_{p,q} 2^{8(p+q)} A_p B_q^T; the products with
-//    p + q >= 5 (34 of 49 slice pairs) are accumulated exactly in int32 in
-//    TMEM, one 64-column block per diagonal e = p + q (8 blocks = 512 cols).
-//    The dropped terms are < 2^-50 relative to max|v| max|w| per entry;
-//  * every 1024-entry chunk the diagonals are drained into FP64 accumulators
-//    (Horner in 2^8, times 2^{40 - S_row - T_c}).
+//    p + q >= 4 (26 of 36 slice pairs) are accumulated exactly in int32 in
+//    TMEM, one 64-column block per diagonal e = p + q (7 blocks = 448 cols).
+//    The dropped terms are < 2^-53 relative to max|v| max|w| per entry, the
+//    rounding to integers 2^-47 / 2^-46 relative to the row / column bound;
+//  * every chunk the diagonals are drained into FP64 accumulators (Horner in
+//    2^8, times 2^{32 - S_row - T_c}).
 // Complex: A_re slices multiply G1 = [B(Re x) | B(Im x)] and A_im slices
 // multiply G2 = [B(-Im x) | B(Re x)] into the same accumulator, so TMEM block
 // columns hold [Re y | Im y] directly.  For slice A_p the needed B_q
@@ -51,8 +53,19 @@ namespace bfly {
 
 namespace {
 
-constexpr int OZ_NSL = 7;                         // slices per operand
-constexpr int OZ_NDIAG = 8;                       // kept diagonals e = 5..12
+// Slice scheme (BFLY_OZ_SLICES): 6 slices per operand, |v| < 2^47 (A, two's
+// complement bytes) and |x| < 2^46 (B, balanced digits), diagonals e >= 4 kept
+// (26 slice-pair products; dropped terms < 2^-53 relative); or 7 slices,
+// |v|, |x| < 2^50, e >= 5 kept (34 products; dropped < 2^-50 relative).
+#ifndef BFLY_OZ_SLICES
+#define BFLY_OZ_SLICES 6
+#endif
+constexpr int OZ_NSL = BFLY_OZ_SLICES;            // slices per operand
+static_assert(OZ_NSL == 6 || OZ_NSL == 7, "6 or 7 slices");
+constexpr int OZ_E0 = OZ_NSL - 2;                 // lowest kept diagonal e = p + q
+constexpr int OZ_NDIAG = OZ_NSL + 1;              // kept diagonals e = E0 .. 2 NSL - 2
+constexpr int OZ_ABITS = OZ_NSL == 6 ? 47 : 50;   // |v| < 2^ABITS (scaled, rounded kernel entries)
+constexpr int OZ_BBITS = OZ_NSL == 6 ? 46 : 50;   // |x| < 2^BBITS (scaled, rounded probe entries)
 constexpr int OZ_KS = 32;                         // input entries per stage (MMA K)
 // drain / scale chunk: 2048 entries (int32 diagonal sums stay < 2^30); the 3D
 // kernel keeps 1024 (its z coordinates must fit shared memory too)
@@ -87,12 +100,15 @@ constexpr uint32_t mma_code(int h, int p, int jlo, int nb, int init) {
 constexpr OzSched make_sched(int maxb) {
   OzSched sc{};
   sc.n = 0;
+  constexpr int T = OZ_NSL - 1, D = OZ_NDIAG;
   for (int h = 0; h < 2; ++h) {
     const int init = h == 0 ? 1 : 0;
-    for (int j = 1; j <= 7; j += maxb) sc.code[sc.n++] = mma_code(h, 6, j, (8 - j) < maxb ? 8 - j : maxb, init);
-    sc.code[sc.n++] = mma_code(h, 5, 0, 1, init);
-    for (int j = 1; j <= 6; j += maxb) sc.code[sc.n++] = mma_code(h, 5, j, (7 - j) < maxb ? 7 - j : maxb, 0);
-    for (int p = 4; p >= 0; --p)
+    // top slice over blocks 1..D-1 and the next one over block 0: the first
+    // writes of plane 0 cover every block once
+    for (int j = 1; j <= D - 1; j += maxb) sc.code[sc.n++] = mma_code(h, T, j, (D - j) < maxb ? D - j : maxb, init);
+    sc.code[sc.n++] = mma_code(h, T - 1, 0, 1, init);
+    for (int j = 1; j <= T; j += maxb) sc.code[sc.n++] = mma_code(h, T - 1, j, (T + 1 - j) < maxb ? T + 1 - j : maxb, 0);
+    for (int p = T - 2; p >= 0; --p)
       for (int j = 0; j <= p + 1; j += maxb) sc.code[sc.n++] = mma_code(h, p, j, (p + 2 - j) < maxb ? p + 2 - j : maxb, 0);
   }
   return sc;
@@ -256,7 +272,7 @@ __device__ __forceinline__ void entry_rounded(double tx, double ty, double tz, d
 }
 
 // ------------------------------------------------------- probe slicing
-// T_c = 49 - floor(log2 max_k |x_kc|_inf)  (scaled |x| < 2^50)
+// T_c = (BBITS - 1) - floor(log2 max_k |x_kc|_inf)  (scaled |x| < 2^BBITS)
 __global__ void oz_colscale_kernel(const double2* __restrict__ X, const OzItem* __restrict__ items,
                                    int32_t* __restrict__ T) {
   const OzItem it = items[blockIdx.y];
@@ -277,11 +293,11 @@ __global__ void oz_colscale_kernel(const double2* __restrict__ X, const OzItem* 
   if (threadIdx.x == 0) {
     const double mx = red[0];
     // zero or non-finite columns: scale 0 (non-finite values trip the slice check)
-    T[blockIdx.y * OZ_MAXCB + c] = (mx > 0.0 && mx < 1e300) ? 49 - ilogb(mx) : 0;
+    T[blockIdx.y * OZ_MAXCB + c] = (mx > 0.0 && mx < 1e300) ? (OZ_BBITS - 1) - ilogb(mx) : 0;
   }
 }
 
-// balanced base-256 digits of round(x), |x| < 2^50
+// balanced base-256 digits of round(x), |x| < 2^BBITS (the last one fits int8)
 __device__ __forceinline__ void digits7(double x, int (&d)[OZ_NSL]) {
   long long q = d2ll(x);
 #pragma unroll
@@ -310,7 +326,8 @@ __global__ void oz_slice_kernel(const double2* __restrict__ X, const OzItem* __r
   if (c < it.ncols && k < it.rows) v = X[it.x_off + k + (int64_t)c * it.ldx];
   const double sc = pow2(T[blockIdx.y * OZ_MAXCB + c]);
   const double xr = v.x * sc, xi = v.y * sc;
-  if (!(fabs(xr) < 1125899906842624.0 && fabs(xi) < 1125899906842624.0)) {  // 2^50; NaN fails too
+  constexpr double lim = (double)(1ll << OZ_BBITS);
+  if (!(fabs(xr) < lim && fabs(xi) < lim)) {  // NaN fails too
     atomicOr(flag, 1);
     return;
   }
@@ -442,7 +459,7 @@ __global__ void __launch_bounds__(OZ_THREADS, 1)
     const int S = Srow[(d & 1) * OZ_BM + drow];
     const int c0 = (dq & 1) * DC;
 #pragma unroll
-    for (int c = 0; c < DC; ++c) yacc[c] = fma(t[c], pow2(40 - S - Ts[c0 + c]), yacc[c]);
+    for (int c = 0; c < DC; ++c) yacc[c] = fma(t[c], pow2(8 * OZ_E0 - S - Ts[c0 + c]), yacc[c]);
   };
 
   // One MMA of a stage (index i < OZ_NMMA of the fixed schedule kMmaList)
@@ -452,7 +469,7 @@ __global__ void __launch_bounds__(OZ_THREADS, 1)
     const int h = e & 1, p = (e >> 1) & 7, jlo = (e >> 4) & 15, nb = (e >> 8) & 31;
     const bool init = (e >> 13) & 1;
     const uint64_t da = smem_desc(a0 + h * OZ_APLANE + p * OZ_ASLICE, (OZ_BM / 8) * 128, 128);
-    const int q0 = jlo + 5 - p;
+    const int q0 = jlo + OZ_E0 - p;
     const uint64_t db = smem_desc(b0 + h * Z::BOPER + q0 * Z::BN2 * 16, (Z::BROWS / 8) * 128, 128);
     mma_i8(tmem + jlo * Z::BN2, da, db, idesc_i8(128, nb * Z::BN2, p == OZ_NSL - 1, true),
            (init && s == 0) ? 0u : 1u);
@@ -559,13 +576,13 @@ __global__ void __launch_bounds__(OZ_THREADS, 1)
     }
     __syncthreads();
     if (tid < OZ_BM) {
-      int S = 49;  // NUFFT: |a| = 1
+      int S = OZ_ABITS - 1;  // NUFFT: |a| = 1
       if (KIND != KK_NUFFT) {
         const float mn = __uint_as_float(Smin[tid]);
         // amplitude bound with a factor-2 margin for the float distance estimate
         double amax = mn > 1e-36f ? 2.0 / sqrt((double)mn) : 1e300;
         if (KIND == KK_PLATES) amax /= keval::kFourPi;
-        S = amax < 1e300 ? 49 - ilogb(amax) : 0;
+        S = amax < 1e300 ? (OZ_ABITS - 1) - ilogb(amax) : 0;
       }
       Srow[(d & 1) * OZ_BM + tid] = S;
     }
@@ -626,7 +643,7 @@ __global__ void __launch_bounds__(OZ_THREADS, 1)
 #pragma unroll
         for (int p = 0; p < 4; ++p) *reinterpret_cast<uint2*>(pl + p * OZ_ASLICE) = make_uint2(l0[p], l1[p]);
 #pragma unroll
-        for (int p = 0; p < 3; ++p) *reinterpret_cast<uint2*>(pl + (4 + p) * OZ_ASLICE) = make_uint2(h0[p], h1[p]);
+        for (int p = 0; p < OZ_NSL - 4; ++p) *reinterpret_cast<uint2*>(pl + (4 + p) * OZ_ASLICE) = make_uint2(h0[p], h1[p]);
       }
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
       if (s == 0 && d > 0) drain(d - 1);  // TMEM must be free before this stage's MMAs
@@ -649,8 +666,8 @@ __global__ void __launch_bounds__(OZ_THREADS, 1)
   if (pend_slot >= 0) issue_stage(pend_slot, pend_ph, pend_s, pend_nst);
   __syncwarp();
   if (nchunks > 0) drain(nchunks - 1);
-  // |v| < 2^50 <=> high word of the scaled amplitude < 0x43100000 (NaN / inf fail)
-  if (KIND != KK_NUFFT && amp_hi >= 0x43100000u) atomicOr(flag, 2);
+  // |v| < 2^ABITS <=> high word of the scaled amplitude < (1023 + ABITS) << 20 (NaN / inf fail)
+  if (KIND != KK_NUFFT && amp_hi >= (uint32_t)(1023 + OZ_ABITS) << 20) atomicOr(flag, 2);
 
   // ---- store: thread owns row drow, columns (dq & 1) * DC + c of Re (dq < 2) or Im y
   const int64_t go = i0 + drow;
