@@ -70,7 +70,7 @@ constexpr int OZ_KS = 32;                         // input entries per stage (MM
 // drain / scale chunk: 2048 entries (int32 diagonal sums stay < 2^30); the 3D
 // kernel keeps 1024 (its z coordinates must fit shared memory too)
 constexpr int oz_kd(int kind) { return kind == KK_PLATES ? 1024 : 2048; }
-constexpr int OZ_NST = 3;                         // ring depth (A + B stages)
+constexpr int OZ_NST = 2;                         // ring depth
 constexpr int OZ_BM = 128;                        // output rows per CTA (= TMEM lanes)
 constexpr int OZ_EWARPS = 16;
 constexpr int OZ_THREADS = OZ_EWARPS * 32;        // no dedicated MMA warp
@@ -129,20 +129,19 @@ struct OzT {
   static constexpr int DC = NCB / 2;                 // drained columns per thread
   static constexpr int SM_A = 0;
   static constexpr int SM_B = SM_A + OZ_NST * OZ_ASTAGE;
-  // input points are read from global memory (L1): the ring takes the room.
-  // The chunk setup's sub-box bounds live in the B image of the slot its
-  // first stage will use (free at that point, filled by TMA only afterwards).
-  static constexpr int SM_S = SM_B + OZ_NST * BSTAGE;   // int S_row [2][128]
+  static constexpr int SM_PD = SM_B + OZ_NST * BSTAGE;  // double2 (x, y) [KD]
+  static constexpr int SM_PZ = SM_PD + KD * 16;         // double z [KD] (3D kernels only)
+  static constexpr int SM_S = SM_PZ + (HASZ_ ? KD * 8 : 0);  // int S_row [2][128]
   static constexpr int SM_T = SM_S + 2 * OZ_BM * 4;     // int T [NCB]
   static constexpr int SM_MIN = SM_T + OZ_MAXCB * 4;    // uint min d2 bits [128]
   static constexpr int SM_TAB = SM_MIN + OZ_BM * 4;     // double2 sin/cos table [kTabN]
-  static constexpr int SM_CNT = SM_TAB + keval::kTabN * 16;  // uint stage arrival counters [NST]
-  static constexpr int SM_BAR = SM_CNT + 16;            // mbarriers (8-byte aligned)
+  static constexpr int SM_BOX = SM_TAB + keval::kTabN * 16;  // float4 sub-box bounds [NBOX][2]
+  static constexpr int SM_CNT = SM_BOX + NBOX * 32;     // uint stage arrival counters [NST]
+  static constexpr int SM_BAR = SM_CNT + 16;            // mbarriers
   static constexpr int NBAR = 2 * OZ_NST + 1;
   static constexpr int SM_TMEM = SM_BAR + NBAR * 8;
   static constexpr int SM_TOTAL = SM_TMEM + 16;
   static_assert(SM_TOTAL <= 232448, "shared memory budget");
-  static_assert(NBOX * 32 <= BSTAGE, "sub-box scratch fits a B image");
   static_assert(NCB % 8 == 0 && NCB <= OZ_MAXCB, "tile width");
 };
 
@@ -376,6 +375,8 @@ __global__ void __launch_bounds__(OZ_THREADS, 1)
   const int64_t nk = ke > kb ? ke - kb : 0;
   const int nchunks = (int)ceil_div(nk, (int64_t)Z::KD);
 
+  double2* PD = reinterpret_cast<double2*>(smem + Z::SM_PD);
+  double* PZ = reinterpret_cast<double*>(smem + Z::SM_PZ);
   int* Srow = reinterpret_cast<int*>(smem + Z::SM_S);
   int* Ts = reinterpret_cast<int*>(smem + Z::SM_T);
   unsigned* Smin = reinterpret_cast<unsigned*>(smem + Z::SM_MIN);
@@ -496,32 +497,35 @@ __global__ void __launch_bounds__(OZ_THREADS, 1)
     const int64_t c0 = kb + (int64_t)d * Z::KD;
     const int npts = (int)min((int64_t)Z::KD, ke - c0);
     const int nst = (int)ceil_div((int64_t)npts, (int64_t)OZ_KS);
-    // ---- chunk setup: per-row scale S (bound on |a| over the chunk).  The
-    // slot of the chunk's first stage is claimed here (its MMAs of NST stages
-    // ago are done); its B image is the scratch of the sub-box bounds until the
-    // stage's bulk copy is issued after the setup.
+    // ---- chunk setup: input points, per-row scale S (bound on |a| over the chunk)
     OZT_BEGIN(t6)
+    __syncthreads();  // previous chunk's points no longer read
     const int64_t p0 = it.row0 + c0;
-    const int slot0 = g % OZ_NST;
-    if (g >= OZ_NST) mbar_wait(empty(slot0), ((uint32_t)(g / OZ_NST) & 1u) ^ 1u);
     const double bx = inp.x[p0];
     const double by = KIND == KK_NUFFT ? 0.0 : inp.y[p0];
     const double bz = KIND == KK_PLATES ? inp.z[p0] : 0.0;
-    // entries past the chunk repeat its first point: finite values whose B rows are zero
-    auto pidx = [&](int k) { return p0 + (k < npts ? k : 0); };
-    // Smin of the previous chunk was read before its setup's last barrier
+    for (int k = tid; k < nst * OZ_KS; k += OZ_THREADS) {
+      // entries past the chunk repeat its first point: finite values whose B rows are zero
+      const int64_t pk = p0 + (k < npts ? k : 0);
+      const double x = inp.x[pk];
+      const double y = KIND == KK_NUFFT ? 0.0 : inp.y[pk];
+      const double z = KIND == KK_PLATES ? inp.z[pk] : 0.0;
+      PD[k] = make_double2(x, y);
+      if (KIND == KK_PLATES) PZ[k] = z;
+    }
     if (tid < OZ_BM) Smin[tid] = 0x7F7FFFFFu;  // FLT_MAX bits
     __syncthreads();
     if (KIND != KK_NUFFT) {
       // bounding boxes of the sub-boxes of 32 consecutive (tree-ordered) points,
       // in float coordinates local to the chunk's first point
-      float4* BX = reinterpret_cast<float4*>(smem + Z::SM_B + slot0 * Z::BSTAGE);  // [NBOX][lo, hi]
+      float4* BX = reinterpret_cast<float4*>(smem + Z::SM_BOX);  // [NBOX][lo, hi]
 #pragma unroll
       for (int q = 0; q < Z::NBOX / OZ_EWARPS; ++q) {
         const int sb = warp * (Z::NBOX / OZ_EWARPS) + q;
-        const int64_t pk = pidx(sb * 32 + lane);
-        const float px = (float)(inp.x[pk] - bx), py = (float)(inp.y[pk] - by);
-        const float pz = KIND == KK_PLATES ? (float)(inp.z[pk] - bz) : 0.f;
+        const int k = min(sb * 32 + lane, Z::KD - 1);
+        const double2 pd = PD[k];
+        const float px = (float)(pd.x - bx), py = (float)(pd.y - by);
+        const float pz = KIND == KK_PLATES ? (float)(PZ[k] - bz) : 0.f;
         float lx = px, ly = py, lz = pz, hx = px, hy = py, hz = pz;
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) {
@@ -556,11 +560,11 @@ __global__ void __launch_bounds__(OZ_THREADS, 1)
         if (d2 == 0.f) {
           d2 = 3.0e38f;
           for (int k = b * 32; k < b * 32 + 32; ++k) {
-            const int64_t pk = pidx(k);
-            const float ex = lx - (float)(inp.x[pk] - bx), ey = ly - (float)(inp.y[pk] - by);
+            const double2 pd = PD[k];
+            const float ex = lx - (float)(pd.x - bx), ey = ly - (float)(pd.y - by);
             float e2 = fmaf(ex, ex, ey * ey);
             if (KIND == KK_PLATES) {
-              const float ez = lz - (float)(inp.z[pk] - bz);
+              const float ez = lz - (float)(PZ[k] - bz);
               e2 = fmaf(ez, ez, e2);
             }
             d2 = fminf(d2, e2);
@@ -582,8 +586,6 @@ __global__ void __launch_bounds__(OZ_THREADS, 1)
       }
       Srow[(d & 1) * OZ_BM + tid] = S;
     }
-    // the sub-box scratch (generic proxy) is overwritten by the stage's bulk copy (async proxy)
-    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
     __syncthreads();
     if (lane == 0) { OZT_END(t6, 6) }
     // row scale 2^S, folded with the amplitude constant (see entry_rounded)
@@ -594,7 +596,7 @@ __global__ void __launch_bounds__(OZ_THREADS, 1)
       const int slot = g % OZ_NST;
       const uint32_t ph = (uint32_t)(g / OZ_NST) & 1u;
       OZT_BEGIN(t3)
-      if (s > 0 && g >= OZ_NST) mbar_wait(empty(slot), ph ^ 1u);  // s == 0: claimed in the setup
+      if (g >= OZ_NST) mbar_wait(empty(slot), ph ^ 1u);
       if (lane == 0) { OZT_END(t3, 3) }
       const int64_t k0 = c0 + (int64_t)s * OZ_KS;  // item-relative first entry of the stage
       if (tid == 0) {
@@ -608,15 +610,13 @@ __global__ void __launch_bounds__(OZ_THREADS, 1)
       const int kl = s * OZ_KS + kofs;  // chunk-relative
 #pragma unroll
       for (int e = 0; e < 8; ++e) {
-        const int64_t pk = pidx(kl + e);
-        const double sx = __ldg(inp.x + pk);
-        const double sy = KIND == KK_NUFFT ? 0.0 : __ldg(inp.y + pk);
-        const double sz = KIND == KK_PLATES ? __ldg(inp.z + pk) : 0.0;
+        const double2 sp = PD[kl + e];
+        const double sz = KIND == KK_PLATES ? PZ[kl + e] : 0.0;
         double tr, ti, amp;
         if (MODE == OP_N)
-          entry_rounded<KIND, false>(ox, oy, oz, sx, sy, sz, kappa, p2, tab, tr, ti, amp);
+          entry_rounded<KIND, false>(ox, oy, oz, sp.x, sp.y, sz, kappa, p2, tab, tr, ti, amp);
         else
-          entry_rounded<KIND, MODE == OP_H>(sx, sy, sz, ox, oy, oz, kappa, p2, tab, tr, ti, amp);
+          entry_rounded<KIND, MODE == OP_H>(sp.x, sp.y, sz, ox, oy, oz, kappa, p2, tab, tr, ti, amp);
         amp_hi = max(amp_hi, (uint32_t)__double2hiint(amp));
         lo_r[e] = (uint32_t)__double2loint(tr);
         hi_r[e] = (uint32_t)__double2hiint(tr) - 0x43380000u;
