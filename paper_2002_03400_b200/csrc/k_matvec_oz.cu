@@ -171,6 +171,16 @@ __device__ __forceinline__ void mma_i8(uint32_t d, uint64_t da, uint64_t db, uin
       "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n\t}\n" ::"r"(d),
       "l"(da), "l"(db), "r"(idesc), "r"(acc));
 }
+// one lane of a converged warp (elect.sync)
+__device__ __forceinline__ bool elect_one() {
+  uint32_t pred = 0;
+  asm volatile(
+      "{\n\t.reg .pred P;\n\telect.sync _|P, 0xffffffff;\n\tselp.b32 %0, 1, 0, P;\n\t}\n"
+      : "=r"(pred));
+  return pred != 0;
+}
+// a value the compiler may keep in a uniform register (lane 0's, broadcast)
+__device__ __forceinline__ uint32_t warp_uniform(uint32_t v) { return __shfl_sync(0xffffffffu, v, 0); }
 __device__ __forceinline__ void mbar_init(uint32_t bar, uint32_t count) {
   asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(bar), "r"(count));
 }
@@ -468,27 +478,38 @@ __global__ void __launch_bounds__(OZ_THREADS, 1)
     for (int c = 0; c < DC; ++c) yacc[c] = fma(t[c], pow2(8 * OZ_E0 - S - Ts[c0 + c]), yacc[c]);
   };
 
-  // One MMA of a stage (index i < OZ_NMMA of the fixed schedule kMmaList)
-  auto issue_mma = [&](int i, uint32_t a0, uint32_t b0, int s) {
-    constexpr OzSched kS = make_sched(Z::MAXB);
-    const uint32_t e = kS.code[i];
-    const int h = e & 1, p = (e >> 1) & 7, jlo = (e >> 4) & 15, nb = (e >> 8) & 31;
-    const bool init = (e >> 13) & 1;
-    const uint64_t da = smem_desc(a0 + h * OZ_APLANE + p * OZ_ASLICE, (OZ_BM / 8) * 128, 128);
-    const int q0 = jlo + OZ_E0 - p;
-    const uint64_t db = smem_desc(b0 + h * Z::BOPER + q0 * Z::BN2 * 16, (Z::BROWS / 8) * 128, 128);
-    mma_i8(tmem + jlo * Z::BN2, da, db, idesc_i8(128, nb * Z::BN2, p == OZ_NSL - 1, true),
-           (init && s == 0) ? 0u : 1u);
-  };
-  // all MMAs of a stage (called by the last-arriving warp's lane 0)
-  auto issue_stage = [&](int slot, uint32_t ph, int s, int nst) {
+  // All MMAs of a stage, issued by one converged warp (the group's last to
+  // write it): the base descriptors are warp-uniform values and every MMA adds
+  // a compile-time offset, so the descriptor math stays in uniform registers
+  // and one elected lane issues each tcgen05.mma back to back (round 1 issued
+  // from a divergent lane: ~100 cycles of R2UR / branch loops per MMA, which
+  // starved the tensor pipe on the small N = 64 MMAs).
+  auto issue_stage = [&](int slot_in, uint32_t ph, int s, int nst) {
+    const uint32_t slot = warp_uniform((uint32_t)slot_in);
     mbar_wait(fullB(slot), ph);
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-    const uint32_t a0 = sA + slot * OZ_ASTAGE, b0 = sB + slot * Z::BSTAGE;
+    const uint32_t tm = warp_uniform(tmem);
+    const uint64_t da0 = smem_desc(warp_uniform(sA) + slot * OZ_ASTAGE, (OZ_BM / 8) * 128, 128);
+    const uint64_t db0 = smem_desc(warp_uniform(sB) + slot * Z::BSTAGE, (Z::BROWS / 8) * 128, 128);
+    const bool first = s == 0;
+    constexpr OzSched kS = make_sched(Z::MAXB);
 #pragma unroll
-    for (int i = 0; i < make_sched(Z::MAXB).n; ++i) issue_mma(i, a0, b0, s);
-    mma_commit(empty(slot));
-    if (s == nst - 1) mma_commit(acc_full);
+    for (int i = 0; i < kS.n; ++i) {
+      const uint32_t e = kS.code[i];
+      const int h = e & 1, p = (e >> 1) & 7, jlo = (e >> 4) & 15, nb = (e >> 8) & 31;
+      const bool init = (e >> 13) & 1;
+      const int q0 = jlo + OZ_E0 - p;
+      // descriptor address fields hold addr >> 4 (14 bits; shared addresses < 2^18): offsets add in place
+      const uint64_t da = da0 + (uint64_t)((h * OZ_APLANE + p * OZ_ASLICE) >> 4);
+      const uint64_t db = db0 + (uint64_t)((h * Z::BOPER + q0 * Z::BN2 * 16) >> 4);
+      if (elect_one())
+        mma_i8(tm + jlo * Z::BN2, da, db, idesc_i8(128, nb * Z::BN2, p == OZ_NSL - 1, true), (init && first) ? 0u : 1u);
+    }
+    if (elect_one()) {
+      mma_commit(empty(slot));
+      if (s == nst - 1) mma_commit(acc_full);
+    }
+    __syncwarp();
   };
 
   int g = 0;
@@ -616,6 +637,7 @@ __global__ void __launch_bounds__(OZ_THREADS, 1)
         // 32 bits of the integer, high word - 0x43380000 = high 32 bits)
         uint32_t lo_r[8], hi_r[8], lo_i[8], hi_i[8];
         const int kl = s * OZ_KS + kofs;  // chunk-relative
+        OZT_BEGIN(t0)
 #pragma unroll
         for (int e = 0; e < 8; ++e) {
           const double2 sp = PD[kl + e];
@@ -631,6 +653,14 @@ __global__ void __launch_bounds__(OZ_THREADS, 1)
           lo_i[e] = (uint32_t)__double2loint(ti);
           hi_i[e] = (uint32_t)__double2hiint(ti) - 0x43380000u;
         }
+#ifdef OZ_TRACE
+        uint32_t dep = 0;  // make the timer wait for the evaluated words
+#pragma unroll
+        for (int e = 0; e < 8; ++e) dep ^= lo_r[e] ^ hi_r[e] ^ lo_i[e] ^ hi_i[e];
+        if (dep == 0x12345678u) amp_hi ^= 1u;
+#endif
+        if (lane == 0) { OZT_END(t0, 0) }
+        OZT_BEGIN(t1)
         // ---- byte slices -> canonical K-major A images (4x4 byte transposes)
         const int off = ((kofs >> 4) * (OZ_BM / 8) + (erow >> 3)) * 128 + (erow & 7) * 16 + (kofs & 15);
 #pragma unroll
@@ -649,21 +679,30 @@ __global__ void __launch_bounds__(OZ_THREADS, 1)
           for (int p = 0; p < OZ_NSL - 4; ++p)
             *reinterpret_cast<uint2*>(pl + (4 + p) * OZ_ASLICE) = make_uint2(h0[p], h1[p]);
         }
+        if (lane == 0) { OZT_END(t1, 1) }
       }
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
       asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
       __syncwarp();
+      unsigned last = 0;
       if (lane == 0) {
         __threadfence_block();
-        if (atomicAdd(&cnt[slot], 1u) == OZ_EWARPS / 2 - 1) {  // the group's last warp: issue the stage
+        last = atomicAdd(&cnt[slot], 1u) == OZ_EWARPS / 2 - 1;  // the group's last warp issues the stage
+        if (last) {
           cnt[slot] = 0;
           __threadfence_block();
-          while (*issued != (unsigned)g) {
-          }
-          issue_stage(slot, ph, s, nst);
-          __threadfence_block();
-          *issued = (unsigned)g + 1u;
         }
+      }
+      if (__shfl_sync(0xffffffffu, last, 0)) {
+        OZT_BEGIN(t7)
+        while (*issued != (unsigned)g) {
+        }
+        if (lane == 0) { OZT_END(t7, 7) }
+        OZT_BEGIN(t2)
+        issue_stage(slot, ph, s, nst);
+        if (lane == 0) { OZT_END(t2, 2) }
+        __threadfence_block();
+        if (lane == 0) *issued = (unsigned)g + 1u;
       }
       __syncwarp();
     }
@@ -819,8 +858,11 @@ bool run_oz(Ctx* c, Points outp, Points inp, double kappa, int64_t m_out, const 
     c->sync();
     BFLY_CUDA(cudaMemcpyFromSymbol(tr, g_oz_trace, sizeof(tr)));
     const double ctas = (double)gx * items.size() * nsplit;
-    fprintf(stderr, "[oz] ctas %.0f per-CTA cycles: total %.0f | per warp: wait empty %.0f accF %.0f setup %.0f\n",
-            ctas, tr[5] / ctas, tr[3] / ctas / OZ_EWARPS, tr[4] / ctas / OZ_EWARPS, tr[6] / ctas / OZ_EWARPS);
+    fprintf(stderr,
+            "[oz] ctas %.0f per-CTA cycles: total %.0f | per warp: eval %.0f write %.0f wait-empty %.0f accF %.0f "
+            "setup %.0f | issuer: issue %.0f ticket %.0f (per CTA)\n",
+            ctas, tr[5] / ctas, tr[0] / ctas / OZ_EWARPS, tr[1] / ctas / OZ_EWARPS, tr[3] / ctas / OZ_EWARPS,
+            tr[4] / ctas / OZ_EWARPS, tr[6] / ctas / OZ_EWARPS, tr[2] / ctas, tr[7] / ctas);
     unsigned long long z[8] = {0, 0, 0, 0, 0, 0, 0, 0};
     BFLY_CUDA(cudaMemcpyToSymbol(g_oz_trace, z, sizeof(z)));
   }
