@@ -209,6 +209,8 @@ __device__ __forceinline__ void bulk_g2s(uint32_t dst, const void* src, uint32_t
 }
 #ifdef OZ_TRACE
 __device__ unsigned long long g_oz_trace[8];
+// trace-build experiment switches (BFLY_OZ_MODE): 1 skip the MMAs, 2 skip the entry evaluation
+__device__ int g_oz_mode;
 #define OZT_BEGIN(v) const long long v = clock64();
 #define OZT_END(v, slot) atomicAdd(&g_oz_trace[slot], (unsigned long long)(clock64() - v));
 #else
@@ -502,6 +504,9 @@ __global__ void __launch_bounds__(OZ_THREADS, 1)
       // descriptor address fields hold addr >> 4 (14 bits; shared addresses < 2^18): offsets add in place
       const uint64_t da = da0 + (uint64_t)((h * OZ_APLANE + p * OZ_ASLICE) >> 4);
       const uint64_t db = db0 + (uint64_t)((h * Z::BOPER + q0 * Z::BN2 * 16) >> 4);
+#ifdef OZ_TRACE
+      if (g_oz_mode & 1) continue;
+#endif
       if (elect_one())
         mma_i8(tm + jlo * Z::BN2, da, db, idesc_i8(128, nb * Z::BN2, p == OZ_NSL - 1, true), (init && first) ? 0u : 1u);
     }
@@ -638,6 +643,17 @@ __global__ void __launch_bounds__(OZ_THREADS, 1)
         uint32_t lo_r[8], hi_r[8], lo_i[8], hi_i[8];
         const int kl = s * OZ_KS + kofs;  // chunk-relative
         OZT_BEGIN(t0)
+#ifdef OZ_TRACE
+        if (g_oz_mode & 2) {
+#pragma unroll
+          for (int e = 0; e < 8; ++e) {
+            lo_r[e] = (uint32_t)(kl + e) * 2654435761u;
+            hi_r[e] = lo_r[e] >> 20;
+            lo_i[e] = lo_r[e] ^ 0x9e3779b9u;
+            hi_i[e] = lo_i[e] >> 20;
+          }
+        } else
+#endif
 #pragma unroll
         for (int e = 0; e < 8; ++e) {
           const double2 sp = PD[kl + e];
@@ -835,6 +851,13 @@ bool run_oz(Ctx* c, Points outp, Points inp, double kappa, int64_t m_out, const 
   double nsum = 0;
   for (int i = 0; i < sch.n; ++i) nsum += (double)(((sch.code[i] >> 8) & 31) * Z::BN2);
   const double int8_ops = 2.0 * stages * (double)gx * nsum * OZ_BM * OZ_KS;
+#ifdef OZ_TRACE
+  {
+    const char* om = std::getenv("BFLY_OZ_MODE");
+    const int mode = om ? std::atoi(om) : 0;
+    BFLY_CUDA(cudaMemcpyToSymbol(g_oz_mode, &mode, sizeof(int)));
+  }
+#endif
   {
     KTimer timer(c, "kernel_matvec", kflops, kbytes);
     KTimer timer8(c, "kernel_matvec.int8_ops", int8_ops, 0.0);
@@ -855,6 +878,9 @@ bool run_oz(Ctx* c, Points outp, Points inp, double kappa, int64_t m_out, const 
 #ifdef OZ_TRACE
   {
     unsigned long long tr[8];
+    const char* om = std::getenv("BFLY_OZ_MODE");
+    const int mode = om ? std::atoi(om) : 0;
+    (void)mode;
     c->sync();
     BFLY_CUDA(cudaMemcpyFromSymbol(tr, g_oz_trace, sizeof(tr)));
     const double ctas = (double)gx * items.size() * nsplit;
