@@ -363,17 +363,14 @@ __global__ void oz_slice_kernel(const double2* __restrict__ X, const OzItem* __r
 }
 
 // ------------------------------------------------------------ main kernel
-// Ping-pong warp groups: group q = warp / 8 owns ring slot q and evaluates the
-// stages g with g % 2 == q (16 entries per thread, two batches of 8).  While
-// one group evaluates (FP64) the other slices and stores its stage or waits
-// for its slot, so the FP64 / tensor datapath is not left idle during the
-// integer phases (round 1 ran all 16 warps in lockstep on every stage).  The
-// last warp of a group to write a stage issues its MMAs at once, after the
-// other group's previous stage (a ticket keeps the issue order, so the
-// chunk's initialising MMAs come first and acc_full -- committed by the last
-// stage's issuer -- covers the chunk: tcgen05 MMAs of a CTA execute in issue
-// order).  At a chunk boundary every warp drains the finished chunk before
-// the setup barrier, so TMEM is free when the next chunk's MMAs are issued.
+// Issue scheme: no dedicated MMA warp.  Each warp, after writing its part of
+// an A stage, bumps the stage's arrival counter; the LAST warp to arrive
+// issues the stage's MMAs (after the B bulk copy landed) and commits them to
+// the slot's `empty` barrier (and, on a chunk's last stage, to `acc_full`).
+// Chunk d-1 is drained by every warp BEFORE it arrives for stage 0 of chunk
+// d, so the issuer of that stage knows TMEM is free.  tcgen05 MMAs of a CTA
+// execute in issue order, so acc_full (committed by the last stage's
+// issuer) covers the whole chunk.
 template <int KIND, int MODE, int NCB>
 __global__ void __launch_bounds__(OZ_THREADS, 1)
     matvec_oz_kernel(Points outp, Points inp, double kappa, int64_t m_out, const uint8_t* __restrict__ bimg,
@@ -413,7 +410,6 @@ __global__ void __launch_bounds__(OZ_THREADS, 1)
       mbar_init(empty(s), 1);
       cnt[s] = 0;
     }
-    cnt[2] = 0;
     mbar_init(acc_full, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
@@ -430,11 +426,9 @@ __global__ void __launch_bounds__(OZ_THREADS, 1)
   const uint32_t tmem = *tmem_slot;
   const uint32_t sA = smem_u32(smem + Z::SM_A), sB = smem_u32(smem + Z::SM_B);
 
-  // evaluation: group grp, row (warp & 7) * 16 + lane / 2, entries kofs0 .. kofs0 + 15 of the group's stages
-  const int grp = warp >> 3;
+  // evaluation: row (warp & 7) * 16 + lane / 2, entries kofs .. kofs + 7 of each stage
   const int erow = (warp & 7) * 16 + (lane >> 1);
-  const int kofs0 = (lane & 1) * 16;
-  volatile unsigned* issued = cnt + 2;  // stages whose MMAs have been issued (the ticket)
+  const int kofs = (warp >> 3) * 16 + (lane & 1) * 8;
   const int64_t gi = min(i0 + erow, m_out - 1);  // padded rows evaluate a valid row (never stored)
   const double ox = outp.x[gi];
   const double oy = KIND == KK_NUFFT ? 0.0 : outp.y[gi];
@@ -517,15 +511,18 @@ __global__ void __launch_bounds__(OZ_THREADS, 1)
     __syncwarp();
   };
 
+  // The last warp to finish stage g issues its MMAs only after evaluating its
+  // entries of stage g+1: FP64 and tensor work time-share the datapath, so
+  // the tensor then runs during the integer write phase (transposes, shared
+  // stores) instead of blocking the next evaluation.  Ordering holds: the
+  // issuer writes stage g+1 only after issuing stage g.
+  int pend_slot = -1, pend_s = 0, pend_nst = 0;
+  uint32_t pend_ph = 0;
   int g = 0;
   for (int d = 0; d < nchunks; ++d) {
     const int64_t c0 = kb + (int64_t)d * Z::KD;
     const int npts = (int)min((int64_t)Z::KD, ke - c0);
     const int nst = (int)ceil_div((int64_t)npts, (int64_t)OZ_KS);
-    if (d > 0) {  // every MMA of chunk d-1 is issued (or will be, by the other group): drain it
-      drain(d - 1);
-      asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
-    }
     // ---- chunk setup: input points, per-row scale S (bound on |a| over the chunk)
     OZT_BEGIN(t6)
     __syncthreads();  // previous chunk's points no longer read
@@ -622,107 +619,96 @@ __global__ void __launch_bounds__(OZ_THREADS, 1)
                       : KIND == KK_PLATES ? pow2(Srow[(d & 1) * OZ_BM + erow] + 1) / keval::kFourPi
                                           : pow2(Srow[(d & 1) * OZ_BM + erow] + 1);
     for (int s = 0; s < nst; ++s, ++g) {
-      if ((g & 1) != grp) continue;  // the other group's stage
-      const int slot = grp;
-      const uint32_t ph = (uint32_t)(g >> 1) & 1u;
+      const int slot = g % OZ_NST;
+      const uint32_t ph = (uint32_t)(g / OZ_NST) & 1u;
       OZT_BEGIN(t3)
       if (g >= OZ_NST) mbar_wait(empty(slot), ph ^ 1u);
       if (lane == 0) { OZT_END(t3, 3) }
       const int64_t k0 = c0 + (int64_t)s * OZ_KS;  // item-relative first entry of the stage
-      if (tid == grp * (OZ_THREADS / 2)) {
+      if (tid == 0) {
         mbar_expect_tx(fullB(slot), Z::BSTAGE);
         bulk_g2s(sB + slot * Z::BSTAGE, bimg + (it.bstage0 + k0 / OZ_KS) * (int64_t)Z::BSTAGE, Z::BSTAGE,
                  fullB(slot));
       }
-      uint8_t* a0 = smem + Z::SM_A + slot * OZ_ASTAGE;
-#pragma unroll 1
-      for (int b = 0; b < 2; ++b) {
-        const int kofs = kofs0 + 8 * b;
-        // ---- evaluate 8 entries, scale, round (magic-number: low word = low
-        // 32 bits of the integer, high word - 0x43380000 = high 32 bits)
-        uint32_t lo_r[8], hi_r[8], lo_i[8], hi_i[8];
-        const int kl = s * OZ_KS + kofs;  // chunk-relative
-        OZT_BEGIN(t0)
-#ifdef OZ_TRACE
-        if (g_oz_mode & 2) {
+      // ---- evaluate 8 entries, scale, round (magic-number: low word = low
+      // 32 bits of the integer, high word - 0x43380000 = high 32 bits)
+      uint32_t lo_r[8], hi_r[8], lo_i[8], hi_i[8];
+      const int kl = s * OZ_KS + kofs;  // chunk-relative
+      OZT_BEGIN(t0)
 #pragma unroll
-          for (int e = 0; e < 8; ++e) {
-            lo_r[e] = (uint32_t)(kl + e) * 2654435761u;
-            hi_r[e] = lo_r[e] >> 20;
-            lo_i[e] = lo_r[e] ^ 0x9e3779b9u;
-            hi_i[e] = lo_i[e] >> 20;
-          }
-        } else
-#endif
-#pragma unroll
-        for (int e = 0; e < 8; ++e) {
-          const double2 sp = PD[kl + e];
-          const double sz = KIND == KK_PLATES ? PZ[kl + e] : 0.0;
-          double tr, ti, amp;
-          if (MODE == OP_N)
-            entry_rounded<KIND, false>(ox, oy, oz, sp.x, sp.y, sz, kappa, p2, tab, tr, ti, amp);
-          else
-            entry_rounded<KIND, MODE == OP_H>(sp.x, sp.y, sz, ox, oy, oz, kappa, p2, tab, tr, ti, amp);
-          amp_hi = max(amp_hi, (uint32_t)__double2hiint(amp));
-          lo_r[e] = (uint32_t)__double2loint(tr);
-          hi_r[e] = (uint32_t)__double2hiint(tr) - 0x43380000u;
-          lo_i[e] = (uint32_t)__double2loint(ti);
-          hi_i[e] = (uint32_t)__double2hiint(ti) - 0x43380000u;
-        }
+      for (int e = 0; e < 8; ++e) {
+        const double2 sp = PD[kl + e];
+        const double sz = KIND == KK_PLATES ? PZ[kl + e] : 0.0;
+        double tr, ti, amp;
+        if (MODE == OP_N)
+          entry_rounded<KIND, false>(ox, oy, oz, sp.x, sp.y, sz, kappa, p2, tab, tr, ti, amp);
+        else
+          entry_rounded<KIND, MODE == OP_H>(sp.x, sp.y, sz, ox, oy, oz, kappa, p2, tab, tr, ti, amp);
+        amp_hi = max(amp_hi, (uint32_t)__double2hiint(amp));
+        lo_r[e] = (uint32_t)__double2loint(tr);
+        hi_r[e] = (uint32_t)__double2hiint(tr) - 0x43380000u;
+        lo_i[e] = (uint32_t)__double2loint(ti);
+        hi_i[e] = (uint32_t)__double2hiint(ti) - 0x43380000u;
+      }
 #ifdef OZ_TRACE
-        uint32_t dep = 0;  // make the timer wait for the evaluated words
+      {
+        uint32_t dep = 0;
 #pragma unroll
         for (int e = 0; e < 8; ++e) dep ^= lo_r[e] ^ hi_r[e] ^ lo_i[e] ^ hi_i[e];
         if (dep == 0x12345678u) amp_hi ^= 1u;
+      }
 #endif
-        if (lane == 0) { OZT_END(t0, 0) }
-        OZT_BEGIN(t1)
-        // ---- byte slices -> canonical K-major A images (4x4 byte transposes)
-        const int off = ((kofs >> 4) * (OZ_BM / 8) + (erow >> 3)) * 128 + (erow & 7) * 16 + (kofs & 15);
+      if (lane == 0) { OZT_END(t0, 0) }
+      if (pend_slot >= 0) {  // the last stage's issuing warp (converged)
+        OZT_BEGIN(t2)
+        issue_stage(pend_slot, pend_ph, pend_s, pend_nst);
+        if (lane == 0) { OZT_END(t2, 2) }
+        pend_slot = -1;
+      }
+      OZT_BEGIN(t1)
+      // ---- byte slices -> canonical K-major A images (4x4 byte transposes)
+      uint8_t* a0 = smem + Z::SM_A + slot * OZ_ASTAGE;
+      const int off = ((kofs >> 4) * (OZ_BM / 8) + (erow >> 3)) * 128 + (erow & 7) * 16 + (kofs & 15);
 #pragma unroll
-        for (int h = 0; h < 2; ++h) {
-          const uint32_t* lo = h ? lo_i : lo_r;
-          const uint32_t* hi = h ? hi_i : hi_r;
-          uint32_t l0[4], l1[4], h0[4], h1[4];
-          transpose4(lo[0], lo[1], lo[2], lo[3], l0);
-          transpose4(lo[4], lo[5], lo[6], lo[7], l1);
-          transpose4(hi[0], hi[1], hi[2], hi[3], h0);
-          transpose4(hi[4], hi[5], hi[6], hi[7], h1);
-          uint8_t* pl = a0 + h * OZ_APLANE + off;
+      for (int h = 0; h < 2; ++h) {
+        const uint32_t* lo = h ? lo_i : lo_r;
+        const uint32_t* hi = h ? hi_i : hi_r;
+        uint32_t l0[4], l1[4], h0[4], h1[4];
+        transpose4(lo[0], lo[1], lo[2], lo[3], l0);
+        transpose4(lo[4], lo[5], lo[6], lo[7], l1);
+        transpose4(hi[0], hi[1], hi[2], hi[3], h0);
+        transpose4(hi[4], hi[5], hi[6], hi[7], h1);
+        uint8_t* pl = a0 + h * OZ_APLANE + off;
 #pragma unroll
-          for (int p = 0; p < 4; ++p) *reinterpret_cast<uint2*>(pl + p * OZ_ASLICE) = make_uint2(l0[p], l1[p]);
+        for (int p = 0; p < 4; ++p) *reinterpret_cast<uint2*>(pl + p * OZ_ASLICE) = make_uint2(l0[p], l1[p]);
 #pragma unroll
-          for (int p = 0; p < OZ_NSL - 4; ++p)
-            *reinterpret_cast<uint2*>(pl + (4 + p) * OZ_ASLICE) = make_uint2(h0[p], h1[p]);
-        }
-        if (lane == 0) { OZT_END(t1, 1) }
+        for (int p = 0; p < OZ_NSL - 4; ++p) *reinterpret_cast<uint2*>(pl + (4 + p) * OZ_ASLICE) = make_uint2(h0[p], h1[p]);
       }
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      if (lane == 0) { OZT_END(t1, 1) }
+      if (s == 0 && d > 0) drain(d - 1);  // TMEM must be free before this stage's MMAs
       asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
       __syncwarp();
       unsigned last = 0;
       if (lane == 0) {
         __threadfence_block();
-        last = atomicAdd(&cnt[slot], 1u) == OZ_EWARPS / 2 - 1;  // the group's last warp issues the stage
+        last = atomicAdd(&cnt[slot], 1u) == OZ_EWARPS - 1;  // last warp in: issues the stage (deferred)
         if (last) {
           cnt[slot] = 0;
           __threadfence_block();
         }
       }
       if (__shfl_sync(0xffffffffu, last, 0)) {
-        OZT_BEGIN(t7)
-        while (*issued != (unsigned)g) {
-        }
-        if (lane == 0) { OZT_END(t7, 7) }
-        OZT_BEGIN(t2)
-        issue_stage(slot, ph, s, nst);
-        if (lane == 0) { OZT_END(t2, 2) }
-        __threadfence_block();
-        if (lane == 0) *issued = (unsigned)g + 1u;
+        pend_slot = slot;
+        pend_ph = ph;
+        pend_s = s;
+        pend_nst = nst;
       }
       __syncwarp();
     }
   }
+  if (pend_slot >= 0) issue_stage(pend_slot, pend_ph, pend_s, pend_nst);
+  __syncwarp();
   if (nchunks > 0) drain(nchunks - 1);
   // |v| < 2^ABITS <=> high word of the scaled amplitude < (1023 + ABITS) << 20 (NaN / inf fail)
   if (KIND != KK_NUFFT && amp_hi >= (uint32_t)(1023 + OZ_ABITS) << 20) atomicOr(flag, 2);
