@@ -22,14 +22,20 @@ def main():
     ap.add_argument("--reps", type=int, default=20)
     ap.add_argument("--trans", type=int, default=0)
     ap.add_argument("--cfg", type=int, default=2)
+    ap.add_argument("--synth", action="store_true", help="config 4's input butterfly (n=262144, leaf 64, rank 32)")
     args = ap.parse_args()
     import torch
 
     import paper_2002_03400_b200 as B
 
-    w = B.configs.build(args.cfg)
-    bf, _ = B.factorize(w.op, w.row_tree, w.col_tree, w.recon)
-    stream = torch.cuda.ExternalStream(w.op.ctx.stream)
+    if args.synth:
+        ctx = B.Context(0)
+        bf = B.synth_butterfly(12, 32, 0, leaf=64, perturb=1e-8, ctx=ctx)
+    else:
+        w = B.configs.build(args.cfg)
+        bf, _ = B.factorize(w.op, w.row_tree, w.col_tree, w.recon)
+        ctx = w.op.ctx
+    stream = torch.cuda.ExternalStream(ctx.stream)
     flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
     lib, C = B.api.lib(), B.api.C
     nin, nout = (bf.cols, bf.rows) if args.trans == 0 else (bf.rows, bf.cols)
