@@ -846,7 +846,9 @@ void launch_bgemm(Ctx* c, int op, int M, int K, int S, const cx<R>* A, int64_t l
   const bool dmma_cols = std::is_same<R, double>::value && kcols >= dmma_mink;
   // complex128 with 8..32 columns: the same staged kernel with DMMA tiles
   // (factor image only in shared memory)
-  const bool stage_dm = dmma_cols && kcols <= 32;
+  // (tall blocks, M > 32 -- the config-4 leaf-64 butterfly: up to 16 columns;
+  // wider applies run faster on the block DMMA GEMM, config-4 k = 32: 1.48 vs 1.81 ms)
+  const bool stage_dm = dmma_cols && kcols <= (M > 32 ? 16 : 32);
   const size_t stage_smem = 16 + sizeof(cx<R>) * (size_t)stage_group_elems(op, M, K, S, stage_dm ? 0 : kcols);
   if (pdl && !no_stage && (dmma_cols ? stage_dm : kcols <= 16) && ncols_all > 0 && K > 0 &&
       stage_smem <= 96 * 1024) {
@@ -855,8 +857,9 @@ void launch_bgemm(Ctx* c, int op, int M, int K, int S, const cx<R>* A, int64_t l
     static const int wpe_env = std::getenv("BFLY_STAGE_WPE") ? std::atoi(std::getenv("BFLY_STAGE_WPE")) : 0;
     // DMMA groups: 2 warps up to 16 columns, 4 beyond (measured on the
     // config-2 apply: fewer threads per entry keep ~2 stage grids resident)
+    // (tall blocks, M > 32: 4 warps -- config-4 k = 8 / 16: 0.79 -> 0.74 / 1.25 -> 1.09 ms)
     const int wpe = wpe_env > 0 ? std::min(wpe_env, 8)
-                    : stage_dm ? (kcols <= 16 ? 2 : 4)
+                    : stage_dm ? (kcols <= 16 && M <= 32 ? 2 : 4)
                     : kcols <= 2 ? 1 : kcols <= 8 ? 2 : 4;
     const size_t grp_smem = stage_smem;
     static const int epb_env = std::getenv("BFLY_STAGE_EPB") ? std::atoi(std::getenv("BFLY_STAGE_EPB")) : 0;
