@@ -19,6 +19,23 @@ __global__ void dfma_kernel(double* out, int iters, double a, double b) {
   out[blockIdx.x * blockDim.x + threadIdx.x] = x0 + x1 + x2 + x3 + x4 + x5 + x6 + x7;
 }
 
+// FP32 FFMA peak (the complex64 recompression's pipe)
+__global__ void ffma_kernel(float* out, int iters, float a, float b) {
+  float x[16];
+#pragma unroll
+  for (int j = 0; j < 16; ++j) x[j] = threadIdx.x + j;
+  for (int i = 0; i < iters; ++i) {
+#pragma unroll
+    for (int u = 0; u < 16; ++u)
+#pragma unroll
+      for (int j = 0; j < 16; ++j) x[j] = fmaf(x[j], a, b);
+  }
+  float s = 0;
+#pragma unroll
+  for (int j = 0; j < 16; ++j) s += x[j];
+  out[blockIdx.x * blockDim.x + threadIdx.x] = s;
+}
+
 __global__ void dmma_kernel(double* out, int iters) {
   double a = threadIdx.x * 1e-3, b = threadIdx.x * 2e-3;
   double c[8][2];
@@ -76,6 +93,14 @@ int main() {
     cudaEventRecord(e1); CK(cudaEventSynchronize(e1)); cudaEventElapsedTime(&ms, e0, e1);
     double flops = 2.0 * blocks * threads * (double)iters * 16 * 8;
     printf("DFMA: %.2f TFLOP/s (%.3f ms)\n", flops / ms / 1e9, ms);
+  }
+  for (int rep = 0; rep < 2; ++rep) {
+    int blocks = sms * 4, threads = 512, iters = 4096;
+    cudaEventRecord(e0);
+    ffma_kernel<<<blocks, threads>>>(reinterpret_cast<float*>(out), iters, 0.999f, 1e-3f);
+    cudaEventRecord(e1); CK(cudaEventSynchronize(e1)); cudaEventElapsedTime(&ms, e0, e1);
+    double flops = 2.0 * blocks * threads * (double)iters * 16 * 16;
+    printf("FFMA (fp32): %.2f TFLOP/s (%.3f ms)\n", flops / ms / 1e9, ms);
   }
   for (int rep = 0; rep < 2; ++rep) {
     int blocks = sms * 4, threads = 256, iters = 2048;
