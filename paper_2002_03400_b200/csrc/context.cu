@@ -166,6 +166,7 @@ void Ctx::reserve_pool(size_t bytes) {
   cudaMemPoolGetAttribute(pool, cudaMemPoolAttrReservedMemCurrent, &reserved);
   if (bytes == 0 || reserved >= used + bytes) return;
   BFLY_CUDA(cudaStreamSynchronize(stream));
+  budget = -1;  // re-sampled by the next memory guard
   BFLY_CUDA(cudaMemPoolTrimTo(pool, 0));  // drop free chunks; live allocations stay
   void* q = nullptr;
   if (cudaMallocFromPoolAsync(&q, bytes, pool, stream) == cudaSuccess) {
@@ -178,6 +179,17 @@ void Ctx::reserve_pool(size_t bytes) {
   } else {
     cudaGetLastError();  // not enough memory for one chunk: keep growing on demand
   }
+}
+
+double Ctx::device_budget() {
+  if (budget < 0) {
+    size_t free_b = 0, total_b = 0;
+    BFLY_CUDA(cudaMemGetInfo(&free_b, &total_b));
+    uint64_t reserved = 0;
+    cudaMemPoolGetAttribute(pool, cudaMemPoolAttrReservedMemCurrent, &reserved);
+    budget = (double)free_b + (double)reserved;
+  }
+  return budget;
 }
 
 // start of a factorization: its working set is measured from here

@@ -93,6 +93,11 @@ struct Ctx {
   // previous one's peak (see reserve_pool)
   size_t pool_reserved = 0, pool_hint = 0, pool_used_start = 0;
   void reserve_pool(size_t bytes);
+  // device bytes this context could hold in its pool: free device memory plus
+  // the pool's reservation, sampled on first use and after the pool is
+  // resized (the memory guard's denominator; cudaMemGetInfo is not called per level)
+  double budget = -1;
+  double device_budget();
   void mark_pool_start();
   void note_pool_peak();
 };

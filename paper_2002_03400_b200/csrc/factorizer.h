@@ -55,7 +55,6 @@ class Factorizer {
   double* margins_reset();
   // memory guard: probes per launch that fit next to the level (0: no limit)
   int64_t guard_batch_ = 0;
-  double guard_base_avail_ = -1, guard_base_used_ = 0;  // device memory left / pool use at the first guard
   void memory_guard(const std::string& what, double level_bytes, double per_probe_bytes, int64_t nprobes);
   // sharding
   int world_ = 1, rank_ = 0;
