@@ -339,6 +339,64 @@ __global__ void __launch_bounds__(256) bgemm_stage_kernel(const cx<R>* __restric
     // stale L1 line), 8 k-steps per batch of loads
     const int lane = t & 31, gq = lane >> 2, tq = lane & 3;
     const int mt = (Me + 7) / 8, ntiles = mt * ((ncols + 7) / 8);
+    if (K <= 32) {
+      // one batch per source: the next batch (next source, or the next tile's
+      // first) is requested before the current one's DMMAs, so the L2 latency
+      // of the B fragments overlaps them (config-4 k = 16 apply)
+      const int nw = gthreads >> 5;
+      auto load = [&](int tl, int s, V(&bf)[8]) {
+        const int n = (tl / mt) * 8 + gq;
+        const V* Bb = B + (s == 0 ? e.b0 : e.b1) + (int64_t)n * ldb;
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          const int k = 4 * u + tq;
+          bf[u] = (tl < ntiles && n < ncols && k < Ke) ? __ldcg(Bb + k) : mkc<R>(0, 0);
+        }
+      };
+      V bc[8], bn[8];
+      int tile = t >> 5;
+      load(tile, 0, bc);
+      for (; tile < ntiles; tile += nw) {
+        const int m = (tile % mt) * 8 + gq;
+        double acc[2][2][2] = {};  // [set][re|im][2]
+#pragma unroll
+        for (int s = 0; s < S; ++s) {
+          if (s + 1 < S) load(tile, s + 1, bn);
+          else load(tile + nw, 0, bn);
+          const V* as = As + s * aelems;
+#pragma unroll
+          for (int u = 0; u < 8; ++u) {
+            const int k = 4 * u + tq;
+            if (4 * u >= K) break;
+            V a = mkc<R>(0, 0);
+            if (m < M && k < K) {
+              a = OP == OP_N ? as[k * cpitch + m] : as[m * cpitch + k];
+              if (OP == OP_H) a.y = -a.y;
+            }
+            const V b = bc[u];
+            const int st = u & 1;
+            dmma884(acc[st][0][0], acc[st][0][1], a.x, b.x);
+            dmma884(acc[st][1][0], acc[st][1][1], a.x, b.y);
+            dmma884(acc[st][0][0], acc[st][0][1], -a.y, b.y);
+            dmma884(acc[st][1][0], acc[st][1][1], a.y, b.x);
+          }
+#pragma unroll
+          for (int u = 0; u < 8; ++u) bc[u] = bn[u];
+        }
+        if (m < Me) {
+#pragma unroll
+          for (int v = 0; v < 2; ++v) {
+            const int col = (tile / mt) * 8 + 2 * tq + v;
+            if (col >= ncols) continue;
+            V r = mkc<R>(acc[0][0][v] + acc[1][0][v], acc[0][1][v] + acc[1][1][v]);
+            V* p = C + e.c + m + (int64_t)col * ldc;
+            *p = accumulate ? cadd(*p, r) : r;
+          }
+        }
+      }
+      STAGE_TRACE(slot, 9);
+      return;
+    }
     for (int tile = t >> 5; tile < ntiles; tile += gthreads >> 5) {
       const int m = (tile % mt) * 8 + gq, n = (tile / mt) * 8 + gq;
       double acc[2][2][2] = {};  // [set][re|im][2]
@@ -846,9 +904,11 @@ void launch_bgemm(Ctx* c, int op, int M, int K, int S, const cx<R>* A, int64_t l
   const bool dmma_cols = std::is_same<R, double>::value && kcols >= dmma_mink;
   // complex128 with 8..32 columns: the same staged kernel with DMMA tiles
   // (factor image only in shared memory)
-  // (tall blocks, M > 32 -- the config-4 leaf-64 butterfly: up to 16 columns;
-  // wider applies run faster on the block DMMA GEMM, config-4 k = 32: 1.48 vs 1.81 ms)
-  const bool stage_dm = dmma_cols && kcols <= (M > 32 ? 16 : 32);
+  // (large blocks, M K >= 1024 -- the config-4 leaf-64 rank-32 butterfly: up to
+  // 16 columns; wider applies run faster on the block DMMA GEMM, config-4
+  // k = 32: 1.48 vs 1.81 ms.  Config 2's blocks are <= 512 entries)
+  const bool big_blocks = (int64_t)M * K >= 1024;
+  const bool stage_dm = dmma_cols && kcols <= (big_blocks ? 16 : 32);
   const size_t stage_smem = 16 + sizeof(cx<R>) * (size_t)stage_group_elems(op, M, K, S, stage_dm ? 0 : kcols);
   if (pdl && !no_stage && (dmma_cols ? stage_dm : kcols <= 16) && ncols_all > 0 && K > 0 &&
       stage_smem <= 96 * 1024) {
@@ -857,9 +917,10 @@ void launch_bgemm(Ctx* c, int op, int M, int K, int S, const cx<R>* A, int64_t l
     static const int wpe_env = std::getenv("BFLY_STAGE_WPE") ? std::atoi(std::getenv("BFLY_STAGE_WPE")) : 0;
     // DMMA groups: 2 warps up to 16 columns, 4 beyond (measured on the
     // config-2 apply: fewer threads per entry keep ~2 stage grids resident)
-    // (tall blocks, M > 32: 4 warps -- config-4 k = 8 / 16: 0.79 -> 0.74 / 1.25 -> 1.09 ms)
+    // (large blocks: 4 warps, config-4 k = 8 / 16: 0.79 -> 0.74 / 1.25 -> 1.10 ms;
+    // config 2's blocks keep 2)
     const int wpe = wpe_env > 0 ? std::min(wpe_env, 8)
-                    : stage_dm ? (kcols <= 16 && M <= 32 ? 2 : 4)
+                    : stage_dm ? (kcols <= 16 && !big_blocks ? 2 : 4)
                     : kcols <= 2 ? 1 : kcols <= 8 ? 2 : 4;
     const size_t grp_smem = stage_smem;
     static const int epb_env = std::getenv("BFLY_STAGE_EPB") ? std::atoi(std::getenv("BFLY_STAGE_EPB")) : 0;
