@@ -1,5 +1,8 @@
 """BASELINE configs at their FULL sizes on the GPU, through size-independent
-properties (the CPU oracle cannot factorize n = 16384 .. 262144 in test time):
+properties -- a complement to tests/test_full_parity.py, which compares the
+full-size factorizations with fixtures frozen from the reference / oracle runs
+(minutes of CPU time per config on the GPU box's host, too slow to repeat in
+the test suite):
 
 * the black box itself: sampled output rows / columns of the GPU products
   (int8-slice tensor-core K2 at full size) against the oracle's kernel
