@@ -96,6 +96,13 @@ struct CoreEnt {
   int32_t w;               // probe width
   int32_t pad_;
 };
+// saturated centre blocks (kv >= 64): B = P G^-1 by Newton-Schulz on batched
+// DMMA GEMMs (k_corefit.cu); returns the blocks fitted, the rest (not
+// converged: ill-conditioned coefficients) in `fallback` for launch_core_fit
+template <typename R>
+int64_t core_fit_big(Ctx* c, const cx<R>* Q, int64_t ldq, const cx<R>* Z, int64_t ldz, const cx<R>* Cf, int64_t ldc,
+                     cx<R>* B, int64_t ldb, int bcap, const std::vector<CoreEnt>& ents,
+                     std::vector<CoreEnt>& fallback);
 template <typename R>
 void launch_core_fit(Ctx* c, const cx<R>* Q, int64_t ldq, const cx<R>* Z, int64_t ldz, const cx<R>* Cf, int64_t ldc,
                      cx<R>* B, int64_t ldb, int bcap, const CoreEnt* ents_dev, int nent, int max_ku, int max_kv,

@@ -537,3 +537,23 @@ def test_memory_guard_shrinks_batches_then_refuses(B, monkeypatch):
     monkeypatch.setenv("BFLY_MEM_AVAIL_GB", "0.001")
     with pytest.raises(B.PreconditionError, match="memory guard"):
         B.factorize(w.op, w.row_tree, w.col_tree, w.recon)
+
+
+@pytest.mark.parametrize("n", [1024, 4096])
+def test_saturated_core_fit_newton_schulz(B, monkeypatch, n):
+    """Config 3's saturated centre blocks (kv >= 64): the Newton-Schulz
+    pseudo-inverse on batched DMMA GEMMs (k_corefit.cu) gives the core blocks
+    of the one-sided Jacobi kernel (the reference's pinv_solve semantics,
+    linalg.hpp:128-139): identical ranks, apply within 1e-11."""
+    w = B.configs.build(3, n)
+    a, la = B.factorize(w.op, w.row_tree, w.col_tree, w.recon)
+    monkeypatch.setenv("BFLY_NO_BIG_CORE_FIT", "1")
+    b, lb = B.factorize(w.op, w.row_tree, w.col_tree, w.recon)
+    np.testing.assert_array_equal(a.rank_profile(), b.rank_profile())
+    x = O.gaussian_matrix(n, 8, O.seed_mix(3, 3))
+    e = rel_err(a.apply(x), b.apply(x))
+    ta = la.phases[-1].seconds
+    tb = lb.phases[-1].seconds
+    print(f"config 3 n={n}: max rank {a.max_rank()}, centre level {ta*1e3:.1f} ms (Newton-Schulz) vs "
+          f"{tb*1e3:.1f} ms (Jacobi), apply rel diff {e:.2e}")
+    assert e < 1e-11
