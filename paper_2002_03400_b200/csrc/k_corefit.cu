@@ -7,7 +7,7 @@
 //   pinv(coeff) = coeff^H G^-1,  G = coeff coeff^H  (kv x kv, Hermitian PD),
 // and the pseudo-inverse is unique, so
 //   B = P G^-1,  P = (R^H z) coeff^H.
-// G^-1 comes from the Newton-Schulz iteration X <- X (2I - G X), X0 = G / ||G||_1^2,
+// G^-1 comes from the Newton-Schulz iteration X <- X (2I - G X), X0 = I / ||G||_1,
 // which converges quadratically for any nonsingular G (iterations ~ log2 cond(G));
 // every step is two batched GEMMs (bgemm_dmma_kernel, 64-row bands).  A block
 // whose residual ||I - G X||_F stays above 1e-12 sqrt(kv) -- cond(coeff) ~ 1e6 or
@@ -22,6 +22,8 @@
 // profiles/r02_corefit_ncu.txt).
 #include <algorithm>
 #include <cmath>
+#include <cstdio>
+#include <cstdlib>
 #include <vector>
 
 #include "kernels.cuh"
@@ -49,7 +51,7 @@ __global__ void adjoint_blocks_kernel(const cx<R>* __restrict__ src, const int64
   }
 }
 
-// per block: 1-norm of the Hermitian G (kv x kv, ld), X0 = G / ||G||_1^2
+// per block: 1-norm of the Hermitian G (kv x kv, ld), X0 = I / ||G||_1
 template <typename R>
 __global__ void ns_init_kernel(const cx<R>* __restrict__ G, cx<R>* __restrict__ X, int64_t stride, int64_t ld,
                                const int32_t* __restrict__ kvs) {
@@ -69,12 +71,13 @@ __global__ void ns_init_kernel(const cx<R>* __restrict__ G, cx<R>* __restrict__ 
     if (threadIdx.x < s) red[threadIdx.x] = fmax(red[threadIdx.x], red[threadIdx.x + s]);
     __syncthreads();
   }
+  // X0 = I / ||G||_1: the eigenvalues of G X0 lie in [lambda_min / ||G||_1, 1]
+  // (||G||_1 >= lambda_max), so ~log2(||G||_1 / lambda_min) + 6 steps converge
   const R n1 = red[0];
-  const R a = n1 > R(0) ? R(1) / (n1 * n1) : R(0);
+  const R a = n1 > R(0) ? R(1) / n1 : R(0);
   for (int64_t idx = threadIdx.x; idx < ld * ld; idx += blockDim.x) {
     const int i = (int)(idx % ld), j = (int)(idx / ld);
-    const cx<R> v = (i < kv && j < kv) ? g[idx] : mkc<R>(0, 0);
-    x[idx] = mkc<R>(v.x * a, v.y * a);
+    x[idx] = mkc<R>((i == j && i < kv) ? a : R(0), R(0));
   }
 }
 
@@ -149,6 +152,12 @@ int64_t core_fit_big(Ctx* c, const cx<R>* Q, int64_t ldq, const cx<R>* Z, int64_
     const int nb = (int)std::min<int64_t>(chunk, (int64_t)ents.size() - (int64_t)e0);
     DBuf<V> proj(c, (size_t)(s_proj * nb)), A(c, (size_t)(s_a * nb)), G(c, (size_t)(s_sq * nb)),
         X(c, (size_t)(s_sq * nb)), T(c, (size_t)(s_sq * nb)), P(c, (size_t)(s_p * nb));
+    // the GEMMs read the padding of their A operands (K up to the leading
+    // dimension, only B's rows are masked): it must hold zeros, not NaNs
+    proj.zero();
+    G.zero();
+    T.zero();
+    P.zero();
     std::vector<int64_t> coff(nb), boff(nb);
     std::vector<int32_t> kus(nb), kvs(nb), ws(nb);
     for (int b = 0; b < nb; ++b) {
@@ -257,10 +266,17 @@ int64_t core_fit_big(Ctx* c, const cx<R>* Q, int64_t ldq, const cx<R>* Z, int64_
           ok[b] = hres[b] <= tol2 * (double)kvs[b];
           all = all && ok[b];
         }
+        if (std::getenv("BFLY_DEBUG_CORE_FIT")) {
+          std::fprintf(stderr, "[core_fit_big] it %d:", it);
+          for (int b = 0; b < nb && b < 48; ++b)
+            std::fprintf(stderr, " (ku %d kv %d w %d r %.2e)", kus[b], kvs[b], ws[b], std::sqrt(hres[b]));
+          std::fprintf(stderr, "\n");
+        }
         if (all) break;  // X is the converged inverse (the residual was of this X)
       }
       // X <- X T (out of place)
       DBuf<V> Xn(c, (size_t)(s_sq * nb));
+      Xn.zero();
       launch_bgemm<R>(c, OP_N, 64, (int)ldv, 1, X.p, ldv, T.p, ldv, Xn.p, ldv, dsq.p, (int)sqe.size(), maxkv, false);
       X = std::move(Xn);
     }
