@@ -93,6 +93,12 @@ __global__ void copy_blocks_kernel(cx<R>* dst, const int64_t* idx_dst, const cx<
   }
 }
 
+__global__ void copy_idx_i32_kernel(int32_t* dst, const int64_t* idx_dst, const int32_t* src, const int64_t* idx_src,
+                                    int64_t n) {
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < n; t += (int64_t)gridDim.x * blockDim.x)
+    dst[idx_dst ? idx_dst[t] : t] = src[idx_src ? idx_src[t] : t];
+}
+
 __global__ void d2f_kernel(const double2* s, float2* d, int64_t n) {
   for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < n; t += (int64_t)gridDim.x * blockDim.x)
     d[t] = make_float2((float)s[t].x, (float)s[t].y);
@@ -161,6 +167,13 @@ void launch_copy_blocks(Ctx* c, cx<R>* dst, const int64_t* idx_dst, const cx<R>*
   copy_blocks_kernel<R><<<grid_for(c, nblocks * stride), 256, 0, c->stream>>>(dst, idx_dst, src, idx_src, nblocks,
                                                                                stride);
   BFLY_LAUNCH_CHECK("copy_blocks");
+}
+
+void launch_copy_idx_i32(Ctx* c, int32_t* dst, const int64_t* idx_dst, const int32_t* src, const int64_t* idx_src,
+                         int64_t n) {
+  if (n <= 0) return;
+  copy_idx_i32_kernel<<<grid_for(c, n), 256, 0, c->stream>>>(dst, idx_dst, src, idx_src, n);
+  BFLY_LAUNCH_CHECK("copy_idx_i32");
 }
 
 void launch_d2f(Ctx* c, const double2* s, float2* d, int64_t n) {

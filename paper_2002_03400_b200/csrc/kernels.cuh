@@ -125,6 +125,9 @@ void launch_diff_norms(Ctx* c, const cx<R>* a, const cx<R>* b, int64_t n, double
 template <typename R>
 void launch_copy_blocks(Ctx* c, cx<R>* dst, const int64_t* idx_dst, const cx<R>* src, const int64_t* idx_src,
                         int64_t nblocks, int64_t stride);
+// int32 gather / scatter: dst[idx_dst[t] or t] = src[idx_src[t] or t], t < n
+void launch_copy_idx_i32(Ctx* c, int32_t* dst, const int64_t* idx_dst, const int32_t* src, const int64_t* idx_src,
+                         int64_t n);
 // real-valued copy-converters between precisions
 void launch_d2f(Ctx* c, const double2* src, float2* dst, int64_t n);
 void launch_f2d(Ctx* c, const float2* src, double2* dst, int64_t n);
