@@ -816,14 +816,16 @@ __global__ void __launch_bounds__(256) bgemm_f32_kernel(const float2* __restrict
     __syncthreads();
 #pragma unroll
     for (int kk = 0; kk < BK; ++kk) {
+      // rows follow tx (consecutive lanes: consecutive rows -> coalesced C
+      // stores, conflict-free A reads), columns follow ty (B reads broadcast)
       float2 a[TI], b[TJ];
 #pragma unroll
       for (int i = 0; i < TI; ++i) {
-        a[i] = As[buf][kk][ty + 16 * i];
+        a[i] = As[buf][kk][tx + 16 * i];
         if (OP == OP_H) a[i].y = -a[i].y;
       }
 #pragma unroll
-      for (int j = 0; j < TJ; ++j) b[j] = Bs[buf][kk][tx + 16 * j];
+      for (int j = 0; j < TJ; ++j) b[j] = Bs[buf][kk][ty + 16 * j];
 #pragma unroll
       for (int i = 0; i < TI; ++i)
 #pragma unroll
@@ -839,11 +841,11 @@ __global__ void __launch_bounds__(256) bgemm_f32_kernel(const float2* __restrict
   float2* Cb = C + e.c;
 #pragma unroll
   for (int i = 0; i < TI; ++i) {
-    const int m = m0 + ty + 16 * i;
+    const int m = m0 + tx + 16 * i;
     if (m >= Me) continue;
 #pragma unroll
     for (int j = 0; j < TJ; ++j) {
-      const int gc = n0 + tx + 16 * j;
+      const int gc = n0 + ty + 16 * j;
       if (gc >= ncols) continue;
       float2* p = Cb + m + (int64_t)gc * ldc;
       float2 r = make_float2(acc[i][j][0], acc[i][j][1]);
@@ -1098,18 +1100,20 @@ void launch_bgemm(Ctx* c, int op, int M, int K, int S, const cx<R>* A, int64_t l
     if (!no_f32 && K > 0) {
       // tile shape with the least padded output area (ties: the larger tile)
       static const int f32_env = std::getenv("BFLY_F32_TILE") ? std::atoi(std::getenv("BFLY_F32_TILE")) : -1;
+      // shapes (TI, TJ): (2,2) (2,4) (4,2) (4,4) (2,8); BM = 16 TI, BN = 16 TJ
+      static const int tshape[5][2] = {{2, 2}, {2, 4}, {4, 2}, {4, 4}, {2, 8}};
       int best = 0;
       int64_t best_area = INT64_MAX;
-      for (int i = 0; i < 4; ++i) {
-        const int bm = 32 << (i >> 1), bn = 32 << (i & 1);
+      for (int i = 0; i < 5; ++i) {
+        const int bm = 16 * tshape[i][0], bn = 16 * tshape[i][1];
         const int64_t area = ceil_div((int64_t)M, (int64_t)bm) * bm * ceil_div((int64_t)max_ncols, (int64_t)bn) * bn;
         if (area < best_area || (area == best_area)) {
           best = i;
           best_area = area;
         }
       }
-      if (f32_env >= 0 && f32_env < 4) best = f32_env;
-      const int BMv = 32 << (best >> 1), BNv = 32 << (best & 1);
+      if (f32_env >= 0 && f32_env < 5) best = f32_env;
+      const int BMv = 16 * tshape[best][0], BNv = 16 * tshape[best][1];
       dim3 grid(nent, (unsigned)ceil_div(max_ncols, BNv), (unsigned)ceil_div(M, BMv));
       if (grid.y > 65535 || grid.z > 65535) fail(PRECONDITION, "bgemm: grid too large");
       const double nc = ncols_all > 0 ? ncols_all : max_ncols;
@@ -1124,7 +1128,8 @@ void launch_bgemm(Ctx* c, int op, int M, int K, int S, const cx<R>* A, int64_t l
       case 0: BFT(OPV, SV, 2, 2); break;     \
       case 1: BFT(OPV, SV, 2, 4); break;     \
       case 2: BFT(OPV, SV, 4, 2); break;     \
-      default: BFT(OPV, SV, 4, 4); break;    \
+      case 3: BFT(OPV, SV, 4, 4); break;     \
+      default: BFT(OPV, SV, 2, 8); break;    \
     }                                        \
   } while (0)
       if (S == 1) {
