@@ -93,24 +93,24 @@ __device__ __forceinline__ double2 kernel_entry_fast(double tx, double ty, doubl
 }
 
 
-// ---- table-based sin/cos (K2 integer-slice path): 512 table points over a
-// full turn (tab[j] = (cos, sin)(2 pi j / 512), in shared memory) and short
-// polynomials on |f| <= pi/512 (truncation < 8e-17 absolute).
-// kTabC: 512/(2 pi), (2 pi/512) high / low, 1/120, -1/6, -1/720, 1/24
-constexpr int kTabN = 512;
-static __constant__ double kTabC[8] = {81.487330863050411913668486846728, 0.012271846303085129359367044798,
-                                       4.7837765591693484e-19, 8.3333333333333333333e-03,
-                                       -1.6666666666666666667e-01, -1.3888888888888888889e-03,
-                                       4.1666666666666666667e-02, 0.0};
+// ---- table-based sin/cos (K2 integer-slice path): 2048 table points over a
+// full turn (tab[j] = (cos, sin)(2 pi j / 2048), in shared memory) and short
+// polynomials on |f| <= pi/2048.  sin f = f - f^3/6 (the f^5/120 term is
+// < 7.3e-17, 100x below the 2^-47 rounding of the sliced entries), cos f - 1 =
+// f^2 (-1/2 + f^2/24) (f^6/720 < 2e-20).  Round 1 used 512 points and one more
+// polynomial term: the 2048-point table saves one DFMA per entry (the
+// evaluation's FP64 work is on K2's critical path: a table-free polynomial
+// sin/cos measured 333 vs 300 ms per construction).
+// kTabC: 2048/(2 pi), (2 pi/2048) high / low, -, -1/6, -, 1/24
+constexpr int kTabN = 2048;
+static __constant__ double kTabC[8] = {325.94932345220167, 0.0030679615757712823, 1.195944139792337e-19,
+                                       0.0, -1.6666666666666666667e-01, 0.0, 4.1666666666666666667e-02, 0.0};
 constexpr double kMagic = 6755399441055744.0;  // 1.5 * 2^52
 
 // (s, c) of the angle a_j + f given the table entry (cos a_j, sin a_j)
 __device__ __forceinline__ void tab_poly(double f, double2 tc, double& s, double& c) {
   const double f2 = f * f;
-  const double ps = fma(f2, kTabC[3], kTabC[4]);
-  const double sf = fma(f * f2, ps, f);
-  // cos f - 1 = f2 (-1/2 + f2/24): the f^6/720 term is < 7.3e-17 for
-  // |f| <= pi/512, 12x below the 2^-50 rounding of the sliced entries
+  const double sf = fma(f * f2, kTabC[4], f);
   const double pc = fma(f2, kTabC[6], -0.5);
   const double cm1 = f2 * pc;
   s = fma(tc.x, sf, fma(tc.y, cm1, tc.y));

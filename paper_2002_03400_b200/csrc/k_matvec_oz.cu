@@ -275,7 +275,11 @@ __device__ __forceinline__ void entry_rounded(double tx, double ty, double tz, d
     }
     double h;
     const double r = keval::sqrt_rcp(d2, h);
+#ifdef OZ_POLY_SINCOS
+    keval::fast_sincos(__dmul_rn(kappa, r), sn, cs);  // experiment: no shared-memory table
+#else
     keval::tab_sincos(__dmul_rn(kappa, r), tab, sn, cs);
+#endif
     sc = h * p2;
   }
   amp = sc;
