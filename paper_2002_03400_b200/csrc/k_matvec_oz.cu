@@ -22,10 +22,14 @@
 //  * sum_k v_ik w_kc = sum_{p,q} 2^{8(p+q)} A_p B_q^T; the products with
 //    p + q >= 4 (26 of 36 slice pairs) are accumulated exactly in int32 in
 //    TMEM, one 64-column block per diagonal e = p + q (7 blocks = 448 cols).
-//    The dropped terms are < 2^-53 relative to max|v| max|w| per entry, the
-//    rounding to integers 2^-47 / 2^-46 relative to the row / column bound;
+//    The dropped terms are < 2^-52 relative to max|v| max|w| per entry, the
+//    rounding to integers 2^-47 / 2^-46 relative to the row / column bound.
+//    (`BFLY_OZ_E0=5`, an experiment build, also drops e = 4: 21 pairs, 19 %
+//    less tensor work, 7 % less K2 time, but < 2^-43.6 per entry -- the
+//    black-box products of the Helmholtz circle then differ from the FP64
+//    oracle by ~3e-12 at n = 1024 instead of ~1e-14: not kept.)
 //  * every chunk the diagonals are drained into FP64 accumulators (Horner in
-//    2^8, times 2^{32 - S_row - T_c}).
+//    2^8, times 2^{8 E0 - S_row - T_c}).
 // Complex: A_re slices multiply G1 = [B(Re x) | B(Im x)] and A_im slices
 // multiply G2 = [B(-Im x) | B(Re x)] into the same accumulator, so TMEM block
 // columns hold [Re y | Im y] directly.  For slice A_p the needed B_q
@@ -62,8 +66,14 @@ namespace {
 #endif
 constexpr int OZ_NSL = BFLY_OZ_SLICES;            // slices per operand
 static_assert(OZ_NSL == 6 || OZ_NSL == 7, "6 or 7 slices");
-constexpr int OZ_E0 = OZ_NSL - 2;                 // lowest kept diagonal e = p + q
-constexpr int OZ_NDIAG = OZ_NSL + 1;              // kept diagonals e = E0 .. 2 NSL - 2
+// lowest kept diagonal e = p + q: NSL - 2 (6 slices: e >= 4, 26 slice pairs,
+// 7 diagonals) or NSL - 1 (BFLY_OZ_E0 = 5, experiment: 21 pairs, 6 diagonals)
+#ifndef BFLY_OZ_E0
+#define BFLY_OZ_E0 (BFLY_OZ_SLICES - 2)
+#endif
+constexpr int OZ_E0 = BFLY_OZ_E0;
+static_assert(OZ_E0 == OZ_NSL - 1 || OZ_E0 == OZ_NSL - 2, "kept diagonals");
+constexpr int OZ_NDIAG = 2 * OZ_NSL - 1 - OZ_E0;  // kept diagonals e = E0 .. 2 NSL - 2
 constexpr int OZ_ABITS = OZ_NSL == 6 ? 47 : 50;   // |v| < 2^ABITS (scaled, rounded kernel entries)
 constexpr int OZ_BBITS = OZ_NSL == 6 ? 46 : 50;   // |x| < 2^BBITS (scaled, rounded probe entries)
 constexpr int OZ_KS = 32;                         // input entries per stage (MMA K)
@@ -86,10 +96,24 @@ constexpr int pow2_ceil(int x) { return x <= 32 ? 32 : x <= 64 ? 64 : x <= 128 ?
 // Per-stage MMA schedule.  Plane h (0: A_re x G1, 1: A_im x G2), slice p,
 // first diagonal block jlo, block count nb (N = BN2 nb <= 256), init (first
 // K-step of a chunk writes instead of accumulating).  Diagonal block j holds
-// e = p + q = j + 5, so slice A_p meets B_q for blocks max(0, p-5)..min(7, p+1)
-// -- a contiguous window of the concatenated B slices.  The initialising MMAs
-// (plane 0: A_6 over blocks 1..7 and A_5 over block 0) come first and cover
-// the 8 blocks disjointly.   packed: h | p << 1 | jlo << 4 | nb << 8 | init << 13
+// e = p + q = j + E0, so slice A_p meets B_q for the blocks j with
+// q = j + E0 - p in [0, NSL) -- a contiguous window of the concatenated B
+// slices.
+// OZ_ZERO_ACC (default): the warps that drain a chunk write zeros back into
+// the TMEM they read (and zero it at kernel start), so every MMA accumulates
+// and each slice's block range splits freely into windows of <= 256 columns
+// (18 MMAs per stage instead of 20; tools/microbench/tc_tmem_a.cu: 1796 vs
+// 1933 cycles per stage alone).  Otherwise the initialising MMAs (plane 0)
+// come first and cover every block exactly once: the top slice misses block
+// 0 (with E0 = NSL - 2), which the next slice's first MMA initialises.
+//   packed: h | p << 1 | jlo << 4 | nb << 8 | init << 13
+#ifndef OZ_ZERO_ACC
+#define OZ_ZERO_ACC 1
+#endif
+#ifndef OZ_GACC
+#define OZ_GACC 1
+#endif
+
 struct OzSched {
   uint32_t code[64];
   int n;
@@ -103,13 +127,23 @@ constexpr OzSched make_sched(int maxb) {
   constexpr int T = OZ_NSL - 1, D = OZ_NDIAG;
   for (int h = 0; h < 2; ++h) {
     const int init = h == 0 ? 1 : 0;
-    // top slice over blocks 1..D-1 and the next one over block 0: the first
-    // writes of plane 0 cover every block once
-    for (int j = 1; j <= D - 1; j += maxb) sc.code[sc.n++] = mma_code(h, T, j, (D - j) < maxb ? D - j : maxb, init);
-    sc.code[sc.n++] = mma_code(h, T - 1, 0, 1, init);
-    for (int j = 1; j <= T; j += maxb) sc.code[sc.n++] = mma_code(h, T - 1, j, (T + 1 - j) < maxb ? T + 1 - j : maxb, 0);
-    for (int p = T - 2; p >= 0; --p)
-      for (int j = 0; j <= p + 1; j += maxb) sc.code[sc.n++] = mma_code(h, p, j, (p + 2 - j) < maxb ? p + 2 - j : maxb, 0);
+    if (OZ_ZERO_ACC || OZ_E0 == OZ_NSL - 1) {
+      // slice p meets blocks max(0, p - E0) .. min(D - 1, T + p - E0); with
+      // E0 = NSL - 1 the top slice meets every block and initialises them
+      for (int p = T; p >= 0; --p) {
+        const int jlo = p > OZ_E0 ? p - OZ_E0 : 0;
+        const int jhi = (D - 1) < (T + p - OZ_E0) ? (D - 1) : (T + p - OZ_E0);
+        for (int j = jlo; j <= jhi; j += maxb)
+          sc.code[sc.n++] = mma_code(h, p, j, (jhi + 1 - j) < maxb ? jhi + 1 - j : maxb,
+                                     (!OZ_ZERO_ACC && p == T) ? init : 0);
+      }
+    } else {
+      for (int j = 1; j <= D - 1; j += maxb) sc.code[sc.n++] = mma_code(h, T, j, (D - j) < maxb ? D - j : maxb, init);
+      sc.code[sc.n++] = mma_code(h, T - 1, 0, 1, init);
+      for (int j = 1; j <= T; j += maxb) sc.code[sc.n++] = mma_code(h, T - 1, j, (T + 1 - j) < maxb ? T + 1 - j : maxb, 0);
+      for (int p = T - 2; p >= 0; --p)
+        for (int j = 0; j <= p + 1; j += maxb) sc.code[sc.n++] = mma_code(h, p, j, (p + 2 - j) < maxb ? p + 2 - j : maxb, 0);
+    }
   }
   return sc;
 }
@@ -229,6 +263,24 @@ __device__ __forceinline__ void tmem_ld4(uint32_t addr, uint32_t (&v)[4]) {
   asm volatile("tcgen05.ld.sync.aligned.32x32b.x4.b32 {%0,%1,%2,%3}, [%4];"
                : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3])
                : "r"(addr));
+}
+// zeros into DC consecutive TMEM columns of the warp's lane quarter
+template <int DC>
+__device__ __forceinline__ void tmem_zero(uint32_t addr) {
+  const uint32_t z = 0;
+  if constexpr (DC % 16 == 0) {
+#pragma unroll
+    for (int q = 0; q < DC / 16; ++q)
+      asm volatile(
+          "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1};" ::"r"(
+              addr + 16 * q),
+          "r"(z)
+          : "memory");
+  } else {
+#pragma unroll
+    for (int q = 0; q < DC / 4; ++q)
+      asm volatile("tcgen05.st.sync.aligned.32x32b.x4.b32 [%0], {%1,%1,%1,%1};" ::"r"(addr + 4 * q), "r"(z) : "memory");
+  }
 }
 // exact int32 -> double (magic-number bias: one LOP + one DADD)
 __device__ __forceinline__ double i2d(uint32_t v) {
@@ -442,10 +494,28 @@ __global__ void __launch_bounds__(OZ_THREADS, 1)
   const int drow = (warp & 3) * 32 + lane;
   const int dq = warp >> 2;
   constexpr int DC = Z::DC;
+  // the thread's output entries: row drow, columns (dq & 1) * DC + c of Re
+  // (dq < 2) or Im y.  OZ_GACC (default): each chunk's drained sums are added
+  // straight into them (a read-modify-write once per 64 stages; every entry
+  // has one owner), which frees the DC FP64 running sums' registers for the
+  // stage loop; otherwise they accumulate in registers and are stored once.
+  const int64_t go = i0 + drow;
+  double* const Yb = reinterpret_cast<double*>(Y + it.ybase + (int64_t)blockIdx.z * pstride);
+  const int cb = (dq & 1) * DC;
+  auto yidx = [&](int c) { return 2 * (go + (it.ycol + cb + c) * ldy) + (dq >> 1); };
+#if OZ_GACC
+  double* yacc = nullptr;
+#else
   double yacc[DC];
 #pragma unroll
   for (int c = 0; c < DC; ++c) yacc[c] = 0.0;
+#endif
   uint32_t amp_hi = 0;  // max high word of the scaled amplitudes
+  if (OZ_ZERO_ACC) {  // every warp zeroes the accumulator columns it drains
+#pragma unroll
+    for (int j = 0; j < OZ_NDIAG; ++j) tmem_zero<DC>(tmem + ((uint32_t)((warp & 3) * 32) << 16) + j * Z::BN2 + dq * DC);
+    asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+  }
 
   auto drain = [&](int d) {
     OZT_BEGIN(t4)
@@ -469,13 +539,27 @@ __global__ void __launch_bounds__(OZ_THREADS, 1)
         }
       }
       asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+      if (OZ_ZERO_ACC) tmem_zero<DC>(base);  // the next chunk's MMAs all accumulate
 #pragma unroll
       for (int c = 0; c < DC; ++c) t[c] = (j == OZ_NDIAG - 1) ? i2d(v[c]) : fma(t[c], 256.0, i2d(v[c]));
     }
+    if (OZ_ZERO_ACC) asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
     const int S = Srow[(d & 1) * OZ_BM + drow];
     const int c0 = (dq & 1) * DC;
+#if OZ_GACC
+    if (go < m_out) {
+#pragma unroll
+      for (int c = 0; c < DC; ++c)
+        if (cb + c < it.ncols) {
+          const double v = t[c] * pow2(8 * OZ_E0 - S - Ts[c0 + c]);
+          Yb[yidx(c)] = d == 0 ? v : Yb[yidx(c)] + v;
+        }
+    }
+    (void)yacc;
+#else
 #pragma unroll
     for (int c = 0; c < DC; ++c) yacc[c] = fma(t[c], pow2(8 * OZ_E0 - S - Ts[c0 + c]), yacc[c]);
+#endif
   };
 
   // All MMAs of a stage, issued by one converged warp (the group's last to
@@ -625,10 +709,13 @@ __global__ void __launch_bounds__(OZ_THREADS, 1)
     for (int s = 0; s < nst; ++s, ++g) {
       const int slot = g % OZ_NST;
       const uint32_t ph = (uint32_t)(g / OZ_NST) & 1u;
+      const int64_t k0 = c0 + (int64_t)s * OZ_KS;  // item-relative first entry of the stage
+      // ring slot: free once the MMAs of stage g - 2 completed; then its B
+      // image is refilled (waiting after the evaluation instead measured 5 %
+      // slower: the B copy then lands too late for the stage's MMAs)
       OZT_BEGIN(t3)
       if (g >= OZ_NST) mbar_wait(empty(slot), ph ^ 1u);
       if (lane == 0) { OZT_END(t3, 3) }
-      const int64_t k0 = c0 + (int64_t)s * OZ_KS;  // item-relative first entry of the stage
       if (tid == 0) {
         mbar_expect_tx(fullB(slot), Z::BSTAGE);
         bulk_g2s(sB + slot * Z::BSTAGE, bimg + (it.bstage0 + k0 / OZ_KS) * (int64_t)Z::BSTAGE, Z::BSTAGE,
@@ -717,14 +804,11 @@ __global__ void __launch_bounds__(OZ_THREADS, 1)
   // |v| < 2^ABITS <=> high word of the scaled amplitude < (1023 + ABITS) << 20 (NaN / inf fail)
   if (KIND != KK_NUFFT && amp_hi >= (uint32_t)(1023 + OZ_ABITS) << 20) atomicOr(flag, 2);
 
-  // ---- store: thread owns row drow, columns (dq & 1) * DC + c of Re (dq < 2) or Im y
-  const int64_t go = i0 + drow;
-  if (go < m_out) {
-    double* Yb = reinterpret_cast<double*>(Y + it.ybase + (int64_t)blockIdx.z * pstride);
-    const int cb = (dq & 1) * DC, comp = dq >> 1;
+  // ---- store (OZ_GACC: only an empty input range has not written its zeros)
+  if (go < m_out && (!OZ_GACC || nchunks == 0)) {
 #pragma unroll
     for (int c = 0; c < DC; ++c)
-      if (cb + c < it.ncols) Yb[2 * (go + (it.ycol + cb + c) * ldy) + comp] = yacc[c];
+      if (cb + c < it.ncols) Yb[yidx(c)] = OZ_GACC ? 0.0 : yacc[c];
   }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   __syncthreads();
