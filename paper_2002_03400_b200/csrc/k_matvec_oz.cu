@@ -83,7 +83,7 @@ constexpr int oz_kd(int kind) { return kind == KK_PLATES ? 1024 : 2048; }
 constexpr int OZ_NST = 2;                         // ring depth
 constexpr int OZ_BM = 128;                        // output rows per CTA (= TMEM lanes)
 constexpr int OZ_EWARPS = 16;
-constexpr int OZ_THREADS = OZ_EWARPS * 32;        // no dedicated MMA warp
+constexpr int OZ_THREADS = OZ_EWARPS * 32;        // evaluation threads
 constexpr int OZ_EPT = OZ_BM * OZ_KS / OZ_THREADS;  // 8 entries per thread per stage
 constexpr int OZ_ASLICE = OZ_BM * OZ_KS;           // 4096 B: one A slice (128 rows x 32 B)
 constexpr int OZ_APLANE = OZ_NSL * OZ_ASLICE;      // 28672 B
@@ -113,6 +113,18 @@ constexpr int pow2_ceil(int x) { return x <= 32 ? 32 : x <= 64 ? 64 : x <= 128 ?
 #ifndef OZ_GACC
 #define OZ_GACC 1
 #endif
+// timing experiments only (wrong results): bit 0 skips the MMAs, bit 1 the
+// kernel-entry evaluation, bit 2 the B refills, bit 3 the A-slice writes
+// (tools/k2_bench.py with an experiment build)
+#ifndef OZ_EXP
+#define OZ_EXP 0
+#endif
+// mbarrier waits with a suspend-time hint (round 2) or a plain try_wait
+// loop (default: 18.8 vs 19.5 ms per dense config-2 product)
+#ifndef OZ_WAIT_HINT
+#define OZ_WAIT_HINT 0
+#endif
+
 
 struct OzSched {
   uint32_t code[64];
@@ -223,6 +235,7 @@ __device__ __forceinline__ void mbar_expect_tx(uint32_t bar, uint32_t bytes) {
                : "memory");
 }
 __device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
+#if OZ_WAIT_HINT
   // suspend-time hint: a waiting warp sleeps until the phase completes
   // instead of spinning on issue slots the MMA-issuing warp needs
   asm volatile(
@@ -232,6 +245,15 @@ __device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
       "@!done bra WAIT_%=;\n\t}\n" ::"r"(bar),
       "r"(parity), "r"(1000000u)
       : "memory");
+#else
+  asm volatile(
+      "{\n\t.reg .pred done;\n\t"
+      "WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.acquire.cta.shared::cta.b64 done, [%0], %1;\n\t"
+      "@!done bra WAIT_%=;\n\t}\n" ::"r"(bar),
+      "r"(parity)
+      : "memory");
+#endif
 }
 __device__ __forceinline__ void mma_commit(uint32_t bar) {
   asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(bar) : "memory");
@@ -589,7 +611,7 @@ __global__ void __launch_bounds__(OZ_THREADS, 1)
 #ifdef OZ_TRACE
       if (g_oz_mode & 1) continue;
 #endif
-      if (elect_one())
+      if (!(OZ_EXP & 1) && elect_one())  // experiment bit 1: no MMAs
         mma_i8(tm + jlo * Z::BN2, da, db, idesc_i8(128, nb * Z::BN2, p == OZ_NSL - 1, true), (init && first) ? 0u : 1u);
     }
     if (elect_one()) {
@@ -717,9 +739,13 @@ __global__ void __launch_bounds__(OZ_THREADS, 1)
       if (g >= OZ_NST) mbar_wait(empty(slot), ph ^ 1u);
       if (lane == 0) { OZT_END(t3, 3) }
       if (tid == 0) {
-        mbar_expect_tx(fullB(slot), Z::BSTAGE);
-        bulk_g2s(sB + slot * Z::BSTAGE, bimg + (it.bstage0 + k0 / OZ_KS) * (int64_t)Z::BSTAGE, Z::BSTAGE,
-                 fullB(slot));
+        if (OZ_EXP & 4) {  // experiment: no B refill (the slot's image stays)
+          asm volatile("mbarrier.arrive.release.cta.shared::cta.b64 _, [%0];" ::"r"(fullB(slot)) : "memory");
+        } else {
+          mbar_expect_tx(fullB(slot), Z::BSTAGE);
+          bulk_g2s(sB + slot * Z::BSTAGE, bimg + (it.bstage0 + k0 / OZ_KS) * (int64_t)Z::BSTAGE, Z::BSTAGE,
+                   fullB(slot));
+        }
       }
       // ---- evaluate 8 entries, scale, round (magic-number: low word = low
       // 32 bits of the integer, high word - 0x43380000 = high 32 bits)
@@ -731,7 +757,11 @@ __global__ void __launch_bounds__(OZ_THREADS, 1)
         const double2 sp = PD[kl + e];
         const double sz = KIND == KK_PLATES ? PZ[kl + e] : 0.0;
         double tr, ti, amp;
-        if (MODE == OP_N)
+        if (OZ_EXP & 2) {  // experiment: no evaluation (cheap data-dependent integers)
+          tr = keval::kMagic + (double)(kl + e) + sp.x;
+          ti = keval::kMagic - (double)(kl + e);
+          amp = 0.0;
+        } else if (MODE == OP_N)
           entry_rounded<KIND, false>(ox, oy, oz, sp.x, sp.y, sz, kappa, p2, tab, tr, ti, amp);
         else
           entry_rounded<KIND, MODE == OP_H>(sp.x, sp.y, sz, ox, oy, oz, kappa, p2, tab, tr, ti, amp);
@@ -761,7 +791,7 @@ __global__ void __launch_bounds__(OZ_THREADS, 1)
       uint8_t* a0 = smem + Z::SM_A + slot * OZ_ASTAGE;
       const int off = ((kofs >> 4) * (OZ_BM / 8) + (erow >> 3)) * 128 + (erow & 7) * 16 + (kofs & 15);
 #pragma unroll
-      for (int h = 0; h < 2; ++h) {
+      for (int h = 0; h < ((OZ_EXP & 8) ? 0 : 2); ++h) {  // experiment bit 3: no A writes
         const uint32_t* lo = h ? lo_i : lo_r;
         const uint32_t* hi = h ? hi_i : hi_r;
         uint32_t l0[4], l1[4], h0[4], h1[4];
