@@ -398,45 +398,65 @@ __device__ __forceinline__ void digits7(double x, int (&d)[OZ_NSL]) {
   d[OZ_NSL - 1] = (int)q;
 }
 
-// one thread per (item row k, column c): digits of round(x * 2^T_c) written
-// into the canonical K-major images of the item's stage k/32:
-//   G1 N-row q*64 + c:      Re x      G1 N-row q*64 + 32 + c:  Im x
-//   G2 N-row q*64 + c:     -Im x      G2 N-row q*64 + 32 + c:  Re x
+// one thread per (column c, 16-entry half of a stage): the balanced digits of
+// round(x * 2^T_c) for those 16 input rows, written as whole 16-byte rows of
+// the canonical K-major images of the stage (one N-row x 16 K per store):
+//   G1 N-row q*BN2 + c:      Re x      G1 N-row q*BN2 + NCB + c:  Im x
+//   G2 N-row q*BN2 + c:     -Im x      G2 N-row q*BN2 + NCB + c:  Re x
+// (round 2 stored single bytes: 121 us per config-2 transfer level)
 template <int NCB>
 __global__ void oz_slice_kernel(const double2* __restrict__ X, const OzItem* __restrict__ items,
                                 const int32_t* __restrict__ T, uint8_t* __restrict__ img, int* __restrict__ flag) {
   using Z = OzT<NCB, 1024, false>;  // B image geometry only (independent of KD)
   const OzItem it = items[blockIdx.y];
-  const int64_t kpad = ceil_div(it.rows, (int64_t)OZ_KS) * OZ_KS;
+  const int64_t nst = ceil_div(it.rows, (int64_t)OZ_KS);
   const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (t >= kpad * NCB) return;
+  if (t >= nst * 2 * NCB) return;
   const int c = (int)(t % NCB);
-  const int64_t k = t / NCB;
-  double2 v = make_double2(0.0, 0.0);
-  if (c < it.ncols && k < it.rows) v = X[it.x_off + k + (int64_t)c * it.ldx];
+  const int kh = (int)((t / NCB) & 1);
+  const int64_t st = t / (2 * NCB);
   const double sc = pow2(T[blockIdx.y * OZ_MAXCB + c]);
-  const double xr = v.x * sc, xi = v.y * sc;
   constexpr double lim = (double)(1ll << OZ_BBITS);
-  if (!(fabs(xr) < lim && fabs(xi) < lim)) {  // NaN fails too
+  // digit s of entry j (j = 0..15) collected as bytes of 4 words per slice and part
+  uint32_t wr[OZ_NSL][4], wi[OZ_NSL][4], wn[OZ_NSL][4];
+#pragma unroll
+  for (int q = 0; q < OZ_NSL; ++q)
+#pragma unroll
+    for (int w = 0; w < 4; ++w) wr[q][w] = wi[q][w] = wn[q][w] = 0;
+  bool ok = true;
+#pragma unroll
+  for (int j = 0; j < 16; ++j) {
+    const int64_t k = st * OZ_KS + kh * 16 + j;
+    double2 v = make_double2(0.0, 0.0);
+    if (c < it.ncols && k < it.rows) v = X[it.x_off + k + (int64_t)c * it.ldx];
+    const double xr = v.x * sc, xi = v.y * sc;
+    ok = ok && fabs(xr) < lim && fabs(xi) < lim;  // NaN fails too
+    int dr[OZ_NSL], di[OZ_NSL], dn[OZ_NSL];
+    digits7(xr, dr);
+    digits7(xi, di);
+    digits7(-xi, dn);
+#pragma unroll
+    for (int q = 0; q < OZ_NSL; ++q) {
+      wr[q][j >> 2] |= (uint32_t)(dr[q] & 0xFF) << (8 * (j & 3));
+      wi[q][j >> 2] |= (uint32_t)(di[q] & 0xFF) << (8 * (j & 3));
+      wn[q][j >> 2] |= (uint32_t)(dn[q] & 0xFF) << (8 * (j & 3));
+    }
+  }
+  if (!ok) {
     atomicOr(flag, 1);
     return;
   }
-  uint8_t* g1 = img + (it.bstage0 + k / OZ_KS) * (int64_t)Z::BSTAGE;
+  uint8_t* g1 = img + (it.bstage0 + st) * (int64_t)Z::BSTAGE;
   uint8_t* g2 = g1 + Z::BOPER;
-  const int kk = (int)(k % OZ_KS);
-  int dr[OZ_NSL], di[OZ_NSL], dn[OZ_NSL];
-  digits7(xr, dr);
-  digits7(xi, di);
-  digits7(-xi, dn);
-  auto put = [&](uint8_t* base, int nrow, int d) {
-    base[((kk >> 4) * (Z::BROWS / 8) + (nrow >> 3)) * 128 + (nrow & 7) * 16 + (kk & 15)] = (uint8_t)(d & 0xFF);
+  auto row = [&](uint8_t* base, int nrow) {
+    return reinterpret_cast<uint4*>(base + (kh * (Z::BROWS / 8) + (nrow >> 3)) * 128 + (nrow & 7) * 16);
   };
 #pragma unroll
-  for (int s = 0; s < OZ_NSL; ++s) {
-    put(g1, s * Z::BN2 + c, dr[s]);
-    put(g1, s * Z::BN2 + NCB + c, di[s]);
-    put(g2, s * Z::BN2 + c, dn[s]);
-    put(g2, s * Z::BN2 + NCB + c, dr[s]);
+  for (int q = 0; q < OZ_NSL; ++q) {
+    *row(g1, q * Z::BN2 + c) = make_uint4(wr[q][0], wr[q][1], wr[q][2], wr[q][3]);
+    *row(g1, q * Z::BN2 + NCB + c) = make_uint4(wi[q][0], wi[q][1], wi[q][2], wi[q][3]);
+    *row(g2, q * Z::BN2 + c) = make_uint4(wn[q][0], wn[q][1], wn[q][2], wn[q][3]);
+    *row(g2, q * Z::BN2 + NCB + c) = make_uint4(wr[q][0], wr[q][1], wr[q][2], wr[q][3]);
   }
 }
 
@@ -927,8 +947,8 @@ bool run_oz(Ctx* c, Points outp, Points inp, double kappa, int64_t m_out, const 
     KTimer timer(c, "oz_prep", 0.0, (double)nstages * Z::BSTAGE);
     oz_colscale_kernel<<<dim3(NCB, (unsigned)items.size()), 256, 0, c->stream>>>(X, ditems.p, T.p);
     BFLY_LAUNCH_CHECK("oz_colscale");
-    const int64_t per_item = ceil_div(max_rows, (int64_t)OZ_KS) * OZ_KS * NCB;
-    oz_slice_kernel<NCB><<<dim3((unsigned)ceil_div(per_item, (int64_t)256), (unsigned)items.size()), 256, 0, c->stream>>>(
+    const int64_t per_item = ceil_div(max_rows, (int64_t)OZ_KS) * 2 * NCB;
+    oz_slice_kernel<NCB><<<dim3((unsigned)ceil_div(per_item, (int64_t)128), (unsigned)items.size()), 128, 0, c->stream>>>(
         X, ditems.p, T.p, img.p, flag);
     BFLY_LAUNCH_CHECK("oz_slice");
   }

@@ -14,6 +14,7 @@
 // (parallel round-robin pair ordering), singular values <= 1e-12 smax dropped.
 #include <algorithm>
 #include <cfloat>
+#include <cstdlib>
 
 #include "kernels.cuh"
 
@@ -260,6 +261,205 @@ __global__ void __launch_bounds__(QR_THREADS) cpqr_kernel(const cx<R>* __restric
   if (threadIdx.x == 0) ranks[e.rank_slot] = k;
 }
 
+// ------------------------------------------------- K5, one warp per block
+// The same factorization for blocks of at most 32 rows (config 2's leaves and
+// transfer blocks, r1 + r2 <= 32) with one warp per block and no CTA-wide
+// barriers: the Householder vector of column j is built with lane = row; the
+// trailing update, the norm downdates and the Q formation run with lane =
+// column (each lane sums over the rows of its own column, so no shuffle
+// reductions).  The block sits in shared memory with an odd column stride
+// (33 complex = 1 mod 8 16-byte groups: a quarter-warp's column accesses
+// hit 8 distinct bank groups).  (The 128-thread CTA version spent ~5
+// __syncthreads per pivot step: 260 us per config-2 launch.)
+constexpr int QRW_LD = 33;
+
+// sum_{i in [i0, i1)} conj(a_i) b_i with four independent partial sums (the
+// FP64 FMA latency chain of one running sum dominated the step)
+template <typename V>
+__device__ __forceinline__ V dot_conj(const V* __restrict__ a, const V* __restrict__ b, int i0, int i1) {
+  V s0 = mkc<decltype(a->x)>(0, 0), s1 = s0, s2 = s0, s3 = s0;
+  int i = i0;
+  for (; i + 3 < i1; i += 4) {
+    cfma_conj(s0, a[i], b[i]);
+    cfma_conj(s1, a[i + 1], b[i + 1]);
+    cfma_conj(s2, a[i + 2], b[i + 2]);
+    cfma_conj(s3, a[i + 3], b[i + 3]);
+  }
+  for (; i < i1; ++i) cfma_conj(s0, a[i], b[i]);
+  return cadd(cadd(s0, s1), cadd(s2, s3));
+}
+
+template <typename R>
+__global__ void __launch_bounds__(32) cpqr_warp_kernel(const cx<R>* __restrict__ src, int64_t ld_src,
+                                                       cx<R>* __restrict__ dst, int64_t ld_dst, int cap,
+                                                       const QrEnt* __restrict__ ents, int32_t* ranks, double eps_t,
+                                                       double* margins) {
+  using V = cx<R>;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  const QrEnt e = ents[blockIdx.x];
+  const int r = e.r1 + e.r2, w = e.cols;
+  const int lane = threadIdx.x;
+  V* Z = reinterpret_cast<V*>(smem_raw);  // QRW_LD x w
+  R* nu = reinterpret_cast<R*>(Z + (size_t)QRW_LD * w);
+  R* nd = nu + w;
+  V* tau = reinterpret_cast<V*>(nd + w);
+  V* out = dst + e.dst;
+  auto zero_out = [&]() {
+    for (int64_t i = lane; i < ld_dst * cap; i += 32) out[i] = mkc<R>(0, 0);
+    if (lane == 0) {
+      ranks[e.rank_slot] = 0;
+      if (margins) margins[e.rank_slot] = HUGE_VAL;
+    }
+  };
+  if (r == 0 || w == 0) {
+    zero_out();
+    return;
+  }
+  // load the compact block (lane = row) and the column norms (lane = column)
+  for (int c = 0; c < w; ++c) {
+    const V* sc = src + e.src + (int64_t)c * ld_src;
+    if (lane < r) Z[lane + c * QRW_LD] = lane < e.r1 ? sc[lane] : sc[e.src_gap + (lane - e.r1)];
+  }
+  __syncwarp();
+  R total = 0;
+  for (int c = lane; c < w; c += 32) {
+    R s = 0;
+    for (int i = 0; i < r; ++i) s += cabs2(Z[i + c * QRW_LD]);
+    nu[c] = nd[c] = sqrt(s);
+  }
+  __syncwarp();
+  for (int c = 0; c < w; ++c) total += nu[c] * nu[c];  // uniform
+  if (total == R(0)) {  // all-zero input: rank 0 (linalg.hpp:67-71)
+    zero_out();
+    return;
+  }
+  const int kmax = min(r, w);
+  R head = 0, last_kept = 0, first_dropped = -1;
+  int k = kmax;
+  for (int j = 0; j < kmax; ++j) {
+    // ---- pivot: first column with the largest updated norm
+    R best = -1;
+    int bi = w;
+    for (int c = j + lane; c < w; c += 32)
+      if (nu[c] > best) { best = nu[c]; bi = c; }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      const R ob = __shfl_xor_sync(0xffffffffu, best, o);
+      const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+      if (ob > best || (ob == best && oi < bi)) { best = ob; bi = oi; }
+    }
+    if (bi != j) {
+      if (lane < r) {
+        const V t = Z[lane + j * QRW_LD];
+        Z[lane + j * QRW_LD] = Z[lane + bi * QRW_LD];
+        Z[lane + bi * QRW_LD] = t;
+      }
+      __syncwarp();
+      if (lane == 0) {
+        R t = nu[j]; nu[j] = nu[bi]; nu[bi] = t;
+        t = nd[j]; nd[j] = nd[bi]; nd[bi] = t;
+      }
+    }
+    __syncwarp();
+    // ---- Householder reflector of column j (makeHouseholderInPlace), lane = row
+    const V zi = (lane > j && lane < r) ? Z[lane + j * QRW_LD] : mkc<R>(0, 0);
+    const R tail = warp_sum(cabs2(zi));
+    const V c0 = Z[j + j * QRW_LD];
+    V t;
+    R beta;
+    if (tail <= QrTraits<R>::tiny && c0.y * c0.y <= QrTraits<R>::tiny) {
+      t = mkc<R>(0, 0);
+      beta = c0.x;
+      if (lane > j && lane < r) Z[lane + j * QRW_LD] = mkc<R>(0, 0);
+    } else {
+      beta = sqrt(cabs2(c0) + tail);
+      if (c0.x >= R(0)) beta = -beta;
+      const V d = mkc<R>(c0.x - beta, c0.y);
+      const R dn = cabs2(d);
+      const V inv = mkc<R>(d.x / dn, -d.y / dn);
+      if (lane > j && lane < r) Z[lane + j * QRW_LD] = cmul(zi, inv);
+      t = mkc<R>((beta - c0.x) / beta, c0.y / beta);  // tau = conj((beta - c0) / beta)
+    }
+    __syncwarp();
+    if (lane == 0) {
+      Z[j + j * QRW_LD] = mkc<R>(beta, 0);
+      tau[j] = t;
+    }
+    const R absb = fabs(beta);
+    if (j == 0) head = absb;
+    if (!(absb > R(eps_t) * head)) {
+      k = j;
+      first_dropped = absb;
+      break;
+    }
+    last_kept = absb;
+    __syncwarp();
+    // ---- apply H_j = I - tau v v^H to the trailing columns (lane = column); downdate norms
+    for (int c = j + 1 + lane; c < w; c += 32) {
+      V* zc = Z + c * QRW_LD;
+      const V* v = Z + j * QRW_LD;
+      const V dot = cadd(zc[j], dot_conj(v, zc, j + 1, r));
+      const V tt = cmul(t, dot);
+      for (int i = j + 1; i < r; ++i) zc[i] = csub(zc[i], cmul(v[i], tt));
+      const V top = csub(zc[j], tt);
+      zc[j] = top;
+      // LAWN-176 downdate
+      const R nuc = nu[c], ndc = nd[c];
+      if (nuc != R(0)) {
+        R temp = sqrt(cabs2(top)) / nuc;
+        temp = (R(1) + temp) * (R(1) - temp);
+        if (temp < R(0)) temp = 0;
+        const R ratio = nuc / ndc;
+        const R temp2 = temp * ratio * ratio;
+        if (temp2 <= QrTraits<R>::sqrt_eps) {
+          R s = 0;
+          for (int i = j + 1; i < r; ++i) s += cabs2(zc[i]);
+          nu[c] = nd[c] = sqrt(s);
+        } else {
+          nu[c] = nuc * sqrt(temp);
+        }
+      }
+    }
+    __syncwarp();
+  }
+  if (lane == 0 && margins) {
+    // rank margin at the cut (diagnostic): min(|R_{k-1}|/thr - 1, 1 - |R_k|/thr), thr = eps |R_00|
+    const double thr = eps_t * (double)head;
+    double m = (double)last_kept / thr - 1.0;
+    if (first_dropped >= R(0)) m = fmin(m, 1.0 - (double)first_dropped / thr);
+    margins[e.rank_slot] = m;
+  }
+  __syncwarp();
+  // ---- form Q(:, 0:k) in place: Q = H_0 ... H_{k-1} [I_k; 0], H_i = I - conj(tau_i) v v^H
+  for (int i = k - 1; i >= 0; --i) {
+    const V tq = cconj(tau[i]);
+    const V* v = Z + i * QRW_LD;
+    for (int c = i + 1 + lane; c < k; c += 32) {
+      V* zc = Z + c * QRW_LD;
+      const V dot = cadd(zc[i], dot_conj(v, zc, i + 1, r));  // v_i = 1
+      const V tt = cmul(tq, dot);
+      for (int q = i + 1; q < r; ++q) zc[q] = csub(zc[q], cmul(v[q], tt));
+      zc[i] = csub(zc[i], tt);
+    }
+    __syncwarp();
+    if (lane > i && lane < r) Z[lane + i * QRW_LD] = cmul(mkc<R>(-tq.x, -tq.y), Z[lane + i * QRW_LD]);
+    if (lane == i) Z[i + i * QRW_LD] = mkc<R>(R(1) - tq.x, -tq.y);
+    if (lane < i) Z[lane + i * QRW_LD] = mkc<R>(0, 0);
+    __syncwarp();
+  }
+  // ---- write the padded-stacked Q block
+  for (int c = 0; c < cap; ++c)
+    for (int d = lane; d < ld_dst; d += 32) {
+      V v = mkc<R>(0, 0);
+      if (c < k) {
+        if (d < e.r1) v = Z[d + c * QRW_LD];
+        else if (d >= e.dst_gap && d < e.dst_gap + e.r2) v = Z[e.r1 + (d - e.dst_gap) + c * QRW_LD];
+      }
+      out[d + (int64_t)c * ld_dst] = v;
+    }
+  if (lane == 0) ranks[e.rank_slot] = k;
+}
+
 // --------------------------------------------------------------- core fit
 template <typename R, int QR_THREADS>
 __global__ void __launch_bounds__(QR_THREADS) core_fit_kernel(const cx<R>* __restrict__ Q, int64_t ldq,
@@ -413,6 +613,14 @@ template <typename R>
 void launch_cpqr(Ctx* c, const cx<R>* src, int64_t ld_src, cx<R>* dst, int64_t ld_dst, int cap, const QrEnt* ents,
                  int nent, int max_rows, int max_cols, int32_t* ranks, double eps, double* margins) {
   if (nent <= 0) return;
+  if (max_rows <= 32 && max_cols <= 64 && !std::getenv("BFLY_CPQR_CTA")) {
+    // one warp per block (shared memory: the block with stride QRW_LD, norms, tau)
+    const size_t smem = sizeof(cx<R>) * ((size_t)QRW_LD * max_cols + max_cols) + 2 * sizeof(R) * max_cols;
+    KTimer timer(c, "cpqr", 0.0, (double)sizeof(cx<R>) * nent * ((double)max_rows * max_cols + (double)ld_dst * cap));
+    cpqr_warp_kernel<R><<<nent, 32, smem, c->stream>>>(src, ld_src, dst, ld_dst, cap, ents, ranks, eps, margins);
+    BFLY_LAUNCH_CHECK("cpqr_warp");
+    return;
+  }
   int zld = max_rows > 0 ? max_rows : 1;
   const size_t aux = 2 * sizeof(R) * max_cols + sizeof(cx<R>) * max_cols + 64;
   size_t smem = sizeof(cx<R>) * (size_t)zld * max_cols + aux;
