@@ -1,6 +1,9 @@
 // context.h -- per-GPU context: stream, stream-ordered memory pool, launch
 // accounting, optional NCCL communicator.
 #pragma once
+#include <cstdlib>
+#include <cstdio>
+#include <chrono>
 
 #include <cuda_runtime.h>
 
@@ -108,6 +111,24 @@ Ctx* current_ctx();
 void set_current_ctx(Ctx* c);
 
 // RAII: brackets one kernel launch with events when profiling is on.
+// host-side timeline (BFLY_HOST_TRACE=1): milliseconds since the first call
+inline bool host_trace_on() {
+  static const bool on = std::getenv("BFLY_HOST_TRACE") != nullptr;
+  return on;
+}
+inline double host_ms() {
+  static const auto t0 = std::chrono::steady_clock::now();
+  return std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+}
+#define BFLY_HOST_TRACE(...)                                     \
+  do {                                                           \
+    if (::bfly::host_trace_on()) {                               \
+      fprintf(stderr, "[host %9.3f ms] ", ::bfly::host_ms());    \
+      fprintf(stderr, __VA_ARGS__);                              \
+      fputc('\n', stderr);                                       \
+    }                                                            \
+  } while (0)
+
 struct KTimer {
   Ctx* c;
   KRecord rec{};

@@ -45,6 +45,7 @@
 // coincident point, a bound that did not hold) the launch reports it and the
 // caller recomputes the product with the FP64 DMMA kernel.
 #include <algorithm>
+#include <atomic>
 #include <cstdio>
 #include <cstdlib>
 #include <string>
@@ -460,6 +461,19 @@ __global__ void oz_slice_kernel(const double2* __restrict__ X, const OzItem* __r
   }
 }
 
+// sin/cos table (cos, sin)(2 pi j / kTabN), computed once per device: the
+// per-CTA sincospi evaluation cost about one stage of FP64 work per CTA
+// (1.5 % of the one-chunk CTAs of the deepest transfer levels)
+__device__ double2 g_oz_tab[keval::kTabN];
+__global__ void oz_table_kernel() {
+  const int j = blockIdx.x * blockDim.x + threadIdx.x;
+  if (j < keval::kTabN) {
+    double s_, c_;
+    sincospi(j / (keval::kTabN / 2.0), &s_, &c_);
+    g_oz_tab[j] = make_double2(c_, s_);
+  }
+}
+
 // ------------------------------------------------------------ main kernel
 // Issue scheme: no dedicated MMA warp.  Each warp, after writing its part of
 // an A stage, bumps the stage's arrival counter; the LAST warp to arrive
@@ -513,11 +527,7 @@ __global__ void __launch_bounds__(OZ_THREADS, 1)
   }
   if (tid < NCB) Ts[tid] = Tg[blockIdx.y * OZ_MAXCB + tid];
   double2* tab = reinterpret_cast<double2*>(smem + Z::SM_TAB);
-  for (int j = tid; j < keval::kTabN; j += OZ_THREADS) {
-    double s_, c_;
-    sincospi(j / (keval::kTabN / 2.0), &s_, &c_);
-    tab[j] = make_double2(c_, s_);
-  }
+  for (int j = tid; j < keval::kTabN; j += OZ_THREADS) tab[j] = g_oz_tab[j];  // L2-resident copy
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   __syncthreads();
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
@@ -952,6 +962,15 @@ bool run_oz(Ctx* c, Points outp, Points inp, double kappa, int64_t m_out, const 
         X, ditems.p, T.p, img.p, flag);
     BFLY_LAUNCH_CHECK("oz_slice");
   }
+  {
+    static std::atomic<uint64_t> tab_ready{0};  // per device
+    const uint64_t bit = uint64_t(1) << (c->device & 63);
+    if (!(tab_ready.load() & bit)) {
+      oz_table_kernel<<<keval::kTabN / 256, 256, 0, c->stream>>>();
+      BFLY_LAUNCH_CHECK("oz_table");
+      tab_ready.fetch_or(bit);
+    }
+  }
   auto kern = matvec_oz_kernel<KIND, MODE, NCB>;
   BFLY_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Z::SM_TOTAL));
   dim3 grid((unsigned)gx, (unsigned)items.size(), (unsigned)nsplit);
@@ -985,6 +1004,7 @@ bool run_oz(Ctx* c, Points outp, Points inp, double kappa, int64_t m_out, const 
   {
     KTimer timer(c, "kernel_matvec", kflops, kbytes);
     KTimer timer8(c, "kernel_matvec.int8_ops", int8_ops, 0.0);
+    BFLY_HOST_TRACE("K2 launch");
     kern<<<grid, OZ_THREADS, Z::SM_TOTAL, c->stream>>>(outp, inp, kappa, m_out, img.p, T.p, Yt, ldy, ditems.p,
                                                     rows_per_split, pstride, flag);
     BFLY_LAUNCH_CHECK("kernel_matvec_oz");
