@@ -35,12 +35,12 @@ METRIC = "butterfly construction GFLOP/s at n=65536 complex128 (config 2)"
 FP64_PEAK_TFLOPS = 36.99  # measured DMMA m8n8k4 f64 on this pool (profiles/r01_fp64_peaks.txt)
 INT8_PEAK_TOPS = 4248.7  # measured tcgen05 kind::i8 M128 N256 from shared memory (profiles/r01_tc_i8.txt)
 # dram__bytes_read.sum + dram__bytes_write.sum of one K2 launch (the 9th of a config-2 construction: 32
-# probe segments x 32 columns, profiles/r01_matvec_oz_ncu.txt): 64.9 MB read + 1018.2 MB write (= the
+# probe segments x 32 columns, profiles/r02_k2_ncu_s2.txt): 56.0 MB read + 1018.5 MB write (= the
 # 1.07 GB product it writes); its algorithmic traffic (points + probes in, product out) is 1.11 GB
-K2_DRAM_BYTES_PER_LAUNCH = 1083077840
-# the same capture: FP64 pipe 36.7 % + int8 tensor pipe 38.3 % busy; on B200 both run on one shared
-# datapath (sm__pipe_shared_cycles_active 75.1 %), the utilisation that bounds K2
-K2_PIPES = {"fp64": 0.367, "tensor_int8": 0.383, "shared_datapath": 0.751}
+K2_DRAM_BYTES_PER_LAUNCH = 1074533056
+# the same capture: FP64 pipe 40.3 % + int8 tensor pipe 33.2 % busy; on B200 both run on one shared
+# datapath (sm__pipe_shared_cycles_active 73.5 %), the utilisation that bounds K2
+K2_PIPES = {"fp64": 0.403, "tensor_int8": 0.332, "shared_datapath": 0.735}
 CFG_ID = 2
 
 
@@ -371,7 +371,7 @@ def run_ours(args):
         "peak_source": "measured FP64 DMMA peak (tools/microbench/fp64_peaks.cu, profiles/r01_fp64_peaks.txt; "
                        "MEASURED_PEAKS.json has no FP64 entry); achieved = algorithmic complex128 contraction "
                        "flops, computed exactly via int8 slices, so frac > 1 is possible",
-        "traffic_source": "ncu --set full, one config-2 transfer-level launch (profiles/r01_matvec_oz_ncu.txt)",
+        "traffic_source": "ncu --set full, one config-2 transfer-level launch (profiles/r02_k2_ncu_s2.txt)",
         "flops_per_launch": mv["flops"] / max(1, mv["launches"]), "avg_launch_ms": mv["ms"] / max(1, mv["launches"]),
         "share_of_step": round(mv["ms"] / total_ms, 4) if total_ms else None,
     }
@@ -381,7 +381,7 @@ def run_ours(args):
                             "frac": round(tops / INT8_PEAK_TOPS, 4),
                             "peak_source": "measured tcgen05 kind::i8 M128 N256 (tools/microbench/tc_i8.cu)"}
     roofline["pipes_busy"] = dict(K2_PIPES, source="ncu --set full sm__pipe_*_cycles_active, one config-2 "
-                                                   "transfer-level launch (profiles/r01_matvec_oz_ncu.txt); FP64 "
+                                                   "transfer-level launch (profiles/r02_k2_ncu_s2.txt); FP64 "
                                                    "and int8 tensor ops time-share one datapath "
                                                    "(profiles/r01_tc_i8.txt overlap test)")
 
