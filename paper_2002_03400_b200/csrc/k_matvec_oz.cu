@@ -89,7 +89,8 @@ constexpr int OZ_EPT = OZ_BM * OZ_KS / OZ_THREADS;  // 8 entries per thread per 
 constexpr int OZ_ASLICE = OZ_BM * OZ_KS;           // 4096 B: one A slice (128 rows x 32 B)
 constexpr int OZ_APLANE = OZ_NSL * OZ_ASLICE;      // 28672 B
 constexpr int OZ_ASTAGE = 2 * OZ_APLANE;           // re + im planes
-constexpr int OZ_MAXCB = 32;                       // widest probe tile (complex columns)
+constexpr int OZ_MAXCB = 64;                       // stride of the per-tile column scales
+constexpr int OZ_MAXCB1 = 32;                      // widest probe tile of the single-CTA kernel
 static_assert(OZ_EPT == 8, "thread mapping assumes 8 entries per thread");
 
 constexpr int pow2_ceil(int x) { return x <= 32 ? 32 : x <= 64 ? 64 : x <= 128 ? 128 : x <= 256 ? 256 : 512; }
@@ -185,7 +186,7 @@ struct OzT {
   static constexpr int SM_BOX = SM_TAB + keval::kTabN * 16;  // float4 sub-box bounds [NBOX][2]
   static constexpr int SM_CNT = SM_BOX + NBOX * 32;     // uint stage arrival counters [NST]
   static constexpr int SM_BAR = SM_CNT + 16;            // mbarriers
-  static constexpr int NBAR = 2 * OZ_NST + 1;
+  static constexpr int NBAR = 3 * OZ_NST + 1;  // fullB, empty, acc_full (+ fullA: the pair kernel)
   static constexpr int SM_TMEM = SM_BAR + NBAR * 8;
   static constexpr int SM_TOTAL = SM_TMEM + 16;
   static_assert(SM_TOTAL <= 232448, "shared memory budget");
@@ -879,6 +880,430 @@ __global__ void __launch_bounds__(OZ_THREADS, 1)
   }
 }
 
+// ------------------------------------------------------- K2, CTA pairs
+// Probe tiles of 33..40 columns (config 2's fused leaf rounds, 6 + 10 + 18 =
+// 34; config 1's 34..40-wide levels) need 7 x 80 = 560 accumulator columns,
+// more than TMEM holds, so one CTA cannot take them in one pass; two passes
+// evaluate every kernel entry twice.  A cluster of two CTAs on the same 128
+// output rows and input range instead evaluates each stage ONCE: CTA r
+// evaluates the stage's K-half r (16 of the 32 input entries) and sends its
+// 24 KB of A slices to the peer with one DSMEM bulk copy (async proxy,
+// completing on the peer's fullA barrier), and the pair splits the diagonal
+// blocks: CTA 0 keeps e = 4, 5, 9, 10 (14 slice pairs, 4 x 80 TMEM columns),
+// CTA 1 e = 6, 7, 8 (12 pairs, 3 x 80).  Each CTA drains its own diagonals
+// into its own partial output slice; the split-K reduce adds the two.
+// A stage layout here: [K-half][plane][slice] 2 KB blocks, so a CTA's half is
+// one contiguous 24 KB (the MMA descriptor's K step LBO = 24 KB).
+// The ring slot's `empty` barrier counts BOTH CTAs' MMA commits (multicast):
+// a CTA overwrites its half -- in its own slot and, by the copy, in the
+// peer's -- only when both have finished reading the stage two back.
+constexpr int OZP_NCB = 40;
+constexpr int OZP_HALF = OZ_ASTAGE / 2;  // 24 KB: one CTA's K-half of a stage
+static_assert(OZ_E0 == 4 && OZ_NDIAG == 7, "pair diagonal split assumes e = 4 .. 10");
+__host__ __device__ constexpr int ozp_nloc(int cr) { return cr == 0 ? 4 : 3; }
+// global diagonal block of local block jl
+__host__ __device__ constexpr int ozp_glob(int cr, int jl) { return cr == 0 ? (jl < 2 ? jl : jl + 3) : jl + 2; }
+// local block of global block j, or -1
+__host__ __device__ constexpr int ozp_loc(int cr, int j) {
+  return cr == 0 ? (j < 2 ? j : (j >= 5 ? j - 3 : -1)) : ((j >= 2 && j <= 4) ? j - 2 : -1);
+}
+// schedule of CTA cr: per plane and slice, maximal runs of its blocks (contiguous
+// locally AND globally), windows of <= maxb blocks.  packed as mma_code plus the
+// local first block at bit 14
+constexpr OzSched make_sched_pair(int cr, int maxb) {
+  OzSched sc{};
+  sc.n = 0;
+  constexpr int T = OZ_NSL - 1, D = OZ_NDIAG;
+  for (int h = 0; h < 2; ++h)
+    for (int p = T; p >= 0; --p) {
+      const int jlo = p > OZ_E0 ? p - OZ_E0 : 0;
+      const int jhi = (D - 1) < (T + p - OZ_E0) ? (D - 1) : (T + p - OZ_E0);
+      int j = jlo;
+      while (j <= jhi) {
+        if (ozp_loc(cr, j) < 0) { ++j; continue; }
+        int e = j;
+        while (e + 1 <= jhi && ozp_loc(cr, e + 1) == ozp_loc(cr, e) + 1 && e + 1 - j < maxb) ++e;
+        sc.code[sc.n++] = mma_code(h, p, j, e - j + 1, 0) | ((uint32_t)ozp_loc(cr, j) << 14);
+        j = e + 1;
+      }
+    }
+  return sc;
+}
+template <int CR>
+struct OzPairSched {
+  static constexpr OzSched value = make_sched_pair(CR, OzT<OZP_NCB, 1024, false>::MAXB);
+};
+__device__ __forceinline__ uint32_t cluster_ctarank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ void cluster_sync_all() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+__device__ __forceinline__ uint32_t mapa_peer(uint32_t addr, uint32_t peer) {
+  uint32_t r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(addr), "r"(peer));
+  return r;
+}
+// tcgen05.commit arriving on the barrier at this offset in both CTAs of the pair
+__device__ __forceinline__ void mma_commit_pair(uint32_t bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
+                   bar),
+               "h"((uint16_t)3)
+               : "memory");
+}
+// local shared -> peer shared bulk copy, completing transaction bytes on the peer's barrier
+__device__ __forceinline__ void bulk_s2peer(uint32_t dst_cluster, uint32_t src, uint32_t bytes, uint32_t bar_cluster) {
+  asm volatile("cp.async.bulk.shared::cluster.shared::cta.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                   dst_cluster),
+               "r"(src), "r"(bytes), "r"(bar_cluster)
+               : "memory");
+}
+
+template <int KIND, int MODE>
+__global__ void __launch_bounds__(OZ_THREADS, 1)
+    matvec_oz_pair_kernel(Points outp, Points inp, double kappa, int64_t m_out, const uint8_t* __restrict__ bimg,
+                          const int32_t* __restrict__ Tg, double2* __restrict__ Y, int64_t ldy,
+                          const OzItem* __restrict__ items, int64_t rows_per_split, int64_t pstride,
+                          int* __restrict__ flag) {
+  constexpr int NCB = OZP_NCB;
+  using Z = OzT<NCB, oz_kd(KIND), KIND == KK_PLATES>;
+  extern __shared__ __align__(1024) uint8_t smem[];
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const uint32_t cr = cluster_ctarank(), peer = cr ^ 1u;
+  const OzItem it = items[blockIdx.y];
+  const int64_t i0 = (int64_t)(blockIdx.x >> 1) * OZ_BM;
+  const int64_t kb = (int64_t)blockIdx.z * rows_per_split;
+  const int64_t ke = min(it.rows, kb + rows_per_split);
+  const int64_t nk = ke > kb ? ke - kb : 0;
+  const int nchunks = (int)ceil_div(nk, (int64_t)Z::KD);
+
+  double2* PD = reinterpret_cast<double2*>(smem + Z::SM_PD);
+  double* PZ = reinterpret_cast<double*>(smem + Z::SM_PZ);
+  int* Srow = reinterpret_cast<int*>(smem + Z::SM_S);
+  int* Ts = reinterpret_cast<int*>(smem + Z::SM_T);
+  unsigned* Smin = reinterpret_cast<unsigned*>(smem + Z::SM_MIN);
+  unsigned* cnt = reinterpret_cast<unsigned*>(smem + Z::SM_CNT);
+  const uint32_t bar0 = smem_u32(smem + Z::SM_BAR);
+  auto fullB = [&](int s) { return bar0 + 8u * s; };
+  auto empty = [&](int s) { return bar0 + 8u * (OZ_NST + s); };
+  const uint32_t acc_full = bar0 + 8u * (2 * OZ_NST);
+  auto fullA = [&](int s) { return bar0 + 8u * (2 * OZ_NST + 1 + s); };  // the peer's K-half landed
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + Z::SM_TMEM);
+  constexpr int COLS0 = pow2_ceil(ozp_nloc(0) * Z::BN2), COLS1 = pow2_ceil(ozp_nloc(1) * Z::BN2);
+
+  if (warp == 0) {
+    if (cr == 0)
+      asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                   "n"(COLS0));
+    else
+      asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                   "n"(COLS1));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  if (tid == 32) {
+    for (int s = 0; s < OZ_NST; ++s) {
+      mbar_init(fullB(s), 1);
+      mbar_init(empty(s), 2);  // this CTA's and the peer's MMA commits
+      mbar_init(fullA(s), 1);
+      cnt[s] = 0;
+    }
+    mbar_init(acc_full, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (tid < NCB) Ts[tid] = Tg[blockIdx.y * OZ_MAXCB + tid];
+  double2* tab = reinterpret_cast<double2*>(smem + Z::SM_TAB);
+  for (int j = tid; j < keval::kTabN; j += OZ_THREADS) tab[j] = g_oz_tab[j];
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  cluster_sync_all();  // barriers of both CTAs initialised before any remote arrive
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  const uint32_t tmem = *tmem_slot;
+  const uint32_t sA = smem_u32(smem + Z::SM_A), sB = smem_u32(smem + Z::SM_B);
+
+  // evaluation: row warp * 8 + lane / 4, entries 4 (lane & 3) .. + 3 of this CTA's K-half
+  const int erow = warp * 8 + (lane >> 2);
+  const int kq = (lane & 3) * 4;
+  const int64_t gi = min(i0 + erow, m_out - 1);
+  const double ox = outp.x[gi];
+  const double oy = KIND == KK_NUFFT ? 0.0 : outp.y[gi];
+  const double oz = KIND == KK_PLATES ? outp.z[gi] : 0.0;
+  // drain: TMEM lane quarter = warp & 3, column quarter = warp >> 2 of [Re y | Im y]
+  const int drow = (warp & 3) * 32 + lane;
+  const int dq = warp >> 2;
+  constexpr int DC = Z::DC;  // 20
+  const int nloc = ozp_nloc((int)cr);
+  const int64_t go = i0 + drow;
+  // this CTA's partial output slice (the split-K reduce adds the pair's two)
+  double* const Yb = reinterpret_cast<double*>(Y + it.ybase + ((int64_t)blockIdx.z * 2 + cr) * pstride);
+  const int cb = (dq & 1) * DC;
+  auto yidx = [&](int c) { return 2 * (go + (it.ycol + cb + c) * ldy) + (dq >> 1); };
+  uint32_t amp_hi = 0;
+  for (int jl = 0; jl < nloc; ++jl) tmem_zero<DC>(tmem + ((uint32_t)((warp & 3) * 32) << 16) + jl * Z::BN2 + dq * DC);
+  asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+
+  auto drain = [&](int d) {
+    mbar_wait(acc_full, (uint32_t)d & 1u);
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    // partial Horner over this CTA's diagonals, in global diagonal order
+    double t[DC];
+#pragma unroll
+    for (int c = 0; c < DC; ++c) t[c] = 0.0;
+    int jprev = -1;
+    for (int jl = nloc - 1; jl >= 0; --jl) {
+      const int j = ozp_glob((int)cr, jl);
+      const uint32_t base = tmem + ((uint32_t)((warp & 3) * 32) << 16) + jl * Z::BN2 + dq * DC;
+      uint32_t v[DC];
+#pragma unroll
+      for (int q = 0; q < DC / 4; ++q) {
+        uint32_t w[4];
+        tmem_ld4(base + 4 * q, w);
+#pragma unroll
+        for (int u = 0; u < 4; ++u) v[4 * q + u] = w[u];
+      }
+      asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+      tmem_zero<DC>(base);
+      const double sh = jprev < 0 ? 0.0 : pow2(8 * (jprev - j));  // exact: 2^8 steps
+#pragma unroll
+      for (int c = 0; c < DC; ++c) t[c] = fma(t[c], sh, i2d(v[c]));
+      jprev = j;
+    }
+    asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+    // t holds sum_j d_j 2^{8 (j - jmin)}; jmin = the lowest global block of this CTA
+    const int jmin = jprev;
+    const int S = Srow[(d & 1) * OZ_BM + drow];
+    const int c0 = (dq & 1) * DC;
+    if (go < m_out) {
+#pragma unroll
+      for (int c = 0; c < DC; ++c)
+        if (cb + c < it.ncols) {
+          const double v = t[c] * pow2(8 * (OZ_E0 + jmin) - S - Ts[c0 + c]);
+          Yb[yidx(c)] = d == 0 ? v : Yb[yidx(c)] + v;
+        }
+    }
+  };
+
+  auto issue_stage = [&](int slot_in, uint32_t ph, int s, int nst) {
+    const uint32_t slot = warp_uniform((uint32_t)slot_in);
+    mbar_wait(fullB(slot), ph);
+    mbar_wait(fullA(slot), ph);
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    const uint32_t tm = warp_uniform(tmem);
+    // A: K step = the other CTA's half (LBO 24 KB), 8-row groups 128 B apart
+    const uint64_t da0 = smem_desc(warp_uniform(sA) + slot * OZ_ASTAGE, OZP_HALF, 128);
+    const uint64_t db0 = smem_desc(warp_uniform(sB) + slot * Z::BSTAGE, (Z::BROWS / 8) * 128, 128);
+    auto run = [&](auto sched) {
+      constexpr OzSched kS = decltype(sched)::value;
+      (void)sched;
+#pragma unroll
+      for (int i = 0; i < kS.n; ++i) {
+        const uint32_t e = kS.code[i];
+        const int h = e & 1, p = (e >> 1) & 7, jlo = (e >> 4) & 15, nb = (e >> 8) & 31, jl = (e >> 14) & 15;
+        const int q0 = jlo + OZ_E0 - p;
+        const uint64_t da = da0 + (uint64_t)(((h * OZ_NSL + p) * (OZP_HALF / OZ_NSL / 2)) >> 4);
+        const uint64_t db = db0 + (uint64_t)((h * Z::BOPER + q0 * Z::BN2 * 16) >> 4);
+        if (elect_one()) mma_i8(tm + jl * Z::BN2, da, db, idesc_i8(128, nb * Z::BN2, p == OZ_NSL - 1, true), 1u);
+      }
+    };
+    if (cr == 0)
+      run(OzPairSched<0>{});
+    else
+      run(OzPairSched<1>{});
+    if (elect_one()) {
+      mma_commit_pair(empty(slot));
+      if (s == nst - 1) mma_commit(acc_full);
+    }
+    __syncwarp();
+  };
+
+  int pend_slot = -1, pend_s = 0, pend_nst = 0;
+  uint32_t pend_ph = 0;
+  int g = 0;
+  for (int d = 0; d < nchunks; ++d) {
+    const int64_t c0 = kb + (int64_t)d * Z::KD;
+    const int npts = (int)min((int64_t)Z::KD, ke - c0);
+    const int nst = (int)ceil_div((int64_t)npts, (int64_t)OZ_KS);
+    // ---- chunk setup (both CTAs compute the same row scales S)
+    __syncthreads();
+    const int64_t p0 = it.row0 + c0;
+    const double bx = inp.x[p0];
+    const double by = KIND == KK_NUFFT ? 0.0 : inp.y[p0];
+    const double bz = KIND == KK_PLATES ? inp.z[p0] : 0.0;
+    for (int k = tid; k < nst * OZ_KS; k += OZ_THREADS) {
+      const int64_t pk = p0 + (k < npts ? k : 0);
+      PD[k] = make_double2(inp.x[pk], KIND == KK_NUFFT ? 0.0 : inp.y[pk]);
+      if (KIND == KK_PLATES) PZ[k] = inp.z[pk];
+    }
+    if (tid < OZ_BM) Smin[tid] = 0x7F7FFFFFu;
+    __syncthreads();
+    if (KIND != KK_NUFFT) {
+      float4* BX = reinterpret_cast<float4*>(smem + Z::SM_BOX);
+#pragma unroll
+      for (int q = 0; q < Z::NBOX / OZ_EWARPS; ++q) {
+        const int sb = warp * (Z::NBOX / OZ_EWARPS) + q;
+        const int k = min(sb * 32 + lane, Z::KD - 1);
+        const double2 pd = PD[k];
+        const float px = (float)(pd.x - bx), py = (float)(pd.y - by);
+        const float pz = KIND == KK_PLATES ? (float)(PZ[k] - bz) : 0.f;
+        float lx = px, ly = py, lz = pz, hx = px, hy = py, hz = pz;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+          lx = fminf(lx, __shfl_xor_sync(0xffffffffu, lx, o));
+          ly = fminf(ly, __shfl_xor_sync(0xffffffffu, ly, o));
+          lz = fminf(lz, __shfl_xor_sync(0xffffffffu, lz, o));
+          hx = fmaxf(hx, __shfl_xor_sync(0xffffffffu, hx, o));
+          hy = fmaxf(hy, __shfl_xor_sync(0xffffffffu, hy, o));
+          hz = fmaxf(hz, __shfl_xor_sync(0xffffffffu, hz, o));
+        }
+        if (lane == 0) {
+          BX[2 * sb] = make_float4(lx, ly, lz, 0.f);
+          BX[2 * sb + 1] = make_float4(hx, hy, hz, 0.f);
+        }
+      }
+      __syncthreads();
+      const int r = tid & (OZ_BM - 1), part = tid >> 7;
+      const int64_t gr = min(i0 + r, m_out - 1);
+      const float lx = (float)(outp.x[gr] - bx), ly = (float)(outp.y[gr] - by);
+      const float lz = KIND == KK_PLATES ? (float)(outp.z[gr] - bz) : 0.f;
+      const int nbox = (nst * OZ_KS) / 32;
+      float mn = 3.0e38f;
+      for (int b = part; b < nbox; b += OZ_THREADS / OZ_BM) {
+        const float4 lo = BX[2 * b], hi = BX[2 * b + 1];
+        const float dx = fmaxf(fmaxf(lo.x - lx, lx - hi.x), 0.f);
+        const float dy = fmaxf(fmaxf(lo.y - ly, ly - hi.y), 0.f);
+        const float dz = KIND == KK_PLATES ? fmaxf(fmaxf(lo.z - lz, lz - hi.z), 0.f) : 0.f;
+        float d2 = fmaf(dz, dz, fmaf(dy, dy, dx * dx));
+        if (d2 == 0.f) {
+          d2 = 3.0e38f;
+          for (int k = b * 32; k < b * 32 + 32; ++k) {
+            const double2 pd = PD[k];
+            const float ex = lx - (float)(pd.x - bx), ey = ly - (float)(pd.y - by);
+            float e2 = fmaf(ex, ex, ey * ey);
+            if (KIND == KK_PLATES) {
+              const float ez = lz - (float)(PZ[k] - bz);
+              e2 = fmaf(ez, ez, e2);
+            }
+            d2 = fminf(d2, e2);
+          }
+        }
+        mn = fminf(mn, d2);
+      }
+      atomicMin(&Smin[r], __float_as_uint(mn));
+    }
+    __syncthreads();
+    if (tid < OZ_BM) {
+      int S = OZ_ABITS - 1;
+      if (KIND != KK_NUFFT) {
+        const float mn = __uint_as_float(Smin[tid]);
+        double amax = mn > 1e-36f ? 2.0 / sqrt((double)mn) : 1e300;
+        if (KIND == KK_PLATES) amax /= keval::kFourPi;
+        S = amax < 1e300 ? (OZ_ABITS - 1) - ilogb(amax) : 0;
+      }
+      Srow[(d & 1) * OZ_BM + tid] = S;
+    }
+    __syncthreads();
+    const double p2 = KIND == KK_NUFFT    ? pow2(Srow[(d & 1) * OZ_BM + erow])
+                      : KIND == KK_PLATES ? pow2(Srow[(d & 1) * OZ_BM + erow] + 1) / keval::kFourPi
+                                          : pow2(Srow[(d & 1) * OZ_BM + erow] + 1);
+    for (int s = 0; s < nst; ++s, ++g) {
+      const int slot = g % OZ_NST;
+      const uint32_t ph = (uint32_t)(g / OZ_NST) & 1u;
+      const int64_t k0 = c0 + (int64_t)s * OZ_KS;
+      // slot free: both CTAs' MMAs of stage g - 2 done
+      if (g >= OZ_NST) mbar_wait(empty(slot), ph ^ 1u);
+      if (tid == 0) {
+        mbar_expect_tx(fullB(slot), Z::BSTAGE);
+        bulk_g2s(sB + slot * Z::BSTAGE, bimg + (it.bstage0 + k0 / OZ_KS) * (int64_t)Z::BSTAGE, Z::BSTAGE, fullB(slot));
+        mbar_expect_tx(fullA(slot), OZP_HALF);  // the peer's half of this stage
+      }
+      // ---- evaluate this CTA's 4 entries of its K-half
+      uint32_t lo_r[4], hi_r[4], lo_i[4], hi_i[4];
+      const int kl = s * OZ_KS + (int)cr * 16 + kq;  // chunk-relative
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        const double2 sp = PD[kl + e];
+        const double sz = KIND == KK_PLATES ? PZ[kl + e] : 0.0;
+        double tr, ti, amp;
+        if (MODE == OP_N)
+          entry_rounded<KIND, false>(ox, oy, oz, sp.x, sp.y, sz, kappa, p2, tab, tr, ti, amp);
+        else
+          entry_rounded<KIND, MODE == OP_H>(sp.x, sp.y, sz, ox, oy, oz, kappa, p2, tab, tr, ti, amp);
+        amp_hi = max(amp_hi, (uint32_t)__double2hiint(amp));
+        lo_r[e] = (uint32_t)__double2loint(tr);
+        hi_r[e] = (uint32_t)__double2hiint(tr) - 0x43380000u;
+        lo_i[e] = (uint32_t)__double2loint(ti);
+        hi_i[e] = (uint32_t)__double2hiint(ti) - 0x43380000u;
+      }
+      if (pend_slot >= 0) {
+        issue_stage(pend_slot, pend_ph, pend_s, pend_nst);
+        pend_slot = -1;
+      }
+      // ---- byte slices -> this CTA's K-half of the A images: [plane][slice] 2 KB blocks
+      uint8_t* a0 = smem + Z::SM_A + slot * OZ_ASTAGE + cr * OZP_HALF;
+      const int off = (erow >> 3) * 128 + (erow & 7) * 16 + kq;
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const uint32_t* lo = h ? lo_i : lo_r;
+        const uint32_t* hi = h ? hi_i : hi_r;
+        uint32_t l0[4], h0[4];
+        transpose4(lo[0], lo[1], lo[2], lo[3], l0);
+        transpose4(hi[0], hi[1], hi[2], hi[3], h0);
+        uint8_t* pl = a0 + h * (OZP_HALF / 2) + off;
+#pragma unroll
+        for (int p = 0; p < 4; ++p) *reinterpret_cast<uint32_t*>(pl + p * (OZP_HALF / 2 / OZ_NSL)) = l0[p];
+#pragma unroll
+        for (int p = 0; p < OZ_NSL - 4; ++p)
+          *reinterpret_cast<uint32_t*>(pl + (4 + p) * (OZP_HALF / 2 / OZ_NSL)) = h0[p];
+      }
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      if (s == 0 && d > 0) drain(d - 1);
+      asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+      __syncwarp();
+      unsigned last = 0;
+      if (lane == 0) {
+        __threadfence_block();
+        last = atomicAdd(&cnt[slot], 1u) == OZ_EWARPS - 1;
+        if (last) {
+          cnt[slot] = 0;
+          __threadfence_block();
+          // the whole half is written: send it to the peer's slot
+          const uint32_t src = sA + slot * OZ_ASTAGE + cr * OZP_HALF;
+          bulk_s2peer(mapa_peer(src, peer), src, OZP_HALF, mapa_peer(fullA(slot), peer));
+        }
+      }
+      if (__shfl_sync(0xffffffffu, last, 0)) {
+        pend_slot = slot;
+        pend_ph = ph;
+        pend_s = s;
+        pend_nst = nst;
+      }
+      __syncwarp();
+    }
+  }
+  if (pend_slot >= 0) issue_stage(pend_slot, pend_ph, pend_s, pend_nst);
+  __syncwarp();
+  if (nchunks > 0) drain(nchunks - 1);
+  if (KIND != KK_NUFFT && amp_hi >= (uint32_t)(1023 + OZ_ABITS) << 20) atomicOr(flag, 2);
+  if (go < m_out && nchunks == 0) {
+#pragma unroll
+    for (int c = 0; c < DC; ++c)
+      if (cb + c < it.ncols) Yb[yidx(c)] = 0.0;
+  }
+  // the peer's last multicast commits must have landed here before this CTA
+  // exits: wait for the final phase of each slot's empty barrier
+  if (g >= 1) mbar_wait(empty((g - 1) % OZ_NST), (uint32_t)((g - 1) / OZ_NST) & 1u);
+  if (g >= 2) mbar_wait(empty((g - 2) % OZ_NST), (uint32_t)((g - 2) / OZ_NST) & 1u);
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  cluster_sync_all();
+  if (warp == 0) {
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    if (cr == 0)
+      asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(COLS0));
+    else
+      asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(COLS1));
+  }
+}
+
 __global__ void oz_reduce_kernel(const double2* __restrict__ P, int64_t pstride, int nsplit, double2* Y, int64_t ldy,
                                  int64_t m, int64_t col0, int64_t ncols) {
   const int64_t total = m * ncols;
@@ -895,7 +1320,7 @@ __global__ void oz_reduce_kernel(const double2* __restrict__ P, int64_t pstride,
   }
 }
 
-template <int KIND, int MODE, int NCB>
+template <int KIND, int MODE, int NCB, bool PAIR>
 bool run_oz(Ctx* c, Points outp, Points inp, double kappa, int64_t m_out, const double2* X, double2* Y, int64_t ldy,
             const MatvecSeg* segs, int nseg) {
   using Z = OzT<NCB, oz_kd(KIND), KIND == KK_PLATES>;
@@ -971,15 +1396,18 @@ bool run_oz(Ctx* c, Points outp, Points inp, double kappa, int64_t m_out, const 
       tab_ready.fetch_or(bit);
     }
   }
-  auto kern = matvec_oz_kernel<KIND, MODE, NCB>;
+  static_assert(!PAIR || NCB == OZP_NCB, "pair tile width");
+  auto kern = PAIR ? matvec_oz_pair_kernel<KIND, MODE> : matvec_oz_kernel<KIND, MODE, NCB>;
   BFLY_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Z::SM_TOTAL));
-  dim3 grid((unsigned)gx, (unsigned)items.size(), (unsigned)nsplit);
+  dim3 grid((unsigned)(gx * (PAIR ? 2 : 1)), (unsigned)items.size(), (unsigned)nsplit);
+  // partial output slices: split-K ranges, and the two diagonal halves of a pair
+  const int nparts = nsplit * (PAIR ? 2 : 1);
   DBuf<double2> part;
   int64_t pstride = 0;
   double2* Yt = Y;
-  if (nsplit > 1) {
+  if (nparts > 1) {
     pstride = ldy * max_col;
-    part.reset(c, (size_t)(pstride * nsplit));
+    part.reset(c, (size_t)(pstride * nparts));
     Yt = part.p;
   }
   // tensor work actually executed (int8 ops = 2 per MAC): per stage of 128
@@ -990,9 +1418,14 @@ bool run_oz(Ctx* c, Points outp, Points inp, double kappa, int64_t m_out, const 
       const int64_t k0 = (int64_t)z * rows_per_split, k1 = std::min(it.rows, k0 + rows_per_split);
       if (k1 > k0) stages += (double)ceil_div(k1 - k0, (int64_t)OZ_KS);
     }
-  constexpr OzSched sch = make_sched(Z::MAXB);
   double nsum = 0;
-  for (int i = 0; i < sch.n; ++i) nsum += (double)(((sch.code[i] >> 8) & 31) * Z::BN2);
+  if (PAIR) {
+    for (const OzSched& sch : {OzPairSched<0>::value, OzPairSched<1>::value})
+      for (int i = 0; i < sch.n; ++i) nsum += (double)(((sch.code[i] >> 8) & 31) * Z::BN2);
+  } else {
+    constexpr OzSched sch = make_sched(Z::MAXB);
+    for (int i = 0; i < sch.n; ++i) nsum += (double)(((sch.code[i] >> 8) & 31) * Z::BN2);
+  }
   const double int8_ops = 2.0 * stages * (double)gx * nsum * OZ_BM * OZ_KS;
 #ifdef OZ_TRACE
   {
@@ -1005,17 +1438,34 @@ bool run_oz(Ctx* c, Points outp, Points inp, double kappa, int64_t m_out, const 
     KTimer timer(c, "kernel_matvec", kflops, kbytes);
     KTimer timer8(c, "kernel_matvec.int8_ops", int8_ops, 0.0);
     BFLY_HOST_TRACE("K2 launch");
-    kern<<<grid, OZ_THREADS, Z::SM_TOTAL, c->stream>>>(outp, inp, kappa, m_out, img.p, T.p, Yt, ldy, ditems.p,
-                                                    rows_per_split, pstride, flag);
+    if (PAIR) {
+      cudaLaunchConfig_t cfg{};
+      cfg.gridDim = grid;
+      cfg.blockDim = dim3(OZ_THREADS);
+      cfg.dynamicSmemBytes = Z::SM_TOTAL;
+      cfg.stream = c->stream;
+      cudaLaunchAttribute attr[1];
+      attr[0].id = cudaLaunchAttributeClusterDimension;
+      attr[0].val.clusterDim.x = 2;
+      attr[0].val.clusterDim.y = 1;
+      attr[0].val.clusterDim.z = 1;
+      cfg.attrs = attr;
+      cfg.numAttrs = 1;
+      BFLY_CUDA(cudaLaunchKernelEx(&cfg, kern, outp, inp, kappa, m_out, (const uint8_t*)img.p, (const int32_t*)T.p, Yt,
+                                   ldy, (const OzItem*)ditems.p, rows_per_split, pstride, flag));
+    } else {
+      kern<<<grid, OZ_THREADS, Z::SM_TOTAL, c->stream>>>(outp, inp, kappa, m_out, img.p, T.p, Yt, ldy, ditems.p,
+                                                      rows_per_split, pstride, flag);
+    }
     BFLY_LAUNCH_CHECK("kernel_matvec_oz");
   }
-  if (nsplit > 1) {
+  if (nparts > 1) {
     for (int s = 0; s < nseg; ++s) {
       const MatvecSeg& g = segs[s];
       if (g.ncols <= 0 || g.rows <= 0) continue;
       const int64_t total = m_out * g.ncols;
       const unsigned blocks = (unsigned)std::min<int64_t>(ceil_div(total, (int64_t)256), (int64_t)c->sm_count * 16);
-      oz_reduce_kernel<<<blocks, 256, 0, c->stream>>>(part.p, pstride, nsplit, Y, ldy, m_out, g.col0, g.ncols);
+      oz_reduce_kernel<<<blocks, 256, 0, c->stream>>>(part.p, pstride, nparts, Y, ldy, m_out, g.col0, g.ncols);
       BFLY_LAUNCH_CHECK("oz_reduce");
     }
   }
@@ -1046,17 +1496,25 @@ bool run_oz(Ctx* c, Points outp, Points inp, double kappa, int64_t m_out, const 
   return hflag == 0;
 }
 
+bool oz_pair_enabled() {
+  const char* e = std::getenv("BFLY_OZ_PAIR");
+  return !(e && std::string(e) == "0");
+}
+
 template <int KIND, int MODE>
 bool run_oz_width(Ctx* c, Points outp, Points inp, double kappa, int64_t m_out, const double2* X, double2* Y,
                   int64_t ldy, const MatvecSeg* segs, int nseg) {
-  // tile width = the widest column tile of the launch (tiles of <= 32 columns):
-  // narrow probe blocks (leaf rounds) do proportionally less tensor work
+  // tile width = the widest column tile of the launch: narrow probe blocks
+  // (leaf rounds) do proportionally less tensor work; 33..40 columns run on
+  // CTA pairs (one evaluation for all of them), wider blocks in 32-column tiles
   int w = 0;
   for (int s = 0; s < nseg; ++s) w = std::max(w, std::min(segs[s].ncols, OZ_MAXCB));
-  if (w <= 8) return run_oz<KIND, MODE, 8>(c, outp, inp, kappa, m_out, X, Y, ldy, segs, nseg);
-  if (w <= 16) return run_oz<KIND, MODE, 16>(c, outp, inp, kappa, m_out, X, Y, ldy, segs, nseg);
-  if (w <= 24) return run_oz<KIND, MODE, 24>(c, outp, inp, kappa, m_out, X, Y, ldy, segs, nseg);
-  return run_oz<KIND, MODE, 32>(c, outp, inp, kappa, m_out, X, Y, ldy, segs, nseg);
+  if (w <= 8) return run_oz<KIND, MODE, 8, false>(c, outp, inp, kappa, m_out, X, Y, ldy, segs, nseg);
+  if (w <= 16) return run_oz<KIND, MODE, 16, false>(c, outp, inp, kappa, m_out, X, Y, ldy, segs, nseg);
+  if (w <= 24) return run_oz<KIND, MODE, 24, false>(c, outp, inp, kappa, m_out, X, Y, ldy, segs, nseg);
+  if (w > OZ_MAXCB1 && w <= OZP_NCB && oz_pair_enabled())
+    return run_oz<KIND, MODE, OZP_NCB, true>(c, outp, inp, kappa, m_out, X, Y, ldy, segs, nseg);
+  return run_oz<KIND, MODE, 32, false>(c, outp, inp, kappa, m_out, X, Y, ldy, segs, nseg);
 }
 
 template <int KIND>
@@ -1068,6 +1526,8 @@ bool dispatch_oz_mode(Ctx* c, int mode, Points outp, Points inp, double kappa, i
 }
 
 }  // namespace
+
+int kernel_matvec_pass_cols() { return matvec_oz_enabled() && oz_pair_enabled() ? OZP_NCB : OZ_MAXCB1; }
 
 bool matvec_oz_enabled() {
   const char* e = std::getenv("BFLY_MATVEC");

@@ -46,6 +46,8 @@ void launch_kernel_matvec(Ctx* c, int kind, int mode, Points out_pts, Points in_
 // range (the caller then recomputes on the FP64 DMMA path).  BFLY_MATVEC=fp64
 // selects the FP64 path.
 bool matvec_oz_enabled();
+// widest probe block one kernel-evaluation pass covers (40 on CTA pairs, else 32)
+int kernel_matvec_pass_cols();
 bool launch_kernel_matvec_oz(Ctx* c, int kind, int mode, Points out_pts, Points in_pts, double kappa, int64_t m_out,
                              const double2* X, double2* Y, int64_t ldy, const MatvecSeg* segs_host, int nseg);
 

@@ -77,6 +77,34 @@ def test_black_box_products_match_oracle(B, oracle_threads):
         assert rel_err(w.op.apply_adjoint(xs), op_o.apply_adjoint(xs)) < 1e-12
 
 
+@pytest.mark.parametrize("ncols", [33, 34, 40])
+def test_pair_products_match_oracle(B, oracle_threads, ncols):
+    """K2 on CTA pairs (probe tiles of 33..40 columns: one evaluation shared
+    through DSMEM, diagonal blocks split between the two CTAs) vs the oracle,
+    every kernel operator, N / T / H, dense and structured probes; and against
+    the single-CTA two-tile path of the same library."""
+    import os
+    for cfg_id, n in ((0, 1024), (1, 1024), (2, 2048), (3, 512)):
+        op_o, rt, ct, _ = oracle_config(cfg_id, n)
+        w = B.configs.build(cfg_id, n)
+        x = O.gaussian_matrix(n, ncols, 17)
+        for name, fo, fg in (("N", op_o.apply, w.op.apply), ("T", op_o.apply_transpose, w.op.apply_transpose),
+                             ("H", op_o.apply_adjoint, w.op.apply_adjoint)):
+            yg = fg(x)
+            e = rel_err(yg, fo(x))
+            assert e < 1e-12, (cfg_id, name, ncols, e)
+            os.environ["BFLY_OZ_PAIR"] = "0"
+            try:
+                e2 = rel_err(yg, fg(x))
+            finally:
+                del os.environ["BFLY_OZ_PAIR"]
+            assert e2 < 1e-13, (cfg_id, name, ncols, e2)
+        xs = np.zeros_like(x)
+        b, e_ = rt.node_range(2, 1)
+        xs[b:e_] = x[b:e_]
+        assert rel_err(w.op.apply_adjoint(xs), op_o.apply_adjoint(xs)) < 1e-12
+
+
 def test_gaussian_stream_matches_oracle(B):
     for seed in (0, 1, 123456789):
         for rows, cols in ((1, 1), (7, 3), (1000, 5)):

@@ -21,12 +21,13 @@ def main():
     ap.add_argument("--cfg", type=int, default=2)
     ap.add_argument("--cols", type=int, default=32)
     ap.add_argument("--reps", type=int, default=5)
+    ap.add_argument("--modes", default="NH", help="N and/or H")
     a = ap.parse_args()
     w = B.configs.build(a.cfg)
     n = w.op.cols
     g = torch.Generator(device="cuda").manual_seed(0)
     x = torch.randn(a.cols, n, dtype=torch.complex128, device="cuda", generator=g).t()  # column-major
-    for name in ("N", "H"):
+    for name in a.modes:
         f = w.op.apply if name == "N" else w.op.apply_adjoint
         f(x)
         torch.cuda.synchronize()
