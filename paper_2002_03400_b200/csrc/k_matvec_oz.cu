@@ -83,9 +83,17 @@ constexpr int OZ_KS = 32;                         // input entries per stage (MM
 constexpr int oz_kd(int kind) { return kind == KK_PLATES ? 1024 : 2048; }
 constexpr int OZ_NST = 2;                         // ring depth
 constexpr int OZ_BM = 128;                        // output rows per CTA (= TMEM lanes)
-constexpr int OZ_EWARPS = 16;
+constexpr int OZ_EWARPS = 16;                     // CTA-pair kernel: evaluation warps
 constexpr int OZ_THREADS = OZ_EWARPS * 32;        // evaluation threads
 constexpr int OZ_EPT = OZ_BM * OZ_KS / OZ_THREADS;  // 8 entries per thread per stage
+// single-CTA kernel: OZS_WARPS evaluation warps, OZS_EPT entries per thread per stage
+#ifndef OZ_EW
+#define OZ_EW 16
+#endif
+constexpr int OZS_WARPS = OZ_EW;
+constexpr int OZS_THREADS = OZS_WARPS * 32;
+constexpr int OZS_EPT = OZ_BM * OZ_KS / OZS_THREADS;  // 8 or 16
+static_assert(OZS_EPT == 8 || OZS_EPT == 16, "single-kernel thread mapping");
 constexpr int OZ_ASLICE = OZ_BM * OZ_KS;           // 4096 B: one A slice (128 rows x 32 B)
 constexpr int OZ_APLANE = OZ_NSL * OZ_ASLICE;      // 28672 B
 constexpr int OZ_ASTAGE = 2 * OZ_APLANE;           // re + im planes
@@ -485,7 +493,7 @@ __global__ void oz_table_kernel() {
 // execute in issue order, so acc_full (committed by the last stage's
 // issuer) covers the whole chunk.
 template <int KIND, int MODE, int NCB>
-__global__ void __launch_bounds__(OZ_THREADS, 1)
+__global__ void __launch_bounds__(OZS_THREADS, 1)
     matvec_oz_kernel(Points outp, Points inp, double kappa, int64_t m_out, const uint8_t* __restrict__ bimg,
                      const int32_t* __restrict__ Tg, double2* __restrict__ Y, int64_t ldy,
                      const OzItem* __restrict__ items, int64_t rows_per_split, int64_t pstride, int* __restrict__ flag) {
@@ -528,25 +536,26 @@ __global__ void __launch_bounds__(OZ_THREADS, 1)
   }
   if (tid < NCB) Ts[tid] = Tg[blockIdx.y * OZ_MAXCB + tid];
   double2* tab = reinterpret_cast<double2*>(smem + Z::SM_TAB);
-  for (int j = tid; j < keval::kTabN; j += OZ_THREADS) tab[j] = g_oz_tab[j];  // L2-resident copy
+  for (int j = tid; j < keval::kTabN; j += OZS_THREADS) tab[j] = g_oz_tab[j];  // L2-resident copy
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   __syncthreads();
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
   const uint32_t tmem = *tmem_slot;
   const uint32_t sA = smem_u32(smem + Z::SM_A), sB = smem_u32(smem + Z::SM_B);
 
-  // evaluation: row (warp & 7) * 16 + lane / 2, entries kofs .. kofs + 7 of each stage
+  // evaluation: row (warp & 7) * 16 + lane / 2, entries kofs .. kofs + EPT - 1 of each stage
   const int erow = (warp & 7) * 16 + (lane >> 1);
-  const int kofs = (warp >> 3) * 16 + (lane & 1) * 8;
+  const int kofs = OZS_EPT == 8 ? (warp >> 3) * 16 + (lane & 1) * 8 : (lane & 1) * 16;
   const int64_t gi = min(i0 + erow, m_out - 1);  // padded rows evaluate a valid row (never stored)
   const double ox = outp.x[gi];
   const double oy = KIND == KK_NUFFT ? 0.0 : outp.y[gi];
   const double oz = KIND == KK_PLATES ? outp.z[gi] : 0.0;
-  // drain: TMEM lane quarter = warp & 3, column quarter = warp >> 2
-  // (0, 1: Re y columns 0-15 / 16-31; 2, 3: Im y columns 0-15 / 16-31)
+  // drain: TMEM lane quarter = warp & 3, column part dq = warp >> 2 of DC columns
+  // (16 warps: Re y 0-15 / 16-31, Im y 0-15 / 16-31; 8 warps: Re y, Im y)
   const int drow = (warp & 3) * 32 + lane;
   const int dq = warp >> 2;
-  constexpr int DC = Z::DC;
+  constexpr int DC = OZS_WARPS == 16 ? Z::DC : NCB;
+  constexpr int DPC = NCB / DC;  // column parts per component
   // the thread's output entries: row drow, columns (dq & 1) * DC + c of Re
   // (dq < 2) or Im y.  OZ_GACC (default): each chunk's drained sums are added
   // straight into them (a read-modify-write once per 64 stages; every entry
@@ -554,8 +563,8 @@ __global__ void __launch_bounds__(OZ_THREADS, 1)
   // stage loop; otherwise they accumulate in registers and are stored once.
   const int64_t go = i0 + drow;
   double* const Yb = reinterpret_cast<double*>(Y + it.ybase + (int64_t)blockIdx.z * pstride);
-  const int cb = (dq & 1) * DC;
-  auto yidx = [&](int c) { return 2 * (go + (it.ycol + cb + c) * ldy) + (dq >> 1); };
+  const int cb = (dq % DPC) * DC;
+  auto yidx = [&](int c) { return 2 * (go + (it.ycol + cb + c) * ldy) + dq / DPC; };
 #if OZ_GACC
   double* yacc = nullptr;
 #else
@@ -580,8 +589,14 @@ __global__ void __launch_bounds__(OZ_THREADS, 1)
     for (int j = OZ_NDIAG - 1; j >= 0; --j) {
       const uint32_t base = tmem + ((uint32_t)((warp & 3) * 32) << 16) + j * Z::BN2 + dq * DC;
       uint32_t v[DC];
-      if constexpr (DC == 16) {
-        tmem_ld16(base, v);
+      if constexpr (DC % 16 == 0) {
+#pragma unroll
+        for (int q = 0; q < DC / 16; ++q) {
+          uint32_t w[16];
+          tmem_ld16(base + 16 * q, w);
+#pragma unroll
+          for (int u = 0; u < 16; ++u) v[16 * q + u] = w[u];
+        }
       } else {
 #pragma unroll
         for (int q = 0; q < DC / 4; ++q) {
@@ -598,7 +613,7 @@ __global__ void __launch_bounds__(OZ_THREADS, 1)
     }
     if (OZ_ZERO_ACC) asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
     const int S = Srow[(d & 1) * OZ_BM + drow];
-    const int c0 = (dq & 1) * DC;
+    const int c0 = cb;
 #if OZ_GACC
     if (go < m_out) {
 #pragma unroll
@@ -671,7 +686,7 @@ __global__ void __launch_bounds__(OZ_THREADS, 1)
     const double bx = inp.x[p0];
     const double by = KIND == KK_NUFFT ? 0.0 : inp.y[p0];
     const double bz = KIND == KK_PLATES ? inp.z[p0] : 0.0;
-    for (int k = tid; k < nst * OZ_KS; k += OZ_THREADS) {
+    for (int k = tid; k < nst * OZ_KS; k += OZS_THREADS) {
       // entries past the chunk repeat its first point: finite values whose B rows are zero
       const int64_t pk = p0 + (k < npts ? k : 0);
       const double x = inp.x[pk];
@@ -687,8 +702,8 @@ __global__ void __launch_bounds__(OZ_THREADS, 1)
       // in float coordinates local to the chunk's first point
       float4* BX = reinterpret_cast<float4*>(smem + Z::SM_BOX);  // [NBOX][lo, hi]
 #pragma unroll
-      for (int q = 0; q < Z::NBOX / OZ_EWARPS; ++q) {
-        const int sb = warp * (Z::NBOX / OZ_EWARPS) + q;
+      for (int q = 0; q < Z::NBOX / OZS_WARPS; ++q) {
+        const int sb = warp * (Z::NBOX / OZS_WARPS) + q;
         const int k = min(sb * 32 + lane, Z::KD - 1);
         const double2 pd = PD[k];
         const float px = (float)(pd.x - bx), py = (float)(pd.y - by);
@@ -718,7 +733,7 @@ __global__ void __launch_bounds__(OZ_THREADS, 1)
       const float lz = KIND == KK_PLATES ? (float)(outp.z[gr] - bz) : 0.f;
       const int nbox = (nst * OZ_KS) / 32;
       float mn = 3.0e38f;
-      for (int b = part; b < nbox; b += OZ_THREADS / OZ_BM) {
+      for (int b = part; b < nbox; b += OZS_THREADS / OZ_BM) {
         const float4 lo = BX[2 * b], hi = BX[2 * b + 1];
         const float dx = fmaxf(fmaxf(lo.x - lx, lx - hi.x), 0.f);
         const float dy = fmaxf(fmaxf(lo.y - ly, ly - hi.y), 0.f);
@@ -780,11 +795,11 @@ __global__ void __launch_bounds__(OZ_THREADS, 1)
       }
       // ---- evaluate 8 entries, scale, round (magic-number: low word = low
       // 32 bits of the integer, high word - 0x43380000 = high 32 bits)
-      uint32_t lo_r[8], hi_r[8], lo_i[8], hi_i[8];
+      uint32_t lo_r[OZS_EPT], hi_r[OZS_EPT], lo_i[OZS_EPT], hi_i[OZS_EPT];
       const int kl = s * OZ_KS + kofs;  // chunk-relative
       OZT_BEGIN(t0)
 #pragma unroll
-      for (int e = 0; e < 8; ++e) {
+      for (int e = 0; e < OZS_EPT; ++e) {
         const double2 sp = PD[kl + e];
         const double sz = KIND == KK_PLATES ? PZ[kl + e] : 0.0;
         double tr, ti, amp;
@@ -823,18 +838,22 @@ __global__ void __launch_bounds__(OZ_THREADS, 1)
       const int off = ((kofs >> 4) * (OZ_BM / 8) + (erow >> 3)) * 128 + (erow & 7) * 16 + (kofs & 15);
 #pragma unroll
       for (int h = 0; h < ((OZ_EXP & 8) ? 0 : 2); ++h) {  // experiment bit 3: no A writes
-        const uint32_t* lo = h ? lo_i : lo_r;
-        const uint32_t* hi = h ? hi_i : hi_r;
-        uint32_t l0[4], l1[4], h0[4], h1[4];
-        transpose4(lo[0], lo[1], lo[2], lo[3], l0);
-        transpose4(lo[4], lo[5], lo[6], lo[7], l1);
-        transpose4(hi[0], hi[1], hi[2], hi[3], h0);
-        transpose4(hi[4], hi[5], hi[6], hi[7], h1);
-        uint8_t* pl = a0 + h * OZ_APLANE + off;
 #pragma unroll
-        for (int p = 0; p < 4; ++p) *reinterpret_cast<uint2*>(pl + p * OZ_ASLICE) = make_uint2(l0[p], l1[p]);
+        for (int gq = 0; gq < OZS_EPT / 8; ++gq) {  // groups of 8 entries = 8 bytes per slice
+          const uint32_t* lo = (h ? lo_i : lo_r) + 8 * gq;
+          const uint32_t* hi = (h ? hi_i : hi_r) + 8 * gq;
+          uint32_t l0[4], l1[4], h0[4], h1[4];
+          transpose4(lo[0], lo[1], lo[2], lo[3], l0);
+          transpose4(lo[4], lo[5], lo[6], lo[7], l1);
+          transpose4(hi[0], hi[1], hi[2], hi[3], h0);
+          transpose4(hi[4], hi[5], hi[6], hi[7], h1);
+          uint8_t* pl = a0 + h * OZ_APLANE + off + 8 * gq;
 #pragma unroll
-        for (int p = 0; p < OZ_NSL - 4; ++p) *reinterpret_cast<uint2*>(pl + (4 + p) * OZ_ASLICE) = make_uint2(h0[p], h1[p]);
+          for (int p = 0; p < 4; ++p) *reinterpret_cast<uint2*>(pl + p * OZ_ASLICE) = make_uint2(l0[p], l1[p]);
+#pragma unroll
+          for (int p = 0; p < OZ_NSL - 4; ++p)
+            *reinterpret_cast<uint2*>(pl + (4 + p) * OZ_ASLICE) = make_uint2(h0[p], h1[p]);
+        }
       }
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
       if (lane == 0) { OZT_END(t1, 1) }
@@ -844,7 +863,7 @@ __global__ void __launch_bounds__(OZ_THREADS, 1)
       unsigned last = 0;
       if (lane == 0) {
         __threadfence_block();
-        last = atomicAdd(&cnt[slot], 1u) == OZ_EWARPS - 1;  // last warp in: issues the stage (deferred)
+        last = atomicAdd(&cnt[slot], 1u) == OZS_WARPS - 1;  // last warp in: issues the stage (deferred)
         if (last) {
           cnt[slot] = 0;
           __threadfence_block();
@@ -1454,7 +1473,7 @@ bool run_oz(Ctx* c, Points outp, Points inp, double kappa, int64_t m_out, const 
       BFLY_CUDA(cudaLaunchKernelEx(&cfg, kern, outp, inp, kappa, m_out, (const uint8_t*)img.p, (const int32_t*)T.p, Yt,
                                    ldy, (const OzItem*)ditems.p, rows_per_split, pstride, flag));
     } else {
-      kern<<<grid, OZ_THREADS, Z::SM_TOTAL, c->stream>>>(outp, inp, kappa, m_out, img.p, T.p, Yt, ldy, ditems.p,
+      kern<<<grid, OZS_THREADS, Z::SM_TOTAL, c->stream>>>(outp, inp, kappa, m_out, img.p, T.p, Yt, ldy, ditems.p,
                                                       rows_per_split, pstride, flag);
     }
     BFLY_LAUNCH_CHECK("kernel_matvec_oz");
