@@ -90,6 +90,9 @@ constexpr int OZ_EPT = OZ_BM * OZ_KS / OZ_THREADS;  // 8 entries per thread per 
 #ifndef OZ_EW
 #define OZ_EW 16
 #endif
+#ifndef OZ_LB_PAD
+#define OZ_LB_PAD 0  // experiment: launch-bounds padding (register cap) of the single-CTA kernel
+#endif
 constexpr int OZS_WARPS = OZ_EW;
 constexpr int OZS_THREADS = OZS_WARPS * 32;
 constexpr int OZS_EPT = OZ_BM * OZ_KS / OZS_THREADS;  // 8 or 16
@@ -493,7 +496,7 @@ __global__ void oz_table_kernel() {
 // execute in issue order, so acc_full (committed by the last stage's
 // issuer) covers the whole chunk.
 template <int KIND, int MODE, int NCB>
-__global__ void __launch_bounds__(OZS_THREADS, 1)
+__global__ void __launch_bounds__(OZS_THREADS + OZ_LB_PAD, 1)
     matvec_oz_kernel(Points outp, Points inp, double kappa, int64_t m_out, const uint8_t* __restrict__ bimg,
                      const int32_t* __restrict__ Tg, double2* __restrict__ Y, int64_t ldy,
                      const OzItem* __restrict__ items, int64_t rows_per_split, int64_t pstride, int* __restrict__ flag) {
