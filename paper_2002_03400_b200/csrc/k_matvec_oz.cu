@@ -919,7 +919,8 @@ __global__ void __launch_bounds__(OZS_THREADS + OZ_LB_PAD, 1)
 // The ring slot's `empty` barrier counts BOTH CTAs' MMA commits (multicast):
 // a CTA overwrites its half -- in its own slot and, by the copy, in the
 // peer's -- only when both have finished reading the stage two back.
-constexpr int OZP_NCB = 40;
+constexpr int OZP_NCB = 40;   // pair tile: 33..40 columns
+constexpr int OZP_NCB48 = 48; // 41..48 columns, 3D plates only (its 1024-entry chunks leave the smem room)
 constexpr int OZP_HALF = OZ_ASTAGE / 2;  // 24 KB: one CTA's K-half of a stage
 static_assert(OZ_E0 == 4 && OZ_NDIAG == 7, "pair diagonal split assumes e = 4 .. 10");
 __host__ __device__ constexpr int ozp_nloc(int cr) { return cr == 0 ? 4 : 3; }
@@ -951,9 +952,9 @@ constexpr OzSched make_sched_pair(int cr, int maxb) {
     }
   return sc;
 }
-template <int CR>
+template <int CR, int NCB>
 struct OzPairSched {
-  static constexpr OzSched value = make_sched_pair(CR, OzT<OZP_NCB, 1024, false>::MAXB);
+  static constexpr OzSched value = make_sched_pair(CR, OzT<NCB, 1024, false>::MAXB);
 };
 __device__ __forceinline__ uint32_t cluster_ctarank() {
   uint32_t r;
@@ -983,13 +984,12 @@ __device__ __forceinline__ void bulk_s2peer(uint32_t dst_cluster, uint32_t src, 
                : "memory");
 }
 
-template <int KIND, int MODE>
+template <int KIND, int MODE, int NCB>
 __global__ void __launch_bounds__(OZ_THREADS, 1)
     matvec_oz_pair_kernel(Points outp, Points inp, double kappa, int64_t m_out, const uint8_t* __restrict__ bimg,
                           const int32_t* __restrict__ Tg, double2* __restrict__ Y, int64_t ldy,
                           const OzItem* __restrict__ items, int64_t rows_per_split, int64_t pstride,
                           int* __restrict__ flag) {
-  constexpr int NCB = OZP_NCB;
   using Z = OzT<NCB, oz_kd(KIND), KIND == KK_PLATES>;
   extern __shared__ __align__(1024) uint8_t smem[];
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -1053,7 +1053,7 @@ __global__ void __launch_bounds__(OZ_THREADS, 1)
   // drain: TMEM lane quarter = warp & 3, column quarter = warp >> 2 of [Re y | Im y]
   const int drow = (warp & 3) * 32 + lane;
   const int dq = warp >> 2;
-  constexpr int DC = Z::DC;  // 20
+  constexpr int DC = Z::DC;  // 20 or 24
   const int nloc = ozp_nloc((int)cr);
   const int64_t go = i0 + drow;
   // this CTA's partial output slice (the split-K reduce adds the pair's two)
@@ -1128,9 +1128,9 @@ __global__ void __launch_bounds__(OZ_THREADS, 1)
       }
     };
     if (cr == 0)
-      run(OzPairSched<0>{});
+      run(OzPairSched<0, NCB>{});
     else
-      run(OzPairSched<1>{});
+      run(OzPairSched<1, NCB>{});
     if (elect_one()) {
       mma_commit_pair(empty(slot));
       if (s == nst - 1) mma_commit(acc_full);
@@ -1418,8 +1418,8 @@ bool run_oz(Ctx* c, Points outp, Points inp, double kappa, int64_t m_out, const 
       tab_ready.fetch_or(bit);
     }
   }
-  static_assert(!PAIR || NCB == OZP_NCB, "pair tile width");
-  auto kern = PAIR ? matvec_oz_pair_kernel<KIND, MODE> : matvec_oz_kernel<KIND, MODE, NCB>;
+  static_assert(!PAIR || NCB == OZP_NCB || NCB == OZP_NCB48, "pair tile width");
+  auto kern = PAIR ? matvec_oz_pair_kernel<KIND, MODE, NCB> : matvec_oz_kernel<KIND, MODE, NCB>;
   BFLY_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Z::SM_TOTAL));
   dim3 grid((unsigned)(gx * (PAIR ? 2 : 1)), (unsigned)items.size(), (unsigned)nsplit);
   // partial output slices: split-K ranges, and the two diagonal halves of a pair
@@ -1442,7 +1442,7 @@ bool run_oz(Ctx* c, Points outp, Points inp, double kappa, int64_t m_out, const 
     }
   double nsum = 0;
   if (PAIR) {
-    for (const OzSched& sch : {OzPairSched<0>::value, OzPairSched<1>::value})
+    for (const OzSched& sch : {OzPairSched<0, NCB>::value, OzPairSched<1, NCB>::value})
       for (int i = 0; i < sch.n; ++i) nsum += (double)(((sch.code[i] >> 8) & 31) * Z::BN2);
   } else {
     constexpr OzSched sch = make_sched(Z::MAXB);
@@ -1536,6 +1536,9 @@ bool run_oz_width(Ctx* c, Points outp, Points inp, double kappa, int64_t m_out, 
   if (w <= 24) return run_oz<KIND, MODE, 24, false>(c, outp, inp, kappa, m_out, X, Y, ldy, segs, nseg);
   if (w > OZ_MAXCB1 && w <= OZP_NCB && oz_pair_enabled())
     return run_oz<KIND, MODE, OZP_NCB, true>(c, outp, inp, kappa, m_out, X, Y, ldy, segs, nseg);
+  if constexpr (KIND == KK_PLATES)
+    if (w > OZP_NCB && w <= OZP_NCB48 && oz_pair_enabled())
+      return run_oz<KIND, MODE, OZP_NCB48, true>(c, outp, inp, kappa, m_out, X, Y, ldy, segs, nseg);
   return run_oz<KIND, MODE, 32, false>(c, outp, inp, kappa, m_out, X, Y, ldy, segs, nseg);
 }
 

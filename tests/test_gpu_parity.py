@@ -77,14 +77,15 @@ def test_black_box_products_match_oracle(B, oracle_threads):
         assert rel_err(w.op.apply_adjoint(xs), op_o.apply_adjoint(xs)) < 1e-12
 
 
-@pytest.mark.parametrize("ncols", [33, 34, 40])
+@pytest.mark.parametrize("ncols", [33, 34, 40, 45, 48])
 def test_pair_products_match_oracle(B, oracle_threads, ncols):
-    """K2 on CTA pairs (probe tiles of 33..40 columns: one evaluation shared
-    through DSMEM, diagonal blocks split between the two CTAs) vs the oracle,
-    every kernel operator, N / T / H, dense and structured probes; and against
-    the single-CTA two-tile path of the same library."""
+    """K2 on CTA pairs (probe tiles of 33..40 columns, and 41..48 for the 3D
+    plates: one evaluation shared through DSMEM, diagonal blocks split between
+    the two CTAs) vs the oracle, every kernel operator, N / T / H, dense and
+    structured probes; and against the single-CTA tile path of the library."""
     import os
-    for cfg_id, n in ((0, 1024), (1, 1024), (2, 2048), (3, 512)):
+    cases = ((0, 1024), (1, 1024), (2, 2048), (3, 512)) if ncols <= 40 else ((1, 1024), (1, 2304))
+    for cfg_id, n in cases:
         op_o, rt, ct, _ = oracle_config(cfg_id, n)
         w = B.configs.build(cfg_id, n)
         x = O.gaussian_matrix(n, ncols, 17)
