@@ -90,6 +90,9 @@ constexpr int OZ_EPT = OZ_BM * OZ_KS / OZ_THREADS;  // 8 entries per thread per 
 #ifndef OZ_EW
 #define OZ_EW 16
 #endif
+#ifndef OZ_DEFER
+#define OZ_DEFER 1  // the last warp to write a stage issues its MMAs after its share of the next one
+#endif
 #ifndef OZ_LB_PAD
 #define OZ_LB_PAD 0  // experiment: launch-bounds padding (register cap) of the single-CTA kernel
 #endif
@@ -877,6 +880,10 @@ __global__ void __launch_bounds__(OZS_THREADS + OZ_LB_PAD, 1)
         pend_ph = ph;
         pend_s = s;
         pend_nst = nst;
+        if (!OZ_DEFER) {  // experiment: issue at once (lockstep)
+          issue_stage(pend_slot, pend_ph, pend_s, pend_nst);
+          pend_slot = -1;
+        }
       }
       __syncwarp();
     }
