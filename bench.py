@@ -425,6 +425,7 @@ def run_ours(args):
                           for i, p in enumerate(logs[0].phases)},
             "flops_per_step": fl_total / args.steps, "kernel_evals_per_step": logs[0].kernel_evals,
             "max_rank": bf.max_rank(), "nnz": bf.nnz(),
+            "k2_fp64_recomputes": sum(int(lg.products_recomputed) for lg in logs),
             "roofline": roofline,
             "apply": apply,
             "apply_cfg4": apply4,

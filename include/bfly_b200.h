@@ -221,6 +221,9 @@ typedef struct bfly_log {
   double total_seconds;
   double flops;         /* algorithmic flops of the construction */
   double kernel_evals;  /* black-box kernel-entry evaluations */
+  /* 1 when a kernel entry fell outside the int8-slice range and the whole
+   * factorization was recomputed on the FP64 path (same results, ~2x time) */
+  int32_t products_recomputed;
 } bfly_log;
 
 /* factorize() (reconstruct.hpp:412-419) */

@@ -71,7 +71,7 @@ class Phase(C.Structure):
 class Log(C.Structure):
     _fields_ = [("nphases", C.c_int32), ("phases", Phase * 64), ("peak_probe_bytes", C.c_uint64),
                 ("peak_concurrent_probes", C.c_int64), ("rank_capped", C.c_int32), ("total_seconds", C.c_double),
-                ("flops", C.c_double), ("kernel_evals", C.c_double)]
+                ("flops", C.c_double), ("kernel_evals", C.c_double), ("products_recomputed", C.c_int32)]
 
 
 APPLY_FN = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_int, C.c_void_p, C.c_int64, C.c_void_p, C.c_int64, C.c_int64,

@@ -505,6 +505,7 @@ class FactorizationLog:
     total_seconds: float
     flops: float
     kernel_evals: float
+    products_recomputed: bool = False  # the K2 range check sent the factorization to the FP64 path
 
     @staticmethod
     def _from(lg: Log) -> "FactorizationLog":
@@ -512,7 +513,7 @@ class FactorizationLog:
                         p.rank_margin)
               for p in lg.phases[: lg.nphases]]
         return FactorizationLog(ph, lg.peak_probe_bytes, lg.peak_concurrent_probes, bool(lg.rank_capped),
-                                lg.total_seconds, lg.flops, lg.kernel_evals)
+                                lg.total_seconds, lg.flops, lg.kernel_evals, bool(lg.products_recomputed))
 
     def forward_columns(self) -> int:
         return sum(p.forward_columns for p in self.phases)

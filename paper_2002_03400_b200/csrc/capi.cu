@@ -621,6 +621,7 @@ int bfly_factorize(bfly_ctx* ctx, bfly_op* op, const bfly_tree* rt, const bfly_t
       h->c.reset();
       c->force_fp64 = true;
       run_once();
+      if (log) log->products_recomputed = 1;
     }
     *out = h.release();
   });

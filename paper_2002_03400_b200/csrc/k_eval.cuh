@@ -143,7 +143,7 @@ __device__ __forceinline__ double sqrt_rcp(double x, double& h) {
   double y;
   asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
   double s = x * y;
-  h = 0.5 * y;
+  h = __hiloint2double(__double2hiint(y) - (1 << 20), __double2loint(y));  // 0.5 y: exponent - 1 (integer pipe)
   double e = fma(-s, h, 0.5);
   s = fma(s, e, s);
   h = fma(h, e, h);

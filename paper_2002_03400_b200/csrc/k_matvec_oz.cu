@@ -340,21 +340,23 @@ __device__ __forceinline__ void transpose4(uint32_t w0, uint32_t w1, uint32_t w2
   o[3] = __byte_perm(t2, t3, 0x7632);
 }
 
-// kernel entry scaled by p2 = 2^S and rounded to an integer in one FMA each
-// (magic-number rounding: result = value + 1.5 * 2^52); amp = scaled |entry|
-// bound for the range check.  im is negated for the adjoint.
+// kernel entry scaled by the row scale and rounded to an integer in one FMA
+// each (magic-number rounding: result = value + 1.5 * 2^52); amp = scaled
+// |entry| bound for the range check.  im is negated for the adjoint.
+// NUFFT: the scale is p2 = 2^S.  Helmholtz kernels: the amplitude 1/r = 2h
+// (1/(4 pi r) for the plates, whose table entries carry the 1/(4 pi)) times
+// 2^S is h with S + 1 added to its exponent -- an integer add on the high
+// word (es = (S + 1) << 20) instead of an FP64 multiply.
 template <int KIND, bool CONJ>
 __device__ __forceinline__ void entry_rounded(double tx, double ty, double tz, double sx, double sy, double sz,
-                                              double kappa, double p2, const double2* __restrict__ tab, double& re,
-                                              double& im, double& amp) {
+                                              double kappa, double p2, int es, const double2* __restrict__ tab,
+                                              double& re, double& im, double& amp) {
   double sn, cs, sc;
   if (KIND == KK_NUFFT) {
     const double ph = __dmul_rn(tx, sx);
     keval::tab_sincos_turn(__dsub_rn(ph, rint(ph)), tab, sn, cs);
     sc = p2;
   } else {
-    // p2 here is the row scale pre-multiplied by the amplitude constant:
-    // 2 * 2^S (circle: 1/r = 2h) or 2 * 2^S / (4 pi) (plates)
     const double dx = __dsub_rn(tx, sx), dy = __dsub_rn(ty, sy);
     double d2;
     if (KIND == KK_PLATES) {
@@ -365,16 +367,22 @@ __device__ __forceinline__ void entry_rounded(double tx, double ty, double tz, d
     }
     double h;
     const double r = keval::sqrt_rcp(d2, h);
-#ifdef OZ_POLY_SINCOS
-    keval::fast_sincos(__dmul_rn(kappa, r), sn, cs);  // experiment: no shared-memory table
-#else
     keval::tab_sincos(__dmul_rn(kappa, r), tab, sn, cs);
-#endif
-    sc = h * p2;
+    sc = __hiloint2double(__double2hiint(h) + es, __double2loint(h));
   }
   amp = sc;
   re = fma(cs, sc, keval::kMagic);
   im = fma(sn, CONJ ? -sc : sc, keval::kMagic);
+}
+
+// |v| < 2^ABITS <=> high word of the scaled amplitude below this (NaN / inf
+// fail too).  The plates' amplitude sc = 2h 2^S omits the 1/(4 pi) that their
+// table entries carry, so their limit is the high word of 4 pi 2^ABITS
+// (truncated: a conservative bound)
+template <int KIND>
+__device__ __forceinline__ uint32_t amp_limit_hi() {
+  return KIND == KK_PLATES ? (uint32_t)__double2hiint(keval::kFourPi * (double)(1ll << OZ_ABITS))
+                           : (uint32_t)(1023 + OZ_ABITS) << 20;
 }
 
 // ------------------------------------------------------- probe slicing
@@ -542,7 +550,10 @@ __global__ void __launch_bounds__(OZS_THREADS + OZ_LB_PAD, 1)
   }
   if (tid < NCB) Ts[tid] = Tg[blockIdx.y * OZ_MAXCB + tid];
   double2* tab = reinterpret_cast<double2*>(smem + Z::SM_TAB);
-  for (int j = tid; j < keval::kTabN; j += OZS_THREADS) tab[j] = g_oz_tab[j];  // L2-resident copy
+  for (int j = tid; j < keval::kTabN; j += OZS_THREADS) {  // L2-resident copy (plates: times 1/(4 pi))
+    const double2 t = g_oz_tab[j];
+    tab[j] = KIND == KK_PLATES ? make_double2(t.x * (1.0 / keval::kFourPi), t.y * (1.0 / keval::kFourPi)) : t;
+  }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   __syncthreads();
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
@@ -777,9 +788,8 @@ __global__ void __launch_bounds__(OZS_THREADS + OZ_LB_PAD, 1)
     __syncthreads();
     if (lane == 0) { OZT_END(t6, 6) }
     // row scale 2^S, folded with the amplitude constant (see entry_rounded)
-    const double p2 = KIND == KK_NUFFT    ? pow2(Srow[(d & 1) * OZ_BM + erow])
-                      : KIND == KK_PLATES ? pow2(Srow[(d & 1) * OZ_BM + erow] + 1) / keval::kFourPi
-                                          : pow2(Srow[(d & 1) * OZ_BM + erow] + 1);
+    const double p2 = pow2(Srow[(d & 1) * OZ_BM + erow]);  // NUFFT row scale
+    const int es = (Srow[(d & 1) * OZ_BM + erow] + 1) << 20;  // Helmholtz: 2h 2^S, as an exponent add
     for (int s = 0; s < nst; ++s, ++g) {
       const int slot = g % OZ_NST;
       const uint32_t ph = (uint32_t)(g / OZ_NST) & 1u;
@@ -814,9 +824,9 @@ __global__ void __launch_bounds__(OZS_THREADS + OZ_LB_PAD, 1)
           ti = keval::kMagic - (double)(kl + e);
           amp = 0.0;
         } else if (MODE == OP_N)
-          entry_rounded<KIND, false>(ox, oy, oz, sp.x, sp.y, sz, kappa, p2, tab, tr, ti, amp);
+          entry_rounded<KIND, false>(ox, oy, oz, sp.x, sp.y, sz, kappa, p2, es, tab, tr, ti, amp);
         else
-          entry_rounded<KIND, MODE == OP_H>(sp.x, sp.y, sz, ox, oy, oz, kappa, p2, tab, tr, ti, amp);
+          entry_rounded<KIND, MODE == OP_H>(sp.x, sp.y, sz, ox, oy, oz, kappa, p2, es, tab, tr, ti, amp);
         amp_hi = max(amp_hi, (uint32_t)__double2hiint(amp));
         lo_r[e] = (uint32_t)__double2loint(tr);
         hi_r[e] = (uint32_t)__double2hiint(tr) - 0x43380000u;
@@ -891,8 +901,7 @@ __global__ void __launch_bounds__(OZS_THREADS + OZ_LB_PAD, 1)
   if (pend_slot >= 0) issue_stage(pend_slot, pend_ph, pend_s, pend_nst);
   __syncwarp();
   if (nchunks > 0) drain(nchunks - 1);
-  // |v| < 2^ABITS <=> high word of the scaled amplitude < (1023 + ABITS) << 20 (NaN / inf fail)
-  if (KIND != KK_NUFFT && amp_hi >= (uint32_t)(1023 + OZ_ABITS) << 20) atomicOr(flag, 2);
+  if (KIND != KK_NUFFT && amp_hi >= amp_limit_hi<KIND>()) atomicOr(flag, 2);
 
   // ---- store (OZ_GACC: only an empty input range has not written its zeros)
   if (go < m_out && (!OZ_GACC || nchunks == 0)) {
@@ -1043,7 +1052,10 @@ __global__ void __launch_bounds__(OZ_THREADS, 1)
   }
   if (tid < NCB) Ts[tid] = Tg[blockIdx.y * OZ_MAXCB + tid];
   double2* tab = reinterpret_cast<double2*>(smem + Z::SM_TAB);
-  for (int j = tid; j < keval::kTabN; j += OZ_THREADS) tab[j] = g_oz_tab[j];
+  for (int j = tid; j < keval::kTabN; j += OZ_THREADS) {  // plates: times 1/(4 pi)
+    const double2 t = g_oz_tab[j];
+    tab[j] = KIND == KK_PLATES ? make_double2(t.x * (1.0 / keval::kFourPi), t.y * (1.0 / keval::kFourPi)) : t;
+  }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   cluster_sync_all();  // barriers of both CTAs initialised before any remote arrive
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
@@ -1231,9 +1243,8 @@ __global__ void __launch_bounds__(OZ_THREADS, 1)
       Srow[(d & 1) * OZ_BM + tid] = S;
     }
     __syncthreads();
-    const double p2 = KIND == KK_NUFFT    ? pow2(Srow[(d & 1) * OZ_BM + erow])
-                      : KIND == KK_PLATES ? pow2(Srow[(d & 1) * OZ_BM + erow] + 1) / keval::kFourPi
-                                          : pow2(Srow[(d & 1) * OZ_BM + erow] + 1);
+    const double p2 = pow2(Srow[(d & 1) * OZ_BM + erow]);  // NUFFT row scale
+    const int es = (Srow[(d & 1) * OZ_BM + erow] + 1) << 20;  // Helmholtz: 2h 2^S, as an exponent add
     for (int s = 0; s < nst; ++s, ++g) {
       const int slot = g % OZ_NST;
       const uint32_t ph = (uint32_t)(g / OZ_NST) & 1u;
@@ -1254,9 +1265,9 @@ __global__ void __launch_bounds__(OZ_THREADS, 1)
         const double sz = KIND == KK_PLATES ? PZ[kl + e] : 0.0;
         double tr, ti, amp;
         if (MODE == OP_N)
-          entry_rounded<KIND, false>(ox, oy, oz, sp.x, sp.y, sz, kappa, p2, tab, tr, ti, amp);
+          entry_rounded<KIND, false>(ox, oy, oz, sp.x, sp.y, sz, kappa, p2, es, tab, tr, ti, amp);
         else
-          entry_rounded<KIND, MODE == OP_H>(sp.x, sp.y, sz, ox, oy, oz, kappa, p2, tab, tr, ti, amp);
+          entry_rounded<KIND, MODE == OP_H>(sp.x, sp.y, sz, ox, oy, oz, kappa, p2, es, tab, tr, ti, amp);
         amp_hi = max(amp_hi, (uint32_t)__double2hiint(amp));
         lo_r[e] = (uint32_t)__double2loint(tr);
         hi_r[e] = (uint32_t)__double2hiint(tr) - 0x43380000u;
@@ -1312,7 +1323,7 @@ __global__ void __launch_bounds__(OZ_THREADS, 1)
   if (pend_slot >= 0) issue_stage(pend_slot, pend_ph, pend_s, pend_nst);
   __syncwarp();
   if (nchunks > 0) drain(nchunks - 1);
-  if (KIND != KK_NUFFT && amp_hi >= (uint32_t)(1023 + OZ_ABITS) << 20) atomicOr(flag, 2);
+  if (KIND != KK_NUFFT && amp_hi >= amp_limit_hi<KIND>()) atomicOr(flag, 2);
   if (go < m_out && nchunks == 0) {
 #pragma unroll
     for (int c = 0; c < DC; ++c)

@@ -65,6 +65,8 @@ def test_full_size_matches_reference(B, cfg_id):
     n = int(d["n"])
     w = B.configs.build(cfg_id, n)
     bf, log = B.factorize(w.op, w.row_tree, w.col_tree, w.recon)
+    # the int8-slice products stayed in range (no silent FP64 recompute)
+    assert not log.products_recomputed
     margins = {p.name: p.rank_margin for p in log.phases}
     print(f"cfg {cfg_id} n={n}: GPU {log.total_seconds:.3f} s vs {d['producer']} {float(d['total_seconds']):.1f} s "
           f"({int(d['threads'])} threads); min CPQR cut margin {min(margins.values()):.3e}")
