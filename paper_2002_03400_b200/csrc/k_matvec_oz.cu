@@ -1254,7 +1254,10 @@ __global__ void __launch_bounds__(OZ_THREADS, 1)
       if (tid == 0) {
         mbar_expect_tx(fullB(slot), Z::BSTAGE);
         bulk_g2s(sB + slot * Z::BSTAGE, bimg + (it.bstage0 + k0 / OZ_KS) * (int64_t)Z::BSTAGE, Z::BSTAGE, fullB(slot));
-        mbar_expect_tx(fullA(slot), OZP_HALF);  // the peer's half of this stage
+        if (OZ_EXP & 16)  // experiment: no DSMEM exchange (wrong results)
+          asm volatile("mbarrier.arrive.release.cta.shared::cta.b64 _, [%0];" ::"r"(fullA(slot)) : "memory");
+        else
+          mbar_expect_tx(fullA(slot), OZP_HALF);  // the peer's half of this stage
       }
       // ---- evaluate this CTA's 4 entries of its K-half
       uint32_t lo_r[4], hi_r[4], lo_i[4], hi_i[4];
@@ -1308,7 +1311,7 @@ __global__ void __launch_bounds__(OZ_THREADS, 1)
           __threadfence_block();
           // the whole half is written: send it to the peer's slot
           const uint32_t src = sA + slot * OZ_ASTAGE + cr * OZP_HALF;
-          bulk_s2peer(mapa_peer(src, peer), src, OZP_HALF, mapa_peer(fullA(slot), peer));
+          if (!(OZ_EXP & 16)) bulk_s2peer(mapa_peer(src, peer), src, OZP_HALF, mapa_peer(fullA(slot), peer));
         }
       }
       if (__shfl_sync(0xffffffffu, last, 0)) {
