@@ -1114,6 +1114,8 @@ void launch_bgemm(Ctx* c, int op, int M, int K, int S, const cx<R>* A, int64_t l
       }
       if (f32_env >= 0 && f32_env < 5) best = f32_env;
       const int BMv = 16 * tshape[best][0], BNv = 16 * tshape[best][1];
+      BFLY_HOST_TRACE("bgemm_f32 M %d K %d S %d ncols %lld nent %d tile %dx%d op %d", M, K, S, (long long)max_ncols, nent,
+                      BMv, BNv, op);
       dim3 grid(nent, (unsigned)ceil_div(max_ncols, BNv), (unsigned)ceil_div(M, BMv));
       if (grid.y > 65535 || grid.z > 65535) fail(PRECONDITION, "bgemm: grid too large");
       const double nc = ncols_all > 0 ? ncols_all : max_ncols;

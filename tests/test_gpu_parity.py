@@ -106,6 +106,21 @@ def test_pair_products_match_oracle(B, oracle_threads, ncols):
         assert rel_err(w.op.apply_adjoint(xs), op_o.apply_adjoint(xs)) < 1e-12
 
 
+@pytest.mark.parametrize("cfg_id, n", [(0, 1000), (2, 1500), (1, 1369)])
+def test_pair_products_ragged_and_complex64(B, oracle_threads, cfg_id, n):
+    """CTA-pair K2 at sizes that are not multiples of the 128-row tile (the
+    last row block is partial; split-K ranges are ragged), and the complex64
+    operators on the same path (1e-5 vs the complex128 oracle)."""
+    op_o, rt, ct, _ = oracle_config(cfg_id, n)
+    x = O.gaussian_matrix(n, 34, 23)
+    w = B.configs.build(cfg_id, n)
+    for fo, fg in ((op_o.apply, w.op.apply), (op_o.apply_adjoint, w.op.apply_adjoint)):
+        assert rel_err(fg(x), fo(x)) < 1e-12
+    w64 = B.configs.build(cfg_id, n, scalar=B.COMPLEX64)
+    y64 = w64.op.apply(x.astype(np.complex64)).astype(np.complex128)
+    assert rel_err(y64, op_o.apply(x)) < 1e-5
+
+
 def test_gaussian_stream_matches_oracle(B):
     for seed in (0, 1, 123456789):
         for rows, cols in ((1, 1), (7, 3), (1000, 5)):
