@@ -935,6 +935,13 @@ __global__ void __launch_bounds__(OZS_THREADS + OZ_LB_PAD, 1)
 // The ring slot's `empty` barrier counts BOTH CTAs' MMA commits (multicast):
 // a CTA overwrites its half -- in its own slot and, by the copy, in the
 // peer's -- only when both have finished reading the stage two back.
+#ifndef OZP_EW
+#define OZP_EW 16
+#endif
+constexpr int OZP_WARPS = OZP_EW;                       // evaluation warps per CTA of a pair
+constexpr int OZP_THREADS = OZP_WARPS * 32;
+constexpr int OZP_EPT = OZ_BM * (OZ_KS / 2) / OZP_THREADS;  // entries per thread per stage: 4 or 8
+static_assert(OZP_EPT == 4 || OZP_EPT == 8, "pair thread mapping");
 constexpr int OZP_NCB = 40;   // pair tile: 33..40 columns
 constexpr int OZP_NCB48 = 48; // 41..48 columns, 3D plates only (its 1024-entry chunks leave the smem room)
 constexpr int OZP_HALF = OZ_ASTAGE / 2;  // 24 KB: one CTA's K-half of a stage
@@ -1001,7 +1008,7 @@ __device__ __forceinline__ void bulk_s2peer(uint32_t dst_cluster, uint32_t src, 
 }
 
 template <int KIND, int MODE, int NCB>
-__global__ void __launch_bounds__(OZ_THREADS, 1)
+__global__ void __launch_bounds__(OZP_THREADS, 1)
     matvec_oz_pair_kernel(Points outp, Points inp, double kappa, int64_t m_out, const uint8_t* __restrict__ bimg,
                           const int32_t* __restrict__ Tg, double2* __restrict__ Y, int64_t ldy,
                           const OzItem* __restrict__ items, int64_t rows_per_split, int64_t pstride,
@@ -1052,7 +1059,7 @@ __global__ void __launch_bounds__(OZ_THREADS, 1)
   }
   if (tid < NCB) Ts[tid] = Tg[blockIdx.y * OZ_MAXCB + tid];
   double2* tab = reinterpret_cast<double2*>(smem + Z::SM_TAB);
-  for (int j = tid; j < keval::kTabN; j += OZ_THREADS) {  // plates: times 1/(4 pi)
+  for (int j = tid; j < keval::kTabN; j += OZP_THREADS) {  // plates: times 1/(4 pi)
     const double2 t = g_oz_tab[j];
     tab[j] = KIND == KK_PLATES ? make_double2(t.x * (1.0 / keval::kFourPi), t.y * (1.0 / keval::kFourPi)) : t;
   }
@@ -1062,9 +1069,10 @@ __global__ void __launch_bounds__(OZ_THREADS, 1)
   const uint32_t tmem = *tmem_slot;
   const uint32_t sA = smem_u32(smem + Z::SM_A), sB = smem_u32(smem + Z::SM_B);
 
-  // evaluation: row warp * 8 + lane / 4, entries 4 (lane & 3) .. + 3 of this CTA's K-half
-  const int erow = warp * 8 + (lane >> 2);
-  const int kq = (lane & 3) * 4;
+  // evaluation: 16 warps: row warp * 8 + lane / 4, entries 4 (lane & 3) .. + 3
+  // of this CTA's K-half; 8 warps: row warp * 16 + lane / 2, entries 8 (lane & 1) .. + 7
+  const int erow = OZP_EPT == 4 ? warp * 8 + (lane >> 2) : warp * 16 + (lane >> 1);
+  const int kq = OZP_EPT == 4 ? (lane & 3) * 4 : (lane & 1) * 8;
   const int64_t gi = min(i0 + erow, m_out - 1);
   const double ox = outp.x[gi];
   const double oy = KIND == KK_NUFFT ? 0.0 : outp.y[gi];
@@ -1072,13 +1080,14 @@ __global__ void __launch_bounds__(OZ_THREADS, 1)
   // drain: TMEM lane quarter = warp & 3, column quarter = warp >> 2 of [Re y | Im y]
   const int drow = (warp & 3) * 32 + lane;
   const int dq = warp >> 2;
-  constexpr int DC = Z::DC;  // 20 or 24
+  constexpr int DC = OZP_WARPS == 16 ? Z::DC : NCB;  // drained columns per thread
+  constexpr int DPC = NCB / DC;
   const int nloc = ozp_nloc((int)cr);
   const int64_t go = i0 + drow;
   // this CTA's partial output slice (the split-K reduce adds the pair's two)
   double* const Yb = reinterpret_cast<double*>(Y + it.ybase + ((int64_t)blockIdx.z * 2 + cr) * pstride);
-  const int cb = (dq & 1) * DC;
-  auto yidx = [&](int c) { return 2 * (go + (it.ycol + cb + c) * ldy) + (dq >> 1); };
+  const int cb = (dq % DPC) * DC;
+  auto yidx = [&](int c) { return 2 * (go + (it.ycol + cb + c) * ldy) + dq / DPC; };
   uint32_t amp_hi = 0;
   for (int jl = 0; jl < nloc; ++jl) tmem_zero<DC>(tmem + ((uint32_t)((warp & 3) * 32) << 16) + jl * Z::BN2 + dq * DC);
   asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
@@ -1113,7 +1122,7 @@ __global__ void __launch_bounds__(OZ_THREADS, 1)
     // t holds sum_j d_j 2^{8 (j - jmin)}; jmin = the lowest global block of this CTA
     const int jmin = jprev;
     const int S = Srow[(d & 1) * OZ_BM + drow];
-    const int c0 = (dq & 1) * DC;
+    const int c0 = cb;
     if (go < m_out) {
 #pragma unroll
       for (int c = 0; c < DC; ++c)
@@ -1170,7 +1179,7 @@ __global__ void __launch_bounds__(OZ_THREADS, 1)
     const double bx = inp.x[p0];
     const double by = KIND == KK_NUFFT ? 0.0 : inp.y[p0];
     const double bz = KIND == KK_PLATES ? inp.z[p0] : 0.0;
-    for (int k = tid; k < nst * OZ_KS; k += OZ_THREADS) {
+    for (int k = tid; k < nst * OZ_KS; k += OZP_THREADS) {
       const int64_t pk = p0 + (k < npts ? k : 0);
       PD[k] = make_double2(inp.x[pk], KIND == KK_NUFFT ? 0.0 : inp.y[pk]);
       if (KIND == KK_PLATES) PZ[k] = inp.z[pk];
@@ -1180,8 +1189,8 @@ __global__ void __launch_bounds__(OZ_THREADS, 1)
     if (KIND != KK_NUFFT) {
       float4* BX = reinterpret_cast<float4*>(smem + Z::SM_BOX);
 #pragma unroll
-      for (int q = 0; q < Z::NBOX / OZ_EWARPS; ++q) {
-        const int sb = warp * (Z::NBOX / OZ_EWARPS) + q;
+      for (int q = 0; q < Z::NBOX / OZP_WARPS; ++q) {
+        const int sb = warp * (Z::NBOX / OZP_WARPS) + q;
         const int k = min(sb * 32 + lane, Z::KD - 1);
         const double2 pd = PD[k];
         const float px = (float)(pd.x - bx), py = (float)(pd.y - by);
@@ -1208,7 +1217,7 @@ __global__ void __launch_bounds__(OZ_THREADS, 1)
       const float lz = KIND == KK_PLATES ? (float)(outp.z[gr] - bz) : 0.f;
       const int nbox = (nst * OZ_KS) / 32;
       float mn = 3.0e38f;
-      for (int b = part; b < nbox; b += OZ_THREADS / OZ_BM) {
+      for (int b = part; b < nbox; b += OZP_THREADS / OZ_BM) {
         const float4 lo = BX[2 * b], hi = BX[2 * b + 1];
         const float dx = fmaxf(fmaxf(lo.x - lx, lx - hi.x), 0.f);
         const float dy = fmaxf(fmaxf(lo.y - ly, ly - hi.y), 0.f);
@@ -1260,10 +1269,10 @@ __global__ void __launch_bounds__(OZ_THREADS, 1)
           mbar_expect_tx(fullA(slot), OZP_HALF);  // the peer's half of this stage
       }
       // ---- evaluate this CTA's 4 entries of its K-half
-      uint32_t lo_r[4], hi_r[4], lo_i[4], hi_i[4];
+      uint32_t lo_r[OZP_EPT], hi_r[OZP_EPT], lo_i[OZP_EPT], hi_i[OZP_EPT];
       const int kl = s * OZ_KS + (int)cr * 16 + kq;  // chunk-relative
 #pragma unroll
-      for (int e = 0; e < 4; ++e) {
+      for (int e = 0; e < OZP_EPT; ++e) {
         const double2 sp = PD[kl + e];
         const double sz = KIND == KK_PLATES ? PZ[kl + e] : 0.0;
         double tr, ti, amp;
@@ -1288,15 +1297,27 @@ __global__ void __launch_bounds__(OZ_THREADS, 1)
       for (int h = 0; h < 2; ++h) {
         const uint32_t* lo = h ? lo_i : lo_r;
         const uint32_t* hi = h ? hi_i : hi_r;
-        uint32_t l0[4], h0[4];
-        transpose4(lo[0], lo[1], lo[2], lo[3], l0);
-        transpose4(hi[0], hi[1], hi[2], hi[3], h0);
         uint8_t* pl = a0 + h * (OZP_HALF / 2) + off;
+        constexpr int SL = OZP_HALF / 2 / OZ_NSL;  // 2 KB: one slice of this plane's half
+        if constexpr (OZP_EPT == 4) {
+          uint32_t l0[4], h0[4];
+          transpose4(lo[0], lo[1], lo[2], lo[3], l0);
+          transpose4(hi[0], hi[1], hi[2], hi[3], h0);
 #pragma unroll
-        for (int p = 0; p < 4; ++p) *reinterpret_cast<uint32_t*>(pl + p * (OZP_HALF / 2 / OZ_NSL)) = l0[p];
+          for (int p = 0; p < 4; ++p) *reinterpret_cast<uint32_t*>(pl + p * SL) = l0[p];
 #pragma unroll
-        for (int p = 0; p < OZ_NSL - 4; ++p)
-          *reinterpret_cast<uint32_t*>(pl + (4 + p) * (OZP_HALF / 2 / OZ_NSL)) = h0[p];
+          for (int p = 0; p < OZ_NSL - 4; ++p) *reinterpret_cast<uint32_t*>(pl + (4 + p) * SL) = h0[p];
+        } else {
+          uint32_t l0[4], l1[4], h0[4], h1[4];
+          transpose4(lo[0], lo[1], lo[2], lo[3], l0);
+          transpose4(lo[4], lo[5], lo[6], lo[7], l1);
+          transpose4(hi[0], hi[1], hi[2], hi[3], h0);
+          transpose4(hi[4], hi[5], hi[6], hi[7], h1);
+#pragma unroll
+          for (int p = 0; p < 4; ++p) *reinterpret_cast<uint2*>(pl + p * SL) = make_uint2(l0[p], l1[p]);
+#pragma unroll
+          for (int p = 0; p < OZ_NSL - 4; ++p) *reinterpret_cast<uint2*>(pl + (4 + p) * SL) = make_uint2(h0[p], h1[p]);
+        }
       }
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
       if (s == 0 && d > 0) drain(d - 1);
@@ -1305,7 +1326,7 @@ __global__ void __launch_bounds__(OZ_THREADS, 1)
       unsigned last = 0;
       if (lane == 0) {
         __threadfence_block();
-        last = atomicAdd(&cnt[slot], 1u) == OZ_EWARPS - 1;
+        last = atomicAdd(&cnt[slot], 1u) == OZP_WARPS - 1;
         if (last) {
           cnt[slot] = 0;
           __threadfence_block();
@@ -1484,7 +1505,7 @@ bool run_oz(Ctx* c, Points outp, Points inp, double kappa, int64_t m_out, const 
     if (PAIR) {
       cudaLaunchConfig_t cfg{};
       cfg.gridDim = grid;
-      cfg.blockDim = dim3(OZ_THREADS);
+      cfg.blockDim = dim3(PAIR ? OZP_THREADS : OZS_THREADS);
       cfg.dynamicSmemBytes = Z::SM_TOTAL;
       cfg.stream = c->stream;
       cudaLaunchAttribute attr[1];
