@@ -261,17 +261,18 @@ __global__ void __launch_bounds__(QR_THREADS) cpqr_kernel(const cx<R>* __restric
   if (threadIdx.x == 0) ranks[e.rank_slot] = k;
 }
 
-// ------------------------------------------------- K5, one warp per block
-// The same factorization for blocks of at most 32 rows (config 2's leaves and
-// transfer blocks, r1 + r2 <= 32) with one warp per block and no CTA-wide
-// barriers: the Householder vector of column j is built with lane = row; the
-// trailing update, the norm downdates and the Q formation run with lane =
-// column (each lane sums over the rows of its own column, so no shuffle
-// reductions).  The block sits in shared memory with an odd column stride
-// (33 complex = 1 mod 8 16-byte groups: a quarter-warp's column accesses
-// hit 8 distinct bank groups).  (The 128-thread CTA version spent ~5
-// __syncthreads per pivot step: 260 us per config-2 launch.)
-constexpr int QRW_LD = 33;
+// ------------------------------------------- K5, one or two warps per block
+// The same factorization for blocks of at most 64 rows and 96 columns
+// (config 2's leaves and transfer blocks, config 4's 64 x 66 blocks, config
+// 1's transfer blocks) with NW = 1 or 2 warps per block and no wide barriers:
+// the Householder vector of column j is built with thread = row (warp 0; the
+// other warp waits at a 64-thread barrier); the trailing update, the norm
+// downdates and the Q formation run with thread = column (each thread sums
+// over the rows of its own column, so no shuffle reductions).  The block sits
+// in shared memory with an odd column stride (33 or 65 complex = 1 mod 8
+// 16-byte groups: a quarter-warp's column accesses hit 8 distinct bank
+// groups).  (The 128 / 256-thread CTA version spent ~5 __syncthreads per
+// pivot step: 260 us per config-2 launch, 3.7 ms per config-4 launch.)
 
 // sum_{i in [i0, i1)} conj(a_i) b_i with four independent partial sums (the
 // FP64 FMA latency chain of one running sum dominated the step)
@@ -289,24 +290,35 @@ __device__ __forceinline__ V dot_conj(const V* __restrict__ a, const V* __restri
   return cadd(cadd(s0, s1), cadd(s2, s3));
 }
 
-template <typename R>
-__global__ void __launch_bounds__(32) cpqr_warp_kernel(const cx<R>* __restrict__ src, int64_t ld_src,
-                                                       cx<R>* __restrict__ dst, int64_t ld_dst, int cap,
-                                                       const QrEnt* __restrict__ ents, int32_t* ranks, double eps_t,
-                                                       double* margins) {
+template <typename R, int NW>
+__global__ void __launch_bounds__(32 * NW) cpqr_warp_kernel(const cx<R>* __restrict__ src, int64_t ld_src,
+                                                            cx<R>* __restrict__ dst, int64_t ld_dst, int cap,
+                                                            const QrEnt* __restrict__ ents, int32_t* ranks,
+                                                            double eps_t, double* margins) {
   using V = cx<R>;
+  constexpr int NT = 32 * NW;
+  constexpr int LD = NW == 1 ? 33 : 65;  // column stride (complex), 1 mod 8
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const QrEnt e = ents[blockIdx.x];
   const int r = e.r1 + e.r2, w = e.cols;
-  const int lane = threadIdx.x;
-  V* Z = reinterpret_cast<V*>(smem_raw);  // QRW_LD x w
-  R* nu = reinterpret_cast<R*>(Z + (size_t)QRW_LD * w);
+  const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
+  V* Z = reinterpret_cast<V*>(smem_raw);  // LD x w
+  R* nu = reinterpret_cast<R*>(Z + (size_t)LD * w);
   R* nd = nu + w;
   V* tau = reinterpret_cast<V*>(nd + w);
+  __shared__ R s_red[2];
+  __shared__ int s_idx[2];
+  __shared__ V s_beta_tau[2];  // (beta, 0), tau of the current step
   V* out = dst + e.dst;
+  auto sync = [&]() {
+    if (NW == 1)
+      __syncwarp();
+    else
+      asm volatile("bar.sync 1, %0;" ::"n"(NT) : "memory");
+  };
   auto zero_out = [&]() {
-    for (int64_t i = lane; i < ld_dst * cap; i += 32) out[i] = mkc<R>(0, 0);
-    if (lane == 0) {
+    for (int64_t i = t; i < ld_dst * cap; i += NT) out[i] = mkc<R>(0, 0);
+    if (t == 0) {
       ranks[e.rank_slot] = 0;
       if (margins) margins[e.rank_slot] = HUGE_VAL;
     }
@@ -315,19 +327,19 @@ __global__ void __launch_bounds__(32) cpqr_warp_kernel(const cx<R>* __restrict__
     zero_out();
     return;
   }
-  // load the compact block (lane = row) and the column norms (lane = column)
+  // load the compact block (thread = row) and the column norms (thread = column)
   for (int c = 0; c < w; ++c) {
     const V* sc = src + e.src + (int64_t)c * ld_src;
-    if (lane < r) Z[lane + c * QRW_LD] = lane < e.r1 ? sc[lane] : sc[e.src_gap + (lane - e.r1)];
+    for (int i = t; i < r; i += NT) Z[i + c * LD] = i < e.r1 ? sc[i] : sc[e.src_gap + (i - e.r1)];
   }
-  __syncwarp();
-  R total = 0;
-  for (int c = lane; c < w; c += 32) {
+  sync();
+  for (int c = t; c < w; c += NT) {
     R s = 0;
-    for (int i = 0; i < r; ++i) s += cabs2(Z[i + c * QRW_LD]);
+    for (int i = 0; i < r; ++i) s += cabs2(Z[i + c * LD]);
     nu[c] = nd[c] = sqrt(s);
   }
-  __syncwarp();
+  sync();
+  R total = 0;
   for (int c = 0; c < w; ++c) total += nu[c] * nu[c];  // uniform
   if (total == R(0)) {  // all-zero input: rank 0 (linalg.hpp:67-71)
     zero_out();
@@ -340,7 +352,7 @@ __global__ void __launch_bounds__(32) cpqr_warp_kernel(const cx<R>* __restrict__
     // ---- pivot: first column with the largest updated norm
     R best = -1;
     int bi = w;
-    for (int c = j + lane; c < w; c += 32)
+    for (int c = j + t; c < w; c += NT)
       if (nu[c] > best) { best = nu[c]; bi = c; }
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) {
@@ -348,44 +360,60 @@ __global__ void __launch_bounds__(32) cpqr_warp_kernel(const cx<R>* __restrict__
       const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
       if (ob > best || (ob == best && oi < bi)) { best = ob; bi = oi; }
     }
+    if (NW > 1) {
+      if (lane == 0) {
+        s_red[warp] = best;
+        s_idx[warp] = bi;
+      }
+      sync();
+      best = s_red[0];
+      bi = s_idx[0];
+      if (s_red[1] > best || (s_red[1] == best && s_idx[1] < bi)) { best = s_red[1]; bi = s_idx[1]; }
+    }
     if (bi != j) {
-      if (lane < r) {
-        const V t = Z[lane + j * QRW_LD];
-        Z[lane + j * QRW_LD] = Z[lane + bi * QRW_LD];
-        Z[lane + bi * QRW_LD] = t;
+      for (int i = t; i < r; i += NT) {
+        const V tmp = Z[i + j * LD];
+        Z[i + j * LD] = Z[i + bi * LD];
+        Z[i + bi * LD] = tmp;
+      }
+      if (t == 0) {
+        R tmp = nu[j]; nu[j] = nu[bi]; nu[bi] = tmp;
+        tmp = nd[j]; nd[j] = nd[bi]; nd[bi] = tmp;
+      }
+    }
+    sync();
+    // ---- Householder reflector of column j (makeHouseholderInPlace), warp 0, lane = row
+    if (warp == 0) {
+      R tail = 0;
+      for (int i = j + 1 + lane; i < r; i += 32) tail += cabs2(Z[i + j * LD]);
+      tail = warp_sum(tail);
+      const V c0 = Z[j + j * LD];
+      V tv;
+      R beta;
+      if (tail <= QrTraits<R>::tiny && c0.y * c0.y <= QrTraits<R>::tiny) {
+        tv = mkc<R>(0, 0);
+        beta = c0.x;
+        for (int i = j + 1 + lane; i < r; i += 32) Z[i + j * LD] = mkc<R>(0, 0);
+      } else {
+        beta = sqrt(cabs2(c0) + tail);
+        if (c0.x >= R(0)) beta = -beta;
+        const V d = mkc<R>(c0.x - beta, c0.y);
+        const R dn = cabs2(d);
+        const V inv = mkc<R>(d.x / dn, -d.y / dn);
+        for (int i = j + 1 + lane; i < r; i += 32) Z[i + j * LD] = cmul(Z[i + j * LD], inv);
+        tv = mkc<R>((beta - c0.x) / beta, c0.y / beta);  // tau = conj((beta - c0) / beta)
       }
       __syncwarp();
       if (lane == 0) {
-        R t = nu[j]; nu[j] = nu[bi]; nu[bi] = t;
-        t = nd[j]; nd[j] = nd[bi]; nd[bi] = t;
+        Z[j + j * LD] = mkc<R>(beta, 0);
+        tau[j] = tv;
+        s_beta_tau[0] = mkc<R>(beta, 0);
+        s_beta_tau[1] = tv;
       }
     }
-    __syncwarp();
-    // ---- Householder reflector of column j (makeHouseholderInPlace), lane = row
-    const V zi = (lane > j && lane < r) ? Z[lane + j * QRW_LD] : mkc<R>(0, 0);
-    const R tail = warp_sum(cabs2(zi));
-    const V c0 = Z[j + j * QRW_LD];
-    V t;
-    R beta;
-    if (tail <= QrTraits<R>::tiny && c0.y * c0.y <= QrTraits<R>::tiny) {
-      t = mkc<R>(0, 0);
-      beta = c0.x;
-      if (lane > j && lane < r) Z[lane + j * QRW_LD] = mkc<R>(0, 0);
-    } else {
-      beta = sqrt(cabs2(c0) + tail);
-      if (c0.x >= R(0)) beta = -beta;
-      const V d = mkc<R>(c0.x - beta, c0.y);
-      const R dn = cabs2(d);
-      const V inv = mkc<R>(d.x / dn, -d.y / dn);
-      if (lane > j && lane < r) Z[lane + j * QRW_LD] = cmul(zi, inv);
-      t = mkc<R>((beta - c0.x) / beta, c0.y / beta);  // tau = conj((beta - c0) / beta)
-    }
-    __syncwarp();
-    if (lane == 0) {
-      Z[j + j * QRW_LD] = mkc<R>(beta, 0);
-      tau[j] = t;
-    }
-    const R absb = fabs(beta);
+    sync();
+    const R absb = fabs(s_beta_tau[0].x);
+    const V tj = s_beta_tau[1];
     if (j == 0) head = absb;
     if (!(absb > R(eps_t) * head)) {
       k = j;
@@ -393,13 +421,12 @@ __global__ void __launch_bounds__(32) cpqr_warp_kernel(const cx<R>* __restrict__
       break;
     }
     last_kept = absb;
-    __syncwarp();
-    // ---- apply H_j = I - tau v v^H to the trailing columns (lane = column); downdate norms
-    for (int c = j + 1 + lane; c < w; c += 32) {
-      V* zc = Z + c * QRW_LD;
-      const V* v = Z + j * QRW_LD;
+    // ---- apply H_j = I - tau v v^H to the trailing columns (thread = column); downdate norms
+    for (int c = j + 1 + t; c < w; c += NT) {
+      V* zc = Z + c * LD;
+      const V* v = Z + j * LD;
       const V dot = cadd(zc[j], dot_conj(v, zc, j + 1, r));
-      const V tt = cmul(t, dot);
+      const V tt = cmul(tj, dot);
       for (int i = j + 1; i < r; ++i) zc[i] = csub(zc[i], cmul(v[i], tt));
       const V top = csub(zc[j], tt);
       zc[j] = top;
@@ -412,52 +439,54 @@ __global__ void __launch_bounds__(32) cpqr_warp_kernel(const cx<R>* __restrict__
         const R ratio = nuc / ndc;
         const R temp2 = temp * ratio * ratio;
         if (temp2 <= QrTraits<R>::sqrt_eps) {
-          R s = 0;
-          for (int i = j + 1; i < r; ++i) s += cabs2(zc[i]);
-          nu[c] = nd[c] = sqrt(s);
+          R s2 = 0;
+          for (int i = j + 1; i < r; ++i) s2 += cabs2(zc[i]);
+          nu[c] = nd[c] = sqrt(s2);
         } else {
           nu[c] = nuc * sqrt(temp);
         }
       }
     }
-    __syncwarp();
+    sync();
   }
-  if (lane == 0 && margins) {
+  if (t == 0 && margins) {
     // rank margin at the cut (diagnostic): min(|R_{k-1}|/thr - 1, 1 - |R_k|/thr), thr = eps |R_00|
     const double thr = eps_t * (double)head;
     double m = (double)last_kept / thr - 1.0;
     if (first_dropped >= R(0)) m = fmin(m, 1.0 - (double)first_dropped / thr);
     margins[e.rank_slot] = m;
   }
-  __syncwarp();
+  sync();
   // ---- form Q(:, 0:k) in place: Q = H_0 ... H_{k-1} [I_k; 0], H_i = I - conj(tau_i) v v^H
   for (int i = k - 1; i >= 0; --i) {
     const V tq = cconj(tau[i]);
-    const V* v = Z + i * QRW_LD;
-    for (int c = i + 1 + lane; c < k; c += 32) {
-      V* zc = Z + c * QRW_LD;
+    const V* v = Z + i * LD;
+    for (int c = i + 1 + t; c < k; c += NT) {
+      V* zc = Z + c * LD;
       const V dot = cadd(zc[i], dot_conj(v, zc, i + 1, r));  // v_i = 1
       const V tt = cmul(tq, dot);
       for (int q = i + 1; q < r; ++q) zc[q] = csub(zc[q], cmul(v[q], tt));
       zc[i] = csub(zc[i], tt);
     }
-    __syncwarp();
-    if (lane > i && lane < r) Z[lane + i * QRW_LD] = cmul(mkc<R>(-tq.x, -tq.y), Z[lane + i * QRW_LD]);
-    if (lane == i) Z[i + i * QRW_LD] = mkc<R>(R(1) - tq.x, -tq.y);
-    if (lane < i) Z[lane + i * QRW_LD] = mkc<R>(0, 0);
-    __syncwarp();
+    sync();
+    for (int q = t; q < r; q += NT) {
+      if (q > i) Z[q + i * LD] = cmul(mkc<R>(-tq.x, -tq.y), Z[q + i * LD]);
+      else if (q == i) Z[i + i * LD] = mkc<R>(R(1) - tq.x, -tq.y);
+      else Z[q + i * LD] = mkc<R>(0, 0);
+    }
+    sync();
   }
   // ---- write the padded-stacked Q block
   for (int c = 0; c < cap; ++c)
-    for (int d = lane; d < ld_dst; d += 32) {
+    for (int d = t; d < ld_dst; d += NT) {
       V v = mkc<R>(0, 0);
       if (c < k) {
-        if (d < e.r1) v = Z[d + c * QRW_LD];
-        else if (d >= e.dst_gap && d < e.dst_gap + e.r2) v = Z[e.r1 + (d - e.dst_gap) + c * QRW_LD];
+        if (d < e.r1) v = Z[d + c * LD];
+        else if (d >= e.dst_gap && d < e.dst_gap + e.r2) v = Z[e.r1 + (d - e.dst_gap) + c * LD];
       }
       out[d + (int64_t)c * ld_dst] = v;
     }
-  if (lane == 0) ranks[e.rank_slot] = k;
+  if (t == 0) ranks[e.rank_slot] = k;
 }
 
 // --------------------------------------------------------------- core fit
@@ -613,11 +642,16 @@ template <typename R>
 void launch_cpqr(Ctx* c, const cx<R>* src, int64_t ld_src, cx<R>* dst, int64_t ld_dst, int cap, const QrEnt* ents,
                  int nent, int max_rows, int max_cols, int32_t* ranks, double eps, double* margins) {
   if (nent <= 0) return;
-  if (max_rows <= 32 && max_cols <= 64 && !std::getenv("BFLY_CPQR_CTA")) {
-    // one warp per block (shared memory: the block with stride QRW_LD, norms, tau)
-    const size_t smem = sizeof(cx<R>) * ((size_t)QRW_LD * max_cols + max_cols) + 2 * sizeof(R) * max_cols;
+  if (max_rows <= 64 && max_cols <= 96 && !std::getenv("BFLY_CPQR_CTA")) {
+    // one warp per block (<= 32 rows) or two (<= 64 rows); shared memory: the
+    // block with an odd column stride, norms, tau
+    const int nw = max_rows <= 32 ? 1 : 2;
+    const int ld = nw == 1 ? 33 : 65;
+    const size_t smem = sizeof(cx<R>) * ((size_t)ld * max_cols + max_cols) + 2 * sizeof(R) * max_cols;
     KTimer timer(c, "cpqr", 0.0, (double)sizeof(cx<R>) * nent * ((double)max_rows * max_cols + (double)ld_dst * cap));
-    cpqr_warp_kernel<R><<<nent, 32, smem, c->stream>>>(src, ld_src, dst, ld_dst, cap, ents, ranks, eps, margins);
+    auto kern = nw == 1 ? cpqr_warp_kernel<R, 1> : cpqr_warp_kernel<R, 2>;
+    if (smem > 48 * 1024) BFLY_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    kern<<<nent, 32 * nw, smem, c->stream>>>(src, ld_src, dst, ld_dst, cap, ents, ranks, eps, margins);
     BFLY_LAUNCH_CHECK("cpqr_warp");
     return;
   }
