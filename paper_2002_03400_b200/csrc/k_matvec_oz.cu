@@ -101,8 +101,14 @@ constexpr int OZS_THREADS = OZS_WARPS * 32;
 constexpr int OZS_EPT = OZ_BM * OZ_KS / OZS_THREADS;  // 8 or 16
 static_assert(OZS_EPT == 8 || OZS_EPT == 16, "single-kernel thread mapping");
 constexpr int OZ_ASLICE = OZ_BM * OZ_KS;           // 4096 B: one A slice (128 rows x 32 B)
-constexpr int OZ_APLANE = OZ_NSL * OZ_ASLICE;      // 28672 B
+constexpr int OZ_APLANE = OZ_NSL * OZ_ASLICE;      // 24576 B
 constexpr int OZ_ASTAGE = 2 * OZ_APLANE;           // re + im planes
+// A stage layout (both kernels, and the evaluation cache): [K-half][plane][slice]
+// blocks of 128 rows x 16 B (2 KB; core matrices of 8 rows x 16 B, 128 B
+// apart), so the MMA descriptor's K step (LBO) is half a stage and a stage
+// is one contiguous 48 KB image
+constexpr int OZ_AHALF = OZ_ASTAGE / 2;            // 24 KB: one K-half of a stage
+constexpr int OZ_ABLK = OZ_AHALF / (2 * OZ_NSL);   // 2 KB: one (plane, slice) block of a K-half
 constexpr int OZ_MAXCB = 64;                       // stride of the per-tile column scales
 constexpr int OZ_MAXCB1 = 32;                      // widest probe tile of the single-CTA kernel
 static_assert(OZ_EPT == 8, "thread mapping assumes 8 entries per thread");
@@ -658,7 +664,7 @@ __global__ void __launch_bounds__(OZS_THREADS + OZ_LB_PAD, 1)
     mbar_wait(fullB(slot), ph);
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
     const uint32_t tm = warp_uniform(tmem);
-    const uint64_t da0 = smem_desc(warp_uniform(sA) + slot * OZ_ASTAGE, (OZ_BM / 8) * 128, 128);
+    const uint64_t da0 = smem_desc(warp_uniform(sA) + slot * OZ_ASTAGE, OZ_AHALF, 128);
     const uint64_t db0 = smem_desc(warp_uniform(sB) + slot * Z::BSTAGE, (Z::BROWS / 8) * 128, 128);
     const bool first = s == 0;
     constexpr OzSched kS = make_sched(Z::MAXB);
@@ -669,7 +675,7 @@ __global__ void __launch_bounds__(OZS_THREADS + OZ_LB_PAD, 1)
       const bool init = (e >> 13) & 1;
       const int q0 = jlo + OZ_E0 - p;
       // descriptor address fields hold addr >> 4 (14 bits; shared addresses < 2^18): offsets add in place
-      const uint64_t da = da0 + (uint64_t)((h * OZ_APLANE + p * OZ_ASLICE) >> 4);
+      const uint64_t da = da0 + (uint64_t)(((h * OZ_NSL + p) * OZ_ABLK) >> 4);
       const uint64_t db = db0 + (uint64_t)((h * Z::BOPER + q0 * Z::BN2 * 16) >> 4);
 #ifdef OZ_TRACE
       if (g_oz_mode & 1) continue;
@@ -851,7 +857,7 @@ __global__ void __launch_bounds__(OZS_THREADS + OZ_LB_PAD, 1)
       OZT_BEGIN(t1)
       // ---- byte slices -> canonical K-major A images (4x4 byte transposes)
       uint8_t* a0 = smem + Z::SM_A + slot * OZ_ASTAGE;
-      const int off = ((kofs >> 4) * (OZ_BM / 8) + (erow >> 3)) * 128 + (erow & 7) * 16 + (kofs & 15);
+      const int off = (kofs >> 4) * OZ_AHALF + (erow >> 3) * 128 + (erow & 7) * 16 + (kofs & 15);
 #pragma unroll
       for (int h = 0; h < ((OZ_EXP & 8) ? 0 : 2); ++h) {  // experiment bit 3: no A writes
 #pragma unroll
@@ -863,12 +869,12 @@ __global__ void __launch_bounds__(OZS_THREADS + OZ_LB_PAD, 1)
           transpose4(lo[4], lo[5], lo[6], lo[7], l1);
           transpose4(hi[0], hi[1], hi[2], hi[3], h0);
           transpose4(hi[4], hi[5], hi[6], hi[7], h1);
-          uint8_t* pl = a0 + h * OZ_APLANE + off + 8 * gq;
+          uint8_t* pl = a0 + h * OZ_NSL * OZ_ABLK + off + 8 * gq;
 #pragma unroll
-          for (int p = 0; p < 4; ++p) *reinterpret_cast<uint2*>(pl + p * OZ_ASLICE) = make_uint2(l0[p], l1[p]);
+          for (int p = 0; p < 4; ++p) *reinterpret_cast<uint2*>(pl + p * OZ_ABLK) = make_uint2(l0[p], l1[p]);
 #pragma unroll
           for (int p = 0; p < OZ_NSL - 4; ++p)
-            *reinterpret_cast<uint2*>(pl + (4 + p) * OZ_ASLICE) = make_uint2(h0[p], h1[p]);
+            *reinterpret_cast<uint2*>(pl + (4 + p) * OZ_ABLK) = make_uint2(h0[p], h1[p]);
         }
       }
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
@@ -944,7 +950,7 @@ constexpr int OZP_EPT = OZ_BM * (OZ_KS / 2) / OZP_THREADS;  // entries per threa
 static_assert(OZP_EPT == 4 || OZP_EPT == 8, "pair thread mapping");
 constexpr int OZP_NCB = 40;   // pair tile: 33..40 columns
 constexpr int OZP_NCB48 = 48; // 41..48 columns, 3D plates only (its 1024-entry chunks leave the smem room)
-constexpr int OZP_HALF = OZ_ASTAGE / 2;  // 24 KB: one CTA's K-half of a stage
+constexpr int OZP_HALF = OZ_AHALF;  // 24 KB: one CTA's K-half of a stage
 static_assert(OZ_E0 == 4 && OZ_NDIAG == 7, "pair diagonal split assumes e = 4 .. 10");
 __host__ __device__ constexpr int ozp_nloc(int cr) { return cr == 0 ? 4 : 3; }
 // global diagonal block of local block jl
