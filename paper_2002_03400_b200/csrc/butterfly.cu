@@ -727,6 +727,260 @@ void DevButterfly<R>::apply_h(const cx<R>* yt, int64_t ldy, cx<R>* xt, int64_t l
   run_plan(plan_h_, yt, ldy, xt, ldx, k, buf0, buf1);
 }
 
+// Structured apply (see butterfly.h).  The stages are the ones of
+// build_plan_n / build_plan_h; every entry carries the column window of the
+// probes whose support reaches its block.  pt = the input-side tree, q = a
+// node's level in it; a node at q >= plevel sees the one probe above it, a
+// node at q < plevel the probes below it.  While the two sources of an entry
+// sit at q > plevel they share a window (one S = 2 entry); from q == plevel
+// upwards their windows are disjoint column ranges of the same output block,
+// so the entry splits into two S = 1 entries and nothing reads a column it
+// did not produce (no zero-filled coefficient buffers).
+template <typename R>
+bool DevButterfly<R>::apply_structured(int trans, int plevel, const std::vector<ProbeSeg>& segs, const cx<R>* X,
+                                       int64_t ldx, cx<R>* y, int64_t ldy, double* flops_done) {
+  Ctx* c = ctx;
+  if ((trans != OP_N && trans != OP_H) || !rt.identity || !ct.identity) return false;
+  if (plevel < 0 || plevel > L || segs.empty()) return false;
+  const bool fwd = trans == OP_N;
+  const Tree& pt = fwd ? ct : rt;
+  const Tree& ot = fwd ? rt : ct;
+  const int p = plevel;
+  const int64_t NP = int64_t(1) << p, NB = nb();
+  // cs[j]: first column of probe node j (absent probes have zero width)
+  std::vector<int64_t> cs(NP + 1, -1), xo(NP, -1);
+  {
+    int64_t col = segs[0].col0, prev = -1;
+    for (const auto& s : segs) {
+      if (s.node <= prev || s.node >= NP || s.col0 != col || s.ncols < 0) return false;
+      for (int64_t j = prev + 1; j <= s.node; ++j) cs[j] = col;
+      xo[s.node] = s.x_off;
+      col += s.ncols;
+      prev = s.node;
+    }
+    for (int64_t j = prev + 1; j <= NP; ++j) cs[j] = col;
+  }
+  const int64_t wend = cs[NP];
+  if (wend - cs[0] <= 0) return true;
+  auto win = [&](int q, int64_t t, int64_t& c0, int64_t& nc) {
+    int64_t j0, j1;
+    if (q >= p) {
+      j0 = t >> (q - p);
+      j1 = j0 + 1;
+    } else {
+      j0 = t << (p - q);
+      j1 = (t + 1) << (p - q);
+    }
+    c0 = cs[j0];
+    nc = cs[j1] - cs[j0];
+  };
+  struct Stage {
+    int op, M, K, S;
+    const cx<R>* A;
+    int64_t lda, ld_out;
+    std::vector<GemmEnt> h;
+    int maxc = 0;
+  };
+  std::vector<Stage> st;
+  double flops = 0;
+  auto add = [&](int op, int M, int K, int S, const Level<R>& lv, int64_t ld_out) -> Stage& {
+    st.push_back(Stage{op, M, K, S, lv.data.p, lv.ld, ld_out, {}, 0});
+    return st.back();
+  };
+  // a0/a1/b0/b1/c: element offsets without the window; the window's first
+  // column is added to the coefficient operands (ld_in) and the output (ld_out)
+  auto push = [&](Stage& d, int64_t a0, int64_t a1, int64_t b0, int64_t b1, int64_t cc, int mrows, int krows,
+                  int64_t c0, int64_t nc, int64_t ld_in, int64_t ld_o, double nz) {
+    if (nc <= 0) return;
+    GemmEnt e = ent(a0, a1, b0 + c0 * ld_in, b1 + c0 * ld_in, cc + c0 * ld_o, mrows, krows);
+    e.ncols = (int32_t)nc;
+    d.h.push_back(e);
+    d.maxc = std::max<int>(d.maxc, (int)nc);
+    flops += 8.0 * nz * (double)nc;
+  };
+  const int BIG = 1 << 30;
+  int64_t c0, nc;
+  if (fwd) {
+    {  // V leaves: coefficients of the probes' own rows
+      Stage& d = add(OP_H, PV(0), (int)vleaf.ld, 1, vleaf, NB * PV(0));
+      for (int64_t nu = 0; nu < NB; ++nu) {
+        win(L, nu, c0, nc);
+        if (nc <= 0) continue;
+        const int64_t j = p >= L ? nu : nu >> (L - p);  // p <= L: the probe above the leaf
+        GemmEnt e = ent(nu * vleaf.stride(), 0, xo[j] + (ct.begin(L, nu) - ct.begin(p, j)), 0,
+                        nu * PV(0) + c0 * d.ld_out, BIG, (int)ct.size(L, nu));
+        e.ncols = (int32_t)nc;
+        d.h.push_back(e);
+        d.maxc = std::max<int>(d.maxc, (int)nc);
+        flops += 8.0 * (double)ct.size(L, nu) * vleaf.ranks[nu] * (double)nc;
+      }
+    }
+    for (int l = 1; l <= lm; ++l) {
+      const Level<R>& wl = w[l - 1];
+      const int q = L - l;  // column level of the outputs
+      const bool shared = q >= p;
+      const int64_t ld_in = NB * PV(l - 1);
+      Stage& d = add(OP_H, PV(l), shared ? 2 * PV(l - 1) : PV(l - 1), 1, wl, NB * PV(l));
+      for (int64_t tau = 0; tau < (int64_t(1) << l); ++tau)
+        for (int64_t nu = 0; nu < (int64_t(1) << q); ++nu) {
+          const int64_t i = bidx(L, l, tau, nu), src = bidx(L, l - 1, tau / 2, 2 * nu);
+          if (shared) {
+            win(q, nu, c0, nc);
+            push(d, i * wl.stride(), 0, src * PV(l - 1), 0, i * PV(l), BIG, BIG, c0, nc, ld_in, d.ld_out,
+                 (double)wl.rows[i] * wl.ranks[i]);
+          } else {
+            for (int h = 0; h < 2; ++h) {
+              win(q + 1, 2 * nu + h, c0, nc);
+              push(d, i * wl.stride() + h * wl.gap, 0, (src + h) * PV(l - 1), 0, i * PV(l), BIG, BIG, c0, nc, ld_in,
+                   d.ld_out, (double)v_rank(l - 1, tau / 2, 2 * nu + h) * wl.ranks[i]);
+            }
+          }
+        }
+    }
+    {
+      Stage& d = add(OP_N, PU(lm), PV(lm), 1, b, NB * PU(lm));
+      const int64_t ld_in = NB * PV(lm);
+      for (int64_t i = 0; i < NB; ++i) {
+        win(L - lm, i & ((int64_t(1) << (L - lm)) - 1), c0, nc);
+        push(d, i * b.stride(), 0, i * PV(lm), 0, i * PU(lm), BIG, BIG, c0, nc, ld_in, d.ld_out,
+             (double)b.rows[i] * b.ranks[i]);
+      }
+    }
+    for (int l = lm; l < L; ++l) {
+      const Level<R>& rl = r[l - lm];
+      const int q = L - l - 1;  // column level of the outputs
+      const bool shared = q >= p;
+      const int64_t ld_in = NB * PU(l);
+      Stage& d = add(OP_N, PU(l + 1), PU(l), shared ? 2 : 1, rl, NB * PU(l + 1));
+      for (int64_t tp = 0; tp < (int64_t(1) << (l + 1)); ++tp)
+        for (int64_t np = 0; np < (int64_t(1) << q); ++np) {
+          const int64_t tau = tp >> 1, h = tp & 1;
+          const int64_t i0 = bidx(L, l, tau, 2 * np), i1 = i0 + 1, o = bidx(L, l + 1, tp, np);
+          const double rows_h = (double)u_rank(l + 1, tp, np);
+          if (shared) {
+            win(q, np, c0, nc);
+            push(d, i0 * rl.stride() + h * rl.gap, i1 * rl.stride() + h * rl.gap, i0 * PU(l), i1 * PU(l), o * PU(l + 1),
+                 BIG, BIG, c0, nc, ld_in, d.ld_out, rows_h * (rl.ranks[i0] + rl.ranks[i1]));
+          } else {
+            for (int s = 0; s < 2; ++s) {
+              const int64_t is = i0 + s;
+              win(q + 1, 2 * np + s, c0, nc);
+              push(d, is * rl.stride() + h * rl.gap, 0, is * PU(l), 0, o * PU(l + 1), BIG, BIG, c0, nc, ld_in,
+                   d.ld_out, rows_h * rl.ranks[is]);
+            }
+          }
+        }
+    }
+    {  // U leaves: every probe reaches every row
+      Stage& d = add(OP_N, (int)uleaf.ld, PU(L), 1, uleaf, 0);
+      const int64_t ld_in = NB * PU(L);
+      for (int64_t tau = 0; tau < NB; ++tau)
+        push(d, tau * uleaf.stride(), 0, tau * PU(L), 0, rt.begin(L, tau), (int)rt.size(L, tau), BIG, cs[0],
+             wend - cs[0], ld_in, ldy, (double)rt.size(L, tau) * uleaf.ranks[tau]);
+    }
+  } else {
+    {  // U leaves
+      Stage& d = add(OP_H, PU(L), (int)uleaf.ld, 1, uleaf, NB * PU(L));
+      for (int64_t tau = 0; tau < NB; ++tau) {
+        win(L, tau, c0, nc);
+        if (nc <= 0) continue;
+        const int64_t j = tau >> (L - p);
+        GemmEnt e = ent(tau * uleaf.stride(), 0, xo[j] + (rt.begin(L, tau) - rt.begin(p, j)), 0,
+                        tau * PU(L) + c0 * d.ld_out, BIG, (int)rt.size(L, tau));
+        e.ncols = (int32_t)nc;
+        d.h.push_back(e);
+        d.maxc = std::max<int>(d.maxc, (int)nc);
+        flops += 8.0 * (double)rt.size(L, tau) * uleaf.ranks[tau] * (double)nc;
+      }
+    }
+    for (int l = L - 1; l >= lm; --l) {
+      const Level<R>& rl = r[l - lm];
+      const bool shared = l >= p;  // the outputs' row level
+      const int64_t ld_in = NB * PU(l + 1);
+      Stage& d = add(OP_H, PU(l), PU(l + 1), shared ? 2 : 1, rl, NB * PU(l));
+      for (int64_t tau = 0; tau < (int64_t(1) << l); ++tau)
+        for (int64_t nu = 0; nu < (int64_t(1) << (L - l)); ++nu) {
+          const int64_t i = bidx(L, l, tau, nu);
+          const int64_t s0 = bidx(L, l + 1, 2 * tau, nu / 2), s1 = bidx(L, l + 1, 2 * tau + 1, nu / 2);
+          if (shared) {
+            win(l, tau, c0, nc);
+            push(d, i * rl.stride(), i * rl.stride() + rl.gap, s0 * PU(l + 1), s1 * PU(l + 1), i * PU(l), BIG, BIG, c0,
+                 nc, ld_in, d.ld_out, (double)rl.rows[i] * rl.ranks[i]);
+          } else {
+            for (int h = 0; h < 2; ++h) {
+              win(l + 1, 2 * tau + h, c0, nc);
+              push(d, i * rl.stride() + h * rl.gap, 0, (h ? s1 : s0) * PU(l + 1), 0, i * PU(l), BIG, BIG, c0, nc,
+                   ld_in, d.ld_out, (double)u_rank(l + 1, 2 * tau + h, nu / 2) * rl.ranks[i]);
+            }
+          }
+        }
+    }
+    {
+      Stage& d = add(OP_H, PV(lm), PU(lm), 1, b, NB * PV(lm));
+      const int64_t ld_in = NB * PU(lm);
+      for (int64_t i = 0; i < NB; ++i) {
+        win(lm, i >> (L - lm), c0, nc);
+        push(d, i * b.stride(), 0, i * PU(lm), 0, i * PV(lm), BIG, BIG, c0, nc, ld_in, d.ld_out,
+             (double)b.rows[i] * b.ranks[i]);
+      }
+    }
+    for (int l = lm; l >= 1; --l) {
+      const Level<R>& wl = w[l - 1];
+      const bool shared = l - 1 >= p;  // the outputs' row level
+      const int64_t ld_in = NB * PV(l);
+      Stage& d = add(OP_N, PV(l - 1), PV(l), shared ? 2 : 1, wl, NB * PV(l - 1));
+      for (int64_t tp = 0; tp < (int64_t(1) << (l - 1)); ++tp)
+        for (int64_t npp = 0; npp < (int64_t(1) << (L - l + 1)); ++npp) {
+          const int64_t nu = npp >> 1, h = npp & 1;
+          const int64_t i0 = bidx(L, l, 2 * tp, nu), i1 = bidx(L, l, 2 * tp + 1, nu), o = bidx(L, l - 1, tp, npp);
+          const double rows_h = (double)v_rank(l - 1, tp, npp);
+          if (shared) {
+            win(l - 1, tp, c0, nc);
+            push(d, i0 * wl.stride() + h * wl.gap, i1 * wl.stride() + h * wl.gap, i0 * PV(l), i1 * PV(l), o * PV(l - 1),
+                 BIG, BIG, c0, nc, ld_in, d.ld_out, rows_h * (wl.ranks[i0] + wl.ranks[i1]));
+          } else {
+            for (int s = 0; s < 2; ++s) {
+              const int64_t is = s ? i1 : i0;
+              win(l, 2 * tp + s, c0, nc);
+              push(d, is * wl.stride() + h * wl.gap, 0, is * PV(l), 0, o * PV(l - 1), BIG, BIG, c0, nc, ld_in,
+                   d.ld_out, rows_h * wl.ranks[is]);
+            }
+          }
+        }
+    }
+    {  // V leaves: every probe reaches every column point
+      Stage& d = add(OP_N, (int)vleaf.ld, PV(0), 1, vleaf, 0);
+      const int64_t ld_in = NB * PV(0);
+      for (int64_t nu = 0; nu < NB; ++nu)
+        push(d, nu * vleaf.stride(), 0, nu * PV(0), 0, ct.begin(L, nu), (int)ct.size(L, nu), BIG, cs[0], wend - cs[0],
+             ld_in, ldy, (double)ct.size(L, nu) * vleaf.ranks[nu]);
+    }
+  }
+  (void)ot;
+  // coefficient buffers span every column of the batch
+  const int64_t kall = wend;
+  DBuf<cx<R>> b0(c, (size_t)(NB * max_p() * kall)), b1(c, (size_t)(NB * max_p() * kall));
+  cx<R>* bufs[2] = {b0.p, b1.p};
+  const cx<R>* in = X;
+  int64_t ldin = ldx;
+  const int n = (int)st.size();
+  for (int i = 0; i < n; ++i) {
+    Stage& d = st[i];
+    const bool final = i == n - 1;
+    cx<R>* out = final ? y : bufs[i % 2];
+    const int64_t ldout = final ? ldy : d.ld_out;
+    if (!d.h.empty()) {
+      DBuf<GemmEnt> de = to_device(c, d.h);
+      launch_bgemm<R>(c, d.op, d.M, d.K, d.S, d.A, d.lda, in, ldin, out, ldout, de.p, (int)d.h.size(), d.maxc, false,
+                      0, true);
+    }
+    in = out;
+    ldin = ldout;
+  }
+  if (flops_done) *flops_done = flops;
+  return true;
+}
+
 // ------------------------------------------------------- host <-> device
 namespace {
 template <typename R>

@@ -107,6 +107,24 @@ struct DevButterfly {
   void setup_trees(Ctx* c, const Tree& row, const Tree& col, int levels, int center);
   // K x / K^T y / K^H y ; device buffers, original ordering
   void apply(int trans, const cx<R>* x, int64_t ldx, cx<R>* y, int64_t ldy, int64_t k);
+  // Structured probes (the recompression black box, config 4).  Probe j is
+  // nonzero only on node `node` of level `plevel` of the input-side tree
+  // (row tree for OP_H, column tree for OP_N); its compact values (node rows
+  // x ncols, leading dimension ldx) sit at X + x_off and it owns output
+  // columns [col0, col0 + ncols) of y.  The reference pads every probe to
+  // full height and multiplies the zeros (reconstruct.hpp:72-85,
+  // ButterflyOperator operators.hpp:106-122); here a block is multiplied only
+  // for the columns of the probes whose support reaches it, so the stages
+  // before the supports merge cost one apply for the whole batch.  Column
+  // arithmetic is unchanged: results equal the padded apply's.  segs sorted
+  // by node with contiguous columns; returns false (nothing launched) when
+  // the batch does not fit the scheme (non-identity trees, OP_T, gaps).
+  struct ProbeSeg {
+    int64_t node, x_off, col0;
+    int32_t ncols;
+  };
+  bool apply_structured(int trans, int plevel, const std::vector<ProbeSeg>& segs, const cx<R>* X, int64_t ldx,
+                        cx<R>* y, int64_t ldy, double* flops_done);
   int64_t nnz() const;
   int64_t max_rank() const;
   double apply_flops(int64_t k) const;   // 8 * nnz * k (complex)

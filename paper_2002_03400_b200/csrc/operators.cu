@@ -7,16 +7,39 @@
 namespace bfly {
 
 template <typename R>
-DBuf<cx<R>> DevOp<R>::pad_probes(int mode, const cx<R>* X, const std::vector<MatvecSeg>& segs, int64_t& wtot) {
-  wtot = 0;
-  for (const auto& s : segs) wtot = std::max<int64_t>(wtot, s.col0 + s.ncols);
+DBuf<cx<R>> DevOp<R>::pad_probes(int mode, const cx<R>* X, const std::vector<MatvecSeg>& segs, int64_t& c0,
+                                 int64_t& w) {
+  int64_t lo = INT64_MAX, hi = 0;
+  for (const auto& s : segs) {
+    lo = std::min<int64_t>(lo, s.col0);
+    hi = std::max<int64_t>(hi, s.col0 + s.ncols);
+  }
+  c0 = segs.empty() ? 0 : lo;
+  w = std::max<int64_t>(hi - c0, 0);
   const int64_t nin = in_dim(mode);
-  DBuf<cx<R>> p(ctx, (size_t)(nin * std::max<int64_t>(wtot, 1)));
+  DBuf<cx<R>> p(ctx, (size_t)(nin * std::max<int64_t>(w, 1)));
   p.zero();
   for (const auto& s : segs)
     if (s.rows > 0 && s.ncols > 0)
-      launch_copy2d<R>(ctx, p.p + s.row0 + s.col0 * nin, nin, X + s.x_off, s.ldx, s.rows, s.ncols);
+      launch_copy2d<R>(ctx, p.p + s.row0 + (s.col0 - c0) * nin, nin, X + s.x_off, s.ldx, s.rows, s.ncols);
   return p;
+}
+
+// A padded product writes every column of the span it is given, so a group of
+// segments is cut into runs that tile a column range without gaps: the
+// pieces of a probe split across ranks own interleaved column ranges of Y,
+// and a run must not overwrite the columns of another group with zeros.
+std::vector<std::vector<MatvecSeg>> column_runs(std::vector<MatvecSeg> segs) {
+  std::sort(segs.begin(), segs.end(), [](const MatvecSeg& a, const MatvecSeg& b) { return a.col0 < b.col0; });
+  std::vector<std::vector<MatvecSeg>> runs;
+  int64_t end = -1;
+  for (const auto& s : segs) {
+    if (s.ncols <= 0) continue;
+    if (runs.empty() || s.col0 != end) runs.emplace_back();
+    runs.back().push_back(s);
+    end = s.col0 + s.ncols;
+  }
+  return runs;
 }
 
 namespace {
@@ -104,13 +127,67 @@ struct ButterflyOp : DevOp<R> {
   std::unique_ptr<DevButterfly<R>> bf;
   void do_apply(int mode, const cx<R>* X, const std::vector<MatvecSeg>& segs, cx<R>* Y, int64_t ldy, int64_t o0,
                 int64_t o1) override {
-    int64_t wtot = 0;
-    DBuf<cx<R>> xp = this->pad_probes(mode, X, segs, wtot);
-    if (wtot <= 0) return;
-    bf->apply(mode, xp.p, this->in_dim(mode), Y, ldy, wtot);
-    int64_t cols = 0;
-    for (const auto& s : segs) cols += s.ncols;
-    this->flops += bf->apply_flops(cols);
+    if (structured(mode, X, segs, Y, ldy)) return;
+    for (const auto& run : column_runs(segs)) {
+      int64_t c0 = 0, w = 0;
+      DBuf<cx<R>> xp = this->pad_probes(mode, X, run, c0, w);
+      if (w <= 0) continue;
+      bf->apply(mode, xp.p, this->in_dim(mode), Y + c0 * ldy, ldy, w);
+      this->flops += bf->apply_flops(w);
+    }
+  }
+  // Probes supported on the nodes of one level of this butterfly's own
+  // input-side tree (a recompression over the same trees): blocks the zero
+  // rows cannot reach are skipped (DevButterfly::apply_structured), and the
+  // flops counted are the ones executed.  BFLY_NO_STRUCT_APPLY=1 keeps the
+  // reference's padded products.
+  bool structured(int mode, const cx<R>* X, const std::vector<MatvecSeg>& segs, cx<R>* Y, int64_t ldy) {
+    static const bool off = std::getenv("BFLY_NO_STRUCT_APPLY") != nullptr;
+    if (off || segs.empty() || (mode != OP_N && mode != OP_H)) return false;
+    const Tree& pt = mode == OP_N ? bf->ct : bf->rt;
+    if (!pt.identity || segs[0].rows >= pt.n) return false;
+    int p = -1;
+    for (int l = 1; l <= bf->L && p < 0; ++l) {
+      const auto& rg = pt.ranges[l];
+      auto it = std::lower_bound(rg.begin(), rg.end(), segs[0].row0);
+      if (it != rg.end() && *it == segs[0].row0 && it + 1 != rg.end() && *(it + 1) == segs[0].row0 + segs[0].rows)
+        p = l;
+    }
+    if (p < 0) return false;
+    std::vector<typename DevButterfly<R>::ProbeSeg> ps;
+    const auto& rg = pt.ranges[p];
+    bool uniform = true;
+    int64_t maxrows = 0, cols = 0;
+    for (const auto& s : segs) {
+      auto it = std::lower_bound(rg.begin(), rg.end(), s.row0);
+      if (it == rg.end() || *it != s.row0 || it + 1 == rg.end() || *(it + 1) != s.row0 + s.rows) return false;
+      ps.push_back({(int64_t)(it - rg.begin()), s.x_off, s.col0, s.ncols});
+      uniform = uniform && s.ldx == segs[0].ldx;
+      maxrows = std::max(maxrows, s.rows);
+      cols += std::max<int64_t>(s.ncols, 0);
+    }
+    // ragged nodes: the compact probes get one common leading dimension
+    DBuf<cx<R>> tmp;
+    const cx<R>* Xs = X;
+    int64_t ld = segs[0].ldx;
+    if (!uniform) {
+      tmp.reset(this->ctx, (size_t)std::max<int64_t>(1, maxrows * cols));
+      int64_t off = 0;
+      for (size_t i = 0; i < segs.size(); ++i) {
+        const auto& s = segs[i];
+        if (s.rows > 0 && s.ncols > 0)
+          launch_copy2d<R>(this->ctx, tmp.p + off, maxrows, X + s.x_off, s.ldx, s.rows, s.ncols);
+        ps[i].x_off = off;
+        off += maxrows * std::max<int64_t>(s.ncols, 0);
+      }
+      Xs = tmp.p;
+      ld = maxrows;
+    }
+    std::sort(ps.begin(), ps.end(), [](const auto& a, const auto& b) { return a.node < b.node; });
+    double fl = 0;
+    if (!bf->apply_structured(mode, p, ps, Xs, ld, Y, ldy, &fl)) return false;
+    this->flops += fl;
+    return true;
   }
 };
 
@@ -122,14 +199,16 @@ struct CallbackOp : DevOp<R> {
   void do_apply(int mode, const cx<R>* X, const std::vector<MatvecSeg>& segs, cx<R>* Y, int64_t ldy, int64_t o0,
                 int64_t o1) override {
     Ctx* c = this->ctx;
-    int64_t wtot = 0;
-    DBuf<cx<R>> xp = this->pad_probes(mode, X, segs, wtot);
-    if (wtot <= 0) return;
     const int64_t nin = this->in_dim(mode), nout = this->out_dim(mode);
-    if (mode == OP_H) launch_conj<R>(c, xp.p, nin, wtot, nin);
-    int rc = fn(user, mode == OP_N ? 0 : 1, xp.p, nin, Y, ldy, wtot, (void*)c->stream);
-    if (rc != 0) fail(rc, "black-box callback failed with status " + std::to_string(rc));
-    if (mode == OP_H) launch_conj<R>(c, Y, nout, wtot, ldy);
+    for (const auto& run : column_runs(segs)) {
+      int64_t c0 = 0, w = 0;
+      DBuf<cx<R>> xp = this->pad_probes(mode, X, run, c0, w);
+      if (w <= 0) continue;
+      if (mode == OP_H) launch_conj<R>(c, xp.p, nin, w, nin);
+      int rc = fn(user, mode == OP_N ? 0 : 1, xp.p, nin, Y + c0 * ldy, ldy, w, (void*)c->stream);
+      if (rc != 0) fail(rc, "black-box callback failed with status " + std::to_string(rc));
+      if (mode == OP_H) launch_conj<R>(c, Y + c0 * ldy, nout, w, ldy);
+    }
   }
 };
 
@@ -141,19 +220,19 @@ struct CallbackRangeOp : DevOp<R> {
   void do_apply(int mode, const cx<R>* X, const std::vector<MatvecSeg>& segs, cx<R>* Y, int64_t ldy, int64_t o0,
                 int64_t o1) override {
     Ctx* c = this->ctx;
-    int64_t wtot = 0;
-    DBuf<cx<R>> xp = this->pad_probes(mode, X, segs, wtot);
-    if (wtot <= 0) return;
+    int64_t c0 = 0, w = 0;
+    DBuf<cx<R>> xp = this->pad_probes(mode, X, segs, c0, w);
+    if (w <= 0) return;
     const int64_t nin = this->in_dim(mode), nout = this->out_dim(mode);
-    if (mode == OP_H) launch_conj<R>(c, xp.p, nin, wtot, nin);
+    if (mode == OP_H) launch_conj<R>(c, xp.p, nin, w, nin);
     for (const auto& s : segs) {
       if (s.ncols <= 0) continue;
       const int64_t b = s.rows > 0 ? s.row0 : 0, e = s.rows > 0 ? s.row0 + s.rows : 0;
-      int rc = fn(user, mode == OP_N ? 0 : 1, xp.p + s.col0 * nin, nin, Y + s.col0 * ldy, ldy, s.ncols, b, e,
+      int rc = fn(user, mode == OP_N ? 0 : 1, xp.p + (s.col0 - c0) * nin, nin, Y + s.col0 * ldy, ldy, s.ncols, b, e,
                   (void*)c->stream);
       if (rc != 0) fail(rc, "black-box callback failed with status " + std::to_string(rc));
+      if (mode == OP_H) launch_conj<R>(c, Y + s.col0 * ldy, nout, s.ncols, ldy);
     }
-    if (mode == OP_H) launch_conj<R>(c, Y, nout, wtot, ldy);
   }
 };
 

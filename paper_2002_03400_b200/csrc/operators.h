@@ -59,9 +59,13 @@ struct DevOp {
   virtual void do_apply(int mode, const cx<R>* X, const std::vector<MatvecSeg>& segs, cx<R>* Y, int64_t ldy,
                         int64_t o0, int64_t o1) = 0;
   // materialise the padded probes (zeros outside the segment rows) as one
-  // in_dim x Wtot buffer whose columns line up with Y's
-  DBuf<cx<R>> pad_probes(int mode, const cx<R>* X, const std::vector<MatvecSeg>& segs, int64_t& wtot);
+  // in_dim x w buffer whose column t lines up with column c0 + t of Y
+  // (c0 / w: the column span of the segments)
+  DBuf<cx<R>> pad_probes(int mode, const cx<R>* X, const std::vector<MatvecSeg>& segs, int64_t& c0, int64_t& w);
 };
+
+// segments grouped into runs that tile a column range without gaps
+std::vector<std::vector<MatvecSeg>> column_runs(std::vector<MatvecSeg> segs);
 
 template <typename R>
 std::unique_ptr<DevOp<R>> make_kernel_op(Ctx* c, int kind, int64_t m, int64_t n, const double* tgt, const double* src,

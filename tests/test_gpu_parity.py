@@ -601,3 +601,40 @@ def test_saturated_core_fit_newton_schulz(B, monkeypatch, n):
     print(f"config 3 n={n}: max rank {a.max_rank()}, centre level {ta*1e3:.1f} ms (Newton-Schulz) vs "
           f"{tb*1e3:.1f} ms (Jacobi), apply rel diff {e:.2e}")
     assert e < 1e-11
+
+
+@pytest.mark.parametrize("case,vr", [("cfg4", 0), ("synth_real", 0), ("ragged", 0), ("cfg4", 3), ("cfg4_c64", 0)])
+def test_structured_butterfly_products(tmp_path, case, vr):
+    """Recompression (config 4): the butterfly black box multiplies a block
+    only for the probes whose nonzero rows reach it
+    (DevButterfly::apply_structured); the reference pads the probes and
+    multiplies the zeros (reconstruct.hpp:72-85, operators.hpp:106-122).
+    Skipped terms are exact zeros, so the factorization must be the one the
+    padded products give -- same ranks, same bookkeeping, apply outputs equal
+    to rounding -- with fewer executed flops.  Also ragged leaves / varying
+    ranks, a real butterfly, the rank-sharded schedule and complex64."""
+    import os
+    import subprocess
+    import sys
+
+    worker = os.path.join(os.path.dirname(__file__), "struct_worker.py")
+    res = []
+    for off in (False, True):
+        env = dict(os.environ)
+        env.pop("BFLY_NO_STRUCT_APPLY", None)
+        if off:
+            env["BFLY_NO_STRUCT_APPLY"] = "1"
+        out = str(tmp_path / f"s{int(off)}.npz")
+        cmd = [sys.executable, worker, "--case", case, "--out", out] + (["--vr", str(vr)] if vr else [])
+        subprocess.run(cmd, check=True, env=env, timeout=600)
+        res.append(np.load(out))
+    s, p = res
+    assert bool(s["struct"]) and not bool(p["struct"])
+    np.testing.assert_array_equal(s["profile"], p["profile"])
+    np.testing.assert_array_equal(s["cols"], p["cols"])
+    tol = 1e-5 if case == "cfg4_c64" else 1e-13
+    assert rel_err(s["yn"], p["yn"]) <= tol and rel_err(s["yh"], p["yh"]) <= tol
+    print(f"{case} vr={vr}: apply diff {rel_err(s['yn'], p['yn']):.1e} / {rel_err(s['yh'], p['yh']):.1e}; "
+          f"flops {float(s['flops']):.3e} structured vs {float(p['flops']):.3e} padded; "
+          f"{float(s['seconds'])*1e3:.1f} vs {float(p['seconds'])*1e3:.1f} ms")
+    assert float(s["flops"]) < float(p["flops"])
