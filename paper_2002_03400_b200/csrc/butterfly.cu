@@ -738,7 +738,8 @@ void DevButterfly<R>::apply_h(const cx<R>* yt, int64_t ldy, cx<R>* xt, int64_t l
 // did not produce (no zero-filled coefficient buffers).
 template <typename R>
 bool DevButterfly<R>::apply_structured(int trans, int plevel, const std::vector<ProbeSeg>& segs, const cx<R>* X,
-                                       int64_t ldx, cx<R>* y, int64_t ldy, double* flops_done) {
+                                       int64_t ldx, cx<R>* y, int64_t ldy, int64_t o0, int64_t o1,
+                                       double* flops_done) {
   Ctx* c = ctx;
   if ((trans != OP_N && trans != OP_H) || !rt.identity || !ct.identity) return false;
   if (plevel < 0 || plevel > L || segs.empty()) return false;
@@ -762,6 +763,11 @@ bool DevButterfly<R>::apply_structured(int trans, int plevel, const std::vector<
   }
   const int64_t wend = cs[NP];
   if (wend - cs[0] <= 0) return true;
+  // output restriction: a block is needed when its output-side node holds
+  // requested points (its sources sit at that node's parent, so every block a
+  // kept entry reads was kept too)
+  const bool restrict_out = o1 >= 0 && (o0 > 0 || o1 < ot.n);
+  auto need = [&](int q, int64_t u) { return !restrict_out || (ot.begin(q, u) < o1 && ot.end(q, u) > o0); };
   auto win = [&](int q, int64_t t, int64_t& c0, int64_t& nc) {
     int64_t j0, j1;
     if (q >= p) {
@@ -824,6 +830,7 @@ bool DevButterfly<R>::apply_structured(int trans, int plevel, const std::vector<
       for (int64_t tau = 0; tau < (int64_t(1) << l); ++tau)
         for (int64_t nu = 0; nu < (int64_t(1) << q); ++nu) {
           const int64_t i = bidx(L, l, tau, nu), src = bidx(L, l - 1, tau / 2, 2 * nu);
+          if (!need(l, tau)) continue;
           if (shared) {
             win(q, nu, c0, nc);
             push(d, i * wl.stride(), 0, src * PV(l - 1), 0, i * PV(l), BIG, BIG, c0, nc, ld_in, d.ld_out,
@@ -841,6 +848,7 @@ bool DevButterfly<R>::apply_structured(int trans, int plevel, const std::vector<
       Stage& d = add(OP_N, PU(lm), PV(lm), 1, b, NB * PU(lm));
       const int64_t ld_in = NB * PV(lm);
       for (int64_t i = 0; i < NB; ++i) {
+        if (!need(lm, i >> (L - lm))) continue;
         win(L - lm, i & ((int64_t(1) << (L - lm)) - 1), c0, nc);
         push(d, i * b.stride(), 0, i * PV(lm), 0, i * PU(lm), BIG, BIG, c0, nc, ld_in, d.ld_out,
              (double)b.rows[i] * b.ranks[i]);
@@ -857,6 +865,7 @@ bool DevButterfly<R>::apply_structured(int trans, int plevel, const std::vector<
           const int64_t tau = tp >> 1, h = tp & 1;
           const int64_t i0 = bidx(L, l, tau, 2 * np), i1 = i0 + 1, o = bidx(L, l + 1, tp, np);
           const double rows_h = (double)u_rank(l + 1, tp, np);
+          if (!need(l + 1, tp)) continue;
           if (shared) {
             win(q, np, c0, nc);
             push(d, i0 * rl.stride() + h * rl.gap, i1 * rl.stride() + h * rl.gap, i0 * PU(l), i1 * PU(l), o * PU(l + 1),
@@ -875,8 +884,9 @@ bool DevButterfly<R>::apply_structured(int trans, int plevel, const std::vector<
       Stage& d = add(OP_N, (int)uleaf.ld, PU(L), 1, uleaf, 0);
       const int64_t ld_in = NB * PU(L);
       for (int64_t tau = 0; tau < NB; ++tau)
-        push(d, tau * uleaf.stride(), 0, tau * PU(L), 0, rt.begin(L, tau), (int)rt.size(L, tau), BIG, cs[0],
-             wend - cs[0], ld_in, ldy, (double)rt.size(L, tau) * uleaf.ranks[tau]);
+        if (need(L, tau))
+          push(d, tau * uleaf.stride(), 0, tau * PU(L), 0, rt.begin(L, tau), (int)rt.size(L, tau), BIG, cs[0],
+               wend - cs[0], ld_in, ldy, (double)rt.size(L, tau) * uleaf.ranks[tau]);
     }
   } else {
     {  // U leaves
@@ -902,6 +912,7 @@ bool DevButterfly<R>::apply_structured(int trans, int plevel, const std::vector<
         for (int64_t nu = 0; nu < (int64_t(1) << (L - l)); ++nu) {
           const int64_t i = bidx(L, l, tau, nu);
           const int64_t s0 = bidx(L, l + 1, 2 * tau, nu / 2), s1 = bidx(L, l + 1, 2 * tau + 1, nu / 2);
+          if (!need(L - l, nu)) continue;
           if (shared) {
             win(l, tau, c0, nc);
             push(d, i * rl.stride(), i * rl.stride() + rl.gap, s0 * PU(l + 1), s1 * PU(l + 1), i * PU(l), BIG, BIG, c0,
@@ -919,6 +930,7 @@ bool DevButterfly<R>::apply_structured(int trans, int plevel, const std::vector<
       Stage& d = add(OP_H, PV(lm), PU(lm), 1, b, NB * PV(lm));
       const int64_t ld_in = NB * PU(lm);
       for (int64_t i = 0; i < NB; ++i) {
+        if (!need(L - lm, i & ((int64_t(1) << (L - lm)) - 1))) continue;
         win(lm, i >> (L - lm), c0, nc);
         push(d, i * b.stride(), 0, i * PU(lm), 0, i * PV(lm), BIG, BIG, c0, nc, ld_in, d.ld_out,
              (double)b.rows[i] * b.ranks[i]);
@@ -934,6 +946,7 @@ bool DevButterfly<R>::apply_structured(int trans, int plevel, const std::vector<
           const int64_t nu = npp >> 1, h = npp & 1;
           const int64_t i0 = bidx(L, l, 2 * tp, nu), i1 = bidx(L, l, 2 * tp + 1, nu), o = bidx(L, l - 1, tp, npp);
           const double rows_h = (double)v_rank(l - 1, tp, npp);
+          if (!need(L - l + 1, npp)) continue;
           if (shared) {
             win(l - 1, tp, c0, nc);
             push(d, i0 * wl.stride() + h * wl.gap, i1 * wl.stride() + h * wl.gap, i0 * PV(l), i1 * PV(l), o * PV(l - 1),
@@ -952,11 +965,11 @@ bool DevButterfly<R>::apply_structured(int trans, int plevel, const std::vector<
       Stage& d = add(OP_N, (int)vleaf.ld, PV(0), 1, vleaf, 0);
       const int64_t ld_in = NB * PV(0);
       for (int64_t nu = 0; nu < NB; ++nu)
-        push(d, nu * vleaf.stride(), 0, nu * PV(0), 0, ct.begin(L, nu), (int)ct.size(L, nu), BIG, cs[0], wend - cs[0],
-             ld_in, ldy, (double)ct.size(L, nu) * vleaf.ranks[nu]);
+        if (need(L, nu))
+          push(d, nu * vleaf.stride(), 0, nu * PV(0), 0, ct.begin(L, nu), (int)ct.size(L, nu), BIG, cs[0],
+               wend - cs[0], ld_in, ldy, (double)ct.size(L, nu) * vleaf.ranks[nu]);
     }
   }
-  (void)ot;
   // coefficient buffers span every column of the batch
   const int64_t kall = wend;
   DBuf<cx<R>> b0(c, (size_t)(NB * max_p() * kall)), b1(c, (size_t)(NB * max_p() * kall));

@@ -123,8 +123,11 @@ struct DevButterfly {
     int64_t node, x_off, col0;
     int32_t ncols;
   };
+  // [o0, o1) (output tree order; o1 < 0: all) are the output rows that must be
+  // produced: blocks whose output-side node holds none of them are skipped
+  // too (a probe split across ranks needs only its partner nodes' rows).
   bool apply_structured(int trans, int plevel, const std::vector<ProbeSeg>& segs, const cx<R>* X, int64_t ldx,
-                        cx<R>* y, int64_t ldy, double* flops_done);
+                        cx<R>* y, int64_t ldy, int64_t o0, int64_t o1, double* flops_done);
   int64_t nnz() const;
   int64_t max_rank() const;
   double apply_flops(int64_t k) const;   // 8 * nnz * k (complex)

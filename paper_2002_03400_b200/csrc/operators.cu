@@ -127,7 +127,10 @@ struct ButterflyOp : DevOp<R> {
   std::unique_ptr<DevButterfly<R>> bf;
   void do_apply(int mode, const cx<R>* X, const std::vector<MatvecSeg>& segs, cx<R>* Y, int64_t ldy, int64_t o0,
                 int64_t o1) override {
-    if (structured(mode, X, segs, Y, ldy)) return;
+    if (structured(mode, X, segs, Y, ldy, o0, o1)) {
+      this->last_restricted = true;
+      return;
+    }
     for (const auto& run : column_runs(segs)) {
       int64_t c0 = 0, w = 0;
       DBuf<cx<R>> xp = this->pad_probes(mode, X, run, c0, w);
@@ -141,11 +144,12 @@ struct ButterflyOp : DevOp<R> {
   // rows cannot reach are skipped (DevButterfly::apply_structured), and the
   // flops counted are the ones executed.  BFLY_NO_STRUCT_APPLY=1 keeps the
   // reference's padded products.
-  bool structured(int mode, const cx<R>* X, const std::vector<MatvecSeg>& segs, cx<R>* Y, int64_t ldy) {
+  bool structured(int mode, const cx<R>* X, const std::vector<MatvecSeg>& segs, cx<R>* Y, int64_t ldy, int64_t o0,
+                  int64_t o1) {
     static const bool off = std::getenv("BFLY_NO_STRUCT_APPLY") != nullptr;
     if (off || segs.empty() || (mode != OP_N && mode != OP_H)) return false;
     const Tree& pt = mode == OP_N ? bf->ct : bf->rt;
-    if (!pt.identity || segs[0].rows >= pt.n) return false;
+    if (!pt.identity || segs[0].rows >= pt.n) return false;  // dense probes (leaf phases): the plain apply
     int p = -1;
     for (int l = 1; l <= bf->L && p < 0; ++l) {
       const auto& rg = pt.ranges[l];
@@ -185,7 +189,7 @@ struct ButterflyOp : DevOp<R> {
     }
     std::sort(ps.begin(), ps.end(), [](const auto& a, const auto& b) { return a.node < b.node; });
     double fl = 0;
-    if (!bf->apply_structured(mode, p, ps, Xs, ld, Y, ldy, &fl)) return false;
+    if (!bf->apply_structured(mode, p, ps, Xs, ld, Y, ldy, o0, o1, &fl)) return false;
     this->flops += fl;
     return true;
   }

@@ -32,6 +32,9 @@ struct DevOp {
   // true when do_apply computes only the requested output rows (work and
   // counted flops proportional to them)
   virtual bool restricts_rows() const { return false; }
+  // whether the last apply_segs produced only the requested rows (a kind may
+  // restrict some products only: the butterfly black box's structured path)
+  bool last_restricted = false;
   int64_t in_dim(int mode) const { return mode == OP_N ? n : m; }
   int64_t out_dim(int mode) const { return mode == OP_N ? m : n; }
 
@@ -48,6 +51,7 @@ struct DevOp {
     if (mode == OP_N) fwd += cols;
     else tr += cols;
     if (o1 < 0) o1 = out_dim(mode);
+    last_restricted = restricts_rows();
     do_apply(mode, X, segs, Y, ldy, o0, o1);
   }
   void apply_dense(int mode, const cx<R>* X, int64_t ldx, cx<R>* Y, int64_t ldy, int64_t k) {

@@ -64,7 +64,8 @@ def main():
             t = shares.max() + rest + gather
             total += t
             rows.append({"phase": p.name, "max_share_ms": round(shares.max() * 1e3, 3),
-                         "sum_shares_ms": round(shares.sum() * 1e3, 3), "unsplit_ms": round(rest * 1e3, 3)})
+                         "sum_shares_ms": round(shares.sum() * 1e3, 3), "unsplit_ms": round(rest * 1e3, 3),
+                         "shares_ms": [round(float(x) * 1e3, 3) for x in shares]})
         out["projection"].append({"gpus": nr, "projected_s": round(total, 4), "speedup": round(t1 / total, 2),
                                   "phases": rows})
         print(json.dumps({"gpus": nr, "projected_s": round(total, 4), "speedup_vs_1gpu": round(t1 / total, 2)}),
