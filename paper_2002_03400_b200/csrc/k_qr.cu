@@ -290,7 +290,15 @@ __device__ __forceinline__ V dot_conj(const V* __restrict__ a, const V* __restri
   return cadd(cadd(s0, s1), cadd(s2, s3));
 }
 
-template <typename R, int NW>
+// NH = 2 (four warps, blocks of 33..64 rows): two lanes per trailing column,
+// each summing / updating half of the rows (lane >> 4 picks the half, so a
+// quarter-warp still walks 8 consecutive columns: conflict-free); the partial
+// dots meet through one shuffle.  64 x 66 blocks (config 4): 46.3 -> 39.7 ms of
+// CPQR per construction (profiles/r02_cpqr_nh2.txt).  A register-resident
+// variant (a column in the registers of four lanes, reflector broadcast from
+// shared memory, two barriers per step) measured 111 ms: 2.9x the
+// instructions (row selects, per-quad redundant downdates) at one block per SM.
+template <typename R, int NW, int NH>
 __global__ void __launch_bounds__(32 * NW) cpqr_warp_kernel(const cx<R>* __restrict__ src, int64_t ld_src,
                                                             cx<R>* __restrict__ dst, int64_t ld_dst, int cap,
                                                             const QrEnt* __restrict__ ents, int32_t* ranks,
@@ -306,8 +314,12 @@ __global__ void __launch_bounds__(32 * NW) cpqr_warp_kernel(const cx<R>* __restr
   R* nu = reinterpret_cast<R*>(Z + (size_t)LD * w);
   R* nd = nu + w;
   V* tau = reinterpret_cast<V*>(nd + w);
-  __shared__ R s_red[2];
-  __shared__ int s_idx[2];
+  __shared__ R s_red[NW];
+  __shared__ int s_idx[NW];
+  // trailing-column work split: CP columns per pass, lane half hh of NH
+  constexpr int CP = NT / NH;
+  const int ccol = NH == 1 ? t : warp * 16 + (lane & 15);
+  const int hh = NH == 1 ? 0 : lane >> 4;
   __shared__ V s_beta_tau[2];  // (beta, 0), tau of the current step
   V* out = dst + e.dst;
   auto sync = [&]() {
@@ -368,7 +380,9 @@ __global__ void __launch_bounds__(32 * NW) cpqr_warp_kernel(const cx<R>* __restr
       sync();
       best = s_red[0];
       bi = s_idx[0];
-      if (s_red[1] > best || (s_red[1] == best && s_idx[1] < bi)) { best = s_red[1]; bi = s_idx[1]; }
+#pragma unroll
+      for (int q = 1; q < NW; ++q)
+        if (s_red[q] > best || (s_red[q] == best && s_idx[q] < bi)) { best = s_red[q]; bi = s_idx[q]; }
     }
     if (bi != j) {
       for (int i = t; i < r; i += NT) {
@@ -422,28 +436,45 @@ __global__ void __launch_bounds__(32 * NW) cpqr_warp_kernel(const cx<R>* __restr
     }
     last_kept = absb;
     // ---- apply H_j = I - tau v v^H to the trailing columns (thread = column); downdate norms
-    for (int c = j + 1 + t; c < w; c += NT) {
-      V* zc = Z + c * LD;
+    for (int cb = j + 1; cb < w; cb += CP) {
+      const int c = cb + ccol;
+      const bool act = c < w;
+      V* zc = Z + (act ? c : j) * LD;
       const V* v = Z + j * LD;
-      const V dot = cadd(zc[j], dot_conj(v, zc, j + 1, r));
-      const V tt = cmul(tj, dot);
-      for (int i = j + 1; i < r; ++i) zc[i] = csub(zc[i], cmul(v[i], tt));
-      const V top = csub(zc[j], tt);
-      zc[j] = top;
-      // LAWN-176 downdate
-      const R nuc = nu[c], ndc = nd[c];
-      if (nuc != R(0)) {
-        R temp = sqrt(cabs2(top)) / nuc;
-        temp = (R(1) + temp) * (R(1) - temp);
-        if (temp < R(0)) temp = 0;
-        const R ratio = nuc / ndc;
-        const R temp2 = temp * ratio * ratio;
-        if (temp2 <= QrTraits<R>::sqrt_eps) {
-          R s2 = 0;
-          for (int i = j + 1; i < r; ++i) s2 += cabs2(zc[i]);
-          nu[c] = nd[c] = sqrt(s2);
-        } else {
-          nu[c] = nuc * sqrt(temp);
+      // this lane's rows [i0, i1) of (j, r)
+      const int half = (r - j) / 2;  // rows of the first half (NH = 2)
+      const int i0 = NH == 1 || hh == 0 ? j + 1 : j + 1 + half;
+      const int i1 = NH == 1 || hh == 1 ? r : j + 1 + half;
+      V part = mkc<R>(0, 0);
+      if (act) part = dot_conj(v, zc, i0, i1);
+      if (NH == 2) {
+        part.x += __shfl_xor_sync(0xffffffffu, part.x, 16);
+        part.y += __shfl_xor_sync(0xffffffffu, part.y, 16);
+      }
+      V tt = mkc<R>(0, 0);
+      if (act) {
+        tt = cmul(tj, cadd(zc[j], part));
+        for (int i = i0; i < i1; ++i) zc[i] = csub(zc[i], cmul(v[i], tt));
+      }
+      if (NH == 2) __syncwarp();  // both halves updated before the norm is touched
+      if (act && hh == 0) {
+        const V top = csub(zc[j], tt);
+        zc[j] = top;
+        // LAWN-176 downdate
+        const R nuc = nu[c], ndc = nd[c];
+        if (nuc != R(0)) {
+          R temp = sqrt(cabs2(top)) / nuc;
+          temp = (R(1) + temp) * (R(1) - temp);
+          if (temp < R(0)) temp = 0;
+          const R ratio = nuc / ndc;
+          const R temp2 = temp * ratio * ratio;
+          if (temp2 <= QrTraits<R>::sqrt_eps) {
+            R s2 = 0;
+            for (int i = j + 1; i < r; ++i) s2 += cabs2(zc[i]);
+            nu[c] = nd[c] = sqrt(s2);
+          } else {
+            nu[c] = nuc * sqrt(temp);
+          }
         }
       }
     }
@@ -461,12 +492,26 @@ __global__ void __launch_bounds__(32 * NW) cpqr_warp_kernel(const cx<R>* __restr
   for (int i = k - 1; i >= 0; --i) {
     const V tq = cconj(tau[i]);
     const V* v = Z + i * LD;
-    for (int c = i + 1 + t; c < k; c += NT) {
-      V* zc = Z + c * LD;
-      const V dot = cadd(zc[i], dot_conj(v, zc, i + 1, r));  // v_i = 1
-      const V tt = cmul(tq, dot);
-      for (int q = i + 1; q < r; ++q) zc[q] = csub(zc[q], cmul(v[q], tt));
-      zc[i] = csub(zc[i], tt);
+    for (int cb = i + 1; cb < k; cb += CP) {
+      const int c = cb + ccol;
+      const bool act = c < k;
+      V* zc = Z + (act ? c : i) * LD;
+      const int half = (r - i) / 2;
+      const int i0 = NH == 1 || hh == 0 ? i + 1 : i + 1 + half;
+      const int i1 = NH == 1 || hh == 1 ? r : i + 1 + half;
+      V part = mkc<R>(0, 0);
+      if (act) part = dot_conj(v, zc, i0, i1);  // v_i = 1
+      if (NH == 2) {
+        part.x += __shfl_xor_sync(0xffffffffu, part.x, 16);
+        part.y += __shfl_xor_sync(0xffffffffu, part.y, 16);
+      }
+      V tt = mkc<R>(0, 0);
+      if (act) {
+        tt = cmul(tq, cadd(zc[i], part));
+        for (int q = i0; q < i1; ++q) zc[q] = csub(zc[q], cmul(v[q], tt));
+      }
+      if (NH == 2) __syncwarp();  // the other half has read zc[i]
+      if (act && hh == 0) zc[i] = csub(zc[i], tt);
     }
     sync();
     for (int q = t; q < r; q += NT) {
@@ -645,11 +690,14 @@ void launch_cpqr(Ctx* c, const cx<R>* src, int64_t ld_src, cx<R>* dst, int64_t l
   if (max_rows <= 64 && max_cols <= 96 && !std::getenv("BFLY_CPQR_CTA")) {
     // one warp per block (<= 32 rows) or two (<= 64 rows); shared memory: the
     // block with an odd column stride, norms, tau
-    const int nw = max_rows <= 32 ? 1 : 2;
+    // blocks of 33..64 rows: four warps with two lanes per trailing column
+    // (BFLY_CPQR_NH=1: the two-warp, lane-per-column form)
+    static const bool nh1 = std::getenv("BFLY_CPQR_NH") && std::atoi(std::getenv("BFLY_CPQR_NH")) == 1;
+    const int nw = max_rows <= 32 ? 1 : nh1 ? 2 : 4;
     const int ld = nw == 1 ? 33 : 65;
     const size_t smem = sizeof(cx<R>) * ((size_t)ld * max_cols + max_cols) + 2 * sizeof(R) * max_cols;
     KTimer timer(c, "cpqr", 0.0, (double)sizeof(cx<R>) * nent * ((double)max_rows * max_cols + (double)ld_dst * cap));
-    auto kern = nw == 1 ? cpqr_warp_kernel<R, 1> : cpqr_warp_kernel<R, 2>;
+    auto kern = nw == 1 ? cpqr_warp_kernel<R, 1, 1> : nw == 2 ? cpqr_warp_kernel<R, 2, 1> : cpqr_warp_kernel<R, 4, 2>;
     if (smem > 48 * 1024) BFLY_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     kern<<<nent, 32 * nw, smem, c->stream>>>(src, ld_src, dst, ld_dst, cap, ents, ranks, eps, margins);
     BFLY_LAUNCH_CHECK("cpqr_warp");
