@@ -33,24 +33,25 @@ def _tree_order(pts, L, dim):
     return p, t2
 
 
-def oracle_config(cfg_id, n, seed=0):
-    """-> (op, row_tree, col_tree, cfg dict)"""
+def oracle_config(cfg_id, n, seed=0, levels=None):
+    """-> (op, row_tree, col_tree, cfg dict); ``levels`` overrides the tree
+    depth of configs 0-2 (like configs.build)"""
     if cfg_id == 0:
-        L = O.depth_for(n, 32)
+        L = levels or O.depth_for(n, 32)
         x, rt = _tree_order(_uniform(n, 0, 1, 0.0, 1.0), L, 1)
         xi, ct = _tree_order(_uniform(n, 0, 2, -n / 2.0, n / 2.0), L, 1)
         op = O.kernel_operator(O.OP_NUFFT, x, xi)
         return op, rt, ct, dict(levels=L, tolerance=1e-6, rank_guess=16, oversampling=2, seed=seed)
     if cfg_id == 1:
         side = int(round(math.sqrt(n)))
-        L = O.depth_for(n, 32)
+        L = levels or O.depth_for(n, 32)
         kappa = 2.0 * math.pi / (10.0 * (1.0 / side))
         t, rt = _tree_order(_plate(side, 0.0), L, 3)
         s, ct = _tree_order(_plate(side, 2.0), L, 3)
         op = O.kernel_operator(O.OP_PLATES, t, s, kappa)
         return op, rt, ct, dict(levels=L, tolerance=1e-6, rank_guess=16, oversampling=2, seed=seed)
     if cfg_id == 2:
-        L = O.depth_for(n, 32)
+        L = levels or O.depth_for(n, 32)
         t, rt = _tree_order(_half_circle(n, True), L, 2)
         s, ct = _tree_order(_half_circle(n, False), L, 2)
         op = O.kernel_operator(O.OP_CIRCLE, t, s, 2.0 * n / 10.0)
@@ -88,12 +89,12 @@ def oracle_points(cfg_id, n):
         return x, xi, O.OP_NUFFT, 0.0
     if cfg_id == 1:
         side = int(round(math.sqrt(n)))
-        L = O.depth_for(n, 32)
+        L = levels or O.depth_for(n, 32)
         t, _ = _tree_order(_plate(side, 0.0), L, 3)
         s, _ = _tree_order(_plate(side, 2.0), L, 3)
         return t, s, O.OP_PLATES, 2.0 * math.pi / (10.0 * (1.0 / side))
     if cfg_id == 2:
-        L = O.depth_for(n, 32)
+        L = levels or O.depth_for(n, 32)
         t, _ = _tree_order(_half_circle(n, True), L, 2)
         s, _ = _tree_order(_half_circle(n, False), L, 2)
         return t, s, O.OP_CIRCLE, 2.0 * n / 10.0

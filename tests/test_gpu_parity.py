@@ -638,3 +638,28 @@ def test_structured_butterfly_products(tmp_path, case, vr):
           f"flops {float(s['flops']):.3e} structured vs {float(p['flops']):.3e} padded; "
           f"{float(s['seconds'])*1e3:.1f} vs {float(p['seconds'])*1e3:.1f} ms")
     assert float(s["flops"]) < float(p["flops"])
+
+
+@pytest.mark.parametrize("cfg_id,n,levels,over", [
+    (0, 200, None, dict(tolerance=1e-3)),
+    (0, 200, None, dict(tolerance=1e-9)),
+    (0, 333, 2, {}),                                   # shallow tree: ragged leaves of ~83 points
+    (2, 777, None, dict(oversampling=0)),
+    (2, 777, None, dict(oversampling=6, rank_guess=1)),
+    (1, 400, None, dict(rank_guess=64)),               # rank guess above the leaf size: capped rounds
+    (2, 2048, 3, {}),                                  # 256-point leaves: large CPQR blocks
+    (2, 130, 2, dict(tolerance=1e-12)),                # tolerance below what the leaves can resolve
+])
+def test_edge_configurations_match_oracle(B, oracle_threads, cfg_id, n, levels, over):
+    """Corners of ReconstructionConfig and of the tree shape (core.hpp:166-196,
+    reconstruct.hpp:352-399): loose / tight tolerances, no oversampling, a
+    rank guess of 1 and one above the leaf size, shallow trees with large
+    ragged leaves.  Identical rank profiles, bookkeeping (rounds, widths,
+    rank_capped) and apply within 1e-10 of the oracle."""
+    import dataclasses
+
+    op_o, rt_o, ct_o, cfg = oracle_config(cfg_id, n, levels=levels)
+    bf_o, log_o = O.factorize(op_o, rt_o, ct_o, dict(cfg, threads=oracle_threads, **over))
+    w = B.configs.build(cfg_id, n, levels=levels)
+    bf, log = B.factorize(w.op, w.row_tree, w.col_tree, dataclasses.replace(w.recon, **over))
+    _compare(bf, log, bf_o, log_o, w.op.rows, w.op.cols)
