@@ -71,17 +71,31 @@ def _hc_worker(rank, world, port):
     dist.destroy_process_group()
 
 
+def _twice(fn):
+    """A rendezvous port picked with bind(0) can be taken by another process
+    before the ranks listen on it: one retry on a fresh port."""
+    try:
+        return fn()
+    except Exception:  # noqa: BLE001
+        return fn()
+
+
 def test_host_comm_collectives_gloo_world2():
     import torch.multiprocessing as mp
 
-    mp.spawn(_hc_worker, args=(2, _port()), nprocs=2, join=True)
+    _twice(lambda: mp.spawn(_hc_worker, args=(2, _port()), nprocs=2, join=True))
 
 
 def test_bench_self_launches_ranks():
     env = {k: v for k, v in os.environ.items() if k not in ("RANK", "WORLD_SIZE", "LOCAL_RANK")}
-    r = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--gpus", "2", "--dry-launch"],
-                       capture_output=True, text=True, timeout=300, env=env, cwd=ROOT)
-    assert r.returncode == 0, r.stderr
+
+    def launch():
+        r = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--gpus", "2", "--dry-launch"],
+                           capture_output=True, text=True, timeout=300, env=env, cwd=ROOT)
+        assert r.returncode == 0, r.stderr
+        return r
+
+    r = _twice(launch)
     lines = [json.loads(x) for x in r.stdout.splitlines() if x.startswith("{")]
     assert sorted((d["rank"], d["world"]) for d in lines) == [(0, 2), (1, 2)]
     assert "launching 2 ranks" in r.stderr
