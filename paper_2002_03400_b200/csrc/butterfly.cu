@@ -781,17 +781,43 @@ bool DevButterfly<R>::apply_structured(int trans, int plevel, const std::vector<
     nc = cs[j1] - cs[j0];
   };
   struct Stage {
-    int op, M, K, S;
-    const cx<R>* A;
-    int64_t lda, ld_out;
+    int op = 0, M = 0, K = 0, S = 1;
+    const cx<R>* A = nullptr;
+    int64_t lda = 0, ld_out = 0;
     std::vector<GemmEnt> h;
     int maxc = 0;
   };
-  std::vector<Stage> st;
+  // coefficient buffers span every column of the batch
+  DBuf<cx<R>> b0(c, (size_t)(NB * max_p() * wend)), b1(c, (size_t)(NB * max_p() * wend));
+  cx<R>* bufs[2] = {b0.p, b1.p};
+  const cx<R>* in = X;
+  int64_t ldin = ldx;
+  int nlaunched = 0;
+  Stage cur;
+  bool have_cur = false;
+  // a stage is launched as soon as the next one begins (or at the end, as the
+  // final stage writing y): the host plans stage i + 1 while the GPU runs stage i
+  auto flush = [&](bool final) {
+    if (!have_cur) return;
+    cx<R>* out = final ? y : bufs[nlaunched % 2];
+    const int64_t ldout = final ? ldy : cur.ld_out;
+    if (!cur.h.empty()) {
+      DBuf<GemmEnt> de = to_device(c, cur.h);
+      launch_bgemm<R>(c, cur.op, cur.M, cur.K, cur.S, cur.A, cur.lda, in, ldin, out, ldout, de.p, (int)cur.h.size(),
+                      cur.maxc, false, 0, true);
+    }
+    in = out;
+    ldin = ldout;
+    ++nlaunched;
+    have_cur = false;
+  };
   double flops = 0;
   auto add = [&](int op, int M, int K, int S, const Level<R>& lv, int64_t ld_out) -> Stage& {
-    st.push_back(Stage{op, M, K, S, lv.data.p, lv.ld, ld_out, {}, 0});
-    return st.back();
+    flush(false);
+    cur = Stage();
+    cur.op = op; cur.M = M; cur.K = K; cur.S = S; cur.A = lv.data.p; cur.lda = lv.ld; cur.ld_out = ld_out;
+    have_cur = true;
+    return cur;
   };
   // a0/a1/b0/b1/c: element offsets without the window; the window's first
   // column is added to the coefficient operands (ld_in) and the output (ld_out)
@@ -970,26 +996,7 @@ bool DevButterfly<R>::apply_structured(int trans, int plevel, const std::vector<
                wend - cs[0], ld_in, ldy, (double)ct.size(L, nu) * vleaf.ranks[nu]);
     }
   }
-  // coefficient buffers span every column of the batch
-  const int64_t kall = wend;
-  DBuf<cx<R>> b0(c, (size_t)(NB * max_p() * kall)), b1(c, (size_t)(NB * max_p() * kall));
-  cx<R>* bufs[2] = {b0.p, b1.p};
-  const cx<R>* in = X;
-  int64_t ldin = ldx;
-  const int n = (int)st.size();
-  for (int i = 0; i < n; ++i) {
-    Stage& d = st[i];
-    const bool final = i == n - 1;
-    cx<R>* out = final ? y : bufs[i % 2];
-    const int64_t ldout = final ? ldy : d.ld_out;
-    if (!d.h.empty()) {
-      DBuf<GemmEnt> de = to_device(c, d.h);
-      launch_bgemm<R>(c, d.op, d.M, d.K, d.S, d.A, d.lda, in, ldin, out, ldout, de.p, (int)d.h.size(), d.maxc, false,
-                      0, true);
-    }
-    in = out;
-    ldin = ldout;
-  }
+  flush(true);
   if (flops_done) *flops_done = flops;
   return true;
 }
