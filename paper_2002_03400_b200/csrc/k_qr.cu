@@ -541,8 +541,10 @@ __global__ void __launch_bounds__(QR_THREADS) core_fit_kernel(const cx<R>* __res
                                                               const cx<R>* __restrict__ Cf, int64_t ldc,
                                                               cx<R>* __restrict__ B, int64_t ldb, int bcap,
                                                               const CoreEnt* __restrict__ ents, cx<R>* scratch,
-                                                              int64_t scratch_stride, bool literal, int32_t* err_flag) {
+                                                              int64_t scratch_stride, bool literal, int32_t* err_flag,
+                                                              int use_smem) {
   using V = cx<R>;
+  extern __shared__ __align__(16) unsigned char cf_smem[];
   const CoreEnt e = ents[blockIdx.x];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int ku = e.ku, kv = e.kv, w = e.w;
@@ -555,10 +557,15 @@ __global__ void __launch_bounds__(QR_THREADS) core_fit_kernel(const cx<R>* __res
   }
   if (ku == 0 || kv == 0) return;
   V* proj = scratch + blockIdx.x * scratch_stride;  // ku x w
-  V* A = proj + (int64_t)ku * w;                    // w x kvp (coeff^H)
   const int kvp = kv + (kv & 1);
-  V* Vm = A + (int64_t)w * kvp;                     // kvp x kvp
-  V* T = Vm + (int64_t)kvp * kvp;                   // ku x kvp
+  // the Jacobi operands (coeff^H: w x kvp, and V: kvp x kvp) live in shared
+  // memory when they fit (use_smem): every rotation is then a shared-memory
+  // round trip instead of an L2 one; results are the same either way
+  V* Ag = proj + (int64_t)ku * w;
+  V* Vg = Ag + (int64_t)w * kvp;
+  V* T = Vg + (int64_t)kvp * kvp;  // ku x kvp
+  V* A = use_smem ? reinterpret_cast<V*>(cf_smem) : Ag;
+  V* Vm = use_smem ? A + (int64_t)w * kvp : Vg;
   R* sv = reinterpret_cast<R*>(T + (int64_t)ku * kvp);
   __syncthreads();
   // proj = Q^H z
@@ -613,13 +620,17 @@ __global__ void __launch_bounds__(QR_THREADS) core_fit_kernel(const cx<R>* __res
         beta = warp_sum(beta);
         g.x = warp_sum(g.x);
         g.y = warp_sum(g.y);
-        R gm = sqrt(cabs2(g));
-        if (gm == R(0) || gm <= QrTraits<R>::jacobi_tol * sqrt(alpha * beta)) continue;
+        // every lane runs this scalar chain, so it is written with reciprocal
+        // square roots: 2 rsqrt + 1 sqrt + 1 division (it was 3 sqrt + 5
+        // divisions, and the FP64 pipe was the bound of config 4's 4096 fits)
+        const R g2 = cabs2(g);
+        if (g2 == R(0) || g2 <= QrTraits<R>::jacobi_tol * QrTraits<R>::jacobi_tol * (alpha * beta)) continue;
         if (lane == 0) s_rot = 1;
-        V ph = mkc<R>(g.x / gm, -g.y / gm);  // conj(e^{i phi})
-        R zeta = (beta - alpha) / (R(2) * gm);
+        const R ig = rsqrt(g2);                // 1 / |g|
+        V ph = mkc<R>(g.x * ig, -g.y * ig);    // conj(e^{i phi})
+        R zeta = (beta - alpha) * (R(0.5) * ig);
         R t = (zeta >= R(0) ? R(1) : R(-1)) / (fabs(zeta) + sqrt(R(1) + zeta * zeta));
-        R cs = R(1) / sqrt(R(1) + t * t);
+        R cs = rsqrt(R(1) + t * t);
         R sn = cs * t;
         for (int i = lane; i < w; i += 32) {
           V x = ap[i], y = cmul(aq[i], ph);
@@ -740,12 +751,24 @@ void launch_core_fit(Ctx* c, const cx<R>* Q, int64_t ldq, const cx<R>* Z, int64_
   int64_t stride = (int64_t)max_ku * max_w + (int64_t)max_w * kvp + (int64_t)kvp * kvp + (int64_t)max_ku * kvp + kvp + 8;
   DBuf<cx<R>> scratch(c, (size_t)stride * nent);
   KTimer timer(c, "core_fit", 0.0, 0.0);
-  if (max_kv >= 64)
-    core_fit_kernel<R, QR_BIG><<<nent, QR_BIG, 0, c->stream>>>(Q, ldq, Z, ldz, Cf, ldc, B, ldb, bcap, ents, scratch.p,
-                                                                 stride, literal, err_flag);
-  else
-    core_fit_kernel<R, QR_SMALL><<<nent, QR_SMALL, 0, c->stream>>>(Q, ldq, Z, ldz, Cf, ldc, B, ldb, bcap, ents, scratch.p,
-                                                                     stride, literal, err_flag);
+  // Jacobi operands in shared memory when they fit (BFLY_COREFIT_SMEM=0: global scratch);
+  // one warp per column pair of a round: 8 / 16 / 32 warps by the pair count
+  static const bool smem_off = std::getenv("BFLY_COREFIT_SMEM") && std::atoi(std::getenv("BFLY_COREFIT_SMEM")) == 0;
+  const size_t jbytes = sizeof(cx<R>) * ((size_t)max_w * kvp + (size_t)kvp * kvp);
+  const int use_smem = !smem_off && !literal && jbytes <= 200 * 1024;
+  const int npair = kvp / 2;
+#define CF_LAUNCH(NTV)                                                                                              \
+  do {                                                                                                              \
+    auto kern = core_fit_kernel<R, NTV>;                                                                            \
+    if (use_smem && jbytes > 48 * 1024)                                                                             \
+      BFLY_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)jbytes));              \
+    kern<<<nent, NTV, use_smem ? jbytes : 0, c->stream>>>(Q, ldq, Z, ldz, Cf, ldc, B, ldb, bcap, ents, scratch.p, stride, \
+                                                          literal, err_flag, use_smem);                             \
+  } while (0)
+  if (use_smem && npair > 16) CF_LAUNCH(1024);
+  else if (max_kv >= 64 || (use_smem && npair > 8)) CF_LAUNCH(QR_BIG);
+  else CF_LAUNCH(QR_SMALL);
+#undef CF_LAUNCH
   BFLY_LAUNCH_CHECK("core_fit");
 }
 
