@@ -27,6 +27,27 @@ namespace {
 // (config 4), 512 for saturated ones (more warps on the per-column work)
 constexpr int QR_TINY = 128, QR_SMALL = 256, QR_BIG = 512;
 
+// four warp sums at once, every lane receiving all four: the halves of the
+// warp trade the values they do not keep (4 -> 2 -> 1 value per lane), three
+// more butterfly steps, four broadcasts: 10 shuffles instead of 20
+template <typename T> __device__ __forceinline__ void warp_sum4(T& a, T& b, T& c, T& d) {
+  const int lane = threadIdx.x & 31;
+  const bool hi = lane & 16;
+  T k0 = hi ? c : a, k1 = hi ? d : b;
+  k0 += __shfl_xor_sync(0xffffffffu, hi ? a : c, 16);
+  k1 += __shfl_xor_sync(0xffffffffu, hi ? b : d, 16);
+  const bool h8 = lane & 8;
+  T k = h8 ? k1 : k0;
+  k += __shfl_xor_sync(0xffffffffu, h8 ? k0 : k1, 8);
+  k += __shfl_xor_sync(0xffffffffu, k, 4);
+  k += __shfl_xor_sync(0xffffffffu, k, 2);
+  k += __shfl_xor_sync(0xffffffffu, k, 1);
+  a = __shfl_sync(0xffffffffu, k, 0);
+  b = __shfl_sync(0xffffffffu, k, 8);
+  c = __shfl_sync(0xffffffffu, k, 16);
+  d = __shfl_sync(0xffffffffu, k, 24);
+}
+
 template <typename T> __device__ __forceinline__ T warp_sum(T v) {
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
@@ -604,8 +625,13 @@ __global__ void __launch_bounds__(QR_THREADS) core_fit_kernel(const cx<R>* __res
     for (int round = 0; round < kvp - 1; ++round) {
       for (int pi = warp; pi < npair; pi += (QR_THREADS / 32)) {
         // round-robin tournament: position 0 fixed, others rotate
-        int a = (pi == 0) ? 0 : 1 + (pi - 1 + round) % (kvp - 1);
-        int b = 1 + (kvp - 2 - pi + round) % (kvp - 1);
+        // (both arguments of the rotation lie in [0, 2 (kvp - 1)): a conditional
+        // subtract instead of two integer divisions per pair)
+        int ra = pi - 1 + round, rb = kvp - 2 - pi + round;
+        if (ra >= kvp - 1) ra -= kvp - 1;
+        if (rb >= kvp - 1) rb -= kvp - 1;
+        int a = (pi == 0) ? 0 : 1 + ra;
+        int b = 1 + rb;
         int p = min(a, b), q = max(a, b);
         V* ap = A + (int64_t)p * w;
         V* aq = A + (int64_t)q * w;
@@ -616,10 +642,7 @@ __global__ void __launch_bounds__(QR_THREADS) core_fit_kernel(const cx<R>* __res
           beta += cabs2(aq[i]);
           cfma_conj(g, ap[i], aq[i]);
         }
-        alpha = warp_sum(alpha);
-        beta = warp_sum(beta);
-        g.x = warp_sum(g.x);
-        g.y = warp_sum(g.y);
+        warp_sum4(alpha, beta, g.x, g.y);
         // every lane runs this scalar chain, so it is written with reciprocal
         // square roots: 2 rsqrt + 1 sqrt + 1 division (it was 3 sqrt + 5
         // divisions, and the FP64 pipe was the bound of config 4's 4096 fits)
