@@ -89,12 +89,12 @@ def oracle_points(cfg_id, n):
         return x, xi, O.OP_NUFFT, 0.0
     if cfg_id == 1:
         side = int(round(math.sqrt(n)))
-        L = levels or O.depth_for(n, 32)
+        L = O.depth_for(n, 32)
         t, _ = _tree_order(_plate(side, 0.0), L, 3)
         s, _ = _tree_order(_plate(side, 2.0), L, 3)
         return t, s, O.OP_PLATES, 2.0 * math.pi / (10.0 * (1.0 / side))
     if cfg_id == 2:
-        L = levels or O.depth_for(n, 32)
+        L = O.depth_for(n, 32)
         t, _ = _tree_order(_half_circle(n, True), L, 2)
         s, _ = _tree_order(_half_circle(n, False), L, 2)
         return t, s, O.OP_CIRCLE, 2.0 * n / 10.0
