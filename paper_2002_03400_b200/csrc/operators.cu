@@ -189,7 +189,12 @@ struct ButterflyOp : DevOp<R> {
     }
     std::sort(ps.begin(), ps.end(), [](const auto& a, const auto& b) { return a.node < b.node; });
     double fl = 0;
-    if (!bf->apply_structured(mode, p, ps, Xs, ld, Y, ldy, o0, o1, &fl)) return false;
+    LeafProj<R>* lp = this->cur_lp;
+    bool used = false;
+    if (!bf->apply_structured(mode, p, ps, Xs, ld, Y, ldy, o0, o1, &fl, lp ? lp->leaf : nullptr, lp ? lp->tree : nullptr,
+                              lp ? lp->C : nullptr, lp ? lp->ldc : 0, &used))
+      return false;
+    if (lp) lp->done = used;
     this->flops += fl;
     return true;
   }

@@ -19,6 +19,22 @@
 
 namespace bfly {
 
+// A transfer level needs only the leaf coefficients of a product in the NEW
+// factorization's leaf bases, L_nu^H (op(A) X)[leaf nu] (the first step of the
+// partial V / U chain, butterfly.hpp:330-354).  A kind that can fuse this
+// projection into its own last stage (the butterfly black box: its leaf
+// stage and the projection collapse into one P x P block per leaf) writes
+// the coefficients straight into the chain buffer C (slot nu at nu * P, ld
+// ldc, same columns as Y) and sets done; Y is then not written.
+template <typename R>
+struct LeafProj {
+  const Level<R>* leaf = nullptr;  // the factorization's leaf level on the output side
+  const Tree* tree = nullptr;      // its tree
+  cx<R>* C = nullptr;
+  int64_t ldc = 0;
+  bool done = false;
+};
+
 template <typename R>
 struct DevOp {
   int kind = 0;
@@ -43,8 +59,9 @@ struct DevOp {
   // [o0, o1) restricts the output rows that must be produced (the rank's
   // leaves in a sharded leaf phase); kinds that cannot restrict compute all.
   // count_cols >= 0 overrides the columns added to the counters
+  LeafProj<R>* cur_lp = nullptr;  // the running apply_segs' projection request
   void apply_segs(int mode, const cx<R>* X, const std::vector<MatvecSeg>& segs, cx<R>* Y, int64_t ldy,
-                  int64_t o0 = 0, int64_t o1 = -1, int64_t count_cols = -1) {
+                  int64_t o0 = 0, int64_t o1 = -1, int64_t count_cols = -1, LeafProj<R>* lp = nullptr) {
     int64_t cols = 0;
     for (const auto& s : segs) cols += s.ncols;
     if (count_cols >= 0) cols = count_cols;
@@ -52,7 +69,9 @@ struct DevOp {
     else tr += cols;
     if (o1 < 0) o1 = out_dim(mode);
     last_restricted = restricts_rows();
+    cur_lp = lp;
     do_apply(mode, X, segs, Y, ldy, o0, o1);
+    cur_lp = nullptr;
   }
   void apply_dense(int mode, const cx<R>* X, int64_t ldx, cx<R>* Y, int64_t ldy, int64_t k) {
     MatvecSeg s{0, in_dim(mode), 0, ldx, 0, (int32_t)k, 0};

@@ -1,10 +1,11 @@
 """Worker of test_structured_butterfly_products (not collected by pytest).
 
 Recompresses a butterfly operator over its own trees and writes the result.
-The parent runs it twice -- with and without BFLY_NO_STRUCT_APPLY -- so the
-structured products (DevButterfly::apply_structured: blocks the probes' zero
-rows cannot reach are skipped) are compared with the reference's padded
-products (reconstruct.hpp:72-85) on the same seeds.
+The parent runs it with BFLY_NO_STRUCT_APPLY (the reference's padded products,
+reconstruct.hpp:72-85), with BFLY_NO_LEAF_FUSE (structured products:
+DevButterfly::apply_structured skips the blocks the probes' zero rows cannot
+reach) and with neither (structured, the chain's leaf projection fused into
+the black box's last stage), on the same seeds.
 """
 import argparse
 import os
