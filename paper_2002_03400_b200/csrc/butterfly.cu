@@ -739,10 +739,9 @@ void DevButterfly<R>::apply_h(const cx<R>* yt, int64_t ldy, cx<R>* xt, int64_t l
 template <typename R>
 bool DevButterfly<R>::apply_structured(int trans, int plevel, const std::vector<ProbeSeg>& segs, const cx<R>* X,
                                        int64_t ldx, cx<R>* y, int64_t ldy, int64_t o0, int64_t o1,
-                                       double* flops_done, const Level<R>* proj_leaf, const Tree* proj_tree,
-                                       cx<R>* proj_c, int64_t proj_ldc, bool* proj_used) {
+                                       double* flops_done, const Level<R>* G, int glevel, cx<R>* proj_c,
+                                       int64_t proj_ldc) {
   Ctx* c = ctx;
-  if (proj_used) *proj_used = false;
   if ((trans != OP_N && trans != OP_H) || !rt.identity || !ct.identity) return false;
   if (plevel < 0 || plevel > L || segs.empty()) return false;
   const bool fwd = trans == OP_N;
@@ -750,12 +749,10 @@ bool DevButterfly<R>::apply_structured(int trans, int plevel, const std::vector<
   const Tree& ot = fwd ? rt : ct;
   const int p = plevel;
   const int64_t NP = int64_t(1) << p, NB = nb();
-  // fused leaf projection: the other butterfly's leaves must be this one's
-  static const bool no_fuse = std::getenv("BFLY_NO_LEAF_FUSE") != nullptr;
-  const Level<R>& oleaf = fwd ? uleaf : vleaf;
-  const bool proj = !no_fuse && proj_leaf && proj_tree && proj_c && proj_tree->identity && proj_tree->levels == ot.levels &&
-                    (int)proj_tree->ranges.size() > L && proj_tree->ranges[L] == ot.ranges[L] &&
-                    proj_leaf->ld >= ot.max_size(L) && proj_leaf->P > 0 && oleaf.P > 0;
+  // basis projection at level glevel (see butterfly.h): V side levels 0..lm-1
+  // for OP_H products, U side levels lm+1..L for OP_N products
+  const bool proj = G != nullptr && proj_c != nullptr && (fwd ? (glevel > lm && glevel <= L) : (glevel >= 0 && glevel < lm));
+  if (G && !proj) return false;
   // cs[j]: first column of probe node j (absent probes have zero width)
   std::vector<int64_t> cs(NP + 1, -1), xo(NP, -1);
   {
@@ -839,22 +836,6 @@ bool DevButterfly<R>::apply_structured(int trans, int plevel, const std::vector<
     flops += 8.0 * nz * (double)nc;
   };
   const int BIG = 1 << 30;
-  // G = proj_leaf^H leaf, one P_new x P block per output leaf (built per call:
-  // the other butterfly's leaf bases belong to a factorization in progress)
-  Level<R> gproj;
-  auto project_leaves = [&](const Level<R>& lf, const Tree& tr) {
-    gproj.alloc(c, NB, proj_leaf->P, lf.P);
-    gproj.data.zero();
-    std::vector<GemmEnt> ge;
-    for (int64_t t = 0; t < NB; ++t) {
-      GemmEnt e = ent(t * proj_leaf->stride(), 0, t * lf.stride(), 0, t * gproj.stride(), BIG, (int)tr.size(L, t));
-      e.ncols = lf.P;
-      ge.push_back(e);
-    }
-    DBuf<GemmEnt> de = to_device(c, ge);
-    launch_bgemm<R>(c, OP_H, proj_leaf->P, (int)proj_leaf->ld, 1, proj_leaf->data.p, proj_leaf->ld, lf.data.p, lf.ld,
-                    gproj.data.p, gproj.ld, de.p, (int)ge.size(), lf.P, false, lf.P);
-  };
   int64_t c0, nc;
   if (fwd) {
     {  // V leaves: coefficients of the probes' own rows
@@ -904,7 +885,7 @@ bool DevButterfly<R>::apply_structured(int trans, int plevel, const std::vector<
              (double)b.rows[i] * b.ranks[i]);
       }
     }
-    for (int l = lm; l < L; ++l) {
+    for (int l = lm; l < (proj ? glevel : L); ++l) {
       const Level<R>& rl = r[l - lm];
       const int q = L - l - 1;  // column level of the outputs
       const bool shared = q >= p;
@@ -930,14 +911,18 @@ bool DevButterfly<R>::apply_structured(int trans, int plevel, const std::vector<
           }
         }
     }
-    if (proj) {  // U leaves folded with the other butterfly's: G_tau = proj_leaf_tau^H U_tau
-      project_leaves(uleaf, rt);
-      Stage& d = add(OP_N, proj_leaf->P, PU(L), 1, gproj, 0);
-      const int64_t ld_in = NB * PU(L);
-      for (int64_t tau = 0; tau < NB; ++tau)
-        if (need(L, tau))
-          push(d, tau * gproj.stride(), 0, tau * PU(L), 0, tau * proj_leaf->P, BIG, BIG, cs[0], wend - cs[0], ld_in,
-               proj_ldc, (double)proj_leaf->ranks[tau] * uleaf.ranks[tau]);
+    if (proj) {  // coefficients in the other butterfly's U basis of level glevel
+      const int t = glevel, q = L - t;
+      Stage& d = add(OP_N, G->P, PU(t), 1, *G, 0);
+      const int64_t ld_in = NB * PU(t);
+      for (int64_t tp = 0; tp < (int64_t(1) << t); ++tp)
+        for (int64_t np = 0; np < (int64_t(1) << q); ++np) {
+          if (!need(t, tp)) continue;
+          const int64_t i = bidx(L, t, tp, np);
+          win(q, np, c0, nc);
+          push(d, i * G->stride(), 0, i * PU(t), 0, tp * G->P, BIG, BIG, c0, nc, ld_in, proj_ldc,
+               (double)G->ranks[i] * G->rows[i]);
+        }
     } else {  // U leaves: every probe reaches every row
       Stage& d = add(OP_N, (int)uleaf.ld, PU(L), 1, uleaf, 0);
       const int64_t ld_in = NB * PU(L);
@@ -994,7 +979,7 @@ bool DevButterfly<R>::apply_structured(int trans, int plevel, const std::vector<
              (double)b.rows[i] * b.ranks[i]);
       }
     }
-    for (int l = lm; l >= 1; --l) {
+    for (int l = lm; l >= (proj ? glevel + 1 : 1); --l) {
       const Level<R>& wl = w[l - 1];
       const bool shared = l - 1 >= p;  // the outputs' row level
       const int64_t ld_in = NB * PV(l);
@@ -1019,14 +1004,18 @@ bool DevButterfly<R>::apply_structured(int trans, int plevel, const std::vector<
           }
         }
     }
-    if (proj) {  // V leaves folded with the other butterfly's: G_nu = proj_leaf_nu^H V_nu
-      project_leaves(vleaf, ct);
-      Stage& d = add(OP_N, proj_leaf->P, PV(0), 1, gproj, 0);
-      const int64_t ld_in = NB * PV(0);
-      for (int64_t nu = 0; nu < NB; ++nu)
-        if (need(L, nu))
-          push(d, nu * gproj.stride(), 0, nu * PV(0), 0, nu * proj_leaf->P, BIG, BIG, cs[0], wend - cs[0], ld_in,
-               proj_ldc, (double)proj_leaf->ranks[nu] * vleaf.ranks[nu]);
+    if (proj) {  // coefficients in the other butterfly's V basis of level glevel
+      const int t = glevel, q = L - t;
+      Stage& d = add(OP_N, G->P, PV(t), 1, *G, 0);
+      const int64_t ld_in = NB * PV(t);
+      for (int64_t tt = 0; tt < (int64_t(1) << t); ++tt)
+        for (int64_t nu = 0; nu < (int64_t(1) << q); ++nu) {
+          if (!need(q, nu)) continue;
+          const int64_t i = bidx(L, t, tt, nu);
+          win(t, tt, c0, nc);
+          push(d, i * G->stride(), 0, i * PV(t), 0, nu * G->P, BIG, BIG, c0, nc, ld_in, proj_ldc,
+               (double)G->ranks[i] * G->rows[i]);
+        }
     } else {  // V leaves: every probe reaches every column point
       Stage& d = add(OP_N, (int)vleaf.ld, PV(0), 1, vleaf, 0);
       const int64_t ld_in = NB * PV(0);
@@ -1038,7 +1027,6 @@ bool DevButterfly<R>::apply_structured(int trans, int plevel, const std::vector<
   }
   flush(true);
   if (flops_done) *flops_done = flops;
-  if (proj_used) *proj_used = proj;
   return true;
 }
 

@@ -126,17 +126,19 @@ struct DevButterfly {
   // [o0, o1) (output tree order; o1 < 0: all) are the output rows that must be
   // produced: blocks whose output-side node holds none of them are skipped
   // too (a probe split across ranks needs only its partner nodes' rows).
-  // proj_leaf / proj_tree / proj_c / proj_ldc (optional): instead of y, write
-  // the product's leaf coefficients in another butterfly's leaf bases on the
-  // output side, proj_leaf_nu^H y[leaf nu], at proj_c + nu * P (ld proj_ldc):
-  // the last stage then multiplies G_nu = proj_leaf_nu^H leaf_nu (P x P, one
-  // small GEMM per leaf and call) instead of the leaf basis, and the caller's
-  // projection GEMM disappears.  *proj_used tells whether that was done
-  // (same leaf ranges required; otherwise y is written as usual).
+  // G / glevel / proj_c / proj_ldc (optional): instead of y, write the
+  // product's coefficients in ANOTHER butterfly's nested basis of level
+  // glevel on the output side (V side for OP_H, U side for OP_N).  With
+  // G(tau,nu) = B_other(glevel,tau,nu)^H B_this(glevel,tau,nu) (P_other x P_this
+  // per block; G.ranks = the other's ranks, G.rows = this one's) the chain
+  // stops at level glevel -- the stages between it and the leaves, the
+  // leaf stage and the caller's whole projection chain back up disappear --
+  // and block (tau,nu) writes G c into slot nu (OP_H) / tau (OP_N) of proj_c
+  // (P_other rows per slot, ld proj_ldc, same columns as y).  The caller
+  // guarantees both butterflies share trees and centre level.
   bool apply_structured(int trans, int plevel, const std::vector<ProbeSeg>& segs, const cx<R>* X, int64_t ldx,
                         cx<R>* y, int64_t ldy, int64_t o0, int64_t o1, double* flops_done,
-                        const Level<R>* proj_leaf = nullptr, const Tree* proj_tree = nullptr, cx<R>* proj_c = nullptr,
-                        int64_t proj_ldc = 0, bool* proj_used = nullptr);
+                        const Level<R>* G = nullptr, int glevel = 0, cx<R>* proj_c = nullptr, int64_t proj_ldc = 0);
   int64_t nnz() const;
   int64_t max_rank() const;
   double apply_flops(int64_t k) const;   // 8 * nnz * k (complex)

@@ -64,6 +64,7 @@ class Factorizer {
   // (BFLY_VRANK_TIMING=1 with virtual ranks; diagnostics for a scaling
   // projection, see vrank_table())
   bool vr_timing_ = false;
+  uint64_t gen_ = 0;  // distinct per Factorizer (operators cache per-factorization state by it)
   struct VrTimer {
     Factorizer* f;
     int rank;

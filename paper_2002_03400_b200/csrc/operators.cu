@@ -131,6 +131,9 @@ struct ButterflyOp : DevOp<R> {
       this->last_restricted = true;
       return;
     }
+    // a basis projection was expected (LeafProj) and no product buffer came
+    // along: nothing is computed, the caller multiplies again the plain way
+    if (!Y) return;
     for (const auto& run : column_runs(segs)) {
       int64_t c0 = 0, w = 0;
       DBuf<cx<R>> xp = this->pad_probes(mode, X, run, c0, w);
@@ -138,6 +141,138 @@ struct ButterflyOp : DevOp<R> {
       bf->apply(mode, xp.p, this->in_dim(mode), Y + c0 * ldy, ldy, w);
       this->flops += bf->apply_flops(w);
     }
+  }
+  // G levels of the factorization in progress (LeafProj, operators.h), built
+  // level by level as its transfer levels complete:
+  //   V side: G(0) = Vn_leaf^H V_leaf;  G(j) = Wn_j^H blockdiag(G(j-1) children) W_j
+  //   U side: G(L) = Un_leaf^H U_leaf;  G(j) = Rn_j^H blockdiag(G(j+1) children) R_j
+  // (n = the new butterfly).  Two batched GEMMs per level.
+  const DevButterfly<R>* g_owner = nullptr;
+  uint64_t g_gen = 0;
+  std::vector<std::unique_ptr<Level<R>>> gv, gu;  // gv[j] = level j; gu[k] = level L - k
+  bool can_project(int mode, const LeafProj<R>& lp) override {
+    static const bool off = std::getenv("BFLY_NO_STRUCT_APPLY") != nullptr;
+    return !off && basis_product(mode, lp) != nullptr;
+  }
+  const Level<R>* basis_product(int mode, const LeafProj<R>& lp) {
+    static const bool off = std::getenv("BFLY_NO_LEAF_FUSE") != nullptr;
+    const DevButterfly<R>* nb = lp.nbf;
+    if (off || !nb || !lp.C) return nullptr;
+    const int L = bf->L, lm = bf->lm;
+    if (nb->L != L || nb->lm != lm || !nb->rt.identity || !nb->ct.identity || !bf->rt.identity || !bf->ct.identity ||
+        nb->rt.ranges != bf->rt.ranges || nb->ct.ranges != bf->ct.ranges)
+      return nullptr;
+    if (g_owner != nb || g_gen != lp.gen) {
+      gv.clear();
+      gu.clear();
+      g_owner = nb;
+      g_gen = lp.gen;
+    }
+    Ctx* c = this->ctx;
+    const int64_t NB = bf->nb();
+    const int BIG = 1 << 30;
+    auto gent = [](int64_t a0, int64_t b0, int64_t cc, int krows) {
+      GemmEnt e{};
+      e.a0 = a0; e.b0 = b0; e.c = cc;
+      e.mrows = 1 << 30; e.krows = krows;
+      return e;
+    };
+    auto gemm = [&](int op, int M, int K, const cx<R>* A, int64_t lda, const cx<R>* B, int64_t ldb, cx<R>* C,
+                    int64_t ldc, std::vector<GemmEnt>& e, int ncols) {
+      if (e.empty() || M <= 0 || K <= 0 || ncols <= 0) return;
+      for (auto& x : e) x.ncols = ncols;
+      DBuf<GemmEnt> de = to_device(c, e);
+      launch_bgemm<R>(c, op, M, K, 1, A, lda, B, ldb, C, ldc, de.p, (int)e.size(), ncols, false, ncols);
+    };
+    auto fresh = [&](int Pn, int Pi) {
+      auto lv = std::make_unique<Level<R>>();
+      lv->alloc(c, NB, std::max(Pn, 1), std::max(Pi, 1));
+      lv->P = Pn;
+      lv->data.zero();
+      return lv;
+    };
+    if (mode == OP_H) {  // V side
+      if (lp.level < 0 || lp.level >= lm) return nullptr;
+      while ((int)gv.size() <= lp.level) {
+        const int j = (int)gv.size();
+        const int Pn = nb->PV(j), Pi = bf->PV(j);
+        if (Pn <= 0 || Pi <= 0) return nullptr;
+        auto g = fresh(Pn, Pi);
+        std::vector<GemmEnt> e;
+        if (j == 0) {
+          if (nb->vleaf.ld < bf->ct.max_size(L)) return nullptr;
+          for (int64_t nu = 0; nu < NB; ++nu)
+            e.push_back(gent(nu * nb->vleaf.stride(), nu * bf->vleaf.stride(), nu * g->stride(), (int)bf->ct.size(L, nu)));
+          gemm(OP_H, Pn, (int)nb->vleaf.ld, nb->vleaf.data.p, nb->vleaf.ld, bf->vleaf.data.p, bf->vleaf.ld, g->data.p,
+               g->ld, e, Pi);
+        } else {
+          const Level<R>&wi = bf->w[j - 1], &wn = nb->w[j - 1], &gp = *gv[j - 1];
+          const int Pnp = nb->PV(j - 1), Pip = bf->PV(j - 1);
+          DBuf<cx<R>> T(c, (size_t)(NB * 2 * Pnp * std::max(Pi, 1)));
+          T.zero();
+          const int64_t tst = (int64_t)2 * Pnp * Pi;
+          for (int64_t tau = 0; tau < (int64_t(1) << j); ++tau)
+            for (int64_t nu = 0; nu < (int64_t(1) << (L - j)); ++nu) {
+              const int64_t i = bidx(L, j, tau, nu);
+              for (int h = 0; h < 2; ++h)
+                e.push_back(gent(bidx(L, j - 1, tau / 2, 2 * nu + h) * gp.stride(), i * wi.stride() + h * wi.gap,
+                                 i * tst + h * Pnp, BIG));
+            }
+          gemm(OP_N, Pnp, Pip, gp.data.p, gp.ld, wi.data.p, wi.ld, T.p, 2 * Pnp, e, Pi);
+          std::vector<GemmEnt> e2;
+          for (int64_t i = 0; i < NB; ++i) e2.push_back(gent(i * wn.stride(), i * tst, i * g->stride(), BIG));
+          gemm(OP_H, Pn, 2 * Pnp, wn.data.p, wn.ld, T.p, 2 * Pnp, g->data.p, g->ld, e2, Pi);
+        }
+        for (int64_t tau = 0; tau < (int64_t(1) << j); ++tau)
+          for (int64_t nu = 0; nu < (int64_t(1) << (L - j)); ++nu) {
+            const int64_t i = bidx(L, j, tau, nu);
+            g->ranks[i] = nb->v_rank(j, tau, nu);
+            g->rows[i] = bf->v_rank(j, tau, nu);
+          }
+        gv.push_back(std::move(g));
+      }
+      return gv[lp.level].get();
+    }
+    if (mode != OP_N || lp.level <= lm || lp.level > L) return nullptr;
+    while ((int)gu.size() <= L - lp.level) {  // U side
+      const int j = L - (int)gu.size();
+      const int Pn = nb->PU(j), Pi = bf->PU(j);
+      if (Pn <= 0 || Pi <= 0) return nullptr;
+      auto g = fresh(Pn, Pi);
+      std::vector<GemmEnt> e;
+      if (j == L) {
+        if (nb->uleaf.ld < bf->rt.max_size(L)) return nullptr;
+        for (int64_t tau = 0; tau < NB; ++tau)
+          e.push_back(gent(tau * nb->uleaf.stride(), tau * bf->uleaf.stride(), tau * g->stride(), (int)bf->rt.size(L, tau)));
+        gemm(OP_H, Pn, (int)nb->uleaf.ld, nb->uleaf.data.p, nb->uleaf.ld, bf->uleaf.data.p, bf->uleaf.ld, g->data.p,
+             g->ld, e, Pi);
+      } else {
+        const Level<R>&ri = bf->r[j - lm], &rn = nb->r[j - lm], &gp = *gu[L - (j + 1)];
+        const int Pnp = nb->PU(j + 1), Pip = bf->PU(j + 1);
+        DBuf<cx<R>> T(c, (size_t)(NB * 2 * Pnp * std::max(Pi, 1)));
+        T.zero();
+        const int64_t tst = (int64_t)2 * Pnp * Pi;
+        for (int64_t tau = 0; tau < (int64_t(1) << j); ++tau)
+          for (int64_t nu = 0; nu < (int64_t(1) << (L - j)); ++nu) {
+            const int64_t i = bidx(L, j, tau, nu);
+            for (int h = 0; h < 2; ++h)
+              e.push_back(gent(bidx(L, j + 1, 2 * tau + h, nu / 2) * gp.stride(), i * ri.stride() + h * ri.gap,
+                               i * tst + h * Pnp, BIG));
+          }
+        gemm(OP_N, Pnp, Pip, gp.data.p, gp.ld, ri.data.p, ri.ld, T.p, 2 * Pnp, e, Pi);
+        std::vector<GemmEnt> e2;
+        for (int64_t i = 0; i < NB; ++i) e2.push_back(gent(i * rn.stride(), i * tst, i * g->stride(), BIG));
+        gemm(OP_H, Pn, 2 * Pnp, rn.data.p, rn.ld, T.p, 2 * Pnp, g->data.p, g->ld, e2, Pi);
+      }
+      for (int64_t tau = 0; tau < (int64_t(1) << j); ++tau)
+        for (int64_t nu = 0; nu < (int64_t(1) << (L - j)); ++nu) {
+          const int64_t i = bidx(L, j, tau, nu);
+          g->ranks[i] = nb->u_rank(j, tau, nu);
+          g->rows[i] = bf->u_rank(j, tau, nu);
+        }
+      gu.push_back(std::move(g));
+    }
+    return gu[L - lp.level].get();
   }
   // Probes supported on the nodes of one level of this butterfly's own
   // input-side tree (a recompression over the same trees): blocks the zero
@@ -190,11 +325,14 @@ struct ButterflyOp : DevOp<R> {
     std::sort(ps.begin(), ps.end(), [](const auto& a, const auto& b) { return a.node < b.node; });
     double fl = 0;
     LeafProj<R>* lp = this->cur_lp;
-    bool used = false;
-    if (!bf->apply_structured(mode, p, ps, Xs, ld, Y, ldy, o0, o1, &fl, lp ? lp->leaf : nullptr, lp ? lp->tree : nullptr,
-                              lp ? lp->C : nullptr, lp ? lp->ldc : 0, &used))
+    // (BFLY_DEBUG_REJECT_PROJ: test hook -- decline every offered projection so the caller's retry runs)
+    static const bool reject = std::getenv("BFLY_DEBUG_REJECT_PROJ") != nullptr;
+    const Level<R>* G = lp && !reject ? basis_product(mode, *lp) : nullptr;
+    if (!G && !Y) return false;  // neither a projection nor a product buffer: see do_apply
+    if (!bf->apply_structured(mode, p, ps, Xs, ld, Y, ldy, o0, o1, &fl, G, lp ? lp->level : 0, G ? lp->C : nullptr,
+                              G ? lp->ldc : 0))
       return false;
-    if (lp) lp->done = used;
+    if (lp) lp->done = G != nullptr;
     this->flops += fl;
     return true;
   }

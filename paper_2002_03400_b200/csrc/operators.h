@@ -19,17 +19,22 @@
 
 namespace bfly {
 
-// A transfer level needs only the leaf coefficients of a product in the NEW
-// factorization's leaf bases, L_nu^H (op(A) X)[leaf nu] (the first step of the
-// partial V / U chain, butterfly.hpp:330-354).  A kind that can fuse this
-// projection into its own last stage (the butterfly black box: its leaf
-// stage and the projection collapse into one P x P block per leaf) writes
-// the coefficients straight into the chain buffer C (slot nu at nu * P, ld
-// ldc, same columns as Y) and sets done; Y is then not written.
+// A transfer level never uses a product y = op(A) X itself, only its
+// coefficients in the NEW factorization's nested basis one level above the
+// probes: B_new(level)^H y, which the reference obtains by projecting y on
+// the leaf bases and running the partial V / U chain (butterfly.hpp:330-354).
+// A kind that knows y in a nested basis of its own can answer directly: the
+// butterfly black box stops its apply at `level` and multiplies
+// G = B_new(level)^H B_in(level) (one P x P block per butterfly block), so
+// its remaining stages, the n x w product and the caller's whole chain
+// disappear.  The coefficients go to the chain buffer C of that level (slot
+// = column node for OP_H products / row node for OP_N, P_new(level) rows per
+// slot, ld ldc, same columns as Y); done reports it, and Y is then not written.
 template <typename R>
 struct LeafProj {
-  const Level<R>* leaf = nullptr;  // the factorization's leaf level on the output side
-  const Tree* tree = nullptr;      // its tree
+  const DevButterfly<R>* nbf = nullptr;  // the factorization in progress
+  uint64_t gen = 0;                      // changes with every factorization (cached G levels)
+  int level = 0;                         // V side 0..lm-1 (OP_H products), U side lm+1..L (OP_N)
   cx<R>* C = nullptr;
   int64_t ldc = 0;
   bool done = false;
@@ -60,6 +65,10 @@ struct DevOp {
   // leaves in a sharded leaf phase); kinds that cannot restrict compute all.
   // count_cols >= 0 overrides the columns added to the counters
   LeafProj<R>* cur_lp = nullptr;  // the running apply_segs' projection request
+  // whether this kind would answer the request (the caller then does not
+  // allocate the product; a group that still comes back unanswered is
+  // multiplied again the plain way)
+  virtual bool can_project(int mode, const LeafProj<R>& lp) { return false; }
   void apply_segs(int mode, const cx<R>* X, const std::vector<MatvecSeg>& segs, cx<R>* Y, int64_t ldy,
                   int64_t o0 = 0, int64_t o1 = -1, int64_t count_cols = -1, LeafProj<R>* lp = nullptr) {
     int64_t cols = 0;

@@ -610,13 +610,14 @@ def test_structured_butterfly_products(tmp_path, case, vr):
     (DevButterfly::apply_structured); the reference pads the probes and
     multiplies the zeros (reconstruct.hpp:72-85, operators.hpp:106-122).
     Three runs on the same seeds: padded (P), structured (S), structured with
-    the chain's leaf projection fused into the black box's last stage (F, the
-    default).  S skips exact zeros only, so it must reproduce P -- same ranks,
-    same bookkeeping, apply outputs equal to rounding -- with fewer executed
-    flops.  F associates the leaf products differently (G = L_new^H L_in
-    first): identical ranks and apply within 1e-12 at complex128; at
-    complex64, where the ranks sit on the FP32 noise floor, it may only lower
-    them.  Also ragged leaves / varying ranks, a real butterfly and the
+    the basis projection answered by the black box (F, the default: the apply
+    stops one level above the probes and multiplies G = B_new^H B_in, so the
+    rest of its stages and the factorizer's projection chain disappear).  S
+    skips exact zeros only, so it must reproduce P -- same ranks, same
+    bookkeeping, apply outputs equal to rounding -- with fewer executed
+    flops.  F associates the products differently: identical ranks and apply
+    within 1e-12 at complex128; at complex64, where the ranks sit on the FP32
+    noise floor, it may only lower them.  Also ragged leaves / varying ranks, a real butterfly and the
     rank-sharded schedule."""
     import os
     import subprocess
@@ -624,16 +625,24 @@ def test_structured_butterfly_products(tmp_path, case, vr):
 
     worker = os.path.join(os.path.dirname(__file__), "struct_worker.py")
     res = {}
-    for tag, extra in (("P", {"BFLY_NO_STRUCT_APPLY": "1"}), ("S", {"BFLY_NO_LEAF_FUSE": "1"}), ("F", {})):
+    runs = [("P", {"BFLY_NO_STRUCT_APPLY": "1"}), ("S", {"BFLY_NO_LEAF_FUSE": "1"}), ("F", {})]
+    if case == "cfg4" and vr == 0:
+        # the projection is offered and declined: the factorizer multiplies again the plain way
+        runs.append(("R", {"BFLY_DEBUG_REJECT_PROJ": "1"}))
+    for tag, extra in runs:
         env = dict(os.environ)
-        env.pop("BFLY_NO_STRUCT_APPLY", None)
-        env.pop("BFLY_NO_LEAF_FUSE", None)
+        for k in ("BFLY_NO_STRUCT_APPLY", "BFLY_NO_LEAF_FUSE", "BFLY_DEBUG_REJECT_PROJ"):
+            env.pop(k, None)
         env.update(extra)
         out = str(tmp_path / f"{tag}.npz")
         cmd = [sys.executable, worker, "--case", case, "--out", out] + (["--vr", str(vr)] if vr else [])
         subprocess.run(cmd, check=True, env=env, timeout=600)
         res[tag] = np.load(out)
     p, s, f = res["P"], res["S"], res["F"]
+    if "R" in res:  # declined offers end in the structured products
+        np.testing.assert_array_equal(res["R"]["profile"], s["profile"])
+        np.testing.assert_array_equal(res["R"]["cols"], s["cols"])
+        assert rel_err(res["R"]["yn"], s["yn"]) <= 1e-13 and float(res["R"]["flops"]) == float(s["flops"])
     assert bool(s["struct"]) and bool(f["struct"]) and not bool(p["struct"])
     c64 = case == "cfg4_c64"
     # structured = padded minus exact zeros
