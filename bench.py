@@ -402,7 +402,7 @@ def run_ours(args):
                     ts_x.append(lx.total_seconds)
             med = statistics.median(ts_x)
             # flops = the ones executed (config 4's butterfly black box skips the blocks a
-            # structured probe's zero rows cannot reach and fuses the leaf projection: 3.5 TFLOP instead of the padded 18.7)
+            # structured probe's zero rows cannot reach and answers the basis projection itself: 1.0 TFLOP instead of the padded 18.7)
             other[wx.name] = {"construct_s": round(med, 4), "GFLOP/s": round(lx.flops / med / 1e9, 1),
                               "TFLOP_executed": round(lx.flops / 1e12, 3), "max_rank": bx.max_rank(), "nnz": bx.nnz()}
             del bx, wx
