@@ -88,7 +88,7 @@ class Factorizer {
   void probe_products(int mode, const Tree& probe_tree, int level, const std::vector<int64_t>& nodes,
                       const std::vector<int>& widths, const std::vector<int64_t>& col0, const std::vector<int64_t>& goff,
                       const V* G, int64_t wtot, DBuf<V>& Y, const std::vector<std::pair<int64_t, int64_t>>& orange,
-                      const std::vector<char>& counted, LeafProj<R>* lp = nullptr, std::vector<char>* fused = nullptr);
+                      const std::vector<char>& counted, BasisProj<R>* lp = nullptr, std::vector<char>* fused = nullptr);
   // W level: probe pieces (tau, partner nodes nu in [p0, p1)) of one rank
   void w_probes(int l, const std::vector<int>& width, const std::vector<ProbePiece>& pieces, int maxw);
   // R level: probe pieces (nu, partner nodes tau in [p0, p1)) of one rank

@@ -131,7 +131,7 @@ struct ButterflyOp : DevOp<R> {
       this->last_restricted = true;
       return;
     }
-    // a basis projection was expected (LeafProj) and no product buffer came
+    // a basis projection was expected (BasisProj) and no product buffer came
     // along: nothing is computed, the caller multiplies again the plain way
     if (!Y) return;
     for (const auto& run : column_runs(segs)) {
@@ -142,7 +142,7 @@ struct ButterflyOp : DevOp<R> {
       this->flops += bf->apply_flops(w);
     }
   }
-  // G levels of the factorization in progress (LeafProj, operators.h), built
+  // G levels of the factorization in progress (BasisProj, operators.h), built
   // level by level as its transfer levels complete:
   //   V side: G(0) = Vn_leaf^H V_leaf;  G(j) = Wn_j^H blockdiag(G(j-1) children) W_j
   //   U side: G(L) = Un_leaf^H U_leaf;  G(j) = Rn_j^H blockdiag(G(j+1) children) R_j
@@ -150,11 +150,11 @@ struct ButterflyOp : DevOp<R> {
   const DevButterfly<R>* g_owner = nullptr;
   uint64_t g_gen = 0;
   std::vector<std::unique_ptr<Level<R>>> gv, gu;  // gv[j] = level j; gu[k] = level L - k
-  bool can_project(int mode, const LeafProj<R>& lp) override {
+  bool can_project(int mode, const BasisProj<R>& lp) override {
     static const bool off = std::getenv("BFLY_NO_STRUCT_APPLY") != nullptr;
     return !off && basis_product(mode, lp) != nullptr;
   }
-  const Level<R>* basis_product(int mode, const LeafProj<R>& lp) {
+  const Level<R>* basis_product(int mode, const BasisProj<R>& lp) {
     static const bool off = std::getenv("BFLY_NO_LEAF_FUSE") != nullptr;
     const DevButterfly<R>* nb = lp.nbf;
     if (off || !nb || !lp.C) return nullptr;
@@ -324,7 +324,7 @@ struct ButterflyOp : DevOp<R> {
     }
     std::sort(ps.begin(), ps.end(), [](const auto& a, const auto& b) { return a.node < b.node; });
     double fl = 0;
-    LeafProj<R>* lp = this->cur_lp;
+    BasisProj<R>* lp = this->cur_lp;
     // (BFLY_DEBUG_REJECT_PROJ: test hook -- decline every offered projection so the caller's retry runs)
     static const bool reject = std::getenv("BFLY_DEBUG_REJECT_PROJ") != nullptr;
     const Level<R>* G = lp && !reject ? basis_product(mode, *lp) : nullptr;

@@ -31,7 +31,7 @@ namespace bfly {
 // = column node for OP_H products / row node for OP_N, P_new(level) rows per
 // slot, ld ldc, same columns as Y); done reports it, and Y is then not written.
 template <typename R>
-struct LeafProj {
+struct BasisProj {
   const DevButterfly<R>* nbf = nullptr;  // the factorization in progress
   uint64_t gen = 0;                      // changes with every factorization (cached G levels)
   int level = 0;                         // V side 0..lm-1 (OP_H products), U side lm+1..L (OP_N)
@@ -64,13 +64,13 @@ struct DevOp {
   // [o0, o1) restricts the output rows that must be produced (the rank's
   // leaves in a sharded leaf phase); kinds that cannot restrict compute all.
   // count_cols >= 0 overrides the columns added to the counters
-  LeafProj<R>* cur_lp = nullptr;  // the running apply_segs' projection request
+  BasisProj<R>* cur_lp = nullptr;  // the running apply_segs' projection request
   // whether this kind would answer the request (the caller then does not
   // allocate the product; a group that still comes back unanswered is
   // multiplied again the plain way)
-  virtual bool can_project(int mode, const LeafProj<R>& lp) { return false; }
+  virtual bool can_project(int mode, const BasisProj<R>& lp) { return false; }
   void apply_segs(int mode, const cx<R>* X, const std::vector<MatvecSeg>& segs, cx<R>* Y, int64_t ldy,
-                  int64_t o0 = 0, int64_t o1 = -1, int64_t count_cols = -1, LeafProj<R>* lp = nullptr) {
+                  int64_t o0 = 0, int64_t o1 = -1, int64_t count_cols = -1, BasisProj<R>* lp = nullptr) {
     int64_t cols = 0;
     for (const auto& s : segs) cols += s.ncols;
     if (count_cols >= 0) cols = count_cols;
