@@ -360,10 +360,23 @@ __global__ void __launch_bounds__(32 * NW) cpqr_warp_kernel(const cx<R>* __restr
     zero_out();
     return;
   }
-  // load the compact block (thread = row) and the column norms (thread = column)
-  for (int c = 0; c < w; ++c) {
-    const V* sc = src + e.src + (int64_t)c * ld_src;
-    for (int i = t; i < r; i += NT) Z[i + c * LD] = i < e.r1 ? sc[i] : sc[e.src_gap + (i - e.r1)];
+  // load the compact block (threads sweep the elements column by column: every
+  // thread busy and the loads independent -- with thread = row only r of the NT
+  // threads loaded, one dependent-latency round per column) and the column norms
+  // (thread = column)
+  if (NW == 1) {
+    for (int c = 0; c < w; ++c) {
+      const V* sc = src + e.src + (int64_t)c * ld_src;
+      for (int i = t; i < r; i += NT) Z[i + c * LD] = i < e.r1 ? sc[i] : sc[e.src_gap + (i - e.r1)];
+    }
+  } else {
+    const int tot = r * w;
+#pragma unroll 4
+    for (int idx = t; idx < tot; idx += NT) {
+      const int c = idx / r, i = idx - c * r;
+      const V* sc = src + e.src + (int64_t)c * ld_src;
+      Z[i + c * LD] = i < e.r1 ? sc[i] : sc[e.src_gap + (i - e.r1)];
+    }
   }
   sync();
   for (int c = t; c < w; c += NT) {
