@@ -405,6 +405,10 @@ def run_ours(args):
             # structured probe's zero rows cannot reach and answers the basis projection itself: 1.0 TFLOP instead of the padded 18.7)
             other[wx.name] = {"construct_s": round(med, 4), "GFLOP/s": round(lx.flops / med / 1e9, 1),
                               "TFLOP_executed": round(lx.flops / 1e12, 3), "max_rank": bx.max_rank(), "nnz": bx.nnz()}
+            if cid == 4:
+                # the same factorization through the reference's padded products (BFLY_NO_STRUCT_APPLY=1)
+                # executes 18.67 TFLOP in 0.715 s on this GPU (profiles/r02_cfg4_structured.txt)
+                other[wx.name]["padded_reference_path"] = {"TFLOP": 18.67, "construct_s": 0.715}
             del bx, wx
         del ctx_x
 
